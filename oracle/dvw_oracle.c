@@ -1,0 +1,215 @@
+/*
+ * dvw_oracle.c -- plain, slow, obviously correct CPU oracle of autoregressive
+ * WaveNet sample generation (Deep Voice, arXiv 1702.07825).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.  It
+ * shares no code with the CUDA path (paper_1702_07825_b200/csrc): it has its
+ * own weight-offset bookkeeping, its own sampler, its own everything.
+ *
+ * Arithmetic: scalar C, double throughout, no SIMD intrinsics, compiled
+ * without -ffast-math.  Weights, conditioning and uniforms arrive as the fp32
+ * values the GPU receives and are promoted to double.
+ *
+ * Algorithm, in the paper's order and notation (PAPER.md = /root/reference):
+ *   state: ring_j[d_j][r] = 0 ; y_{-1} = y_{-2} = a/2 = 128       (R4)
+ *   for n = 0 .. N-1:
+ *     f   = floor(n / hop)                                      (App. A.2 repetition)
+ *     x   = W_emb_prev[:, y_{n-2}] + W_emb_cur[:, y_{n-1}] + B_emb  (§5.1 step 1; R3)
+ *     q   = B_skip                                              (§5.1 step 2d)
+ *     for j = 1 .. l:
+ *       xp  = ring_j[n mod d_j]          (x^{(j-1)}_{n-d_j}, 0 if n < d_j)   (step 2a)
+ *       a   = W_prev xp + W_cur x + B + L^{(j)}_n               (steps 2a-2c)
+ *       h   = tanh(a[0:r]) * sigmoid(a[r:2r])                   (step 2c)
+ *       ring_j[n mod d_j] = x            (store x^{(j-1)}_n after reading)
+ *       x   = x + W_res h + B_res                               (App. A.1; R1)
+ *       q   = q + W_skip^{(j)} h                                (step 2d)
+ *     z_s = relu(q); z_a = relu(W_relu z_s + B_relu); l = W_out z_a + B_out   (step 3)
+ *     p   = softmax(l); y_n = inverse-CDF draw with u_n         (R11)
+ *
+ * Weight blob (include/dvw.h, restated here independently):
+ *   per layer j: W_prev[2r][r] W_cur[2r][r] B[2r] W_res[r][r] B_res[r] W_skip[s][r]
+ *   then W_emb_prev[r][a] W_emb_cur[r][a] B_emb[r] B_skip[s] W_relu[a][s]
+ *        B_relu[a] W_out[a][a] B_out[a]
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORACLE_API __attribute__((visibility("default")))
+
+ORACLE_API int64_t oracle_weights_numel(int L, int r, int s, int a) {
+  int64_t per_layer = (int64_t)2 * r * r + (int64_t)2 * r * r + 2 * r + (int64_t)r * r + r + (int64_t)s * r;
+  return L * per_layer + (int64_t)2 * r * a + r + s + (int64_t)a * s + a + (int64_t)a * a + a;
+}
+
+/* Inverse-CDF direct sampling (App. A.4 "Sample randomly from P(y)";
+ * reading R11): e_k = exp(l_k - max l); P_k = sum_{i<=k} e_i in ascending k;
+ * y = min{k : u * P_{a-1} < P_k}; fallback the largest k with e_k > 0. */
+static int sample_inverse_cdf(const double* logit, int a, double u, double* e) {
+  double m = logit[0];
+  for (int k = 1; k < a; ++k)
+    if (logit[k] > m) m = logit[k];
+  double S = 0.0;
+  for (int k = 0; k < a; ++k) {
+    e[k] = exp(logit[k] - m);
+    S += e[k];
+  }
+  double t = u * S, P = 0.0;
+  for (int k = 0; k < a; ++k) {
+    P += e[k];
+    if (t < P) return k;
+  }
+  for (int k = a - 1; k >= 0; --k)
+    if (e[k] > 0.0) return k;
+  return a - 1;
+}
+
+ORACLE_API int oracle_sample(const double* logits, int a, float u) {
+  double* e = (double*)malloc(sizeof(double) * a);
+  int y = sample_inverse_cdf(logits, a, (double)u, e);
+  free(e);
+  return y;
+}
+
+static double sigmoid(double v) { return 1.0 / (1.0 + exp(-v)); }
+
+/* y[i] = sum_k W[i][k] x[k], W row-major rows x cols (plain definition). */
+static void matvec(const double* W, int rows, int cols, const double* x, double* y) {
+  for (int i = 0; i < rows; ++i) {
+    double acc = 0.0;
+    for (int k = 0; k < cols; ++k) acc += W[(int64_t)i * cols + k] * x[k];
+    y[i] = acc;
+  }
+}
+
+/*
+ * One utterance.  Returns 0 on success, negative on bad arguments.
+ *   dilations   : length L, each >= 1 (NULL -> 2^((j-1) mod 10))
+ *   weights     : fp32 blob, numel must equal oracle_weights_numel
+ *   cond        : fp32 [n_frames][L][2r]; frame for sample n is n / hop
+ *   uniforms    : fp32 [N] (may be NULL only when forced != NULL)
+ *   forced      : uint8 [N] teacher-forced history, or NULL for free running
+ *   out_codes   : uint8 [N] the code fed back at step n (forced[n] or the draw)
+ *   out_logits  : double [N][a] pre-softmax logits (may be NULL)
+ *   out_sampled : uint8 [N] the draw with u_n even when teacher-forced (may be NULL)
+ */
+ORACLE_API int oracle_run(int L, int r, int s, int a, const int32_t* dilations,
+                          const float* weights, int64_t numel, const float* cond,
+                          int64_t n_frames, int hop, const float* uniforms,
+                          const uint8_t* forced, int64_t N, uint8_t* out_codes,
+                          double* out_logits, uint8_t* out_sampled) {
+  if (L < 1 || r < 1 || s < 1 || a < 2 || a > 256 || hop < 1 || N < 0) return -1;
+  if (numel != oracle_weights_numel(L, r, s, a)) return -2;
+  if (N > 0 && n_frames < (N + hop - 1) / hop) return -3;
+  if (!forced && !uniforms) return -4;
+
+  int* d = (int*)malloc(sizeof(int) * L);
+  int64_t ring_total = 0;
+  for (int j = 0; j < L; ++j) {
+    d[j] = dilations ? dilations[j] : (1 << (j % 10));
+    if (d[j] < 1) { free(d); return -5; }
+    ring_total += d[j];
+  }
+
+  /* promote the blob to double once */
+  double* W = (double*)malloc(sizeof(double) * numel);
+  for (int64_t i = 0; i < numel; ++i) W[i] = (double)weights[i];
+
+  /* offsets, written out from the roster */
+  int64_t per_layer = (int64_t)4 * r * r + 2 * r + (int64_t)r * r + r + (int64_t)s * r;
+  const double** Wprev = (const double**)malloc(sizeof(double*) * L);
+  const double** Wcur = (const double**)malloc(sizeof(double*) * L);
+  const double** Bj = (const double**)malloc(sizeof(double*) * L);
+  const double** Wres = (const double**)malloc(sizeof(double*) * L);
+  const double** Bres = (const double**)malloc(sizeof(double*) * L);
+  const double** Wskip = (const double**)malloc(sizeof(double*) * L);
+  for (int j = 0; j < L; ++j) {
+    const double* p = W + j * per_layer;
+    Wprev[j] = p;            p += (int64_t)2 * r * r;
+    Wcur[j] = p;             p += (int64_t)2 * r * r;
+    Bj[j] = p;               p += 2 * r;
+    Wres[j] = p;             p += (int64_t)r * r;
+    Bres[j] = p;             p += r;
+    Wskip[j] = p;
+  }
+  const double* g = W + L * per_layer;
+  const double* Wemb_prev = g; g += (int64_t)r * a;
+  const double* Wemb_cur = g;  g += (int64_t)r * a;
+  const double* Bemb = g;      g += r;
+  const double* Bskip = g;     g += s;
+  const double* Wrelu = g;     g += (int64_t)a * s;
+  const double* Brelu = g;     g += a;
+  const double* Wout = g;      g += (int64_t)a * a;
+  const double* Bout = g;
+
+  double* ring = (double*)calloc(ring_total * r, sizeof(double));
+  int64_t* ring_off = (int64_t*)malloc(sizeof(int64_t) * L);
+  int64_t acc_off = 0;
+  for (int j = 0; j < L; ++j) { ring_off[j] = acc_off; acc_off += (int64_t)d[j] * r; }
+
+  double* x = (double*)malloc(sizeof(double) * r);
+  double* xnew = (double*)malloc(sizeof(double) * r);
+  double* ap = (double*)malloc(sizeof(double) * 2 * r);
+  double* ac = (double*)malloc(sizeof(double) * 2 * r);
+  double* h = (double*)malloc(sizeof(double) * r);
+  double* rh = (double*)malloc(sizeof(double) * r);
+  double* q = (double*)malloc(sizeof(double) * s);
+  double* sk = (double*)malloc(sizeof(double) * s);
+  double* zs = (double*)malloc(sizeof(double) * s);
+  double* za = (double*)malloc(sizeof(double) * a);
+  double* lg = (double*)malloc(sizeof(double) * a);
+  double* e = (double*)malloc(sizeof(double) * a);
+
+  /* y_{n-1}, y_{n-2}: codes at negative times are mu-law(0) = a/2 (= 128 at a = 256; R4) */
+  int y1 = a / 2, y2 = a / 2;
+  for (int64_t n = 0; n < N; ++n) {
+    int64_t f = n / hop;
+    /* step 1: sample embedding, two column lookups */
+    for (int i = 0; i < r; ++i)
+      x[i] = Wemb_prev[(int64_t)i * a + y2] + Wemb_cur[(int64_t)i * a + y1] + Bemb[i];
+    for (int i = 0; i < s; ++i) q[i] = Bskip[i];
+    /* step 2: layers */
+    for (int j = 0; j < L; ++j) {
+      double* slot = ring + ring_off[j] + (int64_t)(n % d[j]) * r;
+      const float* Lj = cond + ((int64_t)f * L + j) * 2 * r;
+      matvec(Wprev[j], 2 * r, r, slot, ap);
+      matvec(Wcur[j], 2 * r, r, x, ac);
+      for (int i = 0; i < r; ++i) {
+        double ah = ap[i] + ac[i] + Bj[j][i] + (double)Lj[i];
+        double ag = ap[r + i] + ac[r + i] + Bj[j][r + i] + (double)Lj[r + i];
+        h[i] = tanh(ah) * sigmoid(ag);
+      }
+      memcpy(slot, x, sizeof(double) * r);
+      matvec(Wres[j], r, r, h, rh);
+      for (int i = 0; i < r; ++i) xnew[i] = x[i] + rh[i] + Bres[j][i];
+      memcpy(x, xnew, sizeof(double) * r);
+      matvec(Wskip[j], s, r, h, sk);
+      for (int i = 0; i < s; ++i) q[i] += sk[i];
+    }
+    /* step 3: output */
+    for (int i = 0; i < s; ++i) zs[i] = q[i] > 0.0 ? q[i] : 0.0;
+    matvec(Wrelu, a, s, zs, za);
+    for (int i = 0; i < a; ++i) {
+      double v = za[i] + Brelu[i];
+      za[i] = v > 0.0 ? v : 0.0;
+    }
+    matvec(Wout, a, a, za, lg);
+    for (int i = 0; i < a; ++i) lg[i] += Bout[i];
+    if (out_logits) memcpy(out_logits + n * a, lg, sizeof(double) * a);
+    int drawn = -1;
+    if (uniforms) drawn = sample_inverse_cdf(lg, a, (double)uniforms[n], e);
+    if (out_sampled) out_sampled[n] = (uint8_t)(drawn < 0 ? 0 : drawn);
+    int y = forced ? (int)forced[n] : drawn;
+    out_codes[n] = (uint8_t)y;
+    y2 = y1;
+    y1 = y;
+  }
+
+  free(x); free(xnew); free(ap); free(ac); free(h); free(rh); free(q); free(sk);
+  free(zs); free(za); free(lg); free(e); free(ring); free(ring_off);
+  free(Wprev); free(Wcur); free(Bj); free(Wres); free(Bres); free(Wskip);
+  free(W); free(d);
+  return 0;
+}

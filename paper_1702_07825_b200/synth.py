@@ -1,0 +1,143 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU tests and bench.py.
+
+This module holds NONE of the method's arithmetic: it only draws random numbers
+and lays them out in the boundary's documented order (include/dvw.h).  It is
+the one module both sides may use.
+
+Recipe ("Synthetic inputs"):
+
+* weights: ``np.random.default_rng(seed)`` (PCG64), uniform(+-1/sqrt(fan_in)),
+  drawn in fp64 tensor by tensor in blob order, rounded to fp32.
+  fan_in = r for W_prev, W_cur, B, W_res, B_res; l*r for W_skip, B_skip;
+  s for W_relu, B_relu; a for W_out, B_out, W_emb_prev, W_emb_cur, B_emb.
+  Profile "peaky" multiplies W_out and B_out by 30 (logit std ~0.05 -> ~1.4).
+* conditioning for utterance u: ``default_rng([1, u]).uniform(-0.5, 0.5,
+  (n_frames, l, 2r))`` as fp32, one frame per ``hop`` = 64 samples
+  (App. A.3: 256 Hz features, 16,384 Hz audio).
+* uniforms for utterance u: ``default_rng([2, u]).random(N, dtype=float32)``.
+
+Keying every input by (role, u) makes it independent of batch composition and
+GPU count (SURVEY.md §8(e) sharding invariance).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+LEVELS = 256  # a: mu-law levels (§3.4; App. A.1)
+DEFAULT_HOP = 64  # 16,384 Hz / 256 Hz (App. A.3)
+AUDIO_HZ = 16000  # BASELINE.json real-time rate
+
+
+@dataclasses.dataclass(frozen=True)
+class Config:
+    """WaveNet size (§3.4: l layers, r residual, s skip, a levels)."""
+
+    n_layers: int
+    residual: int
+    skip: int
+    levels: int = LEVELS
+    dilations: Optional[Tuple[int, ...]] = None  # None -> 2^((j-1) mod 10)
+
+    def dilation_list(self) -> List[int]:
+        if self.dilations is not None:
+            assert len(self.dilations) == self.n_layers
+            return list(self.dilations)
+        return [2 ** (j % 10) for j in range(self.n_layers)]
+
+
+# The BASELINE.json configs (SURVEY.md §8(a) shorthand).
+C1 = Config(20, 64, 128)
+C2 = Config(20, 64, 256)
+C3 = Config(40, 64, 256)
+C4 = Config(20, 128, 256)
+C5 = Config(40, 64, 256)
+
+
+def roster(cfg: Config) -> List[Tuple[str, Tuple[int, ...], int]]:
+    """(name, shape, fan_in) in blob order (include/dvw.h "Weight blob")."""
+    L, r, s, a = cfg.n_layers, cfg.residual, cfg.skip, cfg.levels
+    out = []
+    for j in range(L):
+        out += [
+            (f"W_prev.{j}", (2 * r, r), r),
+            (f"W_cur.{j}", (2 * r, r), r),
+            (f"B.{j}", (2 * r,), r),
+            (f"W_res.{j}", (r, r), r),
+            (f"B_res.{j}", (r,), r),
+            (f"W_skip.{j}", (s, r), L * r),
+        ]
+    out += [
+        ("W_emb_prev", (r, a), a),
+        ("W_emb_cur", (r, a), a),
+        ("B_emb", (r,), a),
+        ("B_skip", (s,), L * r),
+        ("W_relu", (a, s), s),
+        ("B_relu", (a,), s),
+        ("W_out", (a, a), a),
+        ("B_out", (a,), a),
+    ]
+    return out
+
+
+def weights_numel(cfg: Config) -> int:
+    return int(sum(int(np.prod(shape)) for _, shape, _ in roster(cfg)))
+
+
+def make_weights(cfg: Config, seed: int = 0, profile: str = "default") -> np.ndarray:
+    """Flat fp32 blob in roster order."""
+    rng = np.random.default_rng(seed)
+    parts = []
+    for name, shape, fan_in in roster(cfg):
+        bound = 1.0 / math.sqrt(fan_in)
+        t = rng.uniform(-bound, bound, size=shape)  # fp64 draw
+        if profile == "peaky" and name in ("W_out", "B_out"):
+            t = t * 30.0
+        elif profile not in ("default", "peaky"):
+            raise ValueError(f"unknown weight profile {profile!r}")
+        parts.append(t.astype(np.float32).ravel())
+    return np.concatenate(parts)
+
+
+def split_weights(cfg: Config, blob: np.ndarray) -> dict:
+    """Views of the blob by roster name (layout bookkeeping only)."""
+    out, off = {}, 0
+    for name, shape, _ in roster(cfg):
+        n = int(np.prod(shape))
+        out[name] = blob[off:off + n].reshape(shape)
+        off += n
+    assert off == blob.size
+    return out
+
+
+def n_frames_for(n_samples: int, hop: int) -> int:
+    return max(1, -(-n_samples // hop))
+
+
+def make_cond(cfg: Config, n_frames: int, utt: int = 0) -> np.ndarray:
+    """fp32 [n_frames][l][2r] frame-rate conditioning for utterance ``utt``."""
+    rng = np.random.default_rng([1, utt])
+    return rng.uniform(-0.5, 0.5, (n_frames, cfg.n_layers, 2 * cfg.residual)).astype(np.float32)
+
+
+def make_uniforms(n_samples: int, utt: int = 0) -> np.ndarray:
+    """fp32 [N] in [0, 1), 24-bit granularity."""
+    rng = np.random.default_rng([2, utt])
+    return rng.random(n_samples, dtype=np.float32)
+
+
+def make_batch(cfg: Config, n_samples: int, utts: Sequence[int], hop: int = DEFAULT_HOP):
+    """Stacked (cond [U][F][l][2r], uniforms [U][N]) for a list of utterance ids."""
+    nf = n_frames_for(n_samples, hop)
+    cond = np.stack([make_cond(cfg, nf, u) for u in utts])
+    uni = np.stack([make_uniforms(n_samples, u) for u in utts])
+    return cond, uni
+
+
+def make_codes(n_samples: int, utt: int = 0, levels: int = LEVELS) -> np.ndarray:
+    """Random uint8 code history for teacher-forced runs (role key 3)."""
+    rng = np.random.default_rng([3, utt])
+    return rng.integers(0, levels, n_samples, dtype=np.int64).astype(np.uint8)
