@@ -1,0 +1,178 @@
+/*
+ * dvw.h -- C ABI of the B200-native autoregressive WaveNet sample generator
+ * (Deep Voice, arXiv 1702.07825).  libdvw.so exports exactly these symbols.
+ *
+ * The operation (PAPER.md = the paper's LaTeX source):
+ *   PAPER.md:416 (App. A)  "auto-regressive process P(y_i | c, y_{i-1}, ..., y_{i-R})"
+ *   PAPER.md:340-377 (§5.1 steps 1-3) and PAPER.md:427-457 (App. A.1): per generated
+ *     sample, the input 2x1 convolution done as two embedding lookups, l gated
+ *     dilated 2x1 convolution layers with residual (r) and skip (s) projections,
+ *     relu -> 1x1 -> relu -> 1x1 -> softmax over a = 256 mu-law levels,
+ *   PAPER.md:376, 501 (App. A.4 direct sampling): draw y from p, feed it back.
+ *   Conditioning is taken already computed, at frame rate, and upsampled by
+ *   repetition inside the kernel (App. A.2).
+ * DESIGN.md lists every reading of a point the paper leaves open (R1..R21);
+ * the ones that fix the ABI's semantics are cited below.
+ *
+ * Conventions for every entry point:
+ *   - returns dvw_status; DVW_OK = 0.  On any other status the thread-local
+ *     text from dvw_last_error() says what was wrong.  No C++ exception ever
+ *     crosses this boundary.
+ *   - all tensors are row-major, little-endian, contiguous.
+ *   - pointers are DEVICE pointers on the model's device unless the entry point
+ *     name ends in _host or the argument says otherwise.  The caller owns every
+ *     buffer it passes; the library never frees or retains them past the call.
+ *   - calls are asynchronous on `cuda_stream` (a cudaStream_t, NULL = legacy
+ *     default stream).  Argument errors and launch errors are returned
+ *     immediately; device-side faults (a spin-wait watchdog firing) surface at
+ *     dvw_sync() or at the next call on the handle.
+ *   - a handle is not re-entrant: one call at a time.  Handles are independent.
+ */
+#ifndef DVW_H_
+#define DVW_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define DVW_API __attribute__((visibility("default")))
+#else
+#define DVW_API
+#endif
+
+typedef struct dvw_model dvw_model; /* opaque, owned by the library */
+
+typedef enum {
+  DVW_OK = 0,
+  DVW_E_INVALID_ARG = 1,    /* null pointer, non-finite weights, bad enum value */
+  DVW_E_SHAPE = 2,          /* sizes inconsistent: numel, n_frames < ceil(N/hop), hop < 1 ... */
+  DVW_E_UNSUPPORTED = 3,    /* (r, s, a) or kernel choice this build does not implement */
+  DVW_E_STATE = 4,          /* generate/logits before load_weights */
+  DVW_E_OOM = 5,            /* device allocation failed */
+  DVW_E_CUDA = 6,           /* CUDA runtime error (text has cudaGetErrorString) */
+  DVW_E_DEVICE_TIMEOUT = 7  /* a persistent kernel's spin-wait watchdog fired */
+} dvw_status;
+
+/* Model sizes (§3.4: l layers, r residual, s skip channels;
+ * a = 256 mu-law levels).
+ *   n_layers  l >= 1
+ *   residual  r in {32, 64, 128}
+ *   skip      s in {128, 256}
+ *   levels    a, must be 256
+ *   dilations length l, each >= 1, copied at create time; NULL selects
+ *             d_j = 2^((j-1) mod 10) (reading R2: the only cycle consistent with
+ *             PAPER.md:166's 83 ms receptive field for l = 40 at 48 kHz)
+ *   device    CUDA ordinal the handle lives on */
+typedef struct {
+  int32_t n_layers;
+  int32_t residual;
+  int32_t skip;
+  int32_t levels;
+  const int32_t* dilations;
+  int32_t device;
+} dvw_config;
+
+/* Kernel selection.  AUTO picks CLUSTER for n_streams == 1
+ * when the model fits its residency plan, else STREAM. */
+typedef enum {
+  DVW_KERNEL_AUTO = 0,
+  DVW_KERNEL_STREAM = 1,  /* one CTA per stream, weights read from L2 every sample */
+  DVW_KERNEL_CLUSTER = 2, /* batch-1 persistent cluster kernel, weights on chip */
+  DVW_KERNEL_TC = 3       /* batched streams, tcgen05 projections (when built) */
+} dvw_kernel;
+
+typedef struct {
+  int32_t last_kernel;       /* dvw_kernel that ran the last generate/logits call */
+  int32_t last_grid;         /* CTAs launched */
+  int32_t last_cluster;      /* cluster size (1 = none) */
+  int32_t last_threads;      /* threads per CTA */
+  int64_t last_launches;     /* kernel launches issued by the last call */
+  int64_t weight_bytes;      /* bytes of packed device weights the handle owns */
+  int64_t workspace_bytes;   /* bytes of per-stream state (dilation rings) */
+} dvw_info;
+
+/* Create a handle on cfg->device.  Validates sizes (DVW_E_SHAPE / DVW_E_UNSUPPORTED).
+ * *out is set only on DVW_OK. */
+DVW_API dvw_status dvw_create(const dvw_config* cfg, dvw_model** out);
+
+/* Expected weight-blob length in floats (no handle needed):
+ *   l (5 r^2 + 3 r + r s) + 2 r a + r + s + a s + a + a^2 + a.
+ * Returns -1 for an invalid config. */
+DVW_API int64_t dvw_weights_numel(const dvw_config* cfg);
+
+/* Load the weights.  blob: fp32, numel floats, in this order:
+ *   for j = 1..l: W_prev[2r][r]  W_cur[2r][r]  B[2r]  W_res[r][r]  B_res[r]  W_skip[s][r]
+ *   then W_emb_prev[r][a]  W_emb_cur[r][a]  B_emb[r]  B_skip[s]
+ *        W_relu[a][s]  B_relu[a]  W_out[a][a]  B_out[a]
+ *   Rows 0..r-1 of W_prev, W_cur, B feed tanh, rows r..2r-1 feed the sigmoid
+ *   (reading R7).  One bias B per layer (reading R8).
+ * blob_on_device != 0: blob is a device pointer on the model's device, else host.
+ * The library builds its own packed device copy (residency layout); the caller may
+ * free blob when this returns.  Synchronous.  Non-finite values -> DVW_E_INVALID_ARG;
+ * numel mismatch -> DVW_E_SHAPE. */
+DVW_API dvw_status dvw_load_weights(dvw_model* m, const float* blob, int64_t numel,
+                                    int32_t blob_on_device);
+
+/* Free-running generation (App. A.4 direct sampling).
+ *   cond      fp32 [n_streams][n_frames][l][2r]: L^(j) for frame f; sample n uses
+ *             frame n / hop (repetition upsampling; readings R5, R6).
+ *             Requires n_frames >= ceil(n_samples / hop) and hop >= 1.
+ *   uniforms  fp32 [n_streams][n_samples] in [0, 1): u_n for the inverse-CDF draw
+ *             y_n = min{k : u_n * P_255 < P_k}, P_k the fp64 running sum of
+ *             exp(l_i - max l) in ascending code order (reading R11).  Values
+ *             outside [0,1) are not validated (precondition).
+ *   out_codes uint8 [n_streams][n_samples]: the emitted mu-law codes.
+ * Every call starts from the fresh state: dilation queues zero, codes at negative
+ * times 128 = mu-law(0) (reading R4).  Results are bitwise deterministic for the
+ * same inputs, independent of n_streams and of the stream's position (R20). */
+DVW_API dvw_status dvw_generate(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop,
+                                const float* uniforms, int64_t n_samples, int32_t n_streams,
+                                uint8_t* out_codes, void* cuda_stream);
+
+/* Teacher-forced evaluation: the same network, but the code fed back after step n
+ * is codes[n] (uint8 [n_streams][n_samples]); writes the PRE-softmax logits
+ * l = W_out z_a + B_out (reading R15) to
+ * out_logits fp32 [n_streams][n_samples][256].  logits[n] depends on codes[0..n-1]. */
+DVW_API dvw_status dvw_logits(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop,
+                              const uint8_t* codes, int64_t n_samples, int32_t n_streams,
+                              float* out_logits, void* cuda_stream);
+
+/* dvw_generate with HOST buffers (pageable or pinned): copies cond and uniforms
+ * to library-owned device staging, generates, copies the codes back, and
+ * synchronizes before returning.  Used for end-to-end timing. */
+DVW_API dvw_status dvw_generate_host(dvw_model* m, const float* cond_host, int64_t n_frames,
+                                     int32_t hop, const float* uniforms_host, int64_t n_samples,
+                                     int32_t n_streams, uint8_t* out_codes_host,
+                                     void* cuda_stream);
+
+/* Pin the kernel used by later calls (DVW_KERNEL_AUTO restores the default).
+ * DVW_E_UNSUPPORTED if that kernel cannot run this model. */
+DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel);
+
+/* Tracing: when device_buf != NULL, persistent kernels record %globaltimer (ns)
+ * at fixed events of samples [first_sample, first_sample + n_samples) into
+ * device_buf, uint64 [n_samples][16 cluster ranks][32 events] (unwritten slots keep
+ * their old value; the caller zero-fills).  Event meaning per role is listed in
+ * DESIGN.md "Tracing".  NULL disables tracing.  Off the hot path when disabled. */
+DVW_API dvw_status dvw_set_trace(dvw_model* m, uint64_t* device_buf, int64_t first_sample, int32_t n_samples);
+
+/* Launch bookkeeping of the last call (filled synchronously, host side). */
+DVW_API dvw_status dvw_get_info(const dvw_model* m, dvw_info* out);
+
+/* Wait for the handle's outstanding work; returns DVW_E_DEVICE_TIMEOUT if a
+ * device watchdog fired, DVW_E_CUDA on an asynchronous CUDA error. */
+DVW_API dvw_status dvw_sync(dvw_model* m);
+
+/* Release the handle and everything it owns.  NULL is a no-op. */
+DVW_API void dvw_destroy(dvw_model* m);
+
+/* Thread-local text for the last non-OK status ("" if none). */
+DVW_API const char* dvw_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DVW_H_ */

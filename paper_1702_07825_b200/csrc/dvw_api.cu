@@ -1,0 +1,385 @@
+// dvw_api.cu -- the C ABI declared in include/dvw.h.
+//
+// Host-side bookkeeping only: argument validation, the library-owned device
+// copies of the weights (raw roster layout + each kernel's packed residency
+// layout), the per-stream dilation-queue workspace, kernel selection and error
+// reporting.  Every step of the generation itself runs in the kernels.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "dvw_internal.cuh"
+#include "kernel_cluster.cuh"
+
+using namespace dvw;
+
+struct dvw_model {
+  int device = 0;
+  int L = 0, r = 0, s = 0, a = 0;
+  std::vector<int32_t> dil;
+  std::vector<int64_t> ring_off;  // floats, per layer, within one stream's ring
+  int64_t ring_floats = 0;
+  Offsets off{};
+  bool loaded = false;
+  int kernel = DVW_KERNEL_AUTO;
+  // device buffers
+  float* d_w = nullptr;
+  int32_t* d_dil = nullptr;
+  int64_t* d_ring_off = nullptr;
+  float* d_ring = nullptr;
+  int64_t ring_streams = 0;  // streams the workspace is sized for
+  int* d_err = nullptr;       // device view of the mapped, pinned error word
+  volatile int* h_err = nullptr;  // host view (read without synchronizing)
+  ClusterPlan cplan{};
+  void* d_packed = nullptr;  // cluster-kernel residency layout
+  size_t packed_bytes = 0;
+  // host-call staging
+  void* d_stage = nullptr;
+  size_t stage_bytes = 0;
+  dvw_info info{};
+  uint64_t* trace = nullptr;
+  int64_t trace_n0 = 0;
+  int trace_count = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+dvw_status fail(dvw_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+dvw_status fail(dvw_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+dvw_status cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(DVW_E_OOM, "%s: %s", what, cudaGetErrorString(e));
+  }
+  return fail(DVW_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define DVW_CUDA(call, what)                        \
+  do {                                              \
+    cudaError_t e_ = (call);                        \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+dvw_status check_config(const dvw_config* c) {
+  if (!c) return fail(DVW_E_INVALID_ARG, "config is NULL");
+  if (c->n_layers < 1) return fail(DVW_E_SHAPE, "n_layers must be >= 1 (got %d)", c->n_layers);
+  if (c->levels != kLevels) return fail(DVW_E_UNSUPPORTED, "levels must be 256 (got %d)", c->levels);
+  if (c->residual != 32 && c->residual != 64 && c->residual != 128)
+    return fail(DVW_E_UNSUPPORTED, "residual must be 32, 64 or 128 (got %d)", c->residual);
+  if (c->skip != 128 && c->skip != 256)
+    return fail(DVW_E_UNSUPPORTED, "skip must be 128 or 256 (got %d)", c->skip);
+  if (c->dilations) {
+    for (int j = 0; j < c->n_layers; ++j)
+      if (c->dilations[j] < 1) return fail(DVW_E_SHAPE, "dilation[%d] = %d < 1", j, c->dilations[j]);
+  }
+  return DVW_OK;
+}
+
+dvw_status ensure_ring(dvw_model* m, int n_streams) {
+  if (m->ring_streams >= n_streams) return DVW_OK;
+  if (m->d_ring) cudaFree(m->d_ring);
+  m->d_ring = nullptr;
+  m->ring_streams = 0;
+  const size_t bytes = sizeof(float) * (size_t)m->ring_floats * n_streams;
+  DVW_CUDA(cudaMalloc(&m->d_ring, bytes), "allocating dilation queues");
+  m->ring_streams = n_streams;
+  m->info.workspace_bytes = (int64_t)bytes;
+  return DVW_OK;
+}
+
+// The error word is mapped pinned host memory written by the kernels' watchdogs,
+// so checking it never synchronizes the stream.
+dvw_status check_device_error(dvw_model* m) {
+  const int h = *m->h_err;
+  if (h != 0) {
+    *m->h_err = 0;
+    return fail(DVW_E_DEVICE_TIMEOUT, "device watchdog fired (code %d): a persistent kernel spin-wait timed out", h);
+  }
+  return DVW_OK;
+}
+
+dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, const float* uniforms,
+               const uint8_t* forced, int64_t n_samples, int32_t n_streams, uint8_t* out_codes,
+               float* out_logits, void* stream) {
+  if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
+  if (!m->loaded) return fail(DVW_E_STATE, "weights not loaded (call dvw_load_weights first)");
+  if (n_samples < 0) return fail(DVW_E_SHAPE, "n_samples must be >= 0");
+  if (n_streams < 1) return fail(DVW_E_SHAPE, "n_streams must be >= 1 (got %d)", n_streams);
+  if (hop < 1) return fail(DVW_E_SHAPE, "hop must be >= 1 (got %d)", hop);
+  if (n_samples > 0 && n_frames < (n_samples + hop - 1) / hop)
+    return fail(DVW_E_SHAPE, "n_frames = %lld < ceil(n_samples / hop) = %lld", (long long)n_frames,
+                (long long)((n_samples + hop - 1) / hop));
+  if (n_samples == 0) return DVW_OK;
+  if (!cond) return fail(DVW_E_INVALID_ARG, "cond is NULL");
+  if (forced) {
+    if (!out_logits) return fail(DVW_E_INVALID_ARG, "out_logits is NULL");
+  } else {
+    if (!uniforms) return fail(DVW_E_INVALID_ARG, "uniforms is NULL");
+    if (!out_codes) return fail(DVW_E_INVALID_ARG, "out_codes is NULL");
+  }
+  DeviceGuard g(m->device);
+  dvw_status st = check_device_error(m);
+  if (st != DVW_OK) return st;
+  st = ensure_ring(m, n_streams);
+  if (st != DVW_OK) return st;
+
+  RunArgs A{};
+  A.w = m->d_w;
+  A.off = m->off;
+  A.L = m->L;
+  A.r = m->r;
+  A.s = m->s;
+  A.dil = m->d_dil;
+  A.ring_off = m->d_ring_off;
+  A.ring_floats = m->ring_floats;
+  A.cond = cond;
+  A.n_frames = n_frames;
+  A.hop = hop;
+  A.uniforms = uniforms;
+  A.forced = forced;
+  A.N = n_samples;
+  A.n_streams = n_streams;
+  A.out_codes = out_codes;
+  A.out_logits = out_logits;
+  A.ring = m->d_ring;
+  A.err = m->d_err;
+  A.trace = m->trace;
+  A.trace_n0 = m->trace_n0;
+  A.trace_count = m->trace_count;
+
+  int kern = m->kernel;
+  if (kern == DVW_KERNEL_AUTO) kern = (n_streams == 1 && m->cplan.ok) ? DVW_KERNEL_CLUSTER : DVW_KERNEL_STREAM;
+  LaunchInfo li{};
+  cudaError_t e;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  if (kern == DVW_KERNEL_CLUSTER) {
+    e = launch_cluster_kernel(A, m->cplan, m->d_packed, cs, &li);
+  } else if (kern == DVW_KERNEL_STREAM) {
+    e = launch_stream_kernel(A, cs, &li);
+  } else {
+    return fail(DVW_E_UNSUPPORTED, "kernel %d is not available in this build", kern);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  m->info.last_kernel = kern;
+  m->info.last_grid = li.grid;
+  m->info.last_cluster = li.cluster;
+  m->info.last_threads = li.threads;
+  m->info.last_launches = li.launches;
+  return DVW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+DVW_API int64_t dvw_weights_numel(const dvw_config* cfg) {
+  if (!cfg || cfg->n_layers < 1 || cfg->residual < 1 || cfg->skip < 1 || cfg->levels != kLevels) return -1;
+  return make_offsets(cfg->n_layers, cfg->residual, cfg->skip).numel;
+}
+
+DVW_API dvw_status dvw_create(const dvw_config* cfg, dvw_model** out) {
+  if (!out) return fail(DVW_E_INVALID_ARG, "out is NULL");
+  dvw_status st = check_config(cfg);
+  if (st != DVW_OK) return st;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (cfg->device < 0 || cfg->device >= ndev)
+    return fail(DVW_E_INVALID_ARG, "device %d out of range (%d devices)", cfg->device, ndev);
+  DeviceGuard g(cfg->device);
+  dvw_model* m = new (std::nothrow) dvw_model();
+  if (!m) return fail(DVW_E_OOM, "host allocation failed");
+  m->device = cfg->device;
+  m->L = cfg->n_layers;
+  m->r = cfg->residual;
+  m->s = cfg->skip;
+  m->a = cfg->levels;
+  m->dil.resize(m->L);
+  m->ring_off.resize(m->L);
+  int64_t acc = 0;
+  for (int j = 0; j < m->L; ++j) {
+    m->dil[j] = cfg->dilations ? cfg->dilations[j] : (1 << (j % 10));
+    m->ring_off[j] = acc;
+    acc += (int64_t)m->dil[j] * m->r;
+  }
+  m->ring_floats = acc;
+  m->off = make_offsets(m->L, m->r, m->s);
+  e = cudaMalloc(&m->d_dil, sizeof(int32_t) * m->L);
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_ring_off, sizeof(int64_t) * m->L);
+  if (e == cudaSuccess) {
+    int* hp = nullptr;
+    e = cudaHostAlloc(reinterpret_cast<void**>(&hp), sizeof(int), cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+      *hp = 0;
+      m->h_err = hp;
+      e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&m->d_err), hp, 0);
+    }
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(m->d_dil, m->dil.data(), sizeof(int32_t) * m->L, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(m->d_ring_off, m->ring_off.data(), sizeof(int64_t) * m->L, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    dvw_destroy(m);
+    return cuda_fail(e, "dvw_create device setup");
+  }
+  m->cplan = plan_cluster(m->L, m->r, m->s, m->device);
+  *out = m;
+  return DVW_OK;
+}
+
+DVW_API dvw_status dvw_load_weights(dvw_model* m, const float* blob, int64_t numel, int32_t blob_on_device) {
+  if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
+  if (!blob) return fail(DVW_E_INVALID_ARG, "blob is NULL");
+  if (numel != m->off.numel)
+    return fail(DVW_E_SHAPE, "weight blob has %lld floats, expected %lld", (long long)numel,
+                (long long)m->off.numel);
+  DeviceGuard g(m->device);
+  std::vector<float> host;
+  const float* hp = blob;
+  if (blob_on_device) {
+    host.resize(numel);
+    DVW_CUDA(cudaMemcpy(host.data(), blob, sizeof(float) * numel, cudaMemcpyDeviceToHost), "reading device blob");
+    hp = host.data();
+  }
+  for (int64_t i = 0; i < numel; ++i)
+    if (!std::isfinite(hp[i])) return fail(DVW_E_INVALID_ARG, "weight %lld is not finite", (long long)i);
+  if (!m->d_w) DVW_CUDA(cudaMalloc(&m->d_w, sizeof(float) * numel), "allocating weights");
+  DVW_CUDA(cudaMemcpy(m->d_w, hp, sizeof(float) * numel, cudaMemcpyHostToDevice), "uploading weights");
+  int64_t wb = sizeof(float) * numel;
+  if (m->cplan.ok) {
+    size_t need = packed_bytes(m->cplan);
+    if (m->d_packed && m->packed_bytes < need) {
+      cudaFree(m->d_packed);
+      m->d_packed = nullptr;
+    }
+    if (!m->d_packed) {
+      DVW_CUDA(cudaMalloc(&m->d_packed, need), "allocating packed weights");
+      m->packed_bytes = need;
+    }
+    DVW_CUDA(pack_cluster_weights(m->cplan, hp, m->off, m->d_packed), "packing weights");
+    wb += (int64_t)need;
+  }
+  m->info.weight_bytes = wb;
+  m->loaded = true;
+  return DVW_OK;
+}
+
+DVW_API dvw_status dvw_generate(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop,
+                                const float* uniforms, int64_t n_samples, int32_t n_streams,
+                                uint8_t* out_codes, void* cuda_stream) {
+  return run(m, cond, n_frames, hop, uniforms, nullptr, n_samples, n_streams, out_codes, nullptr, cuda_stream);
+}
+
+DVW_API dvw_status dvw_logits(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop,
+                              const uint8_t* codes, int64_t n_samples, int32_t n_streams, float* out_logits,
+                              void* cuda_stream) {
+  if (!codes && n_samples > 0) return fail(DVW_E_INVALID_ARG, "codes is NULL");
+  return run(m, cond, n_frames, hop, nullptr, codes, n_samples, n_streams, nullptr, out_logits, cuda_stream);
+}
+
+DVW_API dvw_status dvw_generate_host(dvw_model* m, const float* cond_host, int64_t n_frames, int32_t hop,
+                                     const float* uniforms_host, int64_t n_samples, int32_t n_streams,
+                                     uint8_t* out_codes_host, void* cuda_stream) {
+  if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
+  if (!cond_host || !uniforms_host || !out_codes_host) return fail(DVW_E_INVALID_ARG, "host buffer is NULL");
+  if (n_streams < 1 || n_samples < 0 || n_frames < 0) return fail(DVW_E_SHAPE, "bad sizes");
+  DeviceGuard g(m->device);
+  const size_t cb = sizeof(float) * (size_t)n_streams * n_frames * m->L * 2 * m->r;
+  const size_t ub = sizeof(float) * (size_t)n_streams * n_samples;
+  const size_t ob = (size_t)n_streams * n_samples;
+  const size_t need = ((cb + 255) & ~size_t(255)) + ((ub + 255) & ~size_t(255)) + ob + 256;
+  if (m->stage_bytes < need) {
+    if (m->d_stage) cudaFree(m->d_stage);
+    m->d_stage = nullptr;
+    m->stage_bytes = 0;
+    DVW_CUDA(cudaMalloc(&m->d_stage, need), "allocating staging buffers");
+    m->stage_bytes = need;
+  }
+  char* base = static_cast<char*>(m->d_stage);
+  float* dc = reinterpret_cast<float*>(base);
+  float* du = reinterpret_cast<float*>(base + ((cb + 255) & ~size_t(255)));
+  uint8_t* dout = reinterpret_cast<uint8_t*>(base + ((cb + 255) & ~size_t(255)) + ((ub + 255) & ~size_t(255)));
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(cuda_stream);
+  DVW_CUDA(cudaMemcpyAsync(dc, cond_host, cb, cudaMemcpyHostToDevice, cs), "H2D cond");
+  DVW_CUDA(cudaMemcpyAsync(du, uniforms_host, ub, cudaMemcpyHostToDevice, cs), "H2D uniforms");
+  dvw_status st = dvw_generate(m, dc, n_frames, hop, du, n_samples, n_streams, dout, cuda_stream);
+  if (st != DVW_OK) return st;
+  DVW_CUDA(cudaMemcpyAsync(out_codes_host, dout, ob, cudaMemcpyDeviceToHost, cs), "D2H codes");
+  DVW_CUDA(cudaStreamSynchronize(cs), "synchronizing");
+  return check_device_error(m);
+}
+
+DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel) {
+  if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
+  if (kernel < DVW_KERNEL_AUTO || kernel > DVW_KERNEL_TC) return fail(DVW_E_INVALID_ARG, "unknown kernel %d", kernel);
+  if (kernel == DVW_KERNEL_CLUSTER && !m->cplan.ok)
+    return fail(DVW_E_UNSUPPORTED, "cluster kernel cannot hold this model: %s", m->cplan.why);
+  if (kernel == DVW_KERNEL_TC) return fail(DVW_E_UNSUPPORTED, "tcgen05 batched kernel is not built yet");
+  m->kernel = kernel;
+  return DVW_OK;
+}
+
+DVW_API dvw_status dvw_set_trace(dvw_model* m, uint64_t* device_buf, int64_t first_sample, int32_t n_samples) {
+  if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
+  if (device_buf && (first_sample < 0 || n_samples < 1)) return fail(DVW_E_SHAPE, "bad trace window");
+  m->trace = device_buf;
+  m->trace_n0 = first_sample;
+  m->trace_count = device_buf ? n_samples : 0;
+  return DVW_OK;
+}
+
+DVW_API dvw_status dvw_get_info(const dvw_model* m, dvw_info* out) {
+  if (!m || !out) return fail(DVW_E_INVALID_ARG, "NULL argument");
+  *out = m->info;
+  return DVW_OK;
+}
+
+DVW_API dvw_status dvw_sync(dvw_model* m) {
+  if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
+  DeviceGuard g(m->device);
+  DVW_CUDA(cudaDeviceSynchronize(), "synchronizing");
+  return check_device_error(m);
+}
+
+DVW_API void dvw_destroy(dvw_model* m) {
+  if (!m) return;
+  DeviceGuard g(m->device);
+  cudaFree(m->d_w);
+  cudaFree(m->d_dil);
+  cudaFree(m->d_ring_off);
+  cudaFree(m->d_ring);
+  if (m->h_err) cudaFreeHost(const_cast<int*>(m->h_err));
+  cudaFree(m->d_packed);
+  cudaFree(m->d_stage);
+  delete m;
+}
+
+DVW_API const char* dvw_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

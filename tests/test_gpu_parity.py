@@ -1,0 +1,200 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle on
+identical seeded inputs.  Gates (BASELINE.json north_star):
+  * teacher-forced logits: max |dlogit| <= 1e-3 (the north_star gate), and the
+    fp32-faithful expectation <= 2e-5 (bit-exact sampling needs ~1e-6);
+  * free-running codes bit-exact for the first 1,600 samples;
+  * integer/structural properties bitwise.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from paper_1702_07825_b200 import synth  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+GATE = 1e-3        # north_star teacher-forced tolerance
+FP32_FAITHFUL = 2e-5
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1702_07825_b200 import _lib
+    return _lib
+
+
+KERNELS = ["stream", "cluster"]
+
+
+def model(L, cfg, w, kernel):
+    m = L.Model.from_config(cfg).load(w)
+    try:
+        m.set_kernel(kernel)
+    except L.DvwError as e:
+        if e.name == "DVW_E_UNSUPPORTED":
+            pytest.skip(f"{kernel} kernel unavailable for {cfg}: {e}")
+        raise
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_pair(L, cfg, kernel, N, hop=64, utt=0, profile="default", seed=0):
+    w = synth.make_weights(cfg, seed, profile)
+    cond = synth.make_cond(cfg, synth.n_frames_for(N, hop), utt)
+    u = synth.make_uniforms(N, utt)
+    m = model(L, cfg, w, kernel)
+    codes = m.generate(dev(cond)[None], dev(u)[None], hop)
+    lg = m.logits(dev(cond)[None], codes, hop)
+    m.sync()
+    assert m.info()["last_kernel_name"] == kernel
+    return w, cond, u, codes.cpu().numpy()[0], lg.cpu().numpy()[0]
+
+
+def oracle_tf(cfg, w, cond, hop, codes, u=None):
+    return oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, len(codes), uniforms=u,
+                      forced=codes, dilations=cfg.dilation_list(), want_sampled=u is not None)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("cfg", [synth.C1, synth.C2], ids=["C1", "C2"])
+def test_free_running_bit_exact_1600_and_teacher_forced(L, kernel, cfg):
+    N, hop = 1600, 64
+    w, cond, u, codes, lg = run_pair(L, cfg, kernel, N, hop)
+    ref_codes, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, N, uniforms=u)
+    first_bad = int(np.argmax(codes != ref_codes)) if np.any(codes != ref_codes) else N
+    assert first_bad == N, f"first divergence at n={first_bad}"
+    _, ref_lg, _ = oracle_tf(cfg, w, cond, hop, codes)
+    err = float(np.max(np.abs(lg.astype(np.float64) - ref_lg)))
+    print(f"{kernel} {cfg}: max|dlogit| = {err:.3e}")
+    assert err <= GATE
+    assert err <= FP32_FAITHFUL
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("shape", [(3, 32, 128), (2, 128, 256), (5, 64, 128), (1, 64, 256)])
+def test_shapes_teacher_forced(L, kernel, shape):
+    cfg = synth.Config(*shape)
+    N, hop = 333, 7  # ragged: N not a multiple of hop
+    w, cond, u, codes, lg = run_pair(L, cfg, kernel, N, hop, utt=3, profile="peaky", seed=5)
+    _, ref_lg, _ = oracle_tf(cfg, w, cond, hop, codes)
+    assert float(np.max(np.abs(lg - ref_lg))) <= FP32_FAITHFUL * 30  # peaky logits are ~30x larger
+    ref_codes, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, N, uniforms=u)
+    assert np.array_equal(codes, ref_codes)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_zero_weights_floor_256u_bitwise(L, kernel):
+    cfg = synth.C1
+    w = np.zeros(synth.weights_numel(cfg), np.float32)
+    N = 500
+    cond = synth.make_cond(cfg, synth.n_frames_for(N, 64), 0)
+    u = synth.make_uniforms(N, 4)
+    m = model(L, cfg, w, kernel)
+    codes = m.generate(dev(cond)[None], dev(u)[None], 64).cpu().numpy()[0]
+    assert np.array_equal(codes, np.floor(256 * u.astype(np.float64)).astype(np.uint8))
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_causality_and_sparse_lag_set_bitwise(L, kernel):
+    """Perturbing codes[m] leaves logits[0..m] bitwise unchanged; with d = [5, 5]
+    only lags {1,2,6,7,11,12} change."""
+    cfg = synth.Config(2, 64, 128, dilations=(5, 5))
+    N, hop = 80, 8
+    w = synth.make_weights(cfg, 1)
+    cond = dev(synth.make_cond(cfg, synth.n_frames_for(N, hop), 0))[None]
+    codes = synth.make_codes(N, 1)
+    m = model(L, cfg, w, kernel)
+    base = m.logits(cond, dev(codes)[None], hop).cpu().numpy()[0]
+    mpos = 30
+    pert = codes.copy()
+    pert[mpos] ^= 0x55
+    lg = m.logits(cond, dev(pert)[None], hop).cpu().numpy()[0]
+    changed = {n - mpos for n in range(N) if not np.array_equal(lg[n], base[n])}
+    assert changed == {1, 2, 6, 7, 11, 12}
+    # frame causality
+    c2 = cond.clone()
+    c2[0, 5] += 0.125
+    lg2 = m.logits(c2, dev(codes)[None], hop).cpu().numpy()[0]
+    assert np.array_equal(lg2[:5 * hop], base[:5 * hop]) and not np.array_equal(lg2[5 * hop], base[5 * hop])
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_determinism_and_edge_sizes(L, kernel):
+    cfg = synth.C1
+    w = synth.make_weights(cfg, 0)
+    m = model(L, cfg, w, kernel)
+    for N in (1, 2, 65):
+        cond = dev(synth.make_cond(cfg, synth.n_frames_for(N, 64), 2))[None]
+        u = dev(synth.make_uniforms(N, 2))[None]
+        a = m.generate(cond, u, 64).cpu().numpy()
+        b = m.generate(cond, u, 64).cpu().numpy()
+        assert np.array_equal(a, b)
+        ref, _, _ = oracle.run(20, 64, 128, w, cond.cpu().numpy()[0], 64, N, uniforms=u.cpu().numpy()[0])
+        assert np.array_equal(a[0], ref)
+    # N = 0 is a no-op
+    out = torch.zeros((1, 0), dtype=torch.uint8, device="cuda")
+    m.generate(dev(synth.make_cond(cfg, 1, 0))[None], torch.zeros((1, 0), device="cuda"), 64, out=out)
+
+
+def test_multi_stream_is_position_independent(L):
+    """Stream kernel: utterance u's codes do not depend on batch size or position."""
+    cfg = synth.C1
+    N, hop = 700, 64
+    w = synth.make_weights(cfg, 0)
+    m = L.Model.from_config(cfg).load(w).set_kernel("stream")
+    utts = [5, 1, 9]
+    cond, u = synth.make_batch(cfg, N, utts, hop)
+    batch = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    for i, utt in enumerate(utts):
+        single = m.generate(dev(cond[i:i + 1]), dev(u[i:i + 1]), hop).cpu().numpy()[0]
+        assert np.array_equal(batch[i], single)
+        ref, _, _ = oracle.run(20, 64, 128, w, cond[i], hop, N, uniforms=u[i])
+        assert np.array_equal(single, ref)
+
+
+def test_generate_host_matches_device(L):
+    cfg = synth.C1
+    N = 300
+    w = synth.make_weights(cfg, 0)
+    cond, u = synth.make_batch(cfg, N, [0], 64)
+    m = L.Model.from_config(cfg).load(w)
+    a = m.generate(dev(cond), dev(u), 64).cpu().numpy()
+    b = m.generate_host(cond, u, 64)
+    assert np.array_equal(a, b)
+
+
+def test_abi_negative_on_gpu(L):
+    cfg = synth.C1
+    w = synth.make_weights(cfg, 0)
+    m = L.Model.from_config(cfg)
+    cond = dev(synth.make_cond(cfg, 2, 0))[None]
+    u = dev(synth.make_uniforms(128, 0))[None]
+    with pytest.raises(L.DvwError) as e:
+        m.generate(cond, u, 64)
+    assert e.value.name == "DVW_E_STATE"
+    with pytest.raises(L.DvwError) as e:
+        m.load(w[:-1])
+    assert e.value.name == "DVW_E_SHAPE"
+    bad = w.copy()
+    bad[17] = np.nan
+    with pytest.raises(L.DvwError) as e:
+        m.load(bad)
+    assert e.value.name == "DVW_E_INVALID_ARG"
+    m.load(w)
+    with pytest.raises(L.DvwError) as e:  # 2 frames x hop 32 < 128 samples
+        m.generate(cond, u, 32)
+    assert e.value.name == "DVW_E_SHAPE"
+    with pytest.raises(L.DvwError) as e:
+        m.generate(cond, u, 0)
+    assert e.value.name == "DVW_E_SHAPE"
+    m.load(dev(w))  # device blob path
+    codes = m.generate(cond, u, 64)
+    m.sync()
+    assert codes.shape == (1, 128)
