@@ -1,0 +1,301 @@
+#!/usr/bin/env python3
+"""Benchmark: autoregressive WaveNet sample generation (Deep Voice, arXiv 1702.07825).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C2]
+
+A *step* is one dvw_generate call: one whole utterance of the workload through
+the full hot path (embedding, l gated dilated layers, skip/head, softmax,
+inverse-CDF sampling, feedback), inputs resident in HBM.  The default workload
+is BASELINE.json configs[1] = C2: l=20 r=64 s=256, batch 1, 16,000 samples
+(1 s at 16 kHz), frame-rate conditioning with hop 64.  Under torchrun each rank
+generates its own utterance (utterance id = rank): independent problems, no
+collective on the data path, "scaling": "weak".  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, test infrastructure) on the
+host cores, rank 0 only, each step a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1702_07825_b200 import synth  # noqa: E402
+
+METRIC = "audio samples/sec per stream (batch-1 real-time factor at 16 kHz) and aggregate"
+WORKLOADS = {
+    "C1": dict(cfg=synth.C1, n=1600, desc="C1: l=20 r=64 s=128, batch 1, 1,600 samples (0.1 s @16 kHz), hop 64"),
+    "C2": dict(cfg=synth.C2, n=16000, desc="C2: l=20 r=64 s=256, batch 1, 16,000 samples (1 s @16 kHz), hop 64"),
+    "C3": dict(cfg=synth.C3, n=160000, desc="C3: l=40 r=64 s=256, batch 1, 160,000 samples (10 s @16 kHz), hop 64"),
+}
+HOP = 64
+FP32_FMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 TFLOP/s
+
+
+def macs_per_sample(cfg) -> int:
+    """l (5 r^2 + r s) + a s + a^2 (SURVEY.md §8(a) per-sample totals)."""
+    L, r, s, a = cfg.n_layers, cfg.residual, cfg.skip, cfg.levels
+    return L * (5 * r * r + r * s) + a * s + a * a
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML while the timed region runs."""
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                mask = fn(self.h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "n_samples": len(self.samples)}
+
+
+def load_ncu_traffic(workload: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        d = json.load(open(p))
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_reference(args, wl):
+    """The oracle (CPU, fp64, one core) on bounded samples of the workload."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    cfg, n_total = wl["cfg"], wl["n"]
+    n = min(n_total, args.ref_samples)
+    w = synth.make_weights(cfg, 0)
+    cond = synth.make_cond(cfg, synth.n_frames_for(n_total, HOP), 0)
+    u = synth.make_uniforms(n_total, 0)
+    for _ in range(args.warmup if args.warmup <= 1 else 1):
+        oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, HOP, min(n, 64), uniforms=u,
+                   dilations=cfg.dilation_list(), want_logits=False)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, HOP, n, uniforms=u,
+                   dilations=cfg.dilation_list(), want_logits=False)
+        times.append(time.perf_counter() - t0)
+    sec = float(np.mean(times))
+    value = n / sec
+    sample = f"first {n} samples of the {args.workload} utterance (utterance 0), fp64 scalar C, 1 thread"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "samples_per_step": n, "streams": 1},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, budget_samples):
+    """Oracle timed on this host (1 core) on the same utterance; plus parity on it."""
+    import oracle
+    nb = min(n, budget_samples)
+    t0 = time.perf_counter()
+    ref_codes, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, HOP, nb, uniforms=u[:nb],
+                                 dilations=cfg.dilation_list(), want_logits=False)
+    sec = time.perf_counter() - t0
+    diff = np.nonzero(ref_codes != gpu_codes[:nb])[0]
+    first = int(diff[0]) if diff.size else None
+    # per-step mismatch rate: oracle teacher-forced on the GPU's own codes, drawing with the same u
+    _, _, sampled = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, HOP, nb, uniforms=u[:nb],
+                               forced=gpu_codes[:nb], dilations=cfg.dilation_list(), want_logits=False,
+                               want_sampled=True)
+    mism = int(np.sum(sampled != gpu_codes[:nb]))
+    cpu = {"value": nb / sec, "unit": "samples/s", "cores": 1, "kind": "oracle",
+           "sample": f"{nb} samples of the same utterance (utterance 0), fp64 scalar C oracle, 1 thread"}
+    parity = {"checked_samples": nb, "bit_exact_first_1600": bool(first is None or first >= 1600),
+              "first_divergence": first, "divergence_rate": mism / nb, "mismatches": mism}
+    return cpu, parity
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--kernel", default="auto", choices=["auto", "cluster", "stream"])
+    ap.add_argument("--ref-samples", type=int, default=1600, help="samples per reference step")
+    ap.add_argument("--cpu-samples", type=int, default=16000, help="oracle samples for cpu_baseline")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    from paper_1702_07825_b200._lib import Model
+
+    cfg, n = wl["cfg"], wl["n"]
+    utt = rank
+    w = synth.make_weights(cfg, 0)
+    cond = synth.make_cond(cfg, synth.n_frames_for(n, HOP), utt)
+    u = synth.make_uniforms(n, utt)
+    model = Model.from_config(cfg, device=dev.index).load(w).set_kernel(args.kernel)
+    stream = torch.cuda.current_stream(dev)
+    d_cond = torch.from_numpy(cond)[None].to(dev)
+    d_u = torch.from_numpy(u)[None].to(dev)
+    out = torch.empty((1, n), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        model.generate(d_cond, d_u, HOP, out=out)
+    barrier()
+    info = model.info()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(dev.index) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()  # evict L2 between timed steps (untimed: outside the events)
+            ev[i][0].record(stream)
+            model.generate(d_cond, d_u, HOP, out=out)
+            ev[i][1].record(stream)
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    kernel_ms = float(np.mean(step_ms))
+    model.sync()
+    gpu_codes = out.cpu().numpy()[0].copy()
+
+    # end to end through the public host-buffer entry point (H2D + generate + D2H per step)
+    h_cond = torch.from_numpy(cond)[None].pin_memory()
+    h_u = torch.from_numpy(u)[None].pin_memory()
+    h_out = torch.empty((1, n), dtype=torch.uint8).pin_memory()
+    model.generate_host(h_cond, h_u, HOP, out=h_out)
+    barrier()
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        model.generate_host(h_cond, h_u, HOP, out=h_out)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_step = float(np.mean(e2e_ms))
+    assert np.array_equal(h_out.numpy()[0], gpu_codes), "host-buffer path disagrees with device path"
+
+    # max over ranks
+    t_max, e_max = kernel_ms, e2e_step
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([kernel_ms, e2e_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max, e_max = float(t[0]), float(t[1])
+
+    if rank == 0:
+        total = n * ws
+        value = total / (t_max / 1e3)
+        flop_launch = 2.0 * macs_per_sample(cfg) * n
+        achieved_tflops = flop_launch / (kernel_ms / 1e3) / 1e12
+        us_per_sample = kernel_ms * 1e3 / n
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl["desc"], "samples_per_step": n, "streams_per_gpu": 1,
+                       "parallelism": f"{ws} independent utterances, one per GPU",
+                       "kernel": info["last_kernel_name"], "cluster_ctas": info["last_cluster"],
+                       "l2": "flushed between timed steps (256 MiB write, untimed)"},
+            "per_stream": {"samples_per_s": n / (kernel_ms / 1e3), "us_per_sample": us_per_sample,
+                           "rtf_16khz": n / (kernel_ms / 1e3) / synth.AUDIO_HZ},
+            "clocks": clk.summary(),
+            "e2e": {"value": total / (e_max / 1e3), "unit": "samples/s",
+                    "h2d_bytes_per_step": int(cond.nbytes + u.nbytes), "d2h_bytes_per_step": int(n)},
+            "gpu_launches": int(info["last_launches"]) * args.steps,
+            "roofline": {"bound": "alu", "achieved": achieved_tflops, "peak": FP32_FMA_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved_tflops / FP32_FMA_PEAK_TFLOPS,
+                         "traffic": load_ncu_traffic(args.workload),
+                         "note": "batch-1 is latency-bound: algorithmic FLOP (2 x MAC/sample x samples) / "
+                                 "launch time vs FP32 FFMA peak of the whole chip (DESIGN.md Roofline)"},
+        }
+        if not args.no_cpu:
+            cpu, parity = cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, args.cpu_samples)
+            line["cpu_baseline"] = cpu
+            line["parity"] = parity
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

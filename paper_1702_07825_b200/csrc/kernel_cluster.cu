@@ -3,19 +3,24 @@
 // The paper's GPU kernel (App. D) put two layers per SM in
 // registers and passed each sample round-robin through 23 SMs with spin-locks in
 // L2.  This kernel keeps the idea "one launch, weights on chip" and redesigns the
-// rest for sm_100a:
+// rest for sm_100a (DESIGN.md "Batch-1 cluster kernel"):
 //   * one thread-block cluster; every hand-off is a DSMEM st.async whose
 //     transaction bytes complete on the receiver's mbarrier (no L2 round trip);
-//   * the critical chain (steps 2b-2c + residual) holds W_cur
-//     and W_res in registers (192 per thread, setmaxnreg 232) four layers per SM;
-//   * everything off the chain runs concurrently elsewhere: W_prev x_{n+1-d} for
-//     the next sample (Fig. 2's "aux threads") in a dedicated
-//     warpgroup of each chain CTA, the skip projections in
-//     skip CTAs, the ring buffers in L2;
-//   * the head is split by output rows over 4 CTAs, and CTA 0
-//     samples (App. A.4) and embeds the next input (step 1).
-// Numerics: fp32 FMA everywhere, accurate tanhf/expf, fp64 CDF scan (R11-R13);
-// every reduction has a fixed order, so results are bitwise deterministic.
+//   * chain CTAs own 3 consecutive layers.  Warpgroup A holds W_cur (one full
+//     row per thread; the tanh row and its sigmoid partner sit 16 lanes apart so
+//     the gate needs one shuffle), warpgroup B holds W_res (half a
+//     row per thread).  A and B hand h and x to each other through shared memory
+//     with producer/consumer named barriers (bar.arrive / bar.sync);
+//   * the third warpgroup of a chain CTA does the off-chain work of the coming
+//     sample (Fig. 2's aux threads): dilation-queue read/write in L2,
+//     conditioning fetch, W_prev x_{n+1-d} + B + L from shared memory;
+//   * skip CTAs accumulate W_skip^(j) h^(j) as h arrives; head CTAs
+//     own 64 output rows each of relu -> W_relu -> relu -> W_out
+//     plus W_skip^(l); CTA 0 samples (App. A.4) and embeds the next input (step 1).
+// Shared-memory vectors read in 4 or 2 column chunks are padded (+4 floats per
+// chunk) so the chunks fall in different banks.
+// Numerics: fp32 FMA; gate from ex2.approx/rcp.approx (|err| ~ 1e-7, R13);
+// fp64 CDF scan (R11); every reduction has a fixed order (bitwise deterministic).
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -27,33 +32,45 @@ namespace dvw {
 namespace {
 
 constexpr int R = 64;       // residual channels the kernel is built for
-constexpr int LPC = 4;      // layers per chain CTA
+constexpr int LPC = 3;      // layers per chain CTA
 constexpr int NH = 4;       // head CTAs (64 output rows each)
-constexpr int kMain = 256;  // warps 0-7: chain / head / skip math
-constexpr int kAux = 128;   // warps 8-11: off-chain work of chain CTAs
-constexpr int kThreads = kMain + kAux;
+constexpr int kAux = 128;   // threads [0,128): warpgroup X, off-chain work
+constexpr int kMain = 256;  // threads [128,384): warpgroups A and B
+constexpr int kThreads = kAux + kMain;
 constexpr int kMainRegs = 232;
-constexpr int kAuxRegs = 40;  // 8 warps x 232 + 4 warps x 40 = 384 x 168 (the launch allocation)
-constexpr int kChainRegs = LPC * 48;  // W_cur (2 rows x 16) + W_res (16) per layer
+constexpr int kAuxRegs = 40;  // 128 x (40 + 232 + 232) = 384 x 168, the launch allocation
 constexpr uint64_t kTimeoutNs = 2000000000ull;
+
+// named barriers (0 is __syncthreads)
+constexpr int kBarMain = 1;  // A + B, 256 threads
+constexpr int kBarH = 2;     // A arrives (h ready), B syncs
+constexpr int kBarX = 3;     // B arrives (x ready), A syncs
+constexpr int kBarAux = 4;   // X, 128 threads
 
 enum Role { kChain = 0, kHead = 1, kSkip = 2, kIdle = 3 };
 
+// h vectors (64) are read in 2 halves of 32: half 1 starts 4 floats later
+__device__ __forceinline__ int hpad(int i) { return i + ((i >> 5) << 2); }
+constexpr int kHLen = 72;
+// 256-vectors read in 4 chunks of C (z_a: C = 64; z_s: C = s/4), chunk c starts at c (C + 4)
+template <int C>
+__device__ __forceinline__ int cpad(int i) { return i + (i / C) * 4; }
+constexpr int kVLen = 272;
+
 struct __align__(16) Mail {
-  uint64_t bar_xin, bar_logits, bar_pre, bar_done, bar_part, bar_za;
+  uint64_t bar_xin, bar_logits, bar_pre, bar_done, bar_part, bar_za, bar_exit;
   uint64_t bar_h[kCMaxSlot];
   int abort_flag;
-  int pad_[3];
-  float xs[LPC + 1][R];       // chain: layer inputs; xs[0] is the inbound x
-  float xsave[LPC][R];        // chain: x^(j-1)_n for the aux warpgroup (ring + a_prev)
-  float pre[LPC][2 * R];      // chain: W_prev x_{n-d} + B + L for the coming sample
-  float xp[R];                // chain aux scratch
-  float hs[R];                // chain: h exchange inside the CTA
-  float logits_in[kLevels];   // CTA 0: inbound logits
-  float hbuf[kCMaxSlot][R];   // skip: h^(j) per owned slot; head: slot 0 = h^(l)
-  float part[kCMaxSkip][256]; // head: skip partials
-  float za_in[kLevels];       // head: all-gathered z_a
-  float zs[256];              // head: z_s; skip: partial staging
+  alignas(16) float xs[LPC + 1][R];   // chain: layer inputs; xs[0] is the inbound x
+  float xsave0[R];                    // chain: copy of the inbound x for the aux warpgroup
+  float pre[LPC][2 * R];              // chain: W_prev x_{n-d} + B + L for the coming sample
+  float xp[R];                        // chain aux scratch
+  float hs[LPC][kHLen];               // chain: h handed from A to B (padded halves)
+  float logits_in[kLevels];           // CTA 0: inbound logits
+  float hbuf[kCMaxSlot][kHLen];       // skip: h^(j) per owned slot; head: slot 0 = h^(l)
+  float part[kCMaxSkip][256];         // head: skip partials
+  float za_in[kVLen];                 // head: all-gathered z_a (padded chunks)
+  float zs[kVLen];                    // head: z_s (padded chunks); skip: partial staging
   double dscr[8];
   float fscr[8];
   int iscr[16];
@@ -71,23 +88,30 @@ struct Ctx {
   int size;
 };
 
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 __device__ __forceinline__ void raise_abort(const Ctx& cx, int code) {
   *reinterpret_cast<volatile int*>(cx.err) = code;  // mapped host memory
   __threadfence_system();
   const uint32_t a = ptx::smem_u32(&cx.mail->abort_flag);
+#pragma unroll 1
   for (int r = 0; r < cx.size; ++r) {
     const uint32_t ra = ptx::mapa(a, r);
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(1) : "memory");
   }
 }
 
-// Wait for phase `parity` of a local mbarrier; on the watchdog (2 s without
-// progress) or a cluster-wide abort, return false and let the caller run on
-// without blocking so every CTA reaches the final cluster barrier.
+// Wait for phase `parity` of a local mbarrier (try_wait suspends the warp in
+// hardware).  On the watchdog (2 s without progress) or a cluster-wide abort,
+// return false: the caller runs on without blocking so every CTA reaches the
+// final cluster barrier, and the host sees DVW_E_DEVICE_TIMEOUT.
 __device__ __forceinline__ bool wait(const Ctx& cx, uint64_t* bar, uint32_t parity, int code) {
   const uint32_t b = ptx::smem_u32(bar);
   if (ptx::mbar_try_wait(b, parity)) return true;
   const uint64_t t0 = ptx::globaltimer();
+#pragma unroll 1
   for (uint32_t i = 1;; ++i) {
     if (ptx::mbar_try_wait(b, parity)) return true;
     if ((i & 7) == 0) {
@@ -104,196 +128,249 @@ __device__ __forceinline__ uint32_t remote(const void* local, int rank) {
   return ptx::mapa(ptx::smem_u32(local), (uint32_t)rank);
 }
 
-// Optional per-event %globaltimer stamps (dvw_set_trace); one predicated branch when off.
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// Optional %globaltimer stamps (dvw_set_trace).  Compiled only into the TRACE
+// instantiation of the kernel, so the production kernel carries no trace code.
+template <bool TRACE>
 __device__ __forceinline__ void trace(const RunArgs& A, int64_t n, int ev) {
-  if (A.trace) {
+  if constexpr (TRACE) {
     const int64_t i = n - A.trace_n0;
     if (i >= 0 && i < A.trace_count) A.trace[(i * kCMaxCta + ptx::cluster_rank()) * 32 + ev] = ptx::globaltimer();
   }
 }
 
-// Same, but the SM-local cycle counter (cheap; for events inside one CTA).
+template <bool TRACE>
 __device__ __forceinline__ void trace_clk(const RunArgs& A, int64_t n, int ev) {
-  if (A.trace) {
+  if constexpr (TRACE) {
     const int64_t i = n - A.trace_n0;
     if (i >= 0 && i < A.trace_count) A.trace[(i * kCMaxCta + ptx::cluster_rank()) * 32 + ev] = clock64();
   }
 }
 
-__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+// h = tanh(a) * sigma(g): tanh(a) = 1 - 2 / (1 + 2^(2a log2 e)),
+// sigma(g) = 1 / (1 + 2^(-g log2 e)); MUFU ex2/rcp (rel. err ~2^-22) keep the
+// result within ~1e-7 of the exact value; saturates correctly at +-inf.
+__device__ __forceinline__ float gate_fast(float a, float g) {
+  float ea, eg, ra, rg;
+  const float xa = 2.8853900817779268f * a, xg = -1.4426950408889634f * g;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ea) : "f"(xa));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(eg) : "f"(xg));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(ea + 1.0f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rg) : "f"(eg + 1.0f));
+  return fmaf(-2.0f, ra, 1.0f) * rg;
+}
 
-// ------------------------------------------------------------------ chain CTA, main warps
-template <int S>
-__device__ void chain_main(const Params& P, const Ctx& cx, int c, const float* blk, const float* sw) {
+// dot of K register weights with K consecutive shared floats (4 accumulators)
+template <int K>
+__device__ __forceinline__ float dotK(const float* w, const float* v) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int q = 0; q < K; q += 4) {
+    const float4 x = lds4(v + q);
+    a0 = fmaf(w[q], x.x, a0);
+    a1 = fmaf(w[q + 1], x.y, a1);
+    a2 = fmaf(w[q + 2], x.z, a2);
+    a3 = fmaf(w[q + 3], x.w, a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+// same over a padded h vector (64 values in two 32-halves, see hpad)
+__device__ __forceinline__ float dot_h64(const float* w, const float* hv) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int q = 0; q < 64; q += 4) {
+    const float4 x = lds4(hv + q + ((q >> 5) << 2));
+    a0 = fmaf(w[q], x.x, a0);
+    a1 = fmaf(w[q + 1], x.y, a1);
+    a2 = fmaf(w[q + 2], x.z, a2);
+    a3 = fmaf(w[q + 3], x.w, a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+// ------------------------------------------------------------------ chain CTA 0: sample + embed
+// Draw y_{n-1} from the inbound logits (App. A.4) and write x^(0)_n into xs[0] (step 1).
+// Runs on the 256 main threads (k = 0..255) of both warpgroups.
+template <bool TRACE>
+__device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx, int64_t n, int k, int& y1,
+                                                 int& y2, const float* wembc, const float* bemb) {
+  const RunArgs& A = P.a;
+  Mail& m = *cx.mail;
+  const float* embp_g = P.pk + P.p.embp_off;  // W_emb_prev^T [256][R] in global memory
+  float ep = 0.0f;
+  if (n > 0) {
+    const float u = A.uniforms ? __ldg(A.uniforms + n - 1) : 0.0f;
+    const int yf = A.forced ? (int)__ldg(A.forced + n - 1) : 0;
+    if (k < R) ep = __ldg(embp_g + y1 * R + k);  // W_emb_prev[:, y_{n-2}] (= y1 before the update)
+    if (wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11) && k == 0)
+      ptx::mbar_arm(ptx::smem_u32(&m.bar_logits), kLevels * 4);
+    if (k == 0) trace<TRACE>(A, n - 1, 3);
+    const float l = m.logits_in[k];
+    int y;
+    if (A.forced) {
+      A.out_logits[(n - 1) * kLevels + k] = l;
+      y = yf;
+    } else {
+      y = sample_256(l, u, m.dscr, m.fscr, m.iscr, k, kBarMain);
+      if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
+    }
+    y2 = y1;
+    y1 = y;
+  } else {
+    if (k < R) ep = __ldg(embp_g + y2 * R + k);
+  }
+  // x^(0)_n = W_emb_prev[:, y_{n-2}] + W_emb_cur[:, y_{n-1}] + B_emb
+  if (k < R) m.xs[0][k] = (ep + wembc[y1 * R + k]) + bemb[k];
+  ptx::bar_sync(kBarMain, kMain);
+}
+
+// The final draw (sample N-1) after the last layer pass; all 256 main threads.
+__device__ __forceinline__ void final_draw(const Params& P, const Ctx& cx, int k) {
+  const RunArgs& A = P.a;
+  Mail& m = *cx.mail;
+  const int64_t n = A.N;
+  const float u = A.uniforms ? __ldg(A.uniforms + n - 1) : 0.0f;
+  wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11);
+  const float lg = m.logits_in[k];
+  if (A.forced) {
+    A.out_logits[(n - 1) * kLevels + k] = lg;
+  } else {
+    const int y = sample_256(lg, u, m.dscr, m.fscr, m.iscr, k, kBarMain);
+    if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
+  }
+}
+
+// ------------------------------------------------------------------ chain CTA, warpgroup A (W_cur)
+template <bool TRACE>
+__device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* blk, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
-  const int t = threadIdx.x;
-  const int pr = t >> 2, ch = t & 3;  // row pair (i, i + r) and 16-column chunk
+  const int a = threadIdx.x - kAux;  // 0..127 (also the main-thread index k of the sampler)
+  const int wa = a >> 5, l = a & 31;
+  const int row = (l < 16) ? (16 * wa + l) : (R + 16 * wa + (l - 16));  // tanh row or its sigmoid partner
+  const int hi = 16 * wa + (l & 15);
   const int first = pl.chain_first[c], nl = pl.chain_nl[c];
-  const bool last_cta = (c == pl.nc - 1);
 
-  float wc[LPC][32], wr[LPC][16];
+  float wc[LPC][64];
 #pragma unroll
-  for (int jl = 0; jl < LPC; ++jl) {
+  for (int jl = 0; jl < LPC; ++jl)
 #pragma unroll
-    for (int q = 0; q < 32; ++q) wc[jl][q] = blk[(jl * 48 + q) * kMain + t];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) wr[jl][q] = blk[(jl * 48 + 32 + q) * kMain + t];
-  }
-  const float* bres = sw + LPC * R * 2 * R + LPC * 2 * R;  // [LPC][R]
-  const float* wembc = bres + LPC * R;                     // CTA 0: [256][R]
-  const float* bemb = wembc + kLevels * R;                 // CTA 0: [R]
-  const float* embp_g = P.pk + pl.embp_off;                // [256][R] in global
-
-  const float* uni = A.uniforms;
-  const uint8_t* forced = A.forced;
+    for (int q = 0; q < 64; ++q) wc[jl][q] = blk[(jl * 64 + q) * 128 + a];
+  const float* wembc = sw + LPC * R * 2 * R + LPC * 2 * R + LPC * R;  // CTA 0: [256][R]
+  const float* bemb = wembc + kLevels * R;
   int y1 = kLevels / 2, y2 = kLevels / 2;
 
   for (int64_t n = 0; n < A.N; ++n) {
     if (c == 0) {
-      float ep = 0.0f;
-      if (n > 0) {
-        const float u = uni ? __ldg(uni + n - 1) : 0.0f;
-        const int yf = forced ? (int)__ldg(forced + n - 1) : 0;
-        if (t < R) ep = __ldg(embp_g + y1 * R + t);  // W_emb_prev[:, y_{n-2}] (y1 before the update)
-        if (wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11) && t == 0)
-          ptx::mbar_arm(ptx::smem_u32(&m.bar_logits), kLevels * 4);
-        if (t == 0) trace(A, n - 1, 3);
-        const float l = m.logits_in[t];
-        int y;
-        if (forced) {
-          A.out_logits[(n - 1) * kLevels + t] = l;
-          y = yf;
-        } else {
-          y = sample_256(l, u, m.dscr, m.fscr, m.iscr, t, 1);
-          if (t == 0) A.out_codes[n - 1] = (uint8_t)y;
-        }
-        y2 = y1;
-        y1 = y;
-      } else {
-        if (t < R) ep = __ldg(embp_g + y2 * R + t);
-      }
-      // step 1: x^(0)_n = W_emb_prev[:, y_{n-2}] + W_emb_cur[:, y_{n-1}] + B_emb
-      if (t < R) m.xs[0][t] = (ep + wembc[y1 * R + t]) + bemb[t];
-      ptx::bar_sync(1, kMain);
+      sample_and_embed<TRACE>(P, cx, n, a, y1, y2, wembc, bemb);
     } else {
-      if (wait(cx, &m.bar_xin, (uint32_t)(n & 1), 12) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_xin), R * 4);
+      if (wait(cx, &m.bar_xin, (uint32_t)(n & 1), 12) && a == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_xin), R * 4);
     }
-    if (t == 0) trace(A, n, 0);
+    if (a == 0) trace<TRACE>(A, n, 0);
     wait(cx, &m.bar_pre, (uint32_t)(n & 1), 13);
-    if (t == 0) trace(A, n, 1);
-
 #pragma unroll
     for (int jl = 0; jl < LPC; ++jl) {
       if (jl < nl) {
         const int j = first + jl;
-        if (t == 0) trace_clk(A, n, 8 + 5 * jl);
-        const float* xin = m.xs[jl];
-        float xv[16];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float4 v = lds4(xin + ch * 16 + 4 * k);
-          xv[4 * k] = v.x; xv[4 * k + 1] = v.y; xv[4 * k + 2] = v.z; xv[4 * k + 3] = v.w;
+        if (jl > 0) ptx::bar_sync(kBarX, kMain);  // x^(j-1) from B
+        if (a == 0) trace_clk<TRACE>(A, n, 8 + 2 * jl);
+        // a = W_cur x + (W_prev x_{n-d} + B + L); one row per thread
+        const float av = dotK<64>(wc[jl], m.xs[jl]) + m.pre[jl][row];
+        const float partner = __shfl_xor_sync(0xffffffffu, av, 16);
+        float hv = 0.0f;
+        if (l < 16) {
+          hv = gate_fast(av, partner);  // tanh row in av, sigmoid row in partner
+          m.hs[jl][hpad(hi)] = hv;
         }
-        const float ph = m.pre[jl][pr], pg = m.pre[jl][R + pr];
-        const float xi = xin[pr];
-        // a_cur = W_cur x, both gate halves of row pair pr
-        float h0 = 0.f, h1 = 0.f, g0 = 0.f, g1 = 0.f;
-#pragma unroll
-        for (int q = 0; q < 16; q += 2) {
-          h0 = fmaf(wc[jl][q], xv[q], h0);
-          g0 = fmaf(wc[jl][16 + q], xv[q], g0);
-          h1 = fmaf(wc[jl][q + 1], xv[q + 1], h1);
-          g1 = fmaf(wc[jl][16 + q + 1], xv[q + 1], g1);
-        }
-        float ah = h0 + h1, ag = g0 + g1;
-        ah += __shfl_xor_sync(0xffffffffu, ah, 1);
-        ag += __shfl_xor_sync(0xffffffffu, ag, 1);
-        ah += __shfl_xor_sync(0xffffffffu, ah, 2);
-        ag += __shfl_xor_sync(0xffffffffu, ag, 2);
-        // a = a_prev + a_cur + B + L ; h = tanh(a_h) sigma(a_g)
-        const float hv = gate(ah + ph, ag + pg);
-        if (t == 0) trace_clk(A, n, 9 + 5 * jl);
-        if (ch == 0) {
-          m.hs[pr] = hv;
-          m.xsave[jl][pr] = xi;
+        bar_arrive(kBarH, kMain);
+        if (a == 0) trace_clk<TRACE>(A, n, 9 + 2 * jl);
+        if (l < 16) {  // h^(j) to its skip CTA, or h^(l) to the four heads (off the chain)
           if (j == pl.L - 1) {
 #pragma unroll
             for (int hh = 0; hh < NH; ++hh)
-              ptx::st_async(remote(&m.hbuf[0][pr], pl.nc + hh), hv, remote(&m.bar_h[0], pl.nc + hh));
+              ptx::st_async(remote(&m.hbuf[0][hpad(hi)], pl.nc + hh), hv, remote(&m.bar_h[0], pl.nc + hh));
           } else {
-            const int k = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
-            ptx::st_async(remote(&m.hbuf[sl][pr], k), hv, remote(&m.bar_h[sl], k));
+            const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
+            ptx::st_async(remote(&m.hbuf[sl][hpad(hi)], kk), hv, remote(&m.bar_h[sl], kk));
           }
         }
-        ptx::bar_sync(1, kMain);
-        if (t == 0) trace_clk(A, n, 10 + 5 * jl);
-        if (j < pl.L - 1) {
-          // x^(j) = x^(j-1) + W_res h + B_res (PAPER.md:437)
-          float hvv[16];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float4 v = lds4(m.hs + ch * 16 + 4 * k);
-            hvv[4 * k] = v.x; hvv[4 * k + 1] = v.y; hvv[4 * k + 2] = v.z; hvv[4 * k + 3] = v.w;
-          }
-          float r0 = 0.f, r1 = 0.f;
-#pragma unroll
-          for (int q = 0; q < 16; q += 2) {
-            r0 = fmaf(wr[jl][q], hvv[q], r0);
-            r1 = fmaf(wr[jl][q + 1], hvv[q + 1], r1);
-          }
-          float rr = r0 + r1;
-          rr += __shfl_xor_sync(0xffffffffu, rr, 1);
-          rr += __shfl_xor_sync(0xffffffffu, rr, 2);
-          const float xn = xi + (rr + bres[jl * R + pr]);
-          if (t == 0) trace_clk(A, n, 11 + 5 * jl);
-          if (ch == 0) {
-            if (jl + 1 < nl) m.xs[jl + 1][pr] = xn;
-            else if (!last_cta) ptx::st_async(remote(&m.xs[0][pr], c + 1), xn, remote(&m.bar_xin, c + 1));
-          }
-        }
-        ptx::bar_sync(1, kMain);
       }
     }
-    if (t == 0) {
-      trace(A, n, 2);
+  }
+  if (c == 0 && A.N > 0) final_draw(P, cx, a);
+}
+
+// ------------------------------------------------------------------ chain CTA, warpgroup B (W_res)
+template <bool TRACE>
+__device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* blk, const float* sw) {
+  const RunArgs& A = P.a;
+  const ClusterPlan& pl = P.p;
+  Mail& m = *cx.mail;
+  const int b = threadIdx.x - kAux - 128;  // 0..127
+  const int k = threadIdx.x - kAux;        // main-thread index of the sampler (128..255)
+  const int row = b >> 1, half = b & 1;
+  const int first = pl.chain_first[c], nl = pl.chain_nl[c];
+  const bool last_cta = (c == pl.nc - 1);
+  float wr[LPC][32];
+#pragma unroll
+  for (int jl = 0; jl < LPC; ++jl)
+#pragma unroll
+    for (int q = 0; q < 32; ++q) wr[jl][q] = blk[(LPC * 64 + jl * 32 + q) * 128 + b];
+  const float* bres = sw + LPC * R * 2 * R + LPC * 2 * R;  // [LPC][R]
+  const float* wembc = bres + LPC * R;
+  const float* bemb = wembc + kLevels * R;
+  int y1 = kLevels / 2, y2 = kLevels / 2;
+
+  for (int64_t n = 0; n < A.N; ++n) {
+    if (c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
+#pragma unroll
+    for (int jl = 0; jl < LPC; ++jl) {
+      if (jl < nl) {
+        const int j = first + jl;
+        ptx::bar_sync(kBarH, kMain);  // h^(j) from A (implies xs[jl] is valid)
+        const float xi = m.xs[jl][row];
+        if (jl == 0 && half == 0) m.xsave0[row] = xi;
+        if (j < pl.L - 1) {
+          // x^(j) = x^(j-1) + W_res h + B_res (PAPER.md:437)
+          float rr = dotK<32>(wr[jl], &m.hs[jl][36 * half]);
+          rr += __shfl_xor_sync(0xffffffffu, rr, 1);
+          const float xn = xi + (rr + bres[jl * R + row]);
+          if (half == 0) {
+            if (jl + 1 < nl) m.xs[jl + 1][row] = xn;
+            else if (!last_cta) ptx::st_async(remote(&m.xs[0][row], c + 1), xn, remote(&m.bar_xin, c + 1));
+          }
+          if (jl + 1 < nl) bar_arrive(kBarX, kMain);
+        }
+      }
+    }
+    // the sample's layers are done: the aux warpgroup may read xs / xsave0
+    if (b == 0) {
+      trace<TRACE>(A, n, 2);
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_done));
     }
   }
-
-  if (c == 0 && A.N > 0) {  // draw the last sample
-    const int64_t n = A.N;
-    const float u = uni ? __ldg(uni + n - 1) : 0.0f;
-    const int yf = forced ? (int)__ldg(forced + n - 1) : 0;
-    wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11);
-    const float l = m.logits_in[t];
-    if (forced) {
-      A.out_logits[(n - 1) * kLevels + t] = l;
-      (void)yf;
-    } else {
-      const int y = sample_256(l, u, m.dscr, m.fscr, m.iscr, t, 1);
-      if (t == 0) A.out_codes[n - 1] = (uint8_t)y;
-    }
-  }
+  if (c == 0 && A.N > 0) final_draw(P, cx, k);
 }
 
-// ------------------------------------------------------------------ chain CTA, aux warpgroup
+// ------------------------------------------------------------------ chain CTA, warpgroup X (aux)
 // For the coming sample n: queue write of x^(j-1)_{n-1}, queue read of x^(j-1)_{n-d},
 // pre = B + L^(j)_{n/hop} + W_prev x^(j-1)_{n-d}  (Fig. 2 aux threads).
+template <bool TRACE>
 __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
-  const int at = threadIdx.x - kMain;  // 0..127 = row of a (2r rows)
+  const int at = threadIdx.x;  // 0..127 = row of a (2r rows)
   const int first = pl.chain_first[c], nl = pl.chain_nl[c];
-  const float* wprev = sw;                    // [LPC][R (k)][2R (i)]
-  const float* bj = sw + LPC * R * 2 * R;     // [LPC][2R]
+  const float* wprev = sw;                 // [LPC][R (k)][2R (i)]
+  const float* bj = sw + LPC * R * 2 * R;  // [LPC][2R]
   const int L = A.L;
 
   for (int64_t n = 0; n < A.N; ++n) {
     if (n > 0) wait(cx, &m.bar_done, (uint32_t)((n - 1) & 1), 14);
-    if (at == 0) trace(A, n, 4);
     const int64_t f = n / A.hop;
     for (int jl = 0; jl < nl; ++jl) {
       const int j = first + jl;
@@ -301,142 +378,102 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       const float lv = __ldg(A.cond + (f * L + j) * 2 * R + at);
       if (at < R) {
         float* ring = A.ring + A.ring_off[j];
-        const float xc = m.xsave[jl][at];  // x^(j-1)_{n-1}
+        const float xc = (jl == 0) ? m.xsave0[at] : m.xs[jl][at];  // x^(j-1)_{n-1}
         float xpv = 0.0f;
         if (n - d >= 0) xpv = (d == 1) ? xc : ring[(int64_t)(n % d) * R + at];  // slot of n-d
         if (n > 0 && d >= 2) ring[(int64_t)((n - 1) % d) * R + at] = xc;
         m.xp[at] = xpv;
       }
-      ptx::bar_sync(2, kAux);
+      ptx::bar_sync(kBarAux, kAux);
       const float* w = wprev + jl * R * 2 * R;
-      float a0 = 0.f, a1 = 0.f;
-#pragma unroll 8
-      for (int k = 0; k < R; k += 2) {
-        a0 = fmaf(w[k * 2 * R + at], m.xp[k], a0);
-        a1 = fmaf(w[(k + 1) * 2 * R + at], m.xp[k + 1], a1);
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 4
+      for (int q = 0; q < R; q += 4) {
+        const float4 x = lds4(&m.xp[q]);
+        a0 = fmaf(w[q * 2 * R + at], x.x, a0);
+        a1 = fmaf(w[(q + 1) * 2 * R + at], x.y, a1);
+        a2 = fmaf(w[(q + 2) * 2 * R + at], x.z, a2);
+        a3 = fmaf(w[(q + 3) * 2 * R + at], x.w, a3);
       }
-      m.pre[jl][at] = (bj[jl * 2 * R + at] + lv) + (a0 + a1);
-      ptx::bar_sync(2, kAux);
+      m.pre[jl][at] = (bj[jl * 2 * R + at] + lv) + ((a0 + a1) + (a2 + a3));
+      ptx::bar_sync(kBarAux, kAux);
     }
     if (at == 0) {
-      trace(A, n, 5);
+      trace<TRACE>(A, n, 5);
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_pre));
     }
   }
 }
 
 // ------------------------------------------------------------------ head CTA (rows [64h, 64h+64))
-template <int S>
+template <int S, bool TRACE>
 __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float* blk, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
-  const int t = threadIdx.x;
-  constexpr int QS = S / 4;  // weights per thread of W_skip^(l) and of W_relu
-  float wsk[QS], wrl[QS], wo[64];
+  const int k = threadIdx.x - kAux;  // 0..255
+  constexpr int QS = S / 4;          // columns of W_relu per thread (4 chunks)
+  float wsk[64], wrl[QS], wo[64];
 #pragma unroll
-  for (int q = 0; q < QS; ++q) wsk[q] = blk[q * kMain + t];
+  for (int q = 0; q < 64; ++q) wsk[q] = blk[q * kMain + k];
 #pragma unroll
-  for (int q = 0; q < QS; ++q) wrl[q] = blk[(QS + q) * kMain + t];
+  for (int q = 0; q < QS; ++q) wrl[q] = blk[(64 + q) * kMain + k];
 #pragma unroll
-  for (int q = 0; q < 64; ++q) wo[q] = blk[(2 * QS + q) * kMain + t];
-  const float* bskip = sw;           // [S]
-  const float* brelu = sw + S;       // [64]
-  const float* bout = sw + S + 64;   // [64]
-  const int row = t >> 2, ch = t & 3;
+  for (int q = 0; q < 64; ++q) wo[q] = blk[(64 + QS + q) * kMain + k];
+  const float* bskip = sw;          // [S]
+  const float* brelu = sw + S;      // [64]
+  const float* bout = sw + S + 64;  // [64]
+  const int row = k >> 2, ch = k & 3;
   const int nk = pl.nk;
 
   for (int64_t n = 0; n < A.N; ++n) {
     const uint32_t par = (uint32_t)(n & 1);
-    if (wait(cx, &m.bar_h[0], par, 21) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[0]), R * 4);
-    if (t == 0) trace(A, n, 0);
+    if (wait(cx, &m.bar_h[0], par, 21) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[0]), R * 4);
+    if (k == 0) trace<TRACE>(A, n, 0);
     // q = B_skip + sum_k partial_k + W_skip^(l) h^(l); z_s = relu(q)
-    float dot;
-    int qrow;
-    if constexpr (S == 256) {
-      qrow = t;
-      float d0 = 0.f, d1 = 0.f;
-#pragma unroll
-      for (int q = 0; q < 64; q += 4) {
-        const float4 hv = lds4(&m.hbuf[0][q]);
-        d0 = fmaf(wsk[q], hv.x, d0);
-        d1 = fmaf(wsk[q + 1], hv.y, d1);
-        d0 = fmaf(wsk[q + 2], hv.z, d0);
-        d1 = fmaf(wsk[q + 3], hv.w, d1);
-      }
-      dot = d0 + d1;
-    } else {
-      qrow = t >> 1;
-      const int half = t & 1;
-      float d0 = 0.f, d1 = 0.f;
-#pragma unroll
-      for (int q = 0; q < 32; q += 4) {
-        const float4 hv = lds4(&m.hbuf[0][32 * half + q]);
-        d0 = fmaf(wsk[q], hv.x, d0);
-        d1 = fmaf(wsk[q + 1], hv.y, d1);
-        d0 = fmaf(wsk[q + 2], hv.z, d0);
-        d1 = fmaf(wsk[q + 3], hv.w, d1);
-      }
-      dot = d0 + d1;
-      dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-    }
+    const float dot = (k < S) ? dot_h64(wsk, m.hbuf[0]) : 0.0f;
     if (nk > 0) {
-      if (wait(cx, &m.bar_part, par, 22) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_part), nk * S * 4);
+      if (wait(cx, &m.bar_part, par, 22) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_part), nk * S * 4);
     }
-    if (t == 0) trace(A, n, 1);
-    float qv = bskip[qrow];
-    for (int k = 0; k < nk; ++k) qv += m.part[k][qrow];
-    qv += dot;
-    if (S == 256 || (t & 1) == 0) m.zs[qrow] = fmaxf(qv, 0.0f);
-    ptx::bar_sync(1, kMain);
+    if (k == 0) trace<TRACE>(A, n, 1);
+    if (k < S) {
+      float qv = bskip[k];
+      for (int kk = 0; kk < nk; ++kk) qv += m.part[kk][k];
+      qv += dot;
+      m.zs[cpad<QS>(k)] = fmaxf(qv, 0.0f);
+    }
+    ptx::bar_sync(kBarMain, kMain);
     // z_a = relu(W_relu z_s + B_relu), rows 64h + row
-    float r0 = 0.f, r1 = 0.f;
-#pragma unroll
-    for (int q = 0; q < QS; q += 4) {
-      const float4 zv = lds4(&m.zs[ch * QS + q]);
-      r0 = fmaf(wrl[q], zv.x, r0);
-      r1 = fmaf(wrl[q + 1], zv.y, r1);
-      r0 = fmaf(wrl[q + 2], zv.z, r0);
-      r1 = fmaf(wrl[q + 3], zv.w, r1);
-    }
-    float za = r0 + r1;
+    float za = dotK<QS>(wrl, &m.zs[ch * (QS + 4)]);
     za += __shfl_xor_sync(0xffffffffu, za, 1);
     za += __shfl_xor_sync(0xffffffffu, za, 2);
     za = fmaxf(za + brelu[row], 0.0f);
     if (ch == 0) {
+      const int dst = cpad<64>(64 * hidx + row);
 #pragma unroll
       for (int hh = 0; hh < NH; ++hh)
-        ptx::st_async(remote(&m.za_in[64 * hidx + row], pl.nc + hh), za, remote(&m.bar_za, pl.nc + hh));
+        ptx::st_async(remote(&m.za_in[dst], pl.nc + hh), za, remote(&m.bar_za, pl.nc + hh));
     }
-    if (wait(cx, &m.bar_za, par, 23) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_za), kLevels * 4);
-    if (t == 0) trace(A, n, 2);
+    if (wait(cx, &m.bar_za, par, 23) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_za), kLevels * 4);
+    if (k == 0) trace<TRACE>(A, n, 2);
     // logits = W_out z_a + B_out, rows 64h + row
-    float o0 = 0.f, o1 = 0.f;
-#pragma unroll
-    for (int q = 0; q < 64; q += 4) {
-      const float4 zv = lds4(&m.za_in[ch * 64 + q]);
-      o0 = fmaf(wo[q], zv.x, o0);
-      o1 = fmaf(wo[q + 1], zv.y, o1);
-      o0 = fmaf(wo[q + 2], zv.z, o0);
-      o1 = fmaf(wo[q + 3], zv.w, o1);
-    }
-    float lg = o0 + o1;
+    float lg = dotK<64>(wo, &m.za_in[ch * 68]);
     lg += __shfl_xor_sync(0xffffffffu, lg, 1);
     lg += __shfl_xor_sync(0xffffffffu, lg, 2);
     lg += bout[row];
     if (ch == 0) ptx::st_async(remote(&m.logits_in[64 * hidx + row], 0), lg, remote(&m.bar_logits, 0));
-    if (t == 0) trace(A, n, 3);
+    if (k == 0) trace<TRACE>(A, n, 3);
   }
 }
 
 // ------------------------------------------------------------------ skip CTA
 // partial_k = sum over owned layers j (ascending) of W_skip^(j) h^(j).
-template <int S>
+template <int S, bool TRACE>
 __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* blk, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x - kAux;     // 0..255
   constexpr int QS = S / 4;             // registers per layer per thread
   constexpr int MAXREG = 192 / QS;      // 3 (s=256) or 6 (s=128)
   constexpr int LSTRIDE = (S == 256) ? 64 * 256 : 2 * (32 * 128 + 16);  // floats per smem layer
@@ -452,25 +489,32 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* bl
   for (int64_t n = 0; n < A.N; ++n) {
     const uint32_t par = (uint32_t)(n & 1);
     float part = 0.0f;
+#pragma unroll 1
     for (int sl = 0; sl < nsm; ++sl) {
       if (wait(cx, &m.bar_h[sl], par, 31) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
       const float* ws = sw + sl * LSTRIDE;
-      float d0 = 0.f, d1 = 0.f;
+      float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
       if constexpr (S == 256) {
-#pragma unroll 8
-        for (int q = 0; q < 64; q += 2) {
-          d0 = fmaf(ws[q * 256 + row], m.hbuf[sl][q], d0);
-          d1 = fmaf(ws[(q + 1) * 256 + row], m.hbuf[sl][q + 1], d1);
+#pragma unroll 4
+        for (int q = 0; q < 64; q += 4) {
+          const float4 x = lds4(&m.hbuf[sl][q + ((q >> 5) << 2)]);
+          d0 = fmaf(ws[q * 256 + row], x.x, d0);
+          d1 = fmaf(ws[(q + 1) * 256 + row], x.y, d1);
+          d2 = fmaf(ws[(q + 2) * 256 + row], x.z, d2);
+          d3 = fmaf(ws[(q + 3) * 256 + row], x.w, d3);
         }
       } else {
         const float* wh = ws + half * (32 * 128 + 16);
-#pragma unroll 8
-        for (int q = 0; q < 32; q += 2) {
-          d0 = fmaf(wh[q * 128 + row], m.hbuf[sl][32 * half + q], d0);
-          d1 = fmaf(wh[(q + 1) * 128 + row], m.hbuf[sl][32 * half + q + 1], d1);
+#pragma unroll 4
+        for (int q = 0; q < 32; q += 4) {
+          const float4 x = lds4(&m.hbuf[sl][36 * half + q]);
+          d0 = fmaf(wh[q * 128 + row], x.x, d0);
+          d1 = fmaf(wh[(q + 1) * 128 + row], x.y, d1);
+          d2 = fmaf(wh[(q + 2) * 128 + row], x.z, d2);
+          d3 = fmaf(wh[(q + 3) * 128 + row], x.w, d3);
         }
       }
-      float dot = d0 + d1;
+      float dot = (d0 + d1) + (d2 + d3);
       if (S == 128) dot += __shfl_xor_sync(0xffffffffu, dot, 1);
       part += dot;
     }
@@ -479,32 +523,27 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* bl
       if (rl < nreg) {
         const int sl = nsm + rl;
         if (wait(cx, &m.bar_h[sl], par, 32) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
-        float d0 = 0.f, d1 = 0.f;
-#pragma unroll
-        for (int q = 0; q < QS; q += 4) {
-          const float4 hv = lds4(&m.hbuf[sl][half * 32 + q]);
-          d0 = fmaf(w[rl][q], hv.x, d0);
-          d1 = fmaf(w[rl][q + 1], hv.y, d1);
-          d0 = fmaf(w[rl][q + 2], hv.z, d0);
-          d1 = fmaf(w[rl][q + 3], hv.w, d1);
+        float dot;
+        if constexpr (S == 256) {
+          dot = dot_h64(w[rl], m.hbuf[sl]);
+        } else {
+          dot = dotK<32>(w[rl], &m.hbuf[sl][36 * half]);
+          dot += __shfl_xor_sync(0xffffffffu, dot, 1);
         }
-        float dot = d0 + d1;
-        if (S == 128) dot += __shfl_xor_sync(0xffffffffu, dot, 1);
         part += dot;
       }
     }
     if (half == 0) m.zs[row] = part;
-    if (t == 0) trace(A, n, 1);
-    ptx::bar_sync(1, kMain);
+    if (t == 0) trace<TRACE>(A, n, 1);
+    ptx::bar_sync(kBarMain, kMain);
     if (t < (S / 4) * NH) {
       const int hh = t / (S / 4), e = t % (S / 4);
-      ptx::st_async4(remote(&m.part[k][4 * e], pl.nc + hh), lds4(&m.zs[4 * e]),
-                     remote(&m.bar_part, pl.nc + hh));
+      ptx::st_async4(remote(&m.part[k][4 * e], pl.nc + hh), lds4(&m.zs[4 * e]), remote(&m.bar_part, pl.nc + hh));
     }
   }
 }
 
-template <int S>
+template <int S, bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Mail* mail = reinterpret_cast<Mail*>(smem_raw);
@@ -519,7 +558,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   else if (rank < pl.nc + NH) { role = kHead; idx = rank - pl.nc; }
   else if (rank < pl.nc + NH + pl.nk) { role = kSkip; idx = rank - pl.nc - NH; }
 
-  // barriers + abort flag, then the shared-memory weight image
   if (t == 0) {
     mail->abort_flag = 0;
     ptx::mbar_init(ptx::smem_u32(&mail->bar_xin), 1);
@@ -528,9 +566,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     ptx::mbar_init(ptx::smem_u32(&mail->bar_done), 1);
     ptx::mbar_init(ptx::smem_u32(&mail->bar_part), 1);
     ptx::mbar_init(ptx::smem_u32(&mail->bar_za), 1);
+    ptx::mbar_init(ptx::smem_u32(&mail->bar_exit), 1);
     for (int i = 0; i < kCMaxSlot; ++i) ptx::mbar_init(ptx::smem_u32(&mail->bar_h[i]), 1);
     ptx::fence_mbar_init();
-    // arm phase 0 of every transaction barrier this role receives on
+    // arm phase 0 of every transaction barrier a role receives on
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_xin), R * 4);
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_logits), kLevels * 4);
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_part), pl.nk * S * 4);
@@ -546,34 +585,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   __syncthreads();
   ptx::cluster_sync();
 
-  // Register split: the two math warpgroups grow to 232 registers (W_cur/W_res,
-  // head or skip weights live there), the aux warpgroup shrinks to 48.  Each
-  // branch ends with its own cluster barrier so no code is shared across budgets.
-  if (t < kMain) {
+  // Register split: warpgroups A and B (math) grow to 232 registers, warpgroup X
+  // (aux) shrinks to 40.  Each branch ends with its own cluster barrier.
+  if (t >= kAux) {
     ptx::setmaxnreg_inc<kMainRegs>();
-    if (role == kChain) chain_main<S>(P, cx, idx, blk, sw);
-    else if (role == kHead) head_main<S>(P, cx, idx, blk, sw);
-    else if (role == kSkip) skip_main<S>(P, cx, idx, blk, sw);
+    if (role == kChain) {
+      if (t < kAux + 128) chain_A<TRACE>(P, cx, idx, blk, sw);
+      else chain_B<TRACE>(P, cx, idx, blk, sw);
+    } else if (role == kHead) {
+      head_main<S, TRACE>(P, cx, idx, blk, sw);
+    } else if (role == kSkip) {
+      skip_main<S, TRACE>(P, cx, idx, blk, sw);
+    }
+    ptx::bar_sync(kBarMain, kMain);
+    if (t == kAux) ptx::mbar_arrive(ptx::smem_u32(&mail->bar_exit));
     __syncwarp();
     ptx::cluster_sync();
     return;
   }
   ptx::setmaxnreg_dec<kAuxRegs>();
-  if (role == kChain) chain_aux(P, cx, idx, sw);
+  if (role == kChain) chain_aux<TRACE>(P, cx, idx, sw);
+  // Park until the math warps are done (try_wait suspends the warp).
+  while (!ptx::mbar_try_wait(ptx::smem_u32(&mail->bar_exit), 0)) {
+  }
   __syncwarp();
   ptx::cluster_sync();
 }
 
-template <int S>
+template <int S, bool TRACE>
 cudaError_t configure(int smem) {
-  cudaError_t e = cudaFuncSetAttribute(k_cluster<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cluster<S>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaError_t e = cudaFuncSetAttribute(k_cluster<S, TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_cluster<S, TRACE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
 template <int S>
 int max_active_clusters(int size, int smem) {
-  if (configure<S>(smem) != cudaSuccess) {
+  if (configure<S, false>(smem) != cudaSuccess || configure<S, true>(smem) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -589,17 +638,18 @@ int max_active_clusters(int size, int smem) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_cluster<S>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, k_cluster<S, false>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
   return n;
 }
 
-int smem_chain(const ClusterPlan& p, int c) {
+// floats of a chain CTA's shared-memory image: W_prev (col-major [R][2R]) x LPC,
+// B [LPC][2R], B_res [LPC][R]; CTA 0 adds W_emb_cur^T [256][R] and B_emb [R]
+int smem_chain(int c) {
   int f = LPC * R * 2 * R + LPC * 2 * R + LPC * R;
   if (c == 0) f += kLevels * R + R;
-  (void)p;
   return f;
 }
 
@@ -622,7 +672,7 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
   const int nskip = L - 1;  // W_skip^(l) lives in the head CTAs
   const int qs = s / 4, maxreg = 192 / qs;
   const int lstride = (s == 256) ? 64 * 256 : 2 * (32 * 128 + 16);
-  const int maxsm = std::min(kCMaxSlot - maxreg, (int)((200 * 1024) / (lstride * 4)));
+  const int maxsm = std::min(kCMaxSlot - maxreg, (int)((190 * 1024) / (lstride * 4)));
   const int cap = maxreg + maxsm;
   p.nk = nskip > 0 ? (nskip + cap - 1) / cap : 0;
   if (p.nk > kCMaxSkip) { p.why = "too many skip CTAs"; return p; }
@@ -638,16 +688,17 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
     if (p.skip_n[k] > cap) { p.why = "skip capacity"; return p; }
     p.skip_nsm[k] = std::max(0, p.skip_n[k] - maxreg);  // latest layers in registers
   }
-  // packed layout
   int64_t off = 0;
   int max_sw = 0;
   for (int rank = 0; rank < p.size; ++rank) {
-    int regs = 0, swf = 0;
-    if (rank < p.nc) { regs = kChainRegs; swf = smem_chain(p, rank); }
-    else if (rank < p.nc + p.nh) { regs = 2 * qs + 64; swf = s + 128; }
-    else { const int k = rank - p.nc - p.nh; regs = (p.skip_n[k] - p.skip_nsm[k]) * qs; swf = p.skip_nsm[k] * lstride; }
+    int64_t regfloats = 0;
+    int swf = 0;
+    if (rank < p.nc) { regfloats = (int64_t)(LPC * 64 + LPC * 32) * 128; swf = smem_chain(rank); }
+    else if (rank < p.nc + p.nh) { regfloats = (int64_t)(64 + qs + 64) * kMain; swf = s + 128; }
+    else { const int k = rank - p.nc - p.nh; regfloats = (int64_t)(p.skip_n[k] - p.skip_nsm[k]) * qs * kMain; swf = p.skip_nsm[k] * lstride; }
     p.pk_off[rank] = off;
-    off += (int64_t)regs * kMain;
+    off += regfloats;
+    off = (off + 3) & ~int64_t(3);
     p.pk_smem_off[rank] = off;
     p.pk_smem_floats[rank] = swf;
     off += (swf + 3) & ~3;
@@ -674,6 +725,9 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
 
 size_t packed_bytes(const ClusterPlan& p) { return sizeof(float) * (size_t)p.pk_total; }
 
+// Residency layout, built on the host from the raw roster-order blob (index
+// shuffling only, no arithmetic): register blocks are [register q][thread], so
+// the start-up loads of each thread are coalesced across its warp.
 cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Offsets& o, void* packed) {
   const int s = p.s, qs = s / 4;
   std::vector<float> h((size_t)p.pk_total, 0.0f);
@@ -685,15 +739,14 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
     float* sm = h.data() + p.pk_smem_off[rank];
     if (rank < p.nc) {
       const int first = p.chain_first[rank], nl = p.chain_nl[rank];
-      for (int t = 0; t < kMain; ++t) {
-        const int pr = t >> 2, ch = t & 3;
+      for (int a = 0; a < 128; ++a) {
+        const int wa = a >> 5, l = a & 31;
+        const int row = (l < 16) ? (16 * wa + l) : (R + 16 * wa + (l - 16));
+        const int brow = a >> 1, half = a & 1;
         for (int jl = 0; jl < nl; ++jl) {
           const int j = first + jl;
-          for (int q = 0; q < 16; ++q) {
-            blk[(jl * 48 + q) * kMain + t] = W(j, o.w_cur, pr, ch * 16 + q, R);
-            blk[(jl * 48 + 16 + q) * kMain + t] = W(j, o.w_cur, R + pr, ch * 16 + q, R);
-            blk[(jl * 48 + 32 + q) * kMain + t] = W(j, o.w_res, pr, ch * 16 + q, R);
-          }
+          for (int q = 0; q < 64; ++q) blk[(jl * 64 + q) * 128 + a] = W(j, o.w_cur, row, q, R);
+          for (int q = 0; q < 32; ++q) blk[(LPC * 64 + jl * 32 + q) * 128 + a] = W(j, o.w_res, brow, 32 * half + q, R);
         }
       }
       for (int jl = 0; jl < nl; ++jl) {
@@ -713,15 +766,13 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
     } else if (rank < p.nc + p.nh) {
       const int hidx = rank - p.nc;
       const int jl = p.L - 1;
-      for (int t = 0; t < kMain; ++t) {
-        const int row = t >> 2, ch = t & 3;
-        for (int q = 0; q < qs; ++q) {
-          if (s == 256) blk[q * kMain + t] = W(jl, o.w_skip, t, q, R);
-          else blk[q * kMain + t] = W(jl, o.w_skip, t >> 1, 32 * (t & 1) + q, R);
-          blk[(qs + q) * kMain + t] = w[o.w_relu + (int64_t)(64 * hidx + row) * s + ch * qs + q];
-        }
+      for (int k = 0; k < kMain; ++k) {
+        const int row = k >> 2, ch = k & 3;
+        for (int q = 0; q < 64; ++q) blk[q * kMain + k] = (k < s) ? W(jl, o.w_skip, k, q, R) : 0.0f;
+        for (int q = 0; q < qs; ++q)
+          blk[(64 + q) * kMain + k] = w[o.w_relu + (int64_t)(64 * hidx + row) * s + ch * qs + q];
         for (int q = 0; q < 64; ++q)
-          blk[(2 * qs + q) * kMain + t] = w[o.w_out + (int64_t)(64 * hidx + row) * kLevels + ch * 64 + q];
+          blk[(64 + qs + q) * kMain + k] = w[o.w_out + (int64_t)(64 * hidx + row) * kLevels + ch * 64 + q];
       }
       for (int i = 0; i < s; ++i) sm[i] = w[o.b_skip + i];
       for (int i = 0; i < 64; ++i) {
@@ -769,8 +820,7 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   P.a = a;
   P.p = p;
   P.pk = static_cast<const float*>(packed);
-  cudaError_t e = (p.s == 256) ? configure<256>(p.smem_bytes) : configure<128>(p.smem_bytes);
-  if (e != cudaSuccess) return e;
+  const bool tr = a.trace != nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.size);
   cfg.blockDim = dim3(kThreads);
@@ -783,7 +833,12 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  e = (p.s == 256) ? cudaLaunchKernelEx(&cfg, k_cluster<256>, P) : cudaLaunchKernelEx(&cfg, k_cluster<128>, P);
+  cudaError_t e;
+  if (p.s == 256) {
+    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<256, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<256, false>, P);
+  } else {
+    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<128, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<128, false>, P);
+  }
   info->grid = p.size;
   info->cluster = p.size;
   info->threads = kThreads;

@@ -9,8 +9,10 @@ using namespace dvw;
 
 constexpr int R = 64, LPC = 4, kMain = 256, kThreads = 384;
 
-template <int AUX, bool FASTGATE>
+template <int AUX, int GATE, int FL>
 __global__ void __launch_bounds__(kThreads, 1) probe(const float* wts, int iters, float* out, long long* cyc) {
+  long long ph_acc[6] = {0, 0, 0, 0, 0, 0};
+  long long tp = 0;
   __shared__ __align__(16) float xs[LPC + 1][R];
   __shared__ __align__(16) float hs[R];
   __shared__ __align__(16) float pre[LPC][2 * R];
@@ -41,6 +43,7 @@ __global__ void __launch_bounds__(kThreads, 1) probe(const float* wts, int iters
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int jl = 0; jl < LPC; ++jl) {
+      if (FL & 4) tp = clock64();
       const float* xin = xs[jl];
       float xv[16];
 #pragma unroll
@@ -59,20 +62,30 @@ __global__ void __launch_bounds__(kThreads, 1) probe(const float* wts, int iters
         g1 = fmaf(wc[jl][16 + q + 1], xv[q + 1], g1);
       }
       float ah = h0 + h1, ag = g0 + g1;
-      ah += __shfl_xor_sync(0xffffffffu, ah, 1);
-      ag += __shfl_xor_sync(0xffffffffu, ag, 1);
-      ah += __shfl_xor_sync(0xffffffffu, ah, 2);
-      ag += __shfl_xor_sync(0xffffffffu, ag, 2);
+      if (!(FL & 1)) {
+        ah += __shfl_xor_sync(0xffffffffu, ah, 1);
+        ag += __shfl_xor_sync(0xffffffffu, ag, 1);
+        ah += __shfl_xor_sync(0xffffffffu, ah, 2);
+        ag += __shfl_xor_sync(0xffffffffu, ag, 2);
+      }
       float hv;
-      if (FASTGATE) {
-        const float e2 = exp2f(2.8853900817779268f * (ah + ph));
-        const float eg = exp2f(-1.4426950408889634f * (ag + pg));
-        hv = (1.0f - 2.0f * __frcp_rn(e2 + 1.0f)) * __frcp_rn(1.0f + eg);
+      if (GATE == 1) {
+        float e2, eg, r1, r2;
+        const float a1 = 2.8853900817779268f * (ah + ph), a2 = -1.4426950408889634f * (ag + pg);
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(a1));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(eg) : "f"(a2));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(e2 + 1.0f));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2) : "f"(eg + 1.0f));
+        hv = fmaf(-2.0f, r1, 1.0f) * r2;
+      } else if (GATE == 2) {
+        hv = (ah + ph) * (ag + pg);
       } else {
         hv = gate(ah + ph, ag + pg);
       }
+      if (FL & 4) { long long c = clock64(); ph_acc[0] += c - tp; tp = c; }
       if (ch == 0) hs[pr] = hv;
       ptx::bar_sync(1, kMain);
+      if (FL & 4) { long long c = clock64(); ph_acc[1] += c - tp; tp = c; }
       float hvv[16];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -86,39 +99,46 @@ __global__ void __launch_bounds__(kThreads, 1) probe(const float* wts, int iters
         r1 = fmaf(wr[jl][q + 1], hvv[q + 1], r1);
       }
       float rr = r0 + r1;
-      rr += __shfl_xor_sync(0xffffffffu, rr, 1);
-      rr += __shfl_xor_sync(0xffffffffu, rr, 2);
+      if (!(FL & 1)) {
+        rr += __shfl_xor_sync(0xffffffffu, rr, 1);
+        rr += __shfl_xor_sync(0xffffffffu, rr, 2);
+      }
       const float xn = xi + rr * 0.5f;
+      if (FL & 4) { long long c = clock64(); ph_acc[2] += c - tp; tp = c; }
       if (ch == 0) xs[jl + 1][pr] = xn;
-      ptx::bar_sync(1, kMain);
+      if (!(FL & 2)) ptx::bar_sync(1, kMain);
+      if (FL & 4) { long long c = clock64(); ph_acc[3] += c - tp; tp = c; }
     }
     if (t < R) xs[0][t] = xs[LPC][t] * 0.5f;
     ptx::bar_sync(1, kMain);
   }
   long long t1 = clock64();
-  if (t == 0) { cyc[0] = t1 - t0; stop = 1; }
+  if (t == 0) { cyc[0] = t1 - t0; stop = 1; for (int i = 0; i < 4; ++i) cyc[1 + i] = ph_acc[i]; }
   if (t < R) out[t] = xs[0][t];
 }
 
-template <int AUX, bool FG>
+template <int AUX, int G, int FL>
 void run(const char* name, const float* w, float* out, long long* cyc) {
   const int iters = 2000;
-  probe<AUX, FG><<<1, kThreads>>>(w, iters, out, cyc);
+  probe<AUX, G, FL><<<1, kThreads>>>(w, iters, out, cyc);
   cudaError_t e = cudaDeviceSynchronize();
-  long long h = 0; cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
-  printf("%-28s err=%s cycles/layer=%.1f\n", name, cudaGetErrorString(e), (double)h / iters / LPC);
+  long long h[5] = {0}; cudaMemcpy(h, cyc, 40, cudaMemcpyDeviceToHost);
+  const double L = (double)iters * LPC;
+  printf("%-28s err=%s cycles/layer=%.1f  phases: gemv1+gate=%.0f bar1=%.0f gemv2=%.0f bar2=%.0f\n", name, cudaGetErrorString(e), (double)h[0] / L, h[1] / L, h[2] / L, h[3] / L, h[4] / L);
 }
 
 int main() {
   float *w, *out; long long* cyc;
-  cudaMalloc(&w, sizeof(float) * LPC * 48 * kMain); cudaMalloc(&out, 4096); cudaMalloc(&cyc, 8);
+  cudaMalloc(&w, sizeof(float) * LPC * 48 * kMain); cudaMalloc(&out, 4096); cudaMalloc(&cyc, 64);
   cudaMemset(w, 0, sizeof(float) * LPC * 48 * kMain);
-  for (int rep = 0; rep < 2; ++rep) {
-    run<0, false>("aux exit, accurate gate", w, out, cyc);
-    run<1, false>("aux try_wait spin, accurate", w, out, cyc);
-    run<2, false>("aux nanosleep, accurate", w, out, cyc);
-    run<0, true>("aux exit, fast gate", w, out, cyc);
-    run<1, true>("aux try_wait spin, fast", w, out, cyc);
-  }
+  run<0, 0, 4>("accurate gate, phase clocks", w, out, cyc);
+  run<0, 1, 4>("mufu gate, phase clocks", w, out, cyc);
+  run<0, 0, 0>("accurate gate (baseline)", w, out, cyc);
+  run<0, 1, 0>("mufu gate", w, out, cyc);
+  run<0, 2, 0>("no gate", w, out, cyc);
+  run<0, 0, 1>("accurate, no shuffles", w, out, cyc);
+  run<0, 0, 2>("accurate, no 2nd barrier", w, out, cyc);
+  run<0, 2, 3>("no gate/shfl/2nd bar", w, out, cyc);
+  run<1, 1, 0>("mufu gate, aux spin", w, out, cyc);
   return 0;
 }
