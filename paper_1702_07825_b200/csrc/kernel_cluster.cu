@@ -6,19 +6,22 @@
 // rest for sm_100a:
 //   * one thread-block cluster; every hand-off is a DSMEM st.async whose
 //     transaction bytes complete on the receiver's mbarrier (no L2 round trip);
-//   * chain CTAs own 3 consecutive layers.  Warpgroup A holds W_cur (one full
-//     row per thread; the tanh row and its sigmoid partner sit 16 lanes apart so
-//     the gate needs one shuffle), warpgroup B holds W_res (half a
-//     row per thread).  A and B hand h and x to each other through shared memory
-//     with producer/consumer named barriers (bar.arrive / bar.sync);
+//   * chain CTAs own 3 consecutive layers.  Warpgroup A holds W_cur, warpgroup B
+//     W_res, both as (rows x 16-column chunk) register tiles: each thread reuses
+//     every loaded vector element for 4 (A) or 2 (B) rows, which halves/quarters
+//     the shared-memory -> register traffic that bounds a CUDA-core matvec; the
+//     partial sums meet in a transposing shuffle reduction that leaves the tanh
+//     row and its sigmoid partner in one lane for the gate.  A and B
+//     hand h and x to each other through shared memory with producer/consumer
+//     named barriers (bar.arrive / bar.sync);
 //   * the third warpgroup of a chain CTA does the off-chain work of the coming
 //     sample (Fig. 2's aux threads): dilation-queue read/write in L2,
 //     conditioning fetch, W_prev x_{n+1-d} + B + L from shared memory;
 //   * skip CTAs accumulate W_skip^(j) h^(j) as h arrives; head CTAs
 //     own 64 output rows each of relu -> W_relu -> relu -> W_out
 //     plus W_skip^(l); CTA 0 samples (App. A.4) and embeds the next input (step 1).
-// Shared-memory vectors read in 4 or 2 column chunks are padded (+4 floats per
-// chunk) so the chunks fall in different banks.
+// Shared-memory vectors are stored in padded chunks (16 floats -> stride 20) so
+// the chunks a warp reads at once fall in different banks.
 // Numerics: fp32 FMA; gate from ex2.approx/rcp.approx (|err| ~ 1e-7, R13);
 // fp64 CDF scan (R11); every reduction has a fixed order (bitwise deterministic).
 #include <algorithm>
@@ -49,28 +52,28 @@ constexpr int kBarAux = 4;   // X, 128 threads
 
 enum Role { kChain = 0, kHead = 1, kSkip = 2, kIdle = 3 };
 
-// h vectors (64) are read in 2 halves of 32: half 1 starts 4 floats later
-__device__ __forceinline__ int hpad(int i) { return i + ((i >> 5) << 2); }
-constexpr int kHLen = 72;
-// 256-vectors read in 4 chunks of C (z_a: C = 64; z_s: C = s/4), chunk c starts at c (C + 4)
+// Vectors are read in column chunks of C floats; chunk c starts at c (C + 4), so the
+// (up to 8) chunks one warp instruction touches occupy distinct bank groups.
 template <int C>
 __device__ __forceinline__ int cpad(int i) { return i + (i / C) * 4; }
-constexpr int kVLen = 272;
+__device__ __forceinline__ int pad16(int i) { return i + ((i >> 4) << 2); }
+constexpr int kHLen = 80;   // 64-vector in 4 chunks of 16
+constexpr int kVLen = 320;  // 256-vector in 16 chunks of 16 (or 8)
 
 struct __align__(16) Mail {
   uint64_t bar_xin, bar_logits, bar_pre, bar_done, bar_part, bar_za, bar_exit;
   uint64_t bar_h[kCMaxSlot];
   int abort_flag;
-  alignas(16) float xs[LPC + 1][R];   // chain: layer inputs; xs[0] is the inbound x
-  float xsave0[R];                    // chain: copy of the inbound x for the aux warpgroup
-  float pre[LPC][2 * R];              // chain: W_prev x_{n-d} + B + L for the coming sample
-  float xp[R];                        // chain aux scratch
-  float hs[LPC][kHLen];               // chain: h handed from A to B (padded halves)
-  float logits_in[kLevels];           // CTA 0: inbound logits
-  float hbuf[kCMaxSlot][kHLen];       // skip: h^(j) per owned slot; head: slot 0 = h^(l)
-  float part[kCMaxSkip][256];         // head: skip partials
-  float za_in[kVLen];                 // head: all-gathered z_a (padded chunks)
-  float zs[kVLen];                    // head: z_s (padded chunks); skip: partial staging
+  alignas(16) float xs[LPC + 1][kHLen];  // chain: layer inputs (pad16); xs[0] is the inbound x
+  float xsave0[R];                       // chain: copy of the inbound x for the aux warpgroup
+  float pre[LPC][2 * R];                 // chain: W_prev x_{n-d} + B + L for the coming sample
+  float xp[R];                           // chain aux scratch
+  float hs[LPC][kHLen];                  // chain: h handed from A to B (pad16)
+  float logits_in[kLevels];              // CTA 0: inbound logits
+  float hbuf[kCMaxSlot][kHLen];          // skip: h^(j) per owned slot; head: slot 0 = h^(l) (pad16)
+  float part[kCMaxSkip][256];            // head: skip partials
+  float za_in[kVLen];                    // head: all-gathered z_a (pad16)
+  float zs[kVLen];                       // head: z_s (cpad<s/16>); skip: partial staging
   double dscr[8];
   float fscr[8];
   int iscr[16];
@@ -161,33 +164,41 @@ __device__ __forceinline__ float gate_fast(float a, float g) {
   return fmaf(-2.0f, ra, 1.0f) * rg;
 }
 
-// dot of K register weights with K consecutive shared floats (4 accumulators)
-template <int K>
-__device__ __forceinline__ float dotK(const float* w, const float* v) {
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+// Register tile x vector chunk: acc[m] = sum_c w[m*C + c] * v[c] for RQ rows and a
+// C-float chunk of a shared vector; two accumulators per row (even/odd c) for ILP.
+// Summation order is fixed (bitwise deterministic).
+template <int RQ, int C>
+__device__ __forceinline__ void tile_dot(const float* w, const float* v, float (&acc)[RQ]) {
+  float e[RQ], o[RQ];
 #pragma unroll
-  for (int q = 0; q < K; q += 4) {
-    const float4 x = lds4(v + q);
-    a0 = fmaf(w[q], x.x, a0);
-    a1 = fmaf(w[q + 1], x.y, a1);
-    a2 = fmaf(w[q + 2], x.z, a2);
-    a3 = fmaf(w[q + 3], x.w, a3);
+  for (int m = 0; m < RQ; ++m) e[m] = o[m] = 0.0f;
+#pragma unroll
+  for (int c = 0; c < C; c += 4) {
+    const float4 x = lds4(v + c);
+#pragma unroll
+    for (int m = 0; m < RQ; ++m) {
+      e[m] = fmaf(w[m * C + c], x.x, e[m]);
+      o[m] = fmaf(w[m * C + c + 1], x.y, o[m]);
+      e[m] = fmaf(w[m * C + c + 2], x.z, e[m]);
+      o[m] = fmaf(w[m * C + c + 3], x.w, o[m]);
+    }
   }
-  return (a0 + a1) + (a2 + a3);
+#pragma unroll
+  for (int m = 0; m < RQ; ++m) acc[m] = e[m] + o[m];
 }
 
-// same over a padded h vector (64 values in two 32-halves, see hpad)
-__device__ __forceinline__ float dot_h64(const float* w, const float* hv) {
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+// One transposing level of a butterfly reduction: lanes whose `bit` is set keep
+// the upper half of the row values and send the lower half to their partner,
+// which keeps the lower half.  Halves the row count per lane with N/2 shuffles.
+template <int N>
+__device__ __forceinline__ void xpose_level(float (&v)[N], int lane, int bit) {
+  const bool up = (lane & bit) != 0;
 #pragma unroll
-  for (int q = 0; q < 64; q += 4) {
-    const float4 x = lds4(hv + q + ((q >> 5) << 2));
-    a0 = fmaf(w[q], x.x, a0);
-    a1 = fmaf(w[q + 1], x.y, a1);
-    a2 = fmaf(w[q + 2], x.z, a2);
-    a3 = fmaf(w[q + 3], x.w, a3);
+  for (int i = 0; i < N / 2; ++i) {
+    const float send = up ? v[i] : v[i + N / 2];
+    const float keep = up ? v[i + N / 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
   }
-  return (a0 + a1) + (a2 + a3);
 }
 
 // ------------------------------------------------------------------ chain CTA 0: sample + embed
@@ -222,7 +233,7 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
     if (k < R) ep = __ldg(embp_g + y2 * R + k);
   }
   // x^(0)_n = W_emb_prev[:, y_{n-2}] + W_emb_cur[:, y_{n-1}] + B_emb
-  if (k < R) m.xs[0][k] = (ep + wembc[y1 * R + k]) + bemb[k];
+  if (k < R) m.xs[0][pad16(k)] = (ep + wembc[y1 * R + k]) + bemb[k];
   ptx::bar_sync(kBarMain, kMain);
 }
 
@@ -243,15 +254,17 @@ __device__ __forceinline__ void final_draw(const Params& P, const Ctx& cx, int k
 }
 
 // ------------------------------------------------------------------ chain CTA, warpgroup A (W_cur)
+// Thread a: rows {g, 64+g, 32+g, 96+g} (tanh g, sigmoid g, tanh 32+g, sigmoid 32+g),
+// g = a / 4, columns [16 cc, 16 cc + 16), cc = a % 4.
 template <bool TRACE>
 __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* blk, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
   const int a = threadIdx.x - kAux;  // 0..127 (also the main-thread index k of the sampler)
-  const int wa = a >> 5, l = a & 31;
-  const int row = (l < 16) ? (16 * wa + l) : (R + 16 * wa + (l - 16));  // tanh row or its sigmoid partner
-  const int hi = 16 * wa + (l & 15);
+  const int g = a >> 2, cc = a & 3;
+  const int hrow = g + ((cc & 2) ? 32 : 0);  // h index this lane finishes (tanh row; sigmoid = +64)
+  const bool writer = (cc & 1) == 0;
   const int first = pl.chain_first[c], nl = pl.chain_nl[c];
 
   float wc[LPC][64];
@@ -277,24 +290,26 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* blk,
         const int j = first + jl;
         if (jl > 0) ptx::bar_sync(kBarX, kMain);  // x^(j-1) from B
         if (a == 0) trace_clk<TRACE>(A, n, 8 + 2 * jl);
-        // a = W_cur x + (W_prev x_{n-d} + B + L); one row per thread
-        const float av = dotK<64>(wc[jl], m.xs[jl]) + m.pre[jl][row];
-        const float partner = __shfl_xor_sync(0xffffffffu, av, 16);
-        float hv = 0.0f;
-        if (l < 16) {
-          hv = gate_fast(av, partner);  // tanh row in av, sigmoid row in partner
-          m.hs[jl][hpad(hi)] = hv;
-        }
+        const float ph = m.pre[jl][hrow], pg = m.pre[jl][R + hrow];
+        // a_cur = W_cur x over this lane's 16 columns for its 4 rows
+        float v[4];
+        tile_dot<4, 16>(wc[jl], &m.xs[jl][20 * cc], v);
+        xpose_level<4>(v, cc, 2);  // lanes cc & 2 now carry (tanh 32+g, sigmoid 32+g)
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
+        // a = a_cur + (W_prev x_{n-d} + B + L); h = tanh(a_h) sigma(a_g)
+        const float hv = gate_fast(v[0] + ph, v[1] + pg);
+        if (writer) m.hs[jl][pad16(hrow)] = hv;
         bar_arrive(kBarH, kMain);
         if (a == 0) trace_clk<TRACE>(A, n, 9 + 2 * jl);
-        if (l < 16) {  // h^(j) to its skip CTA, or h^(l) to the four heads (off the chain)
+        if (writer) {  // h^(j) to its skip CTA, or h^(l) to the four heads (off the chain)
           if (j == pl.L - 1) {
 #pragma unroll
             for (int hh = 0; hh < NH; ++hh)
-              ptx::st_async(remote(&m.hbuf[0][hpad(hi)], pl.nc + hh), hv, remote(&m.bar_h[0], pl.nc + hh));
+              ptx::st_async(remote(&m.hbuf[0][pad16(hrow)], pl.nc + hh), hv, remote(&m.bar_h[0], pl.nc + hh));
           } else {
             const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
-            ptx::st_async(remote(&m.hbuf[sl][hpad(hi)], kk), hv, remote(&m.bar_h[sl], kk));
+            ptx::st_async(remote(&m.hbuf[sl][pad16(hrow)], kk), hv, remote(&m.bar_h[sl], kk));
           }
         }
       }
@@ -304,6 +319,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* blk,
 }
 
 // ------------------------------------------------------------------ chain CTA, warpgroup B (W_res)
+// Thread b: rows {g, 32+g}, g = b / 4, columns [16 cc, 16 cc + 16), cc = b % 4.
 template <bool TRACE>
 __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* blk, const float* sw) {
   const RunArgs& A = P.a;
@@ -311,7 +327,9 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* blk,
   Mail& m = *cx.mail;
   const int b = threadIdx.x - kAux - 128;  // 0..127
   const int k = threadIdx.x - kAux;        // main-thread index of the sampler (128..255)
-  const int row = b >> 1, half = b & 1;
+  const int g = b >> 2, cc = b & 3;
+  const int row = g + ((cc & 2) ? 32 : 0);  // row of x this lane finishes
+  const bool writer = (cc & 1) == 0;
   const int first = pl.chain_first[c], nl = pl.chain_nl[c];
   const bool last_cta = (c == pl.nc - 1);
   float wr[LPC][32];
@@ -331,16 +349,19 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* blk,
       if (jl < nl) {
         const int j = first + jl;
         ptx::bar_sync(kBarH, kMain);  // h^(j) from A (implies xs[jl] is valid)
-        const float xi = m.xs[jl][row];
-        if (jl == 0 && half == 0) m.xsave0[row] = xi;
+        const float xi = m.xs[jl][pad16(row)];
+        if (jl == 0 && writer) m.xsave0[row] = xi;
         if (j < pl.L - 1) {
           // x^(j) = x^(j-1) + W_res h + B_res
-          float rr = dotK<32>(wr[jl], &m.hs[jl][36 * half]);
-          rr += __shfl_xor_sync(0xffffffffu, rr, 1);
-          const float xn = xi + (rr + bres[jl * R + row]);
-          if (half == 0) {
-            if (jl + 1 < nl) m.xs[jl + 1][row] = xn;
-            else if (!last_cta) ptx::st_async(remote(&m.xs[0][row], c + 1), xn, remote(&m.bar_xin, c + 1));
+          float v[2];
+          tile_dot<2, 16>(wr[jl], &m.hs[jl][20 * cc], v);
+          xpose_level<2>(v, cc, 2);
+          v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+          const float xn = xi + (v[0] + bres[jl * R + row]);
+          if (writer) {
+            if (jl + 1 < nl) m.xs[jl + 1][pad16(row)] = xn;
+            else if (!last_cta)
+              ptx::st_async(remote(&m.xs[0][pad16(row)], c + 1), xn, remote(&m.bar_xin, c + 1));
           }
           if (jl + 1 < nl) bar_arrive(kBarX, kMain);
         }
@@ -378,7 +399,7 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       const float lv = __ldg(A.cond + (f * L + j) * 2 * R + at);
       if (at < R) {
         float* ring = A.ring + A.ring_off[j];
-        const float xc = (jl == 0) ? m.xsave0[at] : m.xs[jl][at];  // x^(j-1)_{n-1}
+        const float xc = (jl == 0) ? m.xsave0[at] : m.xs[jl][pad16(at)];  // x^(j-1)_{n-1}
         float xpv = 0.0f;
         if (n - d >= 0) xpv = (d == 1) ? xc : ring[(int64_t)(n % d) * R + at];  // slot of n-d
         if (n > 0 && d >= 2) ring[(int64_t)((n - 1) % d) * R + at] = xc;
@@ -406,24 +427,34 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
 }
 
 // ------------------------------------------------------------------ head CTA (rows [64h, 64h+64))
+// Thread k (0..255):
+//   q   : rows {g + 64 m} (m < S/64), columns [16 cc, +16) of W_skip^(l); g = k/4, cc = k%4
+//   z_a : rows 64h + 4 (k/16) + m (m < 4), columns [(k%16) S/16, +S/16) of W_relu
+//   out : rows 64h + 4 (k/16) + m (m < 4), columns [16 (k%16), +16) of W_out
 template <int S, bool TRACE>
 __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float* blk, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
   const int k = threadIdx.x - kAux;  // 0..255
-  constexpr int QS = S / 4;          // columns of W_relu per thread (4 chunks)
-  float wsk[64], wrl[QS], wo[64];
+  constexpr int RQ = S / 64;         // q rows per thread
+  constexpr int CZ = S / 16;         // z_s columns per thread
+  float wsk[RQ * 16], wrl[4 * CZ], wo[64];
 #pragma unroll
-  for (int q = 0; q < 64; ++q) wsk[q] = blk[q * kMain + k];
+  for (int q = 0; q < RQ * 16; ++q) wsk[q] = blk[q * kMain + k];
 #pragma unroll
-  for (int q = 0; q < QS; ++q) wrl[q] = blk[(64 + q) * kMain + k];
+  for (int q = 0; q < 4 * CZ; ++q) wrl[q] = blk[(RQ * 16 + q) * kMain + k];
 #pragma unroll
-  for (int q = 0; q < 64; ++q) wo[q] = blk[(64 + QS + q) * kMain + k];
+  for (int q = 0; q < 64; ++q) wo[q] = blk[(RQ * 16 + 4 * CZ + q) * kMain + k];
   const float* bskip = sw;          // [S]
   const float* brelu = sw + S;      // [64]
   const float* bout = sw + S + 64;  // [64]
-  const int row = k >> 2, ch = k & 3;
+  const int g = k >> 2, cc = k & 3;
+  const int qrow = g + 64 * ((RQ == 4) ? cc : (cc >> 1));  // q row this lane finishes
+  const bool qwriter = (RQ == 4) || ((cc & 1) == 0);
+  const int c16 = k & 15;
+  const int orow = 4 * (k >> 4) + ((k >> 2) & 3);  // z_a / logits row (within the head) this lane finishes
+  const bool owriter = (k & 3) == 0;
   const int nk = pl.nk;
 
   for (int64_t n = 0; n < A.N; ++n) {
@@ -431,60 +462,86 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     if (wait(cx, &m.bar_h[0], par, 21) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[0]), R * 4);
     if (k == 0) trace<TRACE>(A, n, 0);
     // q = B_skip + sum_k partial_k + W_skip^(l) h^(l); z_s = relu(q)
-    const float dot = (k < S) ? dot_h64(wsk, m.hbuf[0]) : 0.0f;
+    float v[RQ];
+    tile_dot<RQ, 16>(wsk, &m.hbuf[0][20 * cc], v);
+    xpose_level<RQ>(v, cc, 2);
+    if constexpr (RQ == 4) {
+      xpose_level<2>(*reinterpret_cast<float(*)[2]>(v), cc, 1);
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    }
     if (nk > 0) {
       if (wait(cx, &m.bar_part, par, 22) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_part), nk * S * 4);
     }
     if (k == 0) trace<TRACE>(A, n, 1);
-    if (k < S) {
-      float qv = bskip[k];
-      for (int kk = 0; kk < nk; ++kk) qv += m.part[kk][k];
-      qv += dot;
-      m.zs[cpad<QS>(k)] = fmaxf(qv, 0.0f);
+    if (qwriter) {
+      float qv = bskip[qrow];
+      for (int kk = 0; kk < nk; ++kk) qv += m.part[kk][qrow];
+      qv += v[0];
+      m.zs[cpad<CZ>(qrow)] = fmaxf(qv, 0.0f);
     }
     ptx::bar_sync(kBarMain, kMain);
-    // z_a = relu(W_relu z_s + B_relu), rows 64h + row
-    float za = dotK<QS>(wrl, &m.zs[ch * (QS + 4)]);
-    za += __shfl_xor_sync(0xffffffffu, za, 1);
-    za += __shfl_xor_sync(0xffffffffu, za, 2);
-    za = fmaxf(za + brelu[row], 0.0f);
-    if (ch == 0) {
-      const int dst = cpad<64>(64 * hidx + row);
+    // z_a = relu(W_relu z_s + B_relu)
+    float za[4];
+    tile_dot<4, CZ>(wrl, &m.zs[(CZ + 4) * c16], za);
+    xpose_level<4>(za, k, 8);
+    xpose_level<2>(*reinterpret_cast<float(*)[2]>(za), k, 4);
+    za[0] += __shfl_xor_sync(0xffffffffu, za[0], 2);
+    za[0] += __shfl_xor_sync(0xffffffffu, za[0], 1);
+    const float zav = fmaxf(za[0] + brelu[orow], 0.0f);
+    if (owriter) {
+      const int dst = pad16(64 * hidx + orow);
 #pragma unroll
       for (int hh = 0; hh < NH; ++hh)
-        ptx::st_async(remote(&m.za_in[dst], pl.nc + hh), za, remote(&m.bar_za, pl.nc + hh));
+        ptx::st_async(remote(&m.za_in[dst], pl.nc + hh), zav, remote(&m.bar_za, pl.nc + hh));
     }
     if (wait(cx, &m.bar_za, par, 23) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_za), kLevels * 4);
     if (k == 0) trace<TRACE>(A, n, 2);
-    // logits = W_out z_a + B_out, rows 64h + row
-    float lg = dotK<64>(wo, &m.za_in[ch * 68]);
-    lg += __shfl_xor_sync(0xffffffffu, lg, 1);
-    lg += __shfl_xor_sync(0xffffffffu, lg, 2);
-    lg += bout[row];
-    if (ch == 0) ptx::st_async(remote(&m.logits_in[64 * hidx + row], 0), lg, remote(&m.bar_logits, 0));
+    // logits = W_out z_a + B_out
+    float lg[4];
+    tile_dot<4, 16>(wo, &m.za_in[20 * c16], lg);
+    xpose_level<4>(lg, k, 8);
+    xpose_level<2>(*reinterpret_cast<float(*)[2]>(lg), k, 4);
+    lg[0] += __shfl_xor_sync(0xffffffffu, lg[0], 2);
+    lg[0] += __shfl_xor_sync(0xffffffffu, lg[0], 1);
+    if (owriter)
+      ptx::st_async(remote(&m.logits_in[64 * hidx + orow], 0), lg[0] + bout[orow], remote(&m.bar_logits, 0));
     if (k == 0) trace<TRACE>(A, n, 3);
   }
 }
 
 // ------------------------------------------------------------------ skip CTA
 // partial_k = sum over owned layers j (ascending) of W_skip^(j) h^(j).
+// Thread t: rows {g + 64 m} (m < S/64), columns [16 cc, +16); g = t/4, cc = t%4.
 template <int S, bool TRACE>
 __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* blk, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
-  const int t = threadIdx.x - kAux;     // 0..255
-  constexpr int QS = S / 4;             // registers per layer per thread
-  constexpr int MAXREG = 192 / QS;      // 3 (s=256) or 6 (s=128)
-  constexpr int LSTRIDE = (S == 256) ? 64 * 256 : 2 * (32 * 128 + 16);  // floats per smem layer
+  const int t = threadIdx.x - kAux;  // 0..255
+  constexpr int RQ = S / 64;
+  constexpr int QS = RQ * 16;        // registers per layer per thread
+  constexpr int MAXREG = 192 / QS;   // 3 (s=256) or 6 (s=128)
+  constexpr int LSTRIDE = QS * kMain;  // floats per shared-memory layer ([q/4][t][4])
   const int nown = pl.skip_n[k], nsm = pl.skip_nsm[k], nreg = nown - nsm;
   float w[MAXREG][QS];
 #pragma unroll
   for (int rl = 0; rl < MAXREG; ++rl)
 #pragma unroll
     for (int q = 0; q < QS; ++q) w[rl][q] = (rl < nreg) ? blk[(rl * QS + q) * kMain + t] : 0.0f;
-  const int row = (S == 256) ? t : (t >> 1);
-  const int half = (S == 256) ? 0 : (t & 1);
+  const int g = t >> 2, cc = t & 3;
+  const int row = g + 64 * ((RQ == 4) ? cc : (cc >> 1));
+  const bool writer = (RQ == 4) || ((cc & 1) == 0);
+
+  auto finish = [&](float (&v)[RQ]) -> float {
+    xpose_level<RQ>(v, cc, 2);
+    if constexpr (RQ == 4) {
+      xpose_level<2>(*reinterpret_cast<float(*)[2]>(v), cc, 1);
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    }
+    return v[0];
+  };
 
   for (int64_t n = 0; n < A.N; ++n) {
     const uint32_t par = (uint32_t)(n & 1);
@@ -493,47 +550,27 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* bl
     for (int sl = 0; sl < nsm; ++sl) {
       if (wait(cx, &m.bar_h[sl], par, 31) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
       const float* ws = sw + sl * LSTRIDE;
-      float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
-      if constexpr (S == 256) {
-#pragma unroll 4
-        for (int q = 0; q < 64; q += 4) {
-          const float4 x = lds4(&m.hbuf[sl][q + ((q >> 5) << 2)]);
-          d0 = fmaf(ws[q * 256 + row], x.x, d0);
-          d1 = fmaf(ws[(q + 1) * 256 + row], x.y, d1);
-          d2 = fmaf(ws[(q + 2) * 256 + row], x.z, d2);
-          d3 = fmaf(ws[(q + 3) * 256 + row], x.w, d3);
-        }
-      } else {
-        const float* wh = ws + half * (32 * 128 + 16);
-#pragma unroll 4
-        for (int q = 0; q < 32; q += 4) {
-          const float4 x = lds4(&m.hbuf[sl][36 * half + q]);
-          d0 = fmaf(wh[q * 128 + row], x.x, d0);
-          d1 = fmaf(wh[(q + 1) * 128 + row], x.y, d1);
-          d2 = fmaf(wh[(q + 2) * 128 + row], x.z, d2);
-          d3 = fmaf(wh[(q + 3) * 128 + row], x.w, d3);
-        }
+      float wl[QS];
+#pragma unroll
+      for (int q = 0; q < QS; q += 4) {
+        const float4 x = lds4(ws + (q / 4 * kMain + t) * 4);
+        wl[q] = x.x; wl[q + 1] = x.y; wl[q + 2] = x.z; wl[q + 3] = x.w;
       }
-      float dot = (d0 + d1) + (d2 + d3);
-      if (S == 128) dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-      part += dot;
+      float v[RQ];
+      tile_dot<RQ, 16>(wl, &m.hbuf[sl][20 * cc], v);
+      part += finish(v);
     }
 #pragma unroll
     for (int rl = 0; rl < MAXREG; ++rl) {
       if (rl < nreg) {
         const int sl = nsm + rl;
         if (wait(cx, &m.bar_h[sl], par, 32) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
-        float dot;
-        if constexpr (S == 256) {
-          dot = dot_h64(w[rl], m.hbuf[sl]);
-        } else {
-          dot = dotK<32>(w[rl], &m.hbuf[sl][36 * half]);
-          dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-        }
-        part += dot;
+        float v[RQ];
+        tile_dot<RQ, 16>(w[rl], &m.hbuf[sl][20 * cc], v);
+        part += finish(v);
       }
     }
-    if (half == 0) m.zs[row] = part;
+    if (writer) m.zs[row] = part;
     if (t == 0) trace<TRACE>(A, n, 1);
     ptx::bar_sync(kBarMain, kMain);
     if (t < (S / 4) * NH) {
@@ -670,8 +707,8 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
   }
   p.nh = NH;
   const int nskip = L - 1;  // W_skip^(l) lives in the head CTAs
-  const int qs = s / 4, maxreg = 192 / qs;
-  const int lstride = (s == 256) ? 64 * 256 : 2 * (32 * 128 + 16);
+  const int qs = s / 4, maxreg = 192 / qs;  // registers per skip layer per thread
+  const int lstride = qs * kMain;            // floats per shared-memory skip layer
   const int maxsm = std::min(kCMaxSlot - maxreg, (int)((190 * 1024) / (lstride * 4)));
   const int cap = maxreg + maxsm;
   p.nk = nskip > 0 ? (nskip + cap - 1) / cap : 0;
@@ -694,7 +731,7 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
     int64_t regfloats = 0;
     int swf = 0;
     if (rank < p.nc) { regfloats = (int64_t)(LPC * 64 + LPC * 32) * 128; swf = smem_chain(rank); }
-    else if (rank < p.nc + p.nh) { regfloats = (int64_t)(64 + qs + 64) * kMain; swf = s + 128; }
+    else if (rank < p.nc + p.nh) { regfloats = (int64_t)(s / 4 + s / 4 + 64) * kMain; swf = s + 128; }
     else { const int k = rank - p.nc - p.nh; regfloats = (int64_t)(p.skip_n[k] - p.skip_nsm[k]) * qs * kMain; swf = p.skip_nsm[k] * lstride; }
     p.pk_off[rank] = off;
     off += regfloats;
@@ -740,13 +777,17 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
     if (rank < p.nc) {
       const int first = p.chain_first[rank], nl = p.chain_nl[rank];
       for (int a = 0; a < 128; ++a) {
-        const int wa = a >> 5, l = a & 31;
-        const int row = (l < 16) ? (16 * wa + l) : (R + 16 * wa + (l - 16));
-        const int brow = a >> 1, half = a & 1;
+        const int g = a >> 2, cc = a & 3;
+        const int arow[4] = {g, R + g, 32 + g, R + 32 + g};  // tanh g, sigmoid g, tanh 32+g, sigmoid 32+g
+        const int brow[2] = {g, 32 + g};
         for (int jl = 0; jl < nl; ++jl) {
           const int j = first + jl;
-          for (int q = 0; q < 64; ++q) blk[(jl * 64 + q) * 128 + a] = W(j, o.w_cur, row, q, R);
-          for (int q = 0; q < 32; ++q) blk[(LPC * 64 + jl * 32 + q) * 128 + a] = W(j, o.w_res, brow, 32 * half + q, R);
+          for (int mm = 0; mm < 4; ++mm)
+            for (int q = 0; q < 16; ++q)
+              blk[(jl * 64 + mm * 16 + q) * 128 + a] = W(j, o.w_cur, arow[mm], 16 * cc + q, R);
+          for (int mm = 0; mm < 2; ++mm)
+            for (int q = 0; q < 16; ++q)
+              blk[(LPC * 64 + jl * 32 + mm * 16 + q) * 128 + a] = W(j, o.w_res, brow[mm], 16 * cc + q, R);
         }
       }
       for (int jl = 0; jl < nl; ++jl) {
@@ -766,13 +807,18 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
     } else if (rank < p.nc + p.nh) {
       const int hidx = rank - p.nc;
       const int jl = p.L - 1;
+      const int rq = s / 64, cz = s / 16;
       for (int k = 0; k < kMain; ++k) {
-        const int row = k >> 2, ch = k & 3;
-        for (int q = 0; q < 64; ++q) blk[q * kMain + k] = (k < s) ? W(jl, o.w_skip, k, q, R) : 0.0f;
-        for (int q = 0; q < qs; ++q)
-          blk[(64 + q) * kMain + k] = w[o.w_relu + (int64_t)(64 * hidx + row) * s + ch * qs + q];
-        for (int q = 0; q < 64; ++q)
-          blk[(64 + qs + q) * kMain + k] = w[o.w_out + (int64_t)(64 * hidx + row) * kLevels + ch * 64 + q];
+        const int g = k >> 2, cc = k & 3, c16 = k & 15, rbase = 64 * hidx + 4 * (k >> 4);
+        for (int mm = 0; mm < rq; ++mm)
+          for (int q = 0; q < 16; ++q) blk[(mm * 16 + q) * kMain + k] = W(jl, o.w_skip, g + 64 * mm, 16 * cc + q, R);
+        for (int mm = 0; mm < 4; ++mm)
+          for (int q = 0; q < cz; ++q)
+            blk[(rq * 16 + mm * cz + q) * kMain + k] = w[o.w_relu + (int64_t)(rbase + mm) * s + c16 * cz + q];
+        for (int mm = 0; mm < 4; ++mm)
+          for (int q = 0; q < 16; ++q)
+            blk[(rq * 16 + 4 * cz + mm * 16 + q) * kMain + k] =
+                w[o.w_out + (int64_t)(rbase + mm) * kLevels + 16 * c16 + q];
       }
       for (int i = 0; i < s; ++i) sm[i] = w[o.b_skip + i];
       for (int i = 0; i < 64; ++i) {
@@ -785,22 +831,17 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
       for (int j = 0; j < p.L - 1; ++j)
         if (p.layer_skip_cta[j] == rank) layers.push_back(j);
       const int nsm = p.skip_nsm[k];
-      const int lstride = (s == 256) ? 64 * 256 : 2 * (32 * 128 + 16);
+      const int rq = s / 64, lstride = qs * kMain;
       for (int sl = 0; sl < (int)layers.size(); ++sl) {
         const int j = layers[sl];
-        if (sl < nsm) {
-          float* ws = sm + sl * lstride;
-          for (int i = 0; i < s; ++i)
-            for (int c = 0; c < R; ++c) {
-              if (s == 256) ws[c * 256 + i] = W(j, o.w_skip, i, c, R);
-              else ws[(c >> 5) * (32 * 128 + 16) + (c & 31) * 128 + i] = W(j, o.w_skip, i, c, R);
-            }
-        } else {
-          const int rl = sl - nsm;
-          for (int t = 0; t < kMain; ++t)
-            for (int q = 0; q < qs; ++q) {
-              if (s == 256) blk[(rl * qs + q) * kMain + t] = W(j, o.w_skip, t, q, R);
-              else blk[(rl * qs + q) * kMain + t] = W(j, o.w_skip, t >> 1, 32 * (t & 1) + q, R);
+        for (int t = 0; t < kMain; ++t) {
+          const int g = t >> 2, cc = t & 3;
+          for (int mm = 0; mm < rq; ++mm)
+            for (int q = 0; q < 16; ++q) {
+              const float v = W(j, o.w_skip, g + 64 * mm, 16 * cc + q, R);
+              const int qq = mm * 16 + q;
+              if (sl < nsm) sm[sl * lstride + ((qq / 4) * kMain + t) * 4 + (qq % 4)] = v;
+              else blk[((sl - nsm) * qs + qq) * kMain + t] = v;
             }
         }
       }
