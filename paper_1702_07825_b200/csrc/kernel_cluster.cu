@@ -202,53 +202,101 @@ __device__ __forceinline__ void xpose_level(float (&v)[N], int lane, int bit) {
 }
 
 // ------------------------------------------------------------------ chain CTA 0: sample + embed
-// Draw y_{n-1} from the inbound logits (App. A.4) and write x^(0)_n into xs[0] (step 1).
-// Runs on the 256 main threads (k = 0..255) of both warpgroups.
+// Inverse-CDF direct sampling (reading R11) by ONE warp, 8 logits per
+// lane, no block barriers: m = max l; e_k = exp(l_k - m) (fp32); P_k = fp64 running
+// sums (lane-sequential, then an fp64 warp scan of the lane totals; P is
+// non-decreasing); y = #{k : P_k <= u * P_255}; fallback the largest k with e_k > 0.
+__device__ __forceinline__ int sample_warp(const float* logits, float u, int lane) {
+  float l[8];
+  {
+    const float4 a = lds4(logits + 8 * lane), b = lds4(logits + 8 * lane + 4);
+    l[0] = a.x; l[1] = a.y; l[2] = a.z; l[3] = a.w; l[4] = b.x; l[5] = b.y; l[6] = b.z; l[7] = b.w;
+  }
+  float mx = fmaxf(fmaxf(fmaxf(l[0], l[1]), fmaxf(l[2], l[3])), fmaxf(fmaxf(l[4], l[5]), fmaxf(l[6], l[7])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float e[8];
+  double p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) e[i] = expf(l[i] - mx);
+  p[0] = (double)e[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) p[i] = p[i - 1] + (double)e[i];
+  double incl = p[7];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const double base = incl - p[7];  // exclusive prefix of the lane totals
+  const double S = __shfl_sync(0xffffffffu, incl, 31);
+  const double thr = (double)u * S;
+  int cnt = 0, lastpos = -1;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    cnt += (base + p[i] <= thr) ? 1 : 0;
+    if (e[i] > 0.0f) lastpos = 8 * lane + i;
+  }
+  const int y = __reduce_add_sync(0xffffffffu, cnt);
+  return y < kLevels ? y : __reduce_max_sync(0xffffffffu, (unsigned)(lastpos + 1)) - 1;
+}
+
+// Draw y_{n-1} from the inbound logits (App. A.4) and write x^(0)_n (step 1) into xs[0]
+// with the first warp of warpgroup A; everyone else waits at the closing barrier.
 template <bool TRACE>
 __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx, int64_t n, int k, int& y1,
                                                  int& y2, const float* wembc, const float* bemb) {
   const RunArgs& A = P.a;
   Mail& m = *cx.mail;
-  const float* embp_g = P.pk + P.p.embp_off;  // W_emb_prev^T [256][R] in global memory
-  float ep = 0.0f;
-  if (n > 0) {
-    const float u = A.uniforms ? __ldg(A.uniforms + n - 1) : 0.0f;
-    const int yf = A.forced ? (int)__ldg(A.forced + n - 1) : 0;
-    if (k < R) ep = __ldg(embp_g + y1 * R + k);  // W_emb_prev[:, y_{n-2}] (= y1 before the update)
-    if (wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11) && k == 0)
-      ptx::mbar_arm(ptx::smem_u32(&m.bar_logits), kLevels * 4);
-    if (k == 0) trace<TRACE>(A, n - 1, 3);
-    const float l = m.logits_in[k];
-    int y;
-    if (A.forced) {
-      A.out_logits[(n - 1) * kLevels + k] = l;
-      y = yf;
+  if (k < 32) {
+    const float* embp_g = P.pk + P.p.embp_off;  // W_emb_prev^T [256][R] in global memory
+    float ep0, ep1;
+    if (n > 0) {
+      const float u = A.uniforms ? __ldg(A.uniforms + n - 1) : 0.0f;
+      const int yf = A.forced ? (int)__ldg(A.forced + n - 1) : 0;
+      ep0 = __ldg(embp_g + y1 * R + k);  // W_emb_prev[:, y_{n-2}] (= y1 before the update)
+      ep1 = __ldg(embp_g + y1 * R + k + 32);
+      if (wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11) && k == 0)
+        ptx::mbar_arm(ptx::smem_u32(&m.bar_logits), kLevels * 4);
+      if (k == 0) trace<TRACE>(A, n - 1, 3);
+      int y;
+      if (A.forced) {
+        float4* o = reinterpret_cast<float4*>(A.out_logits + (n - 1) * kLevels) + 2 * k;
+        o[0] = lds4(m.logits_in + 8 * k);
+        o[1] = lds4(m.logits_in + 8 * k + 4);
+        y = yf;
+      } else {
+        y = sample_warp(m.logits_in, u, k);
+        if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
+      }
+      if (k == 0) trace<TRACE>(A, n, 20);
+      y2 = y1;
+      y1 = y;
     } else {
-      y = sample_256(l, u, m.dscr, m.fscr, m.iscr, k, kBarMain);
-      if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
+      ep0 = __ldg(embp_g + y2 * R + k);
+      ep1 = __ldg(embp_g + y2 * R + k + 32);
     }
-    y2 = y1;
-    y1 = y;
-  } else {
-    if (k < R) ep = __ldg(embp_g + y2 * R + k);
+    // x^(0)_n = W_emb_prev[:, y_{n-2}] + W_emb_cur[:, y_{n-1}] + B_emb
+    m.xs[0][pad16(k)] = (ep0 + wembc[y1 * R + k]) + bemb[k];
+    m.xs[0][pad16(k + 32)] = (ep1 + wembc[y1 * R + k + 32]) + bemb[k + 32];
   }
-  // x^(0)_n = W_emb_prev[:, y_{n-2}] + W_emb_cur[:, y_{n-1}] + B_emb
-  if (k < R) m.xs[0][pad16(k)] = (ep + wembc[y1 * R + k]) + bemb[k];
   ptx::bar_sync(kBarMain, kMain);
 }
 
-// The final draw (sample N-1) after the last layer pass; all 256 main threads.
+// The final draw (sample N-1) after the last layer pass (first warp of A).
 __device__ __forceinline__ void final_draw(const Params& P, const Ctx& cx, int k) {
   const RunArgs& A = P.a;
   Mail& m = *cx.mail;
+  if (k >= 32) return;
   const int64_t n = A.N;
   const float u = A.uniforms ? __ldg(A.uniforms + n - 1) : 0.0f;
   wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11);
-  const float lg = m.logits_in[k];
   if (A.forced) {
-    A.out_logits[(n - 1) * kLevels + k] = lg;
+    float4* o = reinterpret_cast<float4*>(A.out_logits + (n - 1) * kLevels) + 2 * k;
+    o[0] = lds4(m.logits_in + 8 * k);
+    o[1] = lds4(m.logits_in + 8 * k + 4);
   } else {
-    const int y = sample_256(lg, u, m.dscr, m.fscr, m.iscr, k, kBarMain);
+    const int y = sample_warp(m.logits_in, u, k);
     if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
   }
 }
@@ -303,10 +351,11 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* blk,
         bar_arrive(kBarH, kMain);
         if (a == 0) trace_clk<TRACE>(A, n, 9 + 2 * jl);
         if (writer) {  // h^(j) to its skip CTA, or h^(l) to the four heads (off the chain)
-          if (j == pl.L - 1) {
+          if (j >= pl.L - 2) {  // the last two layers' W_skip live in the heads (slot 0: l, slot 1: l-1)
+            const int sl = pl.L - 1 - j;
 #pragma unroll
             for (int hh = 0; hh < NH; ++hh)
-              ptx::st_async(remote(&m.hbuf[0][pad16(hrow)], pl.nc + hh), hv, remote(&m.bar_h[0], pl.nc + hh));
+              ptx::st_async(remote(&m.hbuf[sl][pad16(hrow)], pl.nc + hh), hv, remote(&m.bar_h[sl], pl.nc + hh));
           } else {
             const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
             ptx::st_async(remote(&m.hbuf[sl][pad16(hrow)], kk), hv, remote(&m.bar_h[sl], kk));
@@ -449,6 +498,8 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
   const float* bskip = sw;          // [S]
   const float* brelu = sw + S;      // [64]
   const float* bout = sw + S + 64;  // [64]
+  const float* wsk2 = sw + S + 128; // W_skip^(l-1) in shared memory, [q/4][k][4]
+  const bool has2 = pl.L >= 2;
   const int g = k >> 2, cc = k & 3;
   const int qrow = g + 64 * ((RQ == 4) ? cc : (cc >> 1));  // q row this lane finishes
   const bool qwriter = (RQ == 4) || ((cc & 1) == 0);
@@ -457,19 +508,39 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
   const bool owriter = (k & 3) == 0;
   const int nk = pl.nk;
 
-  for (int64_t n = 0; n < A.N; ++n) {
-    const uint32_t par = (uint32_t)(n & 1);
-    if (wait(cx, &m.bar_h[0], par, 21) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[0]), R * 4);
-    if (k == 0) trace<TRACE>(A, n, 0);
-    // q = B_skip + sum_k partial_k + W_skip^(l) h^(l); z_s = relu(q)
-    float v[RQ];
-    tile_dot<RQ, 16>(wsk, &m.hbuf[0][20 * cc], v);
+  auto finish = [&](float (&v)[RQ]) -> float {
     xpose_level<RQ>(v, cc, 2);
     if constexpr (RQ == 4) {
       xpose_level<2>(*reinterpret_cast<float(*)[2]>(v), cc, 1);
     } else {
       v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
     }
+    return v[0];
+  };
+
+  for (int64_t n = 0; n < A.N; ++n) {
+    const uint32_t par = (uint32_t)(n & 1);
+    // q = B_skip + sum_k partial_k + W_skip^(l-1) h^(l-1) + W_skip^(l) h^(l); z_s = relu(q)
+    // (PAPER.md:365-372).  W_skip^(l-1) is applied here, from shared memory, while the
+    // last layer runs, so no skip CTA sits between the chain and the head.
+    float d2 = 0.0f;
+    if (has2) {
+      if (wait(cx, &m.bar_h[1], par, 24) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[1]), R * 4);
+      float wl[RQ * 16];
+#pragma unroll
+      for (int q = 0; q < RQ * 16; q += 4) {
+        const float4 x = lds4(wsk2 + (q / 4 * kMain + k) * 4);
+        wl[q] = x.x; wl[q + 1] = x.y; wl[q + 2] = x.z; wl[q + 3] = x.w;
+      }
+      float v2[RQ];
+      tile_dot<RQ, 16>(wl, &m.hbuf[1][20 * cc], v2);
+      d2 = finish(v2);
+    }
+    if (wait(cx, &m.bar_h[0], par, 21) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[0]), R * 4);
+    if (k == 0) trace<TRACE>(A, n, 0);
+    float v[RQ];
+    tile_dot<RQ, 16>(wsk, &m.hbuf[0][20 * cc], v);
+    v[0] = finish(v);
     if (nk > 0) {
       if (wait(cx, &m.bar_part, par, 22) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_part), nk * S * 4);
     }
@@ -477,6 +548,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     if (qwriter) {
       float qv = bskip[qrow];
       for (int kk = 0; kk < nk; ++kk) qv += m.part[kk][qrow];
+      qv += d2;
       qv += v[0];
       m.zs[cpad<CZ>(qrow)] = fmaxf(qv, 0.0f);
     }
@@ -549,6 +621,7 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* bl
 #pragma unroll 1
     for (int sl = 0; sl < nsm; ++sl) {
       if (wait(cx, &m.bar_h[sl], par, 31) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
+      if (t == 0) trace<TRACE>(A, n, 8 + sl);
       const float* ws = sw + sl * LSTRIDE;
       float wl[QS];
 #pragma unroll
@@ -565,9 +638,11 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* bl
       if (rl < nreg) {
         const int sl = nsm + rl;
         if (wait(cx, &m.bar_h[sl], par, 32) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
+        if (t == 0) trace<TRACE>(A, n, 8 + sl);
         float v[RQ];
         tile_dot<RQ, 16>(w[rl], &m.hbuf[sl][20 * cc], v);
         part += finish(v);
+        if (t == 0) trace<TRACE>(A, n, 20 + sl);
       }
     }
     if (writer) m.zs[row] = part;
@@ -706,7 +781,7 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
     p.chain_nl[c] = std::min(LPC, L - c * LPC);
   }
   p.nh = NH;
-  const int nskip = L - 1;  // W_skip^(l) lives in the head CTAs
+  const int nskip = std::max(0, L - 2);  // W_skip^(l) and W_skip^(l-1) live in the head CTAs
   const int qs = s / 4, maxreg = 192 / qs;  // registers per skip layer per thread
   const int lstride = qs * kMain;            // floats per shared-memory skip layer
   const int maxsm = std::min(kCMaxSlot - maxreg, (int)((190 * 1024) / (lstride * 4)));
@@ -731,7 +806,7 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
     int64_t regfloats = 0;
     int swf = 0;
     if (rank < p.nc) { regfloats = (int64_t)(LPC * 64 + LPC * 32) * 128; swf = smem_chain(rank); }
-    else if (rank < p.nc + p.nh) { regfloats = (int64_t)(s / 4 + s / 4 + 64) * kMain; swf = s + 128; }
+    else if (rank < p.nc + p.nh) { regfloats = (int64_t)(s / 4 + s / 4 + 64) * kMain; swf = s + 128 + (L >= 2 ? qs * kMain : 0); }
     else { const int k = rank - p.nc - p.nh; regfloats = (int64_t)(p.skip_n[k] - p.skip_nsm[k]) * qs * kMain; swf = p.skip_nsm[k] * lstride; }
     p.pk_off[rank] = off;
     off += regfloats;
@@ -825,10 +900,21 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
         sm[s + i] = w[o.b_relu + 64 * hidx + i];
         sm[s + 64 + i] = w[o.b_out + 64 * hidx + i];
       }
+      if (p.L >= 2) {  // W_skip^(l-1), [q/4][k][4]
+        float* w2 = sm + s + 128;
+        for (int k = 0; k < kMain; ++k) {
+          const int g = k >> 2, cc = k & 3;
+          for (int mm = 0; mm < rq; ++mm)
+            for (int q = 0; q < 16; ++q) {
+              const int qq = mm * 16 + q;
+              w2[((qq / 4) * kMain + k) * 4 + (qq % 4)] = W(p.L - 2, o.w_skip, g + 64 * mm, 16 * cc + q, R);
+            }
+        }
+      }
     } else {
       const int k = rank - p.nc - p.nh;
       std::vector<int> layers;
-      for (int j = 0; j < p.L - 1; ++j)
+      for (int j = 0; j < p.L - 2; ++j)
         if (p.layer_skip_cta[j] == rank) layers.push_back(j);
       const int nsm = p.skip_nsm[k];
       const int rq = s / 64, lstride = qs * kMain;
