@@ -6,14 +6,19 @@
 // rest for sm_100a:
 //   * one thread-block cluster; every hand-off is a DSMEM st.async whose
 //     transaction bytes complete on the receiver's mbarrier (no L2 round trip);
-//   * chain CTAs own 3 consecutive layers.  Warpgroup A holds W_cur, warpgroup B
-//     W_res, both as (rows x 16-column chunk) register tiles: each thread reuses
-//     every loaded vector element for 4 (A) or 2 (B) rows, which halves/quarters
-//     the shared-memory -> register traffic that bounds a CUDA-core matvec; the
+//   * chain CTAs own 3 consecutive layers.  Only ONE matvec per layer sits on
+//     the critical path: a_cur^(j+1) = W_cur^(j+1) x^(j) is evaluated as
+//     M^(j) h^(j) + R^(j+1), with M^(j) = W_cur^(j+1) W_res^(j) folded on the host
+//     (fp64, rounded once) and R^(j+1) = W_cur^(j+1) x^(j-1) + W_cur^(j+1) B_res^(j)
+//     computed concurrently by another warpgroup (same linear map as PAPER.md:
+//     354 + 437, different fp32 rounding order).  Warpgroup A runs the chain
+//     (a, gate), B keeps x up to date (x^(j) = x^(j-1) + W_res h + B_res, for the
+//     queues and the next CTA), C computes R.  Each thread holds a (rows x
+//     16-column) tile and reuses every loaded vector element across its rows;
 //     partial sums meet in a transposing shuffle reduction that leaves the tanh
-//     row and its sigmoid partner in one lane for the gate.  A and B
-//     hand h and x to each other through shared memory with producer/consumer
-//     named barriers (bar.arrive / bar.sync);
+//     row and its sigmoid partner in one lane for the gate;
+//   * all per-thread weight tiles live in tensor memory (TMEM, 256 KB per SM) and
+//     are pulled into registers with tcgen05.ld right before use;
 //   * the third warpgroup of a chain CTA does the off-chain work of the coming
 //     sample (Fig. 2's aux threads): dilation-queue read/write in L2,
 //     conditioning fetch, W_prev x_{n+1-d} + B + L from shared memory;
@@ -38,17 +43,26 @@ constexpr int R = 64;       // residual channels the kernel is built for
 constexpr int LPC = 3;      // layers per chain CTA
 constexpr int NH = 4;       // head CTAs (64 output rows each)
 constexpr int kAux = 128;   // threads [0,128): warpgroup X, off-chain work
-constexpr int kMain = 256;  // threads [128,384): warpgroups A and B
-constexpr int kThreads = kAux + kMain;
-constexpr int kMainRegs = 232;
-constexpr int kAuxRegs = 40;  // 128 x (40 + 232 + 232) = 384 x 168, the launch allocation
+constexpr int kMain = 256;  // head / skip math threads: warpgroups A and B, [128,384)
+constexpr int kMath = 384;  // warpgroups A, B, C: [128,512)
+constexpr int kThreads = kAux + kMath;
+constexpr int kTmemCols = 512;
 constexpr uint64_t kTimeoutNs = 2000000000ull;
 
 // named barriers (0 is __syncthreads)
-constexpr int kBarMain = 1;  // A + B, 256 threads
-constexpr int kBarH = 2;     // A arrives (h ready), B syncs
-constexpr int kBarX = 3;     // B arrives (x ready), A syncs
-constexpr int kBarAux = 4;   // X, 128 threads
+constexpr int kBarMath = 1;  // A + B + C, 384 threads (CTA 0 sampler hand-off, teardown)
+constexpr int kBarH = 2;     // chain: A and B sync (h^(j) ready), 256
+constexpr int kBarXR = 3;    // chain: B arrives (x^(j) ready), C syncs, 256
+constexpr int kBarRA = 4;    // chain: C arrives (R ready), A syncs, 256; kBarRA + 3 for the second R
+                             // of the sample (a separate id, so C can never lap A on one barrier)
+constexpr int kBarAux = 5;   // X, 128
+constexpr int kBarHS = 6;    // head / skip: A + B, 256
+constexpr int kBarHX = 8;    // chain: A arrives (h^(j) in hs), X syncs and forwards it, 256;
+                             // one id per local layer (8, 9, 10) so A can never lap X
+
+// chain TMEM columns (per lane): A [0,192) W_cur^(j0), M^(j0), M^(j0+1);
+// C [192,320) W_cur^(j0+1), W_cur^(j0+2); B [320,416) W_res x 3
+constexpr int kColA = 0, kColC = 192, kColB = 320;
 
 enum Role { kChain = 0, kHead = 1, kSkip = 2, kIdle = 3 };
 
@@ -64,7 +78,9 @@ struct __align__(16) Mail {
   uint64_t bar_xin, bar_logits, bar_pre, bar_done, bar_part, bar_za, bar_exit;
   uint64_t bar_h[kCMaxSlot];
   int abort_flag;
+  uint32_t tmem_base;                    // tensor-memory allocation (column 0, lane 0)
   alignas(16) float xs[LPC + 1][kHLen];  // chain: layer inputs (pad16); xs[0] is the inbound x
+  float rr[LPC][2 * R];                  // chain: R^(j) = W_cur^(j) x^(j-2) + W_cur^(j) B_res^(j-1) from C
   float xsave0[R];                       // chain: copy of the inbound x for the aux warpgroup
   float pre[LPC][2 * R];                 // chain: W_prev x_{n-d} + B + L for the coming sample
   float xp[R];                           // chain aux scratch
@@ -242,7 +258,7 @@ __device__ __forceinline__ int sample_warp(const float* logits, float u, int lan
 }
 
 // Draw y_{n-1} from the inbound logits (App. A.4) and write x^(0)_n (step 1) into xs[0]
-// with the first warp of warpgroup A; everyone else waits at the closing barrier.
+// with the first warp of warpgroup A; warpgroups A, B, C wait at the closing barrier.
 template <bool TRACE>
 __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx, int64_t n, int k, int& y1,
                                                  int& y2, const float* wembc, const float* bemb) {
@@ -280,7 +296,7 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
     m.xs[0][pad16(k)] = (ep0 + wembc[y1 * R + k]) + bemb[k];
     m.xs[0][pad16(k + 32)] = (ep1 + wembc[y1 * R + k + 32]) + bemb[k + 32];
   }
-  ptx::bar_sync(kBarMain, kMain);
+  ptx::bar_sync(kBarMath, kMath);
 }
 
 // The final draw (sample N-1) after the last layer pass (first warp of A).
@@ -301,30 +317,40 @@ __device__ __forceinline__ void final_draw(const Params& P, const Ctx& cx, int k
   }
 }
 
-// ------------------------------------------------------------------ chain CTA, warpgroup A (W_cur)
+// TMEM address of this thread's lane (warp w of a warpgroup owns lanes 32w..32w+31)
+__device__ __forceinline__ uint32_t tmem_lane_addr(const Mail& m) {
+  return m.tmem_base + ((uint32_t)(32 * ((threadIdx.x >> 5) & 3)) << 16);
+}
+
+// Shared-memory image of a chain CTA (floats): W_prev [LPC][R (k)][2R (i)], B [LPC][2R],
+// B_res [LPC][R], c = W_cur^(j+1) B_res^(j) [LPC-1][2R]; CTA 0 adds W_emb_cur^T [256][R], B_emb [R].
+constexpr int kSmB = LPC * R * 2 * R;
+constexpr int kSmBres = kSmB + LPC * 2 * R;
+constexpr int kSmFold = kSmBres + LPC * R;
+constexpr int kSmEmb = kSmFold + (LPC - 1) * 2 * R;
+
+// ------------------------------------------------------------------ chain CTA, warpgroup A (the chain)
 // Thread a: rows {g, 64+g, 32+g, 96+g} (tanh g, sigmoid g, tanh 32+g, sigmoid 32+g),
-// g = a / 4, columns [16 cc, 16 cc + 16), cc = a % 4.
+// g = a / 4, columns [16 cc, 16 cc + 16), cc = a % 4.  Layer jl uses TMEM columns
+// kColA + 64 jl: W_cur^(j0) for jl = 0, M^(j0+jl-1) = W_cur^(j0+jl) W_res^(j0+jl-1) after.
 template <bool TRACE>
-__device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* blk, const float* sw) {
+__device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
-  const int a = threadIdx.x - kAux;  // 0..127 (also the main-thread index k of the sampler)
+  const int a = threadIdx.x - kAux;  // 0..127 (also the sampler's thread index)
   const int g = a >> 2, cc = a & 3;
   const int hrow = g + ((cc & 2) ? 32 : 0);  // h index this lane finishes (tanh row; sigmoid = +64)
   const bool writer = (cc & 1) == 0;
   const int first = pl.chain_first[c], nl = pl.chain_nl[c];
-
-  float wc[LPC][64];
-#pragma unroll
-  for (int jl = 0; jl < LPC; ++jl)
-#pragma unroll
-    for (int q = 0; q < 64; ++q) wc[jl][q] = blk[(jl * 64 + q) * 128 + a];
-  const float* wembc = sw + LPC * R * 2 * R + LPC * 2 * R + LPC * R;  // CTA 0: [256][R]
+  const uint32_t tm = tmem_lane_addr(m) + kColA;
+  const float* wembc = sw + kSmEmb;  // CTA 0: [256][R]
   const float* bemb = wembc + kLevels * R;
   int y1 = kLevels / 2, y2 = kLevels / 2;
+  float w[64];
 
   for (int64_t n = 0; n < A.N; ++n) {
+    ptx::tmem_load_async<64>(tm, w);  // W_cur^(j0), hidden behind the waits
     if (c == 0) {
       sample_and_embed<TRACE>(P, cx, n, a, y1, y2, wembc, bemb);
     } else {
@@ -332,64 +358,61 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* blk,
     }
     if (a == 0) trace<TRACE>(A, n, 0);
     wait(cx, &m.bar_pre, (uint32_t)(n & 1), 13);
+    ptx::tmem_wait_ld<64>(w);
 #pragma unroll
     for (int jl = 0; jl < LPC; ++jl) {
       if (jl < nl) {
         const int j = first + jl;
-        if (jl > 0) ptx::bar_sync(kBarX, kMain);  // x^(j-1) from B
         if (a == 0) trace_clk<TRACE>(A, n, 8 + 2 * jl);
-        const float ph = m.pre[jl][hrow], pg = m.pre[jl][R + hrow];
-        // a_cur = W_cur x over this lane's 16 columns for its 4 rows
+        // layer 0: W_cur^(j0) x_in ; later layers: M^(j-1) h^(j-1) (PAPER.md:354 with 437 folded in)
         float v[4];
-        tile_dot<4, 16>(wc[jl], &m.xs[jl][20 * cc], v);
+        tile_dot<4, 16>(w, jl == 0 ? &m.xs[0][20 * cc] : &m.hs[jl - 1][20 * cc], v);
+        if (jl + 1 < nl) ptx::tmem_load_async<64>(tm + 64 * (jl + 1), w);  // next layer's tile
         xpose_level<4>(v, cc, 2);  // lanes cc & 2 now carry (tanh 32+g, sigmoid 32+g)
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
         v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
-        // a = a_cur + (W_prev x_{n-d} + B + L); h = tanh(a_h) sigma(a_g) (PAPER.md:356-359)
-        const float hv = gate_fast(v[0] + ph, v[1] + pg);
-        if (writer) m.hs[jl][pad16(hrow)] = hv;
-        bar_arrive(kBarH, kMain);
-        if (a == 0) trace_clk<TRACE>(A, n, 9 + 2 * jl);
-        if (writer) {  // h^(j) to its skip CTA, or h^(l) to the four heads (off the chain)
-          if (j >= pl.L - 2) {  // the last two layers' W_skip live in the heads (slot 0: l, slot 1: l-1)
-            const int sl = pl.L - 1 - j;
-#pragma unroll
-            for (int hh = 0; hh < NH; ++hh)
-              ptx::st_async(remote(&m.hbuf[sl][pad16(hrow)], pl.nc + hh), hv, remote(&m.bar_h[sl], pl.nc + hh));
-          } else {
-            const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
-            ptx::st_async(remote(&m.hbuf[sl][pad16(hrow)], kk), hv, remote(&m.bar_h[sl], kk));
-          }
+        if (jl > 0) {
+          ptx::bar_sync(jl == 1 ? kBarRA : kBarRA + 3, kMain);  // R^(j) from C
+          v[0] += m.rr[jl][hrow];
+          v[1] += m.rr[jl][R + hrow];
         }
+        // a = a_cur + (W_prev x_{n-d} + B + L); h = tanh(a_h) sigma(a_g) (PAPER.md:356-359)
+        const float hv = gate_fast(v[0] + m.pre[jl][hrow], v[1] + m.pre[jl][R + hrow]);
+        if (writer) m.hs[jl][pad16(hrow)] = hv;
+        ptx::bar_sync(kBarH, kMain);  // h^(j) complete for A (next layer) and B
+        bar_arrive(kBarHX + jl, kMain);  // ... and for X, which forwards it to the skip / head CTAs
+        if (a == 0) trace_clk<TRACE>(A, n, 9 + 2 * jl);
+        (void)hv;
+        (void)j;
+        if (jl + 1 < nl) ptx::tmem_wait_ld<64>(w);
       }
     }
   }
   if (c == 0 && A.N > 0) final_draw(P, cx, a);
 }
 
-// ------------------------------------------------------------------ chain CTA, warpgroup B (W_res)
-// Thread b: rows {g, 32+g}, g = b / 4, columns [16 cc, 16 cc + 16), cc = b % 4.
+// ------------------------------------------------------------------ chain CTA, warpgroup B (x updates)
+// Thread b: rows {g, 32+g} of W_res, g = b / 4, columns [16 cc, +16), cc = b % 4.
+// x^(j) = x^(j-1) + W_res h^(j) + B_res: for the dilation queues, for
+// C's R^(j+2), and (last layer) for the next chain CTA.
 template <bool TRACE>
-__device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* blk, const float* sw) {
+__device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
   const int b = threadIdx.x - kAux - 128;  // 0..127
-  const int k = threadIdx.x - kAux;        // main-thread index of the sampler (128..255)
+  const int k = threadIdx.x - kAux;        // sampler thread index (>= 128: waits only)
   const int g = b >> 2, cc = b & 3;
   const int row = g + ((cc & 2) ? 32 : 0);  // row of x this lane finishes
   const bool writer = (cc & 1) == 0;
   const int first = pl.chain_first[c], nl = pl.chain_nl[c];
   const bool last_cta = (c == pl.nc - 1);
-  float wr[LPC][32];
-#pragma unroll
-  for (int jl = 0; jl < LPC; ++jl)
-#pragma unroll
-    for (int q = 0; q < 32; ++q) wr[jl][q] = blk[(LPC * 64 + jl * 32 + q) * 128 + b];
-  const float* bres = sw + LPC * R * 2 * R + LPC * 2 * R;  // [LPC][R]
-  const float* wembc = bres + LPC * R;
+  const uint32_t tm = tmem_lane_addr(m) + kColB;
+  const float* bres = sw + kSmBres;  // [LPC][R]
+  const float* wembc = sw + kSmEmb;
   const float* bemb = wembc + kLevels * R;
   int y1 = kLevels / 2, y2 = kLevels / 2;
+  float wr[32];
 
   for (int64_t n = 0; n < A.N; ++n) {
     if (c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
@@ -397,13 +420,14 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* blk,
     for (int jl = 0; jl < LPC; ++jl) {
       if (jl < nl) {
         const int j = first + jl;
-        ptx::bar_sync(kBarH, kMain);  // h^(j) from A (implies xs[jl] is valid)
+        if (j < pl.L - 1) ptx::tmem_load_async<32>(tm + 32 * jl, wr);
+        ptx::bar_sync(kBarH, kMain);  // h^(j) from A (implies xs[0] is valid)
         const float xi = m.xs[jl][pad16(row)];
         if (jl == 0 && writer) m.xsave0[row] = xi;
         if (j < pl.L - 1) {
-          // x^(j) = x^(j-1) + W_res h + B_res
+          ptx::tmem_wait_ld<32>(wr);
           float v[2];
-          tile_dot<2, 16>(wr[jl], &m.hs[jl][20 * cc], v);
+          tile_dot<2, 16>(wr, &m.hs[jl][20 * cc], v);
           xpose_level<2>(v, cc, 2);
           v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
           const float xn = xi + (v[0] + bres[jl * R + row]);
@@ -412,7 +436,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* blk,
             else if (!last_cta)
               ptx::st_async(remote(&m.xs[0][pad16(row)], c + 1), xn, remote(&m.bar_xin, c + 1));
           }
-          if (jl + 1 < nl) bar_arrive(kBarX, kMain);
+          if (jl + 2 < nl) bar_arrive(kBarXR, kMain);  // x^(j) ready: C computes R^(j+2)
         }
       }
     }
@@ -420,6 +444,58 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* blk,
     if (b == 0) {
       trace<TRACE>(A, n, 2);
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_done));
+    }
+  }
+  if (c == 0 && A.N > 0) final_draw(P, cx, k);
+}
+
+// ------------------------------------------------------------------ chain CTA, warpgroup C (R terms)
+// R^(j0+1) = W_cur^(j0+1) x_in + c^(j0) as soon as x_in is there; R^(j0+2) =
+// W_cur^(j0+2) x^(j0) + c^(j0+1) once B has x^(j0).  Same tile mapping as A.
+template <bool TRACE>
+__device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) {
+  const RunArgs& A = P.a;
+  const ClusterPlan& pl = P.p;
+  Mail& m = *cx.mail;
+  const int ct = threadIdx.x - kAux - 256;  // 0..127
+  const int k = threadIdx.x - kAux;         // sampler thread index (>= 256: waits only)
+  const int g = ct >> 2, cc = ct & 3;
+  const int hrow = g + ((cc & 2) ? 32 : 0);
+  const bool writer = (cc & 1) == 0;
+  const int nl = pl.chain_nl[c];
+  const uint32_t tm = tmem_lane_addr(m) + kColC;
+  const float* cf = sw + kSmFold;  // [LPC-1][2R]
+  const float* wembc = sw + kSmEmb;
+  const float* bemb = wembc + kLevels * R;
+  int y1 = kLevels / 2, y2 = kLevels / 2;
+  float w[64];
+
+  for (int64_t n = 0; n < A.N; ++n) {
+    if (nl >= 2) ptx::tmem_load_async<64>(tm, w);
+    if (c == 0) {
+      sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
+    } else {
+      wait(cx, &m.bar_xin, (uint32_t)(n & 1), 15);
+    }
+#pragma unroll
+    for (int jl = 1; jl < LPC; ++jl) {
+      if (jl < nl) {
+        if (jl == 2) {
+          ptx::tmem_load_async<64>(tm + 64, w);
+          ptx::bar_sync(kBarXR, kMain);  // x^(j0) from B
+        }
+        ptx::tmem_wait_ld<64>(w);
+        float v[4];
+        tile_dot<4, 16>(w, &m.xs[jl - 1][20 * cc], v);
+        xpose_level<4>(v, cc, 2);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
+        if (writer) {
+          m.rr[jl][hrow] = v[0] + cf[(jl - 1) * 2 * R + hrow];
+          m.rr[jl][R + hrow] = v[1] + cf[(jl - 1) * 2 * R + R + hrow];
+        }
+        bar_arrive(jl == 1 ? kBarRA : kBarRA + 3, kMain);
+      }
     }
   }
   if (c == 0 && A.N > 0) final_draw(P, cx, k);
@@ -440,7 +516,28 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
   const int L = A.L;
 
   for (int64_t n = 0; n < A.N; ++n) {
-    if (n > 0) wait(cx, &m.bar_done, (uint32_t)((n - 1) & 1), 14);
+    if (n > 0) {
+      // forward h^(j) of sample n-1, layer by layer as A publishes it: to its skip CTA, or
+      // (last two layers) to the four heads; 16 x 16 B per destination.  Kept off A
+      // because a DSMEM store holds its warp for about one hop.
+      for (int jl = 0; jl < nl; ++jl) {
+        const int j = first + jl;
+        ptx::bar_sync(kBarHX + jl, kMain);
+        if (j >= pl.L - 2) {
+          if (at < 16 * NH) {
+            const int hh = at >> 4, e = at & 15, off = 20 * (e >> 2) + 4 * (e & 3);
+            const int sl = pl.L - 1 - j;
+            ptx::st_async4(remote(&m.hbuf[sl][off], pl.nc + hh), lds4(&m.hs[jl][off]),
+                           remote(&m.bar_h[sl], pl.nc + hh));
+          }
+        } else if (at < 16) {
+          const int off = 20 * (at >> 2) + 4 * (at & 3);
+          const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
+          ptx::st_async4(remote(&m.hbuf[sl][off], kk), lds4(&m.hs[jl][off]), remote(&m.bar_h[sl], kk));
+        }
+      }
+      wait(cx, &m.bar_done, (uint32_t)((n - 1) & 1), 14);
+    }
     const int64_t f = n / A.hop;
     for (int jl = 0; jl < nl; ++jl) {
       const int j = first + jl;
@@ -473,6 +570,23 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_pre));
     }
   }
+  if (A.N > 0) {  // forward the last sample's h (same as above)
+    for (int jl = 0; jl < nl; ++jl) {
+      const int j = first + jl;
+      ptx::bar_sync(kBarHX + jl, kMain);
+      if (j >= pl.L - 2) {
+        if (at < 16 * NH) {
+          const int hh = at >> 4, e = at & 15, off = 20 * (e >> 2) + 4 * (e & 3);
+          const int sl = pl.L - 1 - j;
+          ptx::st_async4(remote(&m.hbuf[sl][off], pl.nc + hh), lds4(&m.hs[jl][off]), remote(&m.bar_h[sl], pl.nc + hh));
+        }
+      } else if (at < 16) {
+        const int off = 20 * (at >> 2) + 4 * (at & 3);
+        const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
+        ptx::st_async4(remote(&m.hbuf[sl][off], kk), lds4(&m.hs[jl][off]), remote(&m.bar_h[sl], kk));
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------ head CTA (rows [64h, 64h+64))
@@ -481,20 +595,16 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
 //   z_a : rows 64h + 4 (k/16) + m (m < 4), columns [(k%16) S/16, +S/16) of W_relu
 //   out : rows 64h + 4 (k/16) + m (m < 4), columns [16 (k%16), +16) of W_out
 template <int S, bool TRACE>
-__device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float* blk, const float* sw) {
+__device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
   const int k = threadIdx.x - kAux;  // 0..255
   constexpr int RQ = S / 64;         // q rows per thread
   constexpr int CZ = S / 16;         // z_s columns per thread
-  float wsk[RQ * 16], wrl[4 * CZ], wo[64];
-#pragma unroll
-  for (int q = 0; q < RQ * 16; ++q) wsk[q] = blk[q * kMain + k];
-#pragma unroll
-  for (int q = 0; q < 4 * CZ; ++q) wrl[q] = blk[(RQ * 16 + q) * kMain + k];
-#pragma unroll
-  for (int q = 0; q < 64; ++q) wo[q] = blk[(RQ * 16 + 4 * CZ + q) * kMain + k];
+  // TMEM tiles (this thread's lane): W_skip^(l) [RQ*16], W_relu [4*CZ], W_out [64]
+  const uint32_t tm = tmem_lane_addr(m) + (k < 128 ? 0 : 256);
+  constexpr int cRelu = RQ * 16, cOut = RQ * 16 + 4 * CZ;
   const float* bskip = sw;          // [S]
   const float* brelu = sw + S;      // [64]
   const float* bout = sw + S + 64;  // [64]
@@ -507,6 +617,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
   const int orow = 4 * (k >> 4) + ((k >> 2) & 3);  // z_a / logits row (within the head) this lane finishes
   const bool owriter = (k & 3) == 0;
   const int nk = pl.nk;
+  float w[64];
 
   auto finish = [&](float (&v)[RQ]) -> float {
     xpose_level<RQ>(v, cc, 2);
@@ -520,6 +631,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
 
   for (int64_t n = 0; n < A.N; ++n) {
     const uint32_t par = (uint32_t)(n & 1);
+    ptx::tmem_load_async<RQ * 16>(tm, w);  // W_skip^(l) tile, hidden behind the waits
     // q = B_skip + sum_k partial_k + W_skip^(l-1) h^(l-1) + W_skip^(l) h^(l); z_s = relu(q)
     // (PAPER.md:365-372).  W_skip^(l-1) is applied here, from shared memory, while the
     // last layer runs, so no skip CTA sits between the chain and the head.
@@ -538,8 +650,10 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     }
     if (wait(cx, &m.bar_h[0], par, 21) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[0]), R * 4);
     if (k == 0) trace<TRACE>(A, n, 0);
+    ptx::tmem_wait_ld<RQ * 16>(w);
     float v[RQ];
-    tile_dot<RQ, 16>(wsk, &m.hbuf[0][20 * cc], v);
+    tile_dot<RQ, 16>(w, &m.hbuf[0][20 * cc], v);
+    ptx::tmem_load_async<4 * CZ>(tm + cRelu, w);
     v[0] = finish(v);
     if (nk > 0) {
       if (wait(cx, &m.bar_part, par, 22) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_part), nk * S * 4);
@@ -552,10 +666,12 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
       qv += v[0];
       m.zs[cpad<CZ>(qrow)] = fmaxf(qv, 0.0f);
     }
-    ptx::bar_sync(kBarMain, kMain);
+    ptx::bar_sync(kBarHS, kMain);
     // z_a = relu(W_relu z_s + B_relu)
+    ptx::tmem_wait_ld<4 * CZ>(w);
     float za[4];
-    tile_dot<4, CZ>(wrl, &m.zs[(CZ + 4) * c16], za);
+    tile_dot<4, CZ>(w, &m.zs[(CZ + 4) * c16], za);
+    ptx::tmem_load_async<64>(tm + cOut, w);
     xpose_level<4>(za, k, 8);
     xpose_level<2>(*reinterpret_cast<float(*)[2]>(za), k, 4);
     za[0] += __shfl_xor_sync(0xffffffffu, za[0], 2);
@@ -570,8 +686,9 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     if (wait(cx, &m.bar_za, par, 23) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_za), kLevels * 4);
     if (k == 0) trace<TRACE>(A, n, 2);
     // logits = W_out z_a + B_out
+    ptx::tmem_wait_ld<64>(w);
     float lg[4];
-    tile_dot<4, 16>(wo, &m.za_in[20 * c16], lg);
+    tile_dot<4, 16>(w, &m.za_in[20 * c16], lg);
     xpose_level<4>(lg, k, 8);
     xpose_level<2>(*reinterpret_cast<float(*)[2]>(lg), k, 4);
     lg[0] += __shfl_xor_sync(0xffffffffu, lg[0], 2);
@@ -586,24 +703,20 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
 // partial_k = sum over owned layers j (ascending) of W_skip^(j) h^(j).
 // Thread t: rows {g + 64 m} (m < S/64), columns [16 cc, +16); g = t/4, cc = t%4.
 template <int S, bool TRACE>
-__device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* blk, const float* sw) {
+__device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
-  const int t = threadIdx.x - kAux;  // 0..255
+  const int t = threadIdx.x - kAux;     // 0..255
   constexpr int RQ = S / 64;
-  constexpr int QS = RQ * 16;        // registers per layer per thread
-  constexpr int MAXREG = 192 / QS;   // 3 (s=256) or 6 (s=128)
-  constexpr int LSTRIDE = QS * kMain;  // floats per shared-memory layer ([q/4][t][4])
-  const int nown = pl.skip_n[k], nsm = pl.skip_nsm[k], nreg = nown - nsm;
-  float w[MAXREG][QS];
-#pragma unroll
-  for (int rl = 0; rl < MAXREG; ++rl)
-#pragma unroll
-    for (int q = 0; q < QS; ++q) w[rl][q] = (rl < nreg) ? blk[(rl * QS + q) * kMain + t] : 0.0f;
+  constexpr int QS = RQ * 16;           // floats of one layer's tile per thread
+  constexpr int LSTRIDE = QS * kMain;   // floats per shared-memory layer ([q/4][t][4])
+  const int nown = pl.skip_n[k], nsm = pl.skip_nsm[k];
+  const uint32_t tm = tmem_lane_addr(m) + (t < 128 ? 0 : 256);  // TMEM layers: [QS] each
   const int g = t >> 2, cc = t & 3;
   const int row = g + 64 * ((RQ == 4) ? cc : (cc >> 1));
   const bool writer = (RQ == 4) || ((cc & 1) == 0);
+  float wl[QS];
 
   auto finish = [&](float (&v)[RQ]) -> float {
     xpose_level<RQ>(v, cc, 2);
@@ -619,35 +732,27 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* bl
     const uint32_t par = (uint32_t)(n & 1);
     float part = 0.0f;
 #pragma unroll 1
-    for (int sl = 0; sl < nsm; ++sl) {
+    for (int sl = 0; sl < nown; ++sl) {
+      const bool in_tmem = sl >= nsm;
+      if (in_tmem) ptx::tmem_load_async<QS>(tm + (sl - nsm) * QS, wl);
       if (wait(cx, &m.bar_h[sl], par, 31) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
-      if (t == 0) trace<TRACE>(A, n, 8 + sl);
-      const float* ws = sw + sl * LSTRIDE;
-      float wl[QS];
+      if (in_tmem) {
+        ptx::tmem_wait_ld<QS>(wl);
+      } else {
+        const float* ws = sw + sl * LSTRIDE;
 #pragma unroll
-      for (int q = 0; q < QS; q += 4) {
-        const float4 x = lds4(ws + (q / 4 * kMain + t) * 4);
-        wl[q] = x.x; wl[q + 1] = x.y; wl[q + 2] = x.z; wl[q + 3] = x.w;
+        for (int q = 0; q < QS; q += 4) {
+          const float4 x = lds4(ws + (q / 4 * kMain + t) * 4);
+          wl[q] = x.x; wl[q + 1] = x.y; wl[q + 2] = x.z; wl[q + 3] = x.w;
+        }
       }
       float v[RQ];
       tile_dot<RQ, 16>(wl, &m.hbuf[sl][20 * cc], v);
       part += finish(v);
     }
-#pragma unroll
-    for (int rl = 0; rl < MAXREG; ++rl) {
-      if (rl < nreg) {
-        const int sl = nsm + rl;
-        if (wait(cx, &m.bar_h[sl], par, 32) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
-        if (t == 0) trace<TRACE>(A, n, 8 + sl);
-        float v[RQ];
-        tile_dot<RQ, 16>(w[rl], &m.hbuf[sl][20 * cc], v);
-        part += finish(v);
-        if (t == 0) trace<TRACE>(A, n, 20 + sl);
-      }
-    }
     if (writer) m.zs[row] = part;
     if (t == 0) trace<TRACE>(A, n, 1);
-    ptx::bar_sync(kBarMain, kMain);
+    ptx::bar_sync(kBarHS, kMain);
     if (t < (S / 4) * NH) {
       const int hh = t / (S / 4), e = t % (S / 4);
       ptx::st_async4(remote(&m.part[k][4 * e], pl.nc + hh), lds4(&m.zs[4 * e]), remote(&m.bar_part, pl.nc + hh));
@@ -670,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   else if (rank < pl.nc + NH) { role = kHead; idx = rank - pl.nc; }
   else if (rank < pl.nc + NH + pl.nk) { role = kSkip; idx = rank - pl.nc - NH; }
 
+  if (t < 32) ptx::tmem_alloc(ptx::smem_u32(&mail->tmem_base), kTmemCols);
   if (t == 0) {
     mail->abort_flag = 0;
     ptx::mbar_init(ptx::smem_u32(&mail->bar_xin), 1);
@@ -688,38 +794,68 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_za), kLevels * 4);
     for (int i = 0; i < kCMaxSlot; ++i) ptx::mbar_arm(ptx::smem_u32(&mail->bar_h[i]), R * 4);
   }
-  const float* blk = P.pk + pl.pk_off[rank < kCMaxCta ? rank : 0];
   if (role != kIdle) {
     const float4* src = reinterpret_cast<const float4*>(P.pk + pl.pk_smem_off[rank]);
     float4* dst = reinterpret_cast<float4*>(sw);
     for (int i = t; i < pl.pk_smem_floats[rank] / 4; i += kThreads) dst[i] = __ldg(src + i);
   }
+  ptx::tmem_fence_before();
   __syncthreads();
+  ptx::tmem_fence_after();
+  // Tensor-memory image: [column][128 lanes]; each math thread fills the columns its role
+  // uses in its own lane (chain: A [0,192) C [192,320) B [320,416); head / skip: A-half
+  // [0,256) B-half [256,512)).
+  if (t >= kAux && role != kIdle) {
+    const int wg = (t - kAux) >> 7;  // 0 = A, 1 = B, 2 = C
+    int c0 = 0, c1 = 0;
+    if (role == kChain) {
+      if (wg == 0) { c0 = kColA; c1 = kColC; }
+      else if (wg == 1) { c0 = kColB; c1 = kColB + 3 * 32; }
+      else { c0 = kColC; c1 = kColB; }
+    } else if (wg < 2) {
+      c0 = 256 * wg;
+      c1 = c0 + 256;
+    }
+    c1 = min(c1, pl.tm_cols[rank]);
+    const int lane = (t - kAux) & 127;
+    const float* img = P.pk + pl.pk_off[rank];
+    const uint32_t ta = tmem_lane_addr(*mail);
+    for (int col = c0; col < c1; col += 16) {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __ldg(img + (int64_t)(col + i) * 128 + lane);
+      ptx::tmem_st16(ta + col, v);
+    }
+    ptx::tmem_wait_st();
+  }
+  ptx::tmem_fence_before();
+  __syncthreads();
+  ptx::tmem_fence_after();
   ptx::cluster_sync();
 
-  // Register split: warpgroups A and B (math) grow to 232 registers, warpgroup X
-  // (aux) shrinks to 40.  Each branch ends with its own cluster barrier.
   if (t >= kAux) {
-    ptx::setmaxnreg_inc<kMainRegs>();
     if (role == kChain) {
-      if (t < kAux + 128) chain_A<TRACE>(P, cx, idx, blk, sw);
-      else chain_B<TRACE>(P, cx, idx, blk, sw);
+      if (t < kAux + 128) chain_A<TRACE>(P, cx, idx, sw);
+      else if (t < kAux + 256) chain_B<TRACE>(P, cx, idx, sw);
+      else chain_C<TRACE>(P, cx, idx, sw);
     } else if (role == kHead) {
-      head_main<S, TRACE>(P, cx, idx, blk, sw);
+      if (t < kAux + kMain) head_main<S, TRACE>(P, cx, idx, sw);
     } else if (role == kSkip) {
-      skip_main<S, TRACE>(P, cx, idx, blk, sw);
+      if (t < kAux + kMain) skip_main<S, TRACE>(P, cx, idx, sw);
     }
-    ptx::bar_sync(kBarMain, kMain);
+    ptx::tmem_fence_before();
+    ptx::bar_sync(kBarMath, kMath);
     if (t == kAux) ptx::mbar_arrive(ptx::smem_u32(&mail->bar_exit));
     __syncwarp();
     ptx::cluster_sync();
     return;
   }
-  ptx::setmaxnreg_dec<kAuxRegs>();
   if (role == kChain) chain_aux<TRACE>(P, cx, idx, sw);
-  // Park until the math warps are done (try_wait suspends the warp).
+  // Park until the math warps are done (try_wait suspends the warp), then free TMEM.
   while (!ptx::mbar_try_wait(ptx::smem_u32(&mail->bar_exit), 0)) {
   }
+  ptx::tmem_fence_after();
+  if (t < 32) ptx::tmem_dealloc(mail->tmem_base, kTmemCols);
   __syncwarp();
   ptx::cluster_sync();
 }
@@ -757,13 +893,8 @@ int max_active_clusters(int size, int smem) {
   return n;
 }
 
-// floats of a chain CTA's shared-memory image: W_prev (col-major [R][2R]) x LPC,
-// B [LPC][2R], B_res [LPC][R]; CTA 0 adds W_emb_cur^T [256][R] and B_emb [R]
-int smem_chain(int c) {
-  int f = LPC * R * 2 * R + LPC * 2 * R + LPC * R;
-  if (c == 0) f += kLevels * R + R;
-  return f;
-}
+// floats of a chain CTA's shared-memory image (see kSm*)
+int smem_chain(int c) { return kSmEmb + (c == 0 ? kLevels * R + R : 0); }
 
 }  // namespace
 
@@ -782,10 +913,11 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
   }
   p.nh = NH;
   const int nskip = std::max(0, L - 2);  // W_skip^(l) and W_skip^(l-1) live in the head CTAs
-  const int qs = s / 4, maxreg = 192 / qs;  // registers per skip layer per thread
-  const int lstride = qs * kMain;            // floats per shared-memory skip layer
-  const int maxsm = std::min(kCMaxSlot - maxreg, (int)((190 * 1024) / (lstride * 4)));
-  const int cap = maxreg + maxsm;
+  const int qs = s / 4;                   // floats of one skip layer's tile per thread
+  const int maxtm = 256 / qs;             // skip layers in tensor memory per thread half
+  const int lstride = qs * kMain;         // floats per shared-memory skip layer
+  const int maxsm = std::min(kCMaxSlot - maxtm, (int)((190 * 1024) / (lstride * 4)));
+  const int cap = maxtm + maxsm;
   p.nk = nskip > 0 ? (nskip + cap - 1) / cap : 0;
   if (p.nk > kCMaxSkip) { p.why = "too many skip CTAs"; return p; }
   p.size = p.nc + p.nh + p.nk;
@@ -798,19 +930,18 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
   }
   for (int k = 0; k < p.nk; ++k) {
     if (p.skip_n[k] > cap) { p.why = "skip capacity"; return p; }
-    p.skip_nsm[k] = std::max(0, p.skip_n[k] - maxreg);  // latest layers in registers
+    p.skip_nsm[k] = std::max(0, p.skip_n[k] - maxtm);  // latest layers in tensor memory
   }
   int64_t off = 0;
   int max_sw = 0;
   for (int rank = 0; rank < p.size; ++rank) {
-    int64_t regfloats = 0;
     int swf = 0;
-    if (rank < p.nc) { regfloats = (int64_t)(LPC * 64 + LPC * 32) * 128; swf = smem_chain(rank); }
-    else if (rank < p.nc + p.nh) { regfloats = (int64_t)(s / 4 + s / 4 + 64) * kMain; swf = s + 128 + (L >= 2 ? qs * kMain : 0); }
-    else { const int k = rank - p.nc - p.nh; regfloats = (int64_t)(p.skip_n[k] - p.skip_nsm[k]) * qs * kMain; swf = p.skip_nsm[k] * lstride; }
+    if (rank < p.nc) swf = smem_chain(rank);
+    else if (rank < p.nc + p.nh) swf = s + 128 + (L >= 2 ? qs * kMain : 0);
+    else swf = p.skip_nsm[rank - p.nc - p.nh] * lstride;
     p.pk_off[rank] = off;
-    off += regfloats;
-    off = (off + 3) & ~int64_t(3);
+    p.tm_cols[rank] = kTmemCols;
+    off += (int64_t)kTmemCols * 128;
     p.pk_smem_off[rank] = off;
     p.pk_smem_floats[rank] = swf;
     off += (swf + 3) & ~3;
@@ -837,44 +968,62 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
 
 size_t packed_bytes(const ClusterPlan& p) { return sizeof(float) * (size_t)p.pk_total; }
 
-// Residency layout, built on the host from the raw roster-order blob (index
-// shuffling only, no arithmetic): register blocks are [register q][thread], so
-// the start-up loads of each thread are coalesced across its warp.
+// Residency layout, built on the host from the raw roster-order blob: the tensor-memory
+// images [column][lane], the shared-memory images, W_emb_prev^T.  Index shuffling plus
+// the fold M^(j) = W_cur^(j+1) W_res^(j) and c^(j) = W_cur^(j+1) B_res^(j), computed in
+// double precision and rounded once to fp32.
 cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Offsets& o, void* packed) {
-  const int s = p.s, qs = s / 4;
+  const int s = p.s, qs = s / 4, rq = s / 64, cz = s / 16;
   std::vector<float> h((size_t)p.pk_total, 0.0f);
   auto W = [&](int j, int64_t off_in_layer, int row, int col, int ncol) {
     return w[(int64_t)j * o.layer_stride + off_in_layer + (int64_t)row * ncol + col];
   };
+  auto fold = [&](int j, std::vector<float>& M, std::vector<float>& cvec) {  // j: the W_res layer
+    M.assign(2 * R * R, 0.0f);
+    cvec.assign(2 * R, 0.0f);
+    for (int i = 0; i < 2 * R; ++i) {
+      double cs = 0.0;
+      for (int k = 0; k < R; ++k) {
+        double acc = 0.0;
+        for (int t = 0; t < R; ++t) acc += (double)W(j + 1, o.w_cur, i, t, R) * (double)W(j, o.w_res, t, k, R);
+        M[i * R + k] = (float)acc;
+      }
+      for (int t = 0; t < R; ++t) cs += (double)W(j + 1, o.w_cur, i, t, R) * (double)w[(int64_t)j * o.layer_stride + o.b_res + t];
+      cvec[i] = (float)cs;
+    }
+  };
   for (int rank = 0; rank < p.size; ++rank) {
-    float* blk = h.data() + p.pk_off[rank];
+    float* img = h.data() + p.pk_off[rank];  // [col][128]
     float* sm = h.data() + p.pk_smem_off[rank];
+    auto put = [&](int col, int lane, float v) { img[(int64_t)col * 128 + lane] = v; };
     if (rank < p.nc) {
       const int first = p.chain_first[rank], nl = p.chain_nl[rank];
-      for (int a = 0; a < 128; ++a) {
-        const int g = a >> 2, cc = a & 3;
+      std::vector<std::vector<float>> M(LPC), cf(LPC);
+      for (int jl = 0; jl + 1 < nl; ++jl) fold(first + jl, M[jl], cf[jl]);
+      for (int lane = 0; lane < 128; ++lane) {
+        const int g = lane >> 2, cc = lane & 3;
         const int arow[4] = {g, R + g, 32 + g, R + 32 + g};  // tanh g, sigmoid g, tanh 32+g, sigmoid 32+g
         const int brow[2] = {g, 32 + g};
-        for (int jl = 0; jl < nl; ++jl) {
-          const int j = first + jl;
-          for (int mm = 0; mm < 4; ++mm)
-            for (int q = 0; q < 16; ++q)
-              blk[(jl * 64 + mm * 16 + q) * 128 + a] = W(j, o.w_cur, arow[mm], 16 * cc + q, R);
-          for (int mm = 0; mm < 2; ++mm)
-            for (int q = 0; q < 16; ++q)
-              blk[(LPC * 64 + jl * 32 + mm * 16 + q) * 128 + a] = W(j, o.w_res, brow[mm], 16 * cc + q, R);
-        }
+        for (int jl = 0; jl < nl; ++jl)
+          for (int q = 0; q < 64; ++q) {
+            const int row = arow[q / 16], col = 16 * cc + q % 16;
+            put(kColA + 64 * jl + q, lane, jl == 0 ? W(first, o.w_cur, row, col, R) : M[jl - 1][row * R + col]);
+            if (jl >= 1) put(kColC + 64 * (jl - 1) + q, lane, W(first + jl, o.w_cur, row, col, R));
+          }
+        for (int jl = 0; jl < nl; ++jl)
+          for (int q = 0; q < 32; ++q) put(kColB + 32 * jl + q, lane, W(first + jl, o.w_res, brow[q / 16], 16 * cc + q % 16, R));
       }
       for (int jl = 0; jl < nl; ++jl) {
         const int j = first + jl;
         for (int k = 0; k < R; ++k)
           for (int i = 0; i < 2 * R; ++i) sm[jl * R * 2 * R + k * 2 * R + i] = W(j, o.w_prev, i, k, R);
-        for (int i = 0; i < 2 * R; ++i) sm[LPC * R * 2 * R + jl * 2 * R + i] = w[(int64_t)j * o.layer_stride + o.b + i];
-        for (int i = 0; i < R; ++i)
-          sm[LPC * R * 2 * R + LPC * 2 * R + jl * R + i] = w[(int64_t)j * o.layer_stride + o.b_res + i];
+        for (int i = 0; i < 2 * R; ++i) sm[kSmB + jl * 2 * R + i] = w[(int64_t)j * o.layer_stride + o.b + i];
+        for (int i = 0; i < R; ++i) sm[kSmBres + jl * R + i] = w[(int64_t)j * o.layer_stride + o.b_res + i];
+        if (jl + 1 < nl)
+          for (int i = 0; i < 2 * R; ++i) sm[kSmFold + jl * 2 * R + i] = cf[jl][i];
       }
       if (rank == 0) {
-        float* we = sm + LPC * R * 2 * R + LPC * 2 * R + LPC * R;
+        float* we = sm + kSmEmb;
         for (int y = 0; y < kLevels; ++y)
           for (int i = 0; i < R; ++i) we[y * R + i] = w[o.emb_cur + (int64_t)i * kLevels + y];
         for (int i = 0; i < R; ++i) we[kLevels * R + i] = w[o.b_emb + i];
@@ -882,18 +1031,17 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
     } else if (rank < p.nc + p.nh) {
       const int hidx = rank - p.nc;
       const int jl = p.L - 1;
-      const int rq = s / 64, cz = s / 16;
       for (int k = 0; k < kMain; ++k) {
+        const int lane = k & 127, cbase = (k < 128) ? 0 : 256;
         const int g = k >> 2, cc = k & 3, c16 = k & 15, rbase = 64 * hidx + 4 * (k >> 4);
         for (int mm = 0; mm < rq; ++mm)
-          for (int q = 0; q < 16; ++q) blk[(mm * 16 + q) * kMain + k] = W(jl, o.w_skip, g + 64 * mm, 16 * cc + q, R);
+          for (int q = 0; q < 16; ++q) put(cbase + mm * 16 + q, lane, W(jl, o.w_skip, g + 64 * mm, 16 * cc + q, R));
         for (int mm = 0; mm < 4; ++mm)
           for (int q = 0; q < cz; ++q)
-            blk[(rq * 16 + mm * cz + q) * kMain + k] = w[o.w_relu + (int64_t)(rbase + mm) * s + c16 * cz + q];
+            put(cbase + rq * 16 + mm * cz + q, lane, w[o.w_relu + (int64_t)(rbase + mm) * s + c16 * cz + q]);
         for (int mm = 0; mm < 4; ++mm)
           for (int q = 0; q < 16; ++q)
-            blk[(rq * 16 + 4 * cz + mm * 16 + q) * kMain + k] =
-                w[o.w_out + (int64_t)(rbase + mm) * kLevels + 16 * c16 + q];
+            put(cbase + rq * 16 + 4 * cz + mm * 16 + q, lane, w[o.w_out + (int64_t)(rbase + mm) * kLevels + 16 * c16 + q]);
       }
       for (int i = 0; i < s; ++i) sm[i] = w[o.b_skip + i];
       for (int i = 0; i < 64; ++i) {
@@ -917,7 +1065,7 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
       for (int j = 0; j < p.L - 2; ++j)
         if (p.layer_skip_cta[j] == rank) layers.push_back(j);
       const int nsm = p.skip_nsm[k];
-      const int rq = s / 64, lstride = qs * kMain;
+      const int lstride = qs * kMain;
       for (int sl = 0; sl < (int)layers.size(); ++sl) {
         const int j = layers[sl];
         for (int t = 0; t < kMain; ++t) {
@@ -927,7 +1075,7 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
               const float v = W(j, o.w_skip, g + 64 * mm, 16 * cc + q, R);
               const int qq = mm * 16 + q;
               if (sl < nsm) sm[sl * lstride + ((qq / 4) * kMain + t) * 4 + (qq % 4)] = v;
-              else blk[((sl - nsm) * qs + qq) * kMain + t] = v;
+              else put((t < 128 ? 0 : 256) + (sl - nsm) * qs + qq, t & 127, v);
             }
         }
       }

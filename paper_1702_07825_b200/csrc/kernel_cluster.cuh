@@ -3,10 +3,12 @@
 // One thread-block cluster (<= 16 CTAs, one per SM) holds the whole model on
 // chip and generates every sample of one utterance in a single launch.  CTA
 // roles:
-//   chain CTAs  c = 0..nc-1 : layers [4c, 4c+4): W_cur, W_res in registers, W_prev
-//                             in shared memory; CTA 0 also samples and embeds
-//   head CTAs   h = 0..3    : W_skip^(l), W_relu and W_out row blocks in registers
-//   skip CTAs   k = 0..nk-1 : W_skip^(j) for j < l-1, registers + shared memory
+//   chain CTAs  c = 0..nc-1 : layers [3c, 3c+3): W_cur, the folded W_cur W_res and
+//                             W_res in tensor memory, W_prev in shared memory;
+//                             CTA 0 also samples and embeds
+//   head CTAs   h = 0..3    : W_skip^(l) / W_relu / W_out row blocks in tensor
+//                             memory, W_skip^(l-1) in shared memory
+//   skip CTAs   k = 0..nk-1 : W_skip^(j) for j < l-2, tensor + shared memory
 // Hand-offs are DSMEM st.async stores that complete transaction bytes on the
 // receiver's mbarrier (data and signal in one message), replacing the paper's
 // L2 spin-locks (App. D).
@@ -31,7 +33,8 @@ struct ClusterPlan {
   int skip_nsm[kCMaxSkip] = {};   // of which the first nsm live in shared memory, the rest in registers
   int layer_skip_cta[kCMaxLayers] = {};   // cluster rank owning W_skip^(j) (j < L-1)
   int layer_skip_slot[kCMaxLayers] = {};  // slot inside that CTA
-  int64_t pk_off[kCMaxCta] = {};  // float offset of each CTA's packed block
+  int64_t pk_off[kCMaxCta] = {};  // float offset of each CTA's tensor-memory image [column][128 lanes]
+  int tm_cols[kCMaxCta] = {};     // columns of that image
   int64_t pk_smem_off[kCMaxCta] = {};  // float offset of its shared-memory image (inside the block)
   int pk_smem_floats[kCMaxCta] = {};   // size of that image
   int64_t embp_off = 0;           // W_emb_prev transposed [256][r]
