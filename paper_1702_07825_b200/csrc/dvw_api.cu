@@ -7,12 +7,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <string>
 #include <vector>
 
 #include "dvw_internal.cuh"
+#include "kernel_batch.cuh"
 #include "kernel_cluster.cuh"
 
 using namespace dvw;
@@ -37,6 +39,11 @@ struct dvw_model {
   ClusterPlan cplan{};
   void* d_packed = nullptr;  // cluster-kernel residency layout
   size_t packed_bytes = 0;
+  BatchPlan bplan{};
+  void* d_bpacked = nullptr;  // batched-kernel tile layout
+  size_t bpacked_bytes = 0;
+  void* d_bws = nullptr;      // batched-kernel workspace (activations, queues, barrier)
+  size_t bws_bytes = 0;
   // host-call staging
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
@@ -146,8 +153,27 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   DeviceGuard g(m->device);
   dvw_status st = check_device_error(m);
   if (st != DVW_OK) return st;
-  st = ensure_ring(m, n_streams);
-  if (st != DVW_OK) return st;
+  int kern = m->kernel;
+  if (kern == DVW_KERNEL_AUTO) {
+    if (n_streams == 1 && m->cplan.ok) kern = DVW_KERNEL_CLUSTER;
+    else if (n_streams > 1 && m->bplan.ok) kern = DVW_KERNEL_TC;
+    else kern = DVW_KERNEL_STREAM;
+  }
+  if (kern == DVW_KERNEL_TC) {
+    const int nsb = std::min(m->bplan.max_sb, (n_streams + 127) / 128);
+    const size_t need = batch_workspace_bytes(m->bplan, m->dil.data(), nsb);
+    if (m->bws_bytes < need) {
+      if (m->d_bws) cudaFree(m->d_bws);
+      m->d_bws = nullptr;
+      m->bws_bytes = 0;
+      DVW_CUDA(cudaMalloc(&m->d_bws, need), "allocating batched workspace");
+      m->bws_bytes = need;
+      m->info.workspace_bytes = (int64_t)need;
+    }
+  } else {
+    st = ensure_ring(m, n_streams);
+    if (st != DVW_OK) return st;
+  }
 
   RunArgs A{};
   A.w = m->d_w;
@@ -173,8 +199,6 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   A.trace_n0 = m->trace_n0;
   A.trace_count = m->trace_count;
 
-  int kern = m->kernel;
-  if (kern == DVW_KERNEL_AUTO) kern = (n_streams == 1 && m->cplan.ok) ? DVW_KERNEL_CLUSTER : DVW_KERNEL_STREAM;
   LaunchInfo li{};
   cudaError_t e;
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
@@ -182,6 +206,8 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
     e = launch_cluster_kernel(A, m->cplan, m->d_packed, cs, &li);
   } else if (kern == DVW_KERNEL_STREAM) {
     e = launch_stream_kernel(A, cs, &li);
+  } else if (kern == DVW_KERNEL_TC) {
+    e = launch_batch_kernel(A, m->bplan, m->d_bpacked, m->d_bws, m->bws_bytes, m->dil.data(), cs, &li);
   } else {
     return fail(DVW_E_UNSUPPORTED, "kernel %d is not available in this build", kern);
   }
@@ -249,6 +275,7 @@ DVW_API dvw_status dvw_create(const dvw_config* cfg, dvw_model** out) {
     return cuda_fail(e, "dvw_create device setup");
   }
   m->cplan = plan_cluster(m->L, m->r, m->s, m->device);
+  m->bplan = plan_batch(m->L, m->r, m->s, m->device);
   *out = m;
   return DVW_OK;
 }
@@ -283,6 +310,19 @@ DVW_API dvw_status dvw_load_weights(dvw_model* m, const float* blob, int64_t num
       m->packed_bytes = need;
     }
     DVW_CUDA(pack_cluster_weights(m->cplan, hp, m->off, m->d_packed), "packing weights");
+    wb += (int64_t)need;
+  }
+  if (m->bplan.ok) {
+    const size_t need = sizeof(float) * (size_t)m->bplan.total;
+    if (m->d_bpacked && m->bpacked_bytes < need) {
+      cudaFree(m->d_bpacked);
+      m->d_bpacked = nullptr;
+    }
+    if (!m->d_bpacked) {
+      DVW_CUDA(cudaMalloc(&m->d_bpacked, need), "allocating batched tile weights");
+      m->bpacked_bytes = need;
+    }
+    DVW_CUDA(pack_batch_weights(m->bplan, hp, m->off, m->d_bpacked), "packing batched tile weights");
     wb += (int64_t)need;
   }
   m->info.weight_bytes = wb;
@@ -340,7 +380,8 @@ DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel) {
   if (kernel < DVW_KERNEL_AUTO || kernel > DVW_KERNEL_TC) return fail(DVW_E_INVALID_ARG, "unknown kernel %d", kernel);
   if (kernel == DVW_KERNEL_CLUSTER && !m->cplan.ok)
     return fail(DVW_E_UNSUPPORTED, "cluster kernel cannot hold this model: %s", m->cplan.why);
-  if (kernel == DVW_KERNEL_TC) return fail(DVW_E_UNSUPPORTED, "tcgen05 batched kernel is not built yet");
+  if (kernel == DVW_KERNEL_TC && !m->bplan.ok)
+    return fail(DVW_E_UNSUPPORTED, "batched kernel cannot run this model: %s", m->bplan.why);
   m->kernel = kernel;
   return DVW_OK;
 }
@@ -376,6 +417,8 @@ DVW_API void dvw_destroy(dvw_model* m) {
   cudaFree(m->d_ring);
   if (m->h_err) cudaFreeHost(const_cast<int*>(m->h_err));
   cudaFree(m->d_packed);
+  cudaFree(m->d_bpacked);
+  cudaFree(m->d_bws);
   cudaFree(m->d_stage);
   delete m;
 }

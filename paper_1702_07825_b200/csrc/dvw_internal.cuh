@@ -89,6 +89,19 @@ __device__ __forceinline__ float gate(float ah, float ag) {
   return tanhf(ah) * (1.0f / (1.0f + expf(-ag)));
 }
 
+// h = tanh(a) * sigma(g): tanh(a) = 1 - 2 / (1 + 2^(2a log2 e)),
+// sigma(g) = 1 / (1 + 2^(-g log2 e)); MUFU ex2/rcp (rel. err ~2^-22) keep the
+// result within ~1e-7 of the exact value; saturates correctly at +-inf.
+__device__ __forceinline__ float gate_fast(float a, float g) {
+  float ea, eg, ra, rg;
+  const float xa = 2.8853900817779268f * a, xg = -1.4426950408889634f * g;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ea) : "f"(xa));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(eg) : "f"(xg));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(ea + 1.0f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rg) : "f"(eg + 1.0f));
+  return fmaf(-2.0f, ra, 1.0f) * rg;
+}
+
 // Inverse-CDF direct sampling over a = 256 logits held one per thread by a
 // 256-thread group ("Sample randomly from P(y)"; reading R11):
 //   e_k = exp(l_k - max l) in fp32, P_k = fp64 inclusive running sum in ascending k,

@@ -1,0 +1,50 @@
+// kernel_batch.cuh -- batched multi-stream kernel (tcgen05): plan, packing, launch.
+//
+// Many independent utterances advance in lockstep, one sample per step
+// ("auto-regressive process"; SURVEY.md §8(a) "Batched mode").
+// With 128 streams per stream block the per-layer projections of §8(a) a3/a4/a6/a7
+// and the head a8 become real GEMMs, M = 128 streams x N = a tile of output
+// channels x K = input channels, issued as tcgen05.mma kind::tf32 with three
+// passes (hi*hi + hi*lo + lo*hi; each fp32 operand split into a tf32 head and
+// its exact residual) so the products keep ~fp32 accuracy.  The accumulators live
+// in tensor memory; the epilogue warps own one stream each (TMEM lane = stream),
+// so the gate, residual update and sampler are thread-local per stream.
+//
+// One cooperative, persistent launch runs every step; the steps' phases
+// (one per layer, then z_s, z_a, logits, sample) are separated by a grid-wide
+// barrier.  Weight tiles and activations are staged into shared memory with
+// 1-D bulk copies (cp.async.bulk) from global memory, where they are kept in the
+// K-major "core matrix" order the MMA descriptors read.
+#pragma once
+#include "dvw_internal.cuh"
+
+namespace dvw {
+
+constexpr int kBMaxLayers = 64;
+
+struct BatchPlan {
+  bool ok = false;
+  const char* why = "not planned";
+  int L = 0, r = 0, s = 0;
+  int TA = 0, TQ = 0, TH = 0;  // CTAs per stream block: layer tiles (16 channels), skip tiles, head tiles (32 rows)
+  int per_sb = 0;              // TA + TQ + TH
+  int max_sb = 0;              // stream blocks (128 streams each) per launch
+  // packed weights (floats)
+  int64_t la_off = 0, la_floats = 0;    // [L][TA] layer-tile blocks
+  int64_t q_off = 0, q_floats = 0;      // [L][TQ] skip-tile blocks
+  int64_t hr_off = 0, hr_floats = 0;    // [TH] W_relu tile blocks
+  int64_t ho_off = 0, ho_floats = 0;    // [TH] W_out tile blocks
+  int64_t bias_off = 0;                 // [L][2r] folded gate bias B^(j) + W_cur^(j) B_res^(j-1)
+  int64_t total = 0;
+  int smem_bytes = 0;
+};
+
+BatchPlan plan_batch(int L, int r, int s, int device);
+cudaError_t pack_batch_weights(const BatchPlan& p, const float* host_blob, const Offsets& o, void* packed);
+// Workspace for `nsb` stream blocks with dilations `dil` (host array, length L).
+size_t batch_workspace_bytes(const BatchPlan& p, const int32_t* dil, int nsb);
+// Runs n_streams (any count; groups of max_sb * 128 run back to back on `st`).
+cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void* packed, void* ws, size_t ws_bytes,
+                                const int32_t* dil_host, cudaStream_t st, LaunchInfo* info);
+
+}  // namespace dvw

@@ -167,19 +167,6 @@ __device__ __forceinline__ void trace_clk(const RunArgs& A, int64_t n, int ev) {
   }
 }
 
-// h = tanh(a) * sigma(g): tanh(a) = 1 - 2 / (1 + 2^(2a log2 e)),
-// sigma(g) = 1 / (1 + 2^(-g log2 e)); MUFU ex2/rcp (rel. err ~2^-22) keep the
-// result within ~1e-7 of the exact value; saturates correctly at +-inf.
-__device__ __forceinline__ float gate_fast(float a, float g) {
-  float ea, eg, ra, rg;
-  const float xa = 2.8853900817779268f * a, xg = -1.4426950408889634f * g;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ea) : "f"(xa));
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(eg) : "f"(xg));
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(ea + 1.0f));
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rg) : "f"(eg + 1.0f));
-  return fmaf(-2.0f, ra, 1.0f) * rg;
-}
-
 // Register tile x vector chunk: acc[m] = sum_c w[m*C + c] * v[c] for RQ rows and a
 // C-float chunk of a shared vector; two accumulators per row (even/odd c) for ILP.
 // Summation order is fixed (bitwise deterministic).
