@@ -32,12 +32,32 @@ from paper_1702_07825_b200 import synth  # noqa: E402
 
 METRIC = "audio samples/sec per stream (batch-1 real-time factor at 16 kHz) and aggregate"
 WORKLOADS = {
-    "C1": dict(cfg=synth.C1, n=1600, desc="C1: l=20 r=64 s=128, batch 1, 1,600 samples (0.1 s @16 kHz), hop 64"),
-    "C2": dict(cfg=synth.C2, n=16000, desc="C2: l=20 r=64 s=256, batch 1, 16,000 samples (1 s @16 kHz), hop 64"),
-    "C3": dict(cfg=synth.C3, n=160000, desc="C3: l=40 r=64 s=256, batch 1, 160,000 samples (10 s @16 kHz), hop 64"),
+    "C1": dict(cfg=synth.C1, n=1600, streams=1, split=False,
+               desc="C1: l=20 r=64 s=128, batch 1, 1,600 samples (0.1 s @16 kHz), hop 64"),
+    "C2": dict(cfg=synth.C2, n=16000, streams=1, split=False,
+               desc="C2: l=20 r=64 s=256, batch 1, 16,000 samples (1 s @16 kHz), hop 64"),
+    "C3": dict(cfg=synth.C3, n=160000, streams=1, split=False,
+               desc="C3: l=40 r=64 s=256, batch 1, 160,000 samples (10 s @16 kHz), hop 64"),
+    # batched (tcgen05) workloads: streams per GPU (C4, weak) or in total, sharded (C5, strong)
+    "C4": dict(cfg=synth.C4, n=80000, streams=256, split=False,
+               desc="C4: l=20 r=128 s=256, 256 concurrent utterances per GPU batched (tcgen05), "
+                    "80,000 samples (5 s @16 kHz) each, hop 64"),
+    "C5": dict(cfg=synth.C5, n=80000, streams=2048, split=True,
+               desc="C5: l=40 r=64 s=256, 2,048 utterances of 80,000 samples (5 s) sharded across "
+                    "the GPUs (no collective on the path), batched (tcgen05), hop 64"),
 }
 HOP = 64
 FP32_FMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 TFLOP/s
+TF32_RATIO = 0.5  # dense tf32 / bf16 tensor throughput (B200_PROFILING.md nominal 1.125 / 2.25 PFLOP/s)
+
+
+def tf32_peak_tflops():
+    """Dense tf32 peak = MEASURED_PEAKS.json sustained bf16 x the nominal tf32/bf16 ratio."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return d["bf16_tflops_sustained"] * TF32_RATIO, "MEASURED_PEAKS.json bf16 sustained x 0.5"
+    except Exception:
+        return 1590.0 * TF32_RATIO, "B200_PROFILING.md fallback bf16 1.59 PFLOP/s x 0.5"
 
 
 def macs_per_sample(cfg) -> int:
@@ -175,6 +195,18 @@ def cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, budget_samples):
     return cpu, parity
 
 
+def device_inputs(cfg, n, utts, dev, seed_base=1000):
+    """Batched workloads: conditioning and uniforms drawn on the device, U(-0.5, 0.5) and
+    U[0, 1) like synth.make_cond / make_uniforms, from a torch generator seeded by the
+    first utterance id (host arrays of 2,048 x 5 s would not fit)."""
+    import torch
+    g = torch.Generator(device=dev).manual_seed(seed_base + int(utts[0]))
+    nf = synth.n_frames_for(n, HOP)
+    cond = torch.rand((len(utts), nf, cfg.n_layers, 2 * cfg.residual), generator=g, device=dev) - 0.5
+    u = torch.rand((len(utts), n), generator=g, device=dev)
+    return cond, u
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -182,12 +214,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
-    ap.add_argument("--kernel", default="auto", choices=["auto", "cluster", "stream"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "cluster", "stream", "tc"])
+    ap.add_argument("--samples", type=int, default=0, help="override samples per utterance (0 = workload's)")
     ap.add_argument("--ref-samples", type=int, default=1600, help="samples per reference step")
     ap.add_argument("--cpu-samples", type=int, default=16000, help="oracle samples for cpu_baseline")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.samples:
+        wl["n"] = args.samples
+        wl["desc"] += f" [overridden: {args.samples} samples per utterance]"
     if args.impl == "reference":
         return run_reference(args, wl)
 
@@ -200,17 +237,26 @@ def main():
     dev = torch.device("cuda", local if ws > 1 else 0)
     torch.cuda.set_device(dev)
     from paper_1702_07825_b200._lib import Model
+    from paper_1702_07825_b200.shard import shard_range
 
     cfg, n = wl["cfg"], wl["n"]
-    utt = rank
+    if wl["split"]:
+        start, S = shard_range(wl["streams"], ws, rank)
+    else:
+        S = wl["streams"]
+        start = rank * S
+    utts = list(range(start, start + S))
     w = synth.make_weights(cfg, 0)
-    cond = synth.make_cond(cfg, synth.n_frames_for(n, HOP), utt)
-    u = synth.make_uniforms(n, utt)
+    if S == 1:
+        cond_np = synth.make_cond(cfg, synth.n_frames_for(n, HOP), utts[0])
+        u_np = synth.make_uniforms(n, utts[0])
+        d_cond = torch.from_numpy(cond_np)[None].to(dev)
+        d_u = torch.from_numpy(u_np)[None].to(dev)
+    else:
+        d_cond, d_u = device_inputs(cfg, n, utts, dev)
     model = Model.from_config(cfg, device=dev.index).load(w).set_kernel(args.kernel)
     stream = torch.cuda.current_stream(dev)
-    d_cond = torch.from_numpy(cond)[None].to(dev)
-    d_u = torch.from_numpy(u)[None].to(dev)
-    out = torch.empty((1, n), dtype=torch.uint8, device=dev)
+    out = torch.empty((S, n), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
     def barrier():
@@ -234,60 +280,82 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     kernel_ms = float(np.mean(step_ms))
     model.sync()
-    gpu_codes = out.cpu().numpy()[0].copy()
+    gpu_codes0 = out[0].cpu().numpy().copy()
 
     # end to end through the public host-buffer entry point (H2D + generate + D2H per step)
-    h_cond = torch.from_numpy(cond)[None].pin_memory()
-    h_u = torch.from_numpy(u)[None].pin_memory()
-    h_out = torch.empty((1, n), dtype=torch.uint8).pin_memory()
-    model.generate_host(h_cond, h_u, HOP, out=h_out)
-    barrier()
-    e2e_ms = []
-    for i in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
+    e2e_step, h2d = None, int(d_cond.numel() * 4 + d_u.numel() * 4)
+    if not args.no_e2e and h2d <= 16 * 2 ** 30:
+        h_cond = d_cond.cpu().pin_memory()
+        h_u = d_u.cpu().pin_memory()
+        h_out = torch.empty((S, n), dtype=torch.uint8).pin_memory()
         model.generate_host(h_cond, h_u, HOP, out=h_out)
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_step = float(np.mean(e2e_ms))
-    assert np.array_equal(h_out.numpy()[0], gpu_codes), "host-buffer path disagrees with device path"
+        barrier()
+        e2e_ms = []
+        for i in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            model.generate_host(h_cond, h_u, HOP, out=h_out)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_step = float(np.mean(e2e_ms))
+        assert np.array_equal(h_out[0].numpy(), gpu_codes0), "host-buffer path disagrees with device path"
 
     # max over ranks
-    t_max, e_max = kernel_ms, e2e_step
+    t_max, e_max = kernel_ms, (e2e_step if e2e_step is not None else -1.0)
+    total_streams = S
     if ws > 1:
         import torch.distributed as dist
-        t = torch.tensor([kernel_ms, e2e_step], device=dev)
+        t = torch.tensor([kernel_ms, e_max], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max, e_max = float(t[0]), float(t[1])
+        c = torch.tensor([S], device=dev)
+        dist.all_reduce(c)
+        total_streams = int(c[0])
 
     if rank == 0:
-        total = n * ws
+        total = n * total_streams
         value = total / (t_max / 1e3)
-        flop_launch = 2.0 * macs_per_sample(cfg) * n
+        flop_launch = 2.0 * macs_per_sample(cfg) * n * S
         achieved_tflops = flop_launch / (kernel_ms / 1e3) / 1e12
-        us_per_sample = kernel_ms * 1e3 / n
+        kname = info["last_kernel_name"]
+        if kname == "tc":
+            peak, peak_src = tf32_peak_tflops()
+            roof = {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved_tflops / peak, "traffic": load_ncu_traffic(args.workload),
+                    "note": "algorithmic FLOP (2 x MAC/sample x samples x streams) / launch time vs dense tf32 "
+                            f"peak ({peak_src}); the 3-pass split issues ~3.2x these FLOPs on the tensor pipe; "
+                            "the step is barrier/latency bound (DESIGN.md Batched kernel)"}
+        else:
+            roof = {"bound": "alu", "achieved": achieved_tflops, "peak": FP32_FMA_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": achieved_tflops / FP32_FMA_PEAK_TFLOPS,
+                    "traffic": load_ncu_traffic(args.workload),
+                    "note": "batch-1 is latency-bound: algorithmic FLOP (2 x MAC/sample x samples) / "
+                            "launch time vs FP32 FFMA peak of the whole chip (DESIGN.md Roofline)"}
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": wl["desc"], "samples_per_step": n, "streams_per_gpu": 1,
-                       "parallelism": f"{ws} independent utterances, one per GPU",
-                       "kernel": info["last_kernel_name"], "cluster_ctas": info["last_cluster"],
+            "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True,
+            "scaling": "strong" if wl["split"] else "weak",
+            "vs_baseline": None, "dtype": "f32" if kname != "tc" else "f32 (tf32 x3 tensor passes)",
+            "data": "synthetic",
+            "config": {"workload": wl["desc"], "samples_per_step": n, "streams_per_gpu": S,
+                       "streams_total": total_streams,
+                       "parallelism": f"{ws} GPU(s), independent utterances, no collective on the path",
+                       "kernel": kname, "grid": info["last_grid"], "cluster_ctas": info["last_cluster"],
+                       "launches_per_step": info["last_launches"],
                        "l2": "flushed between timed steps (256 MiB write, untimed)"},
-            "per_stream": {"samples_per_s": n / (kernel_ms / 1e3), "us_per_sample": us_per_sample,
+            "per_stream": {"samples_per_s": n / (kernel_ms / 1e3), "us_per_sample": kernel_ms * 1e3 / n,
                            "rtf_16khz": n / (kernel_ms / 1e3) / synth.AUDIO_HZ},
             "clocks": clk.summary(),
-            "e2e": {"value": total / (e_max / 1e3), "unit": "samples/s",
-                    "h2d_bytes_per_step": int(cond.nbytes + u.nbytes), "d2h_bytes_per_step": int(n)},
+            "e2e": ({"value": total / (e_max / 1e3), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                     "d2h_bytes_per_step": int(n * S)} if e_max > 0 else
+                    {"value": None, "unit": "samples/s", "skipped": f"host inputs {h2d} B > 16 GiB or --no-e2e"}),
             "gpu_launches": int(info["last_launches"]) * args.steps,
-            "roofline": {"bound": "alu", "achieved": achieved_tflops, "peak": FP32_FMA_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved_tflops / FP32_FMA_PEAK_TFLOPS,
-                         "traffic": load_ncu_traffic(args.workload),
-                         "note": "batch-1 is latency-bound: algorithmic FLOP (2 x MAC/sample x samples) / "
-                                 "launch time vs FP32 FFMA peak of the whole chip (DESIGN.md Roofline)"},
+            "roofline": roof,
         }
         if not args.no_cpu:
-            cpu, parity = cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, args.cpu_samples)
+            cond0 = d_cond[0].cpu().numpy()
+            u0 = d_u[0].cpu().numpy()
+            cpu, parity = cpu_baseline_and_parity(cfg, n, w, cond0, u0, gpu_codes0, args.cpu_samples)
             line["cpu_baseline"] = cpu
             line["parity"] = parity
         print(json.dumps(line), flush=True)

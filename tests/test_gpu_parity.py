@@ -27,7 +27,7 @@ def L():
     return _lib
 
 
-KERNELS = ["stream", "cluster"]
+KERNELS = ["stream", "cluster", "tc"]
 
 
 def model(L, cfg, w, kernel):
@@ -143,12 +143,13 @@ def test_determinism_and_edge_sizes(L, kernel):
     m.generate(dev(synth.make_cond(cfg, 1, 0))[None], torch.zeros((1, 0), device="cuda"), 64, out=out)
 
 
-def test_multi_stream_is_position_independent(L):
-    """Stream kernel: utterance u's codes do not depend on batch size or position."""
+@pytest.mark.parametrize("kernel", ["stream", "tc"])
+def test_multi_stream_is_position_independent(L, kernel):
+    """Utterance u's codes do not depend on batch size or position (bitwise)."""
     cfg = synth.C1
     N, hop = 700, 64
     w = synth.make_weights(cfg, 0)
-    m = L.Model.from_config(cfg).load(w).set_kernel("stream")
+    m = L.Model.from_config(cfg).load(w).set_kernel(kernel)
     utts = [5, 1, 9]
     cond, u = synth.make_batch(cfg, N, utts, hop)
     batch = m.generate(dev(cond), dev(u), hop).cpu().numpy()
@@ -198,3 +199,48 @@ def test_abi_negative_on_gpu(L):
     codes = m.generate(cond, u, 64)
     m.sync()
     assert codes.shape == (1, 128)
+
+
+def test_tc_many_streams_two_launches_position_independent(L):
+    """Batched kernel: more streams than one cooperative launch holds (groups run
+    back to back) -- every stream equals its single-stream run bitwise, sampled
+    streams match the oracle, and AUTO picks the batched kernel."""
+    cfg = synth.C2
+    N, hop = 96, 32
+    w = synth.make_weights(cfg, 0)
+    m = L.Model.from_config(cfg).load(w)
+    n_streams = 1100  # > max_sb * 128 on a 148-SM B200 (7 * 128 = 896)
+    utts = list(range(n_streams))
+    cond, u = synth.make_batch(cfg, N, utts, hop)
+    codes = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    info = m.info()
+    assert info["last_kernel_name"] == "tc"
+    assert info["last_launches"] >= 2
+    m.set_kernel("tc")
+    for i in (0, 127, 128, 895, 896, 1099):
+        single = m.generate(dev(cond[i:i + 1]), dev(u[i:i + 1]), hop).cpu().numpy()[0]
+        assert np.array_equal(codes[i], single), i
+    for i in (0, 896, 1099):
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[i], hop, N, uniforms=u[i])
+        assert np.array_equal(codes[i], ref), i
+
+
+@pytest.mark.parametrize("cfg", [synth.C4, synth.C5], ids=["C4", "C5"])
+def test_tc_batched_configs_teacher_forced_and_free_running(L, cfg):
+    """C4 (r = 128) and C5 (l = 40) shapes through the batched kernel: 3 streams,
+    teacher-forced logits within the fp32-faithful bound, free-running codes equal
+    to the oracle's for every stream."""
+    N, hop = 400, 64
+    w = synth.make_weights(cfg, 2)
+    utts = [0, 7, 11]
+    cond, u = synth.make_batch(cfg, N, utts, hop)
+    m = L.Model.from_config(cfg).load(w).set_kernel("tc")
+    codes = m.generate(dev(cond), dev(u), hop)
+    lg = m.logits(dev(cond), codes, hop).cpu().numpy()
+    codes = codes.cpu().numpy()
+    for i in range(len(utts)):
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[i], hop, N, uniforms=u[i])
+        assert np.array_equal(codes[i], ref), i
+        _, ref_lg, _ = oracle_tf(cfg, w, cond[i], hop, codes[i])
+        err = float(np.max(np.abs(lg[i].astype(np.float64) - ref_lg)))
+        assert err <= FP32_FAITHFUL, (i, err)
