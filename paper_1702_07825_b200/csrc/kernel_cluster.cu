@@ -49,20 +49,24 @@ constexpr int kThreads = kAux + kMath;
 constexpr int kTmemCols = 512;
 constexpr uint64_t kTimeoutNs = 2000000000ull;
 
-// named barriers (0 is __syncthreads)
+// named barriers (0 is __syncthreads).  A producer that only arrives gets one id per use
+// within a sample, so it can never lap its consumer on one barrier.
 constexpr int kBarMath = 1;  // A + B + C, 384 threads (CTA 0 sampler hand-off, teardown)
-constexpr int kBarH = 2;     // chain: A and B sync (h^(j) ready), 256
-constexpr int kBarXR = 3;    // chain: B arrives (x^(j) ready), C syncs, 256
-constexpr int kBarRA = 4;    // chain: C arrives (R ready), A syncs, 256; kBarRA + 3 for the second R
-                             // of the sample (a separate id, so C can never lap A on one barrier)
+constexpr int kBarH = 2;     // chain: A and B sync (h of a non-final local layer ready), 256
+__device__ __forceinline__ constexpr int bar_xr(int jl) { return 3 + jl; }  // chain: B arrives x_{j0+jl}
+                                                                            // (jl = 0, 1), C syncs, 256
 constexpr int kBarAux = 5;   // X, 128
 constexpr int kBarHS = 6;    // head / skip: A + B, 256
-constexpr int kBarHX = 8;    // chain: A arrives (h^(j) in hs), X syncs and forwards it, 256;
-                             // one id per local layer (8, 9, 10) so A can never lap X
+__device__ __forceinline__ constexpr int bar_ra(int jl) { return jl == 0 ? 7 : 10 + jl; }  // chain: C arrives
+                                                                            // R_{j0+jl}, A syncs, 256 (7, 11, 12)
+constexpr int kBarHX = 8;    // chain: A arrives (h of local layer jl in hs), X syncs and forwards it,
+                             // 256; one id per local layer (8, 9, 10)
 
-// chain TMEM columns (per lane): A [0,192) W_cur^(j0), M^(j0), M^(j0+1);
-// C [192,320) W_cur^(j0+1), W_cur^(j0+2); B [320,416) W_res x 3
-constexpr int kColA = 0, kColC = 192, kColB = 320;
+// chain TMEM columns (per lane), local layer jl = 0..2 of layers j0..j0+2:
+//   A [0,192)   : W_cur_0 (CTA 0, jl = 0) or M_j = W_cur_j W_res_{j-1}   (64 each)
+//   C [192,384) : W_cur_j                                                 (64 each)
+//   B [384,480) : W_res_{j-1}                                             (32 each)
+constexpr int kColA = 0, kColC = 192, kColB = 384, kColEnd = 480;
 
 enum Role { kChain = 0, kHead = 1, kSkip = 2, kIdle = 3 };
 
@@ -75,21 +79,23 @@ constexpr int kHLen = 80;   // 64-vector in 4 chunks of 16
 constexpr int kVLen = 320;  // 256-vector in 16 chunks of 16 (or 8)
 
 struct __align__(16) Mail {
-  uint64_t bar_xin, bar_logits, bar_pre, bar_done, bar_part, bar_za, bar_exit;
+  uint64_t bar_hin, bar_xin, bar_logits, bar_pre, bar_done, bar_part, bar_za, bar_exit;
   uint64_t bar_h[kCMaxSlot];
   int abort_flag;
-  uint32_t tmem_base;                    // tensor-memory allocation (column 0, lane 0)
-  alignas(16) float xs[LPC + 1][kHLen];  // chain: layer inputs (pad16); xs[0] is the inbound x
-  float rr[LPC][2 * R];                  // chain: R^(j) = W_cur^(j) x^(j-2) + W_cur^(j) B_res^(j-1) from C
-  float xsave0[R];                       // chain: copy of the inbound x for the aux warpgroup
-  float pre[LPC][2 * R];                 // chain: W_prev x_{n-d} + B + L for the coming sample
-  float xp[R];                           // chain aux scratch
-  float hs[LPC][kHLen];                  // chain: h handed from A to B (pad16)
-  float logits_in[kLevels];              // CTA 0: inbound logits
-  float hbuf[kCMaxSlot][kHLen];          // skip: h^(j) per owned slot; head: slot 0 = h^(l) (pad16)
-  float part[kCMaxSkip][256];            // head: skip partials
-  float za_in[kVLen];                    // head: all-gathered z_a (pad16)
-  float zs[kVLen];                       // head: z_s (cpad<s/16>); skip: partial staging
+  uint32_t tmem_base;                       // tensor-memory allocation (column 0, lane 0)
+  // chain CTA with layers j0..j0+nl-1 (x_j = input of layer j, h_j = its gate output):
+  alignas(16) float hin[kHLen];             // h_{j0-1} from the previous chain CTA (pad16)
+  alignas(16) float xin[kHLen];             // x_{j0-1} from the previous chain CTA (pad16)
+  alignas(16) float xs[2][LPC][kHLen];      // [sample parity][jl] x_{j0+jl} (pad16); CTA 0: xs[.][0] = embedding
+  alignas(16) float hs[2][LPC][kHLen];      // [sample parity][jl] h_{j0+jl} (pad16)
+  float rr[LPC][2 * R];                     // R_j = W_cur_j x_{j-1} + W_cur_j B_res_{j-1}, from C
+  float pre[LPC][2 * R];                    // W_prev x_{n-d} + B + L for the coming sample, from X
+  float xp[R];                              // X scratch
+  float logits_in[kLevels];                 // CTA 0: inbound logits
+  float hbuf[kCMaxSlot][kHLen];             // skip: h^(j) per owned slot; head: slot 0 = h^(l) (pad16)
+  float part[kCMaxSkip][256];               // head: skip partials
+  float za_in[kVLen];                       // head: all-gathered z_a (pad16)
+  float zs[kVLen];                          // head: z_s (cpad<s/16>); skip: partial staging
   double dscr[8];
   float fscr[8];
   int iscr[16];
@@ -190,6 +196,29 @@ __device__ __forceinline__ void tile_dot(const float* w, const float* v, float (
   for (int m = 0; m < RQ; ++m) acc[m] = e[m] + o[m];
 }
 
+// Register tile x one 32-column half of a padded 64-vector (two 16-float chunks at v and
+// v + 20): acc[m] = sum_c w[m*32 + c] * vec[c]; four accumulators per row (c % 4) for ILP,
+// combined in a fixed order (bitwise deterministic).
+template <int RQ>
+__device__ __forceinline__ void tile_dot_half(const float* w, const float* v, float (&acc)[RQ]) {
+  float s[RQ][4];
+#pragma unroll
+  for (int m = 0; m < RQ; ++m) s[m][0] = s[m][1] = s[m][2] = s[m][3] = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 32; c += 4) {
+    const float4 x = lds4(v + c + ((c >> 4) << 2));
+#pragma unroll
+    for (int m = 0; m < RQ; ++m) {
+      s[m][0] = fmaf(w[m * 32 + c], x.x, s[m][0]);
+      s[m][1] = fmaf(w[m * 32 + c + 1], x.y, s[m][1]);
+      s[m][2] = fmaf(w[m * 32 + c + 2], x.z, s[m][2]);
+      s[m][3] = fmaf(w[m * 32 + c + 3], x.w, s[m][3]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < RQ; ++m) acc[m] = (s[m][0] + s[m][1]) + (s[m][2] + s[m][3]);
+}
+
 // One transposing level of a butterfly reduction: lanes whose `bit` is set keep
 // the upper half of the row values and send the lower half to their partner,
 // which keeps the lower half.  Halves the row count per lane with N/2 shuffles.
@@ -244,7 +273,7 @@ __device__ __forceinline__ int sample_warp(const float* logits, float u, int lan
   return y < kLevels ? y : __reduce_max_sync(0xffffffffu, (unsigned)(lastpos + 1)) - 1;
 }
 
-// Draw y_{n-1} from the inbound logits (App. A.4) and write x^(0)_n (step 1) into xs[0]
+// Draw y_{n-1} from the inbound logits (App. A.4) and write x^(0)_n (step 1) into xs[n&1][0]
 // with the first warp of warpgroup A; warpgroups A, B, C wait at the closing barrier.
 template <bool TRACE>
 __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx, int64_t n, int k, int& y1,
@@ -280,8 +309,9 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
       ep1 = __ldg(embp_g + y2 * R + k + 32);
     }
     // x^(0)_n = W_emb_prev[:, y_{n-2}] + W_emb_cur[:, y_{n-1}] + B_emb
-    m.xs[0][pad16(k)] = (ep0 + wembc[y1 * R + k]) + bemb[k];
-    m.xs[0][pad16(k + 32)] = (ep1 + wembc[y1 * R + k + 32]) + bemb[k + 32];
+    float* x0 = m.xs[n & 1][0];
+    x0[pad16(k)] = (ep0 + wembc[y1 * R + k]) + bemb[k];
+    x0[pad16(k + 32)] = (ep1 + wembc[y1 * R + k + 32]) + bemb[k + 32];
   }
   ptx::bar_sync(kBarMath, kMath);
 }
@@ -309,27 +339,41 @@ __device__ __forceinline__ uint32_t tmem_lane_addr(const Mail& m) {
   return m.tmem_base + ((uint32_t)(32 * ((threadIdx.x >> 5) & 3)) << 16);
 }
 
-// Shared-memory image of a chain CTA (floats): W_prev [LPC][R (k)][2R (i)], B [LPC][2R],
-// B_res [LPC][R], c = W_cur^(j+1) B_res^(j) [LPC-1][2R]; CTA 0 adds W_emb_cur^T [256][R], B_emb [R].
+// Shared-memory image of a chain CTA (floats), local layer jl of layer j = j0 + jl:
+// W_prev_j [LPC][R (k)][2R (i)], B_j [LPC][2R], B_res_{j-1} [LPC][R], c_j = W_cur_j B_res_{j-1}
+// [LPC][2R]; CTA 0 adds W_emb_cur^T [256][R], B_emb [R].
 constexpr int kSmB = LPC * R * 2 * R;
 constexpr int kSmBres = kSmB + LPC * 2 * R;
 constexpr int kSmFold = kSmBres + LPC * R;
-constexpr int kSmEmb = kSmFold + (LPC - 1) * 2 * R;
+constexpr int kSmEmb = kSmFold + LPC * 2 * R;
+
+// The chain, per chain CTA c with layers j0..j0+nl-1 (x_j = input of layer j, h_j = its gate
+// output, a_j = W_cur_j x_j + pre_j, x_{j+1} = x_j + W_res_j h_j + B_res_j):
+// a_j is evaluated as M_j h_{j-1} + R_j with M_j = W_cur_j W_res_{j-1} (folded on the host, R22)
+// and R_j = W_cur_j x_{j-1} + W_cur_j B_res_{j-1}, so only ONE matvec per layer (A) sits on the
+// sample's critical chain, also across CTAs: CTA c >= 1 receives h_{j0-1} (from the previous A,
+// the critical hop) and x_{j0-1} (from the previous B, one layer earlier).  CTA 0 starts from the
+// embedding x_0 and evaluates a_0 = W_cur_0 x_0 directly.
+//   A: a_j, gate -> h_j (and for the CTA's last layer: h straight to the next CTA / the heads)
+//   B: x_{j0+jl} = x_{j0+jl-1} + W_res h_{j0+jl-1} + B_res (queues, C, next CTA)
+//   C: R_{j0+jl} from x_{j0+jl-1}
+//   X: forwards h to skip / head CTAs, dilation queues, pre for the coming sample
+// Warpgroups A, C: thread a owns rows {g, R+g} (tanh g, sigmoid g), g = a / 2, columns
+// [32 half, 32 half + 32), half = a % 2 -- one shuffle finishes both rows in both lanes of the
+// pair, where the gate runs.  B: row g of W_res, same columns.
 
 // ------------------------------------------------------------------ chain CTA, warpgroup A (the chain)
-// Thread a: rows {g, 64+g, 32+g, 96+g} (tanh g, sigmoid g, tanh 32+g, sigmoid 32+g),
-// g = a / 4, columns [16 cc, 16 cc + 16), cc = a % 4.  Layer jl uses TMEM columns
-// kColA + 64 jl: W_cur^(j0) for jl = 0, M^(j0+jl-1) = W_cur^(j0+jl) W_res^(j0+jl-1) after.
 template <bool TRACE>
 __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
   const int a = threadIdx.x - kAux;  // 0..127 (also the sampler's thread index)
-  const int g = a >> 2, cc = a & 3;
-  const int hrow = g + ((cc & 2) ? 32 : 0);  // h index this lane finishes (tanh row; sigmoid = +64)
-  const bool writer = (cc & 1) == 0;
-  const int first = pl.chain_first[c], nl = pl.chain_nl[c];
+  const int hrow = a >> 1, half = a & 1;  // rows hrow (tanh) and R + hrow (sigmoid), columns [32 half, +32)
+  const bool writer = half == 0;
+  const int voff = 40 * half;             // padded offset of column 32 half
+  const int nl = pl.chain_nl[c];
+  const bool last_cta = (c == pl.nc - 1);
   const uint32_t tm = tmem_lane_addr(m) + kColA;
   const float* wembc = sw + kSmEmb;  // CTA 0: [256][R]
   const float* bemb = wembc + kLevels * R;
@@ -337,41 +381,51 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
   float w[64];
 
   for (int64_t n = 0; n < A.N; ++n) {
-    ptx::tmem_load_async<64>(tm, w);  // W_cur^(j0), hidden behind the waits
+    const int p = (int)(n & 1);
+    ptx::tmem_load_async<64>(tm, w);  // layer j0's tile, hidden behind the waits
     if (c == 0) {
       sample_and_embed<TRACE>(P, cx, n, a, y1, y2, wembc, bemb);
     } else {
-      if (wait(cx, &m.bar_xin, (uint32_t)(n & 1), 12) && a == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_xin), R * 4);
+      if (wait(cx, &m.bar_hin, (uint32_t)p, 12) && a == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_hin), R * 4);
     }
     if (a == 0) trace<TRACE>(A, n, 0);
-    wait(cx, &m.bar_pre, (uint32_t)(n & 1), 13);
+    wait(cx, &m.bar_pre, (uint32_t)p, 13);
     ptx::tmem_wait_ld<64>(w);
 #pragma unroll
     for (int jl = 0; jl < LPC; ++jl) {
       if (jl < nl) {
-        const int j = first + jl;
+        const bool direct = (c == 0 && jl == 0);  // a_0 = W_cur_0 x_0
         if (a == 0) trace_clk<TRACE>(A, n, 8 + 2 * jl);
-        // layer 0: W_cur^(j0) x_in ; later layers: M^(j-1) h^(j-1) (PAPER.md:354 with 437 folded in)
-        float v[4];
-        tile_dot<4, 16>(w, jl == 0 ? &m.xs[0][20 * cc] : &m.hs[jl - 1][20 * cc], v);
+        const float pre0 = m.pre[jl][hrow], pre1 = m.pre[jl][R + hrow];
+        float v[2];
+        tile_dot_half<2>(w, (direct ? m.xs[p][0] : (jl == 0 ? m.hin : m.hs[p][jl - 1])) + voff, v);
         if (jl + 1 < nl) ptx::tmem_load_async<64>(tm + 64 * (jl + 1), w);  // next layer's tile
-        xpose_level<4>(v, cc, 2);  // lanes cc & 2 now carry (tanh 32+g, sigmoid 32+g)
-        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);  // both lanes of the pair: full (tanh, sigmoid) rows
         v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
-        if (jl > 0) {
-          ptx::bar_sync(jl == 1 ? kBarRA : kBarRA + 3, kMain);  // R^(j) from C
+        if (!direct) {
+          ptx::bar_sync(bar_ra(jl), kMain);  // R_j from C
           v[0] += m.rr[jl][hrow];
           v[1] += m.rr[jl][R + hrow];
         }
         // a = a_cur + (W_prev x_{n-d} + B + L); h = tanh(a_h) sigma(a_g)
-        const float hv = gate_fast(v[0] + m.pre[jl][hrow], v[1] + m.pre[jl][R + hrow]);
-        if (writer) m.hs[jl][pad16(hrow)] = hv;
-        ptx::bar_sync(kBarH, kMain);  // h^(j) complete for A (next layer) and B
-        bar_arrive(kBarHX + jl, kMain);  // ... and for X, which forwards it to the skip / head CTAs
-        if (a == 0) trace_clk<TRACE>(A, n, 9 + 2 * jl);
-        (void)hv;
-        (void)j;
-        if (jl + 1 < nl) ptx::tmem_wait_ld<64>(w);
+        const float hv = gate_fast(v[0] + pre0, v[1] + pre1);
+        if (jl + 1 == nl) {
+          // the CTA's last layer: h goes straight to the next chain CTA (or, for layer l, to the
+          // four heads) -- the only hop on the critical chain between two CTAs
+          // four heads: X sends one 16-byte st.async per thread (one instruction)
+          if (writer) {
+            if (!last_cta) ptx::st_async(remote(&m.hin[pad16(hrow)], c + 1), hv, remote(&m.bar_hin, c + 1));
+            m.hs[p][jl][pad16(hrow)] = hv;
+          }
+          bar_arrive(kBarHX + jl, kMain);  // X forwards h_{L-1}, h_{L-2} / skip-layer h
+          if (a == 0) trace_clk<TRACE>(A, n, 9 + 2 * jl);
+        } else {
+          if (writer) m.hs[p][jl][pad16(hrow)] = hv;
+          ptx::bar_sync(kBarH, kMain);     // h_j complete for A (next layer) and B
+          bar_arrive(kBarHX + jl, kMain);  // ... and for X, which forwards it to the skip / head CTAs
+          if (a == 0) trace_clk<TRACE>(A, n, 9 + 2 * jl);
+          ptx::tmem_wait_ld<64>(w);
+        }
       }
     }
   }
@@ -379,9 +433,9 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
 }
 
 // ------------------------------------------------------------------ chain CTA, warpgroup B (x updates)
-// Thread b: rows {g, 32+g} of W_res, g = b / 4, columns [16 cc, +16), cc = b % 4.
-// x^(j) = x^(j-1) + W_res h^(j) + B_res: for the dilation queues, for
-// C's R^(j+2), and (last layer) for the next chain CTA.
+// x_{j0+jl} = x_{j0+jl-1} + W_res_{j0+jl-1} h_{j0+jl-1} + B_res_{j0+jl-1} for
+// jl >= xb (CTA 0 starts from the embedding): for the dilation queues, for C, and (jl = nl-1)
+// for the next chain CTA.
 template <bool TRACE>
 __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
@@ -389,45 +443,53 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
   Mail& m = *cx.mail;
   const int b = threadIdx.x - kAux - 128;  // 0..127
   const int k = threadIdx.x - kAux;        // sampler thread index (>= 128: waits only)
-  const int g = b >> 2, cc = b & 3;
-  const int row = g + ((cc & 2) ? 32 : 0);  // row of x this lane finishes
-  const bool writer = (cc & 1) == 0;
-  const int first = pl.chain_first[c], nl = pl.chain_nl[c];
+  const int row = b >> 1, half = b & 1;    // row of x this lane pair finishes, columns [32 half, +32)
+  const bool writer = half == 0;
+  const int voff = 40 * half;
+  const int nl = pl.chain_nl[c];
+  const int xb = (c == 0) ? 1 : 0;
   const bool last_cta = (c == pl.nc - 1);
   const uint32_t tm = tmem_lane_addr(m) + kColB;
-  const float* bres = sw + kSmBres;  // [LPC][R]
+  const float* bres = sw + kSmBres;  // [LPC][R]: B_res_{j0+jl-1}
   const float* wembc = sw + kSmEmb;
   const float* bemb = wembc + kLevels * R;
   int y1 = kLevels / 2, y2 = kLevels / 2;
   float wr[32];
 
   for (int64_t n = 0; n < A.N; ++n) {
+    const int p = (int)(n & 1);
     if (c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
 #pragma unroll
     for (int jl = 0; jl < LPC; ++jl) {
-      if (jl < nl) {
-        const int j = first + jl;
-        if (j < pl.L - 1) ptx::tmem_load_async<32>(tm + 32 * jl, wr);
-        ptx::bar_sync(kBarH, kMain);  // h^(j) from A (implies xs[0] is valid)
-        const float xi = m.xs[jl][pad16(row)];
-        if (jl == 0 && writer) m.xsave0[row] = xi;
-        if (j < pl.L - 1) {
-          ptx::tmem_wait_ld<32>(wr);
-          float v[2];
-          tile_dot<2, 16>(wr, &m.hs[jl][20 * cc], v);
-          xpose_level<2>(v, cc, 2);
-          v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-          const float xn = xi + (v[0] + bres[jl * R + row]);
-          if (writer) {
-            if (jl + 1 < nl) m.xs[jl + 1][pad16(row)] = xn;
-            else if (!last_cta)
-              ptx::st_async(remote(&m.xs[0][pad16(row)], c + 1), xn, remote(&m.bar_xin, c + 1));
-          }
-          if (jl + 2 < nl) bar_arrive(kBarXR, kMain);  // x^(j) ready: C computes R^(j+2)
+      if (jl < nl && jl >= xb) {
+        ptx::tmem_load_async<32>(tm + 32 * jl, wr);
+        const float* hv;
+        const float* xv;
+        if (jl == 0) {  // inbound h_{j0-1}, x_{j0-1}
+          wait(cx, &m.bar_xin, (uint32_t)p, 16);
+          wait(cx, &m.bar_hin, (uint32_t)p, 17);
+          hv = m.hin;
+          xv = m.xin;
+        } else {
+          ptx::bar_sync(kBarH, kMain);  // h_{j0+jl-1} from A
+          hv = m.hs[p][jl - 1];
+          xv = m.xs[p][jl - 1];
         }
+        const float xi = xv[pad16(row)];
+        ptx::tmem_wait_ld<32>(wr);
+        float v[1];
+        tile_dot_half<1>(wr, hv + voff, v);
+        v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+        const float xn = xi + (v[0] + bres[jl * R + row]);
+        if (writer) {
+          m.xs[p][jl][pad16(row)] = xn;
+          if (jl + 1 == nl && !last_cta)
+            ptx::st_async(remote(&m.xin[pad16(row)], c + 1), xn, remote(&m.bar_xin, c + 1));
+        }
+        if (jl + 1 < nl) bar_arrive(bar_xr(jl), kMain);  // x_{j0+jl} ready: C computes R_{j0+jl+1}
       }
     }
-    // the sample's layers are done: the aux warpgroup may read xs / xsave0
+    // the sample's x are all in xs[p]: the aux warpgroup may read them
     if (b == 0) {
       trace<TRACE>(A, n, 2);
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_done));
@@ -437,8 +499,8 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
 }
 
 // ------------------------------------------------------------------ chain CTA, warpgroup C (R terms)
-// R^(j0+1) = W_cur^(j0+1) x_in + c^(j0) as soon as x_in is there; R^(j0+2) =
-// W_cur^(j0+2) x^(j0) + c^(j0+1) once B has x^(j0).  Same tile mapping as A.
+// R_{j0+jl} = W_cur_{j0+jl} x_{j0+jl-1} + c_{j0+jl} for jl >= xb: jl = 0 from the inbound x_{j0-1},
+// jl >= 1 from x_{j0+jl-1} (B, or the embedding on CTA 0).
 template <bool TRACE>
 __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
@@ -446,42 +508,44 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
   Mail& m = *cx.mail;
   const int ct = threadIdx.x - kAux - 256;  // 0..127
   const int k = threadIdx.x - kAux;         // sampler thread index (>= 256: waits only)
-  const int g = ct >> 2, cc = ct & 3;
-  const int hrow = g + ((cc & 2) ? 32 : 0);
-  const bool writer = (cc & 1) == 0;
+  const int hrow = ct >> 1, half = ct & 1;  // same mapping as A
+  const bool writer = half == 0;
+  const int voff = 40 * half;
   const int nl = pl.chain_nl[c];
+  const int xb = (c == 0) ? 1 : 0;
   const uint32_t tm = tmem_lane_addr(m) + kColC;
-  const float* cf = sw + kSmFold;  // [LPC-1][2R]
+  const float* cf = sw + kSmFold;  // [LPC][2R]
   const float* wembc = sw + kSmEmb;
   const float* bemb = wembc + kLevels * R;
   int y1 = kLevels / 2, y2 = kLevels / 2;
   float w[64];
 
   for (int64_t n = 0; n < A.N; ++n) {
-    if (nl >= 2) ptx::tmem_load_async<64>(tm, w);
-    if (c == 0) {
-      sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
-    } else {
-      wait(cx, &m.bar_xin, (uint32_t)(n & 1), 15);
-    }
+    const int p = (int)(n & 1);
+    if (nl > xb) ptx::tmem_load_async<64>(tm + 64 * xb, w);
+    if (c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
 #pragma unroll
-    for (int jl = 1; jl < LPC; ++jl) {
-      if (jl < nl) {
-        if (jl == 2) {
-          ptx::tmem_load_async<64>(tm + 64, w);
-          ptx::bar_sync(kBarXR, kMain);  // x^(j0) from B
+    for (int jl = 0; jl < LPC; ++jl) {
+      if (jl < nl && jl >= xb) {
+        const float* xv;
+        if (jl == 0) {
+          if (wait(cx, &m.bar_xin, (uint32_t)p, 15) && ct == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_xin), R * 4);
+          xv = m.xin;
+        } else {
+          if (jl - 1 >= xb) ptx::bar_sync(bar_xr(jl - 1), kMain);  // x_{j0+jl-1} from B
+          xv = m.xs[p][jl - 1];
         }
         ptx::tmem_wait_ld<64>(w);
-        float v[4];
-        tile_dot<4, 16>(w, &m.xs[jl - 1][20 * cc], v);
-        xpose_level<4>(v, cc, 2);
+        float v[2];
+        tile_dot_half<2>(w, xv + voff, v);
+        if (jl + 1 < nl) ptx::tmem_load_async<64>(tm + 64 * (jl + 1), w);
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
         v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
         if (writer) {
-          m.rr[jl][hrow] = v[0] + cf[(jl - 1) * 2 * R + hrow];
-          m.rr[jl][R + hrow] = v[1] + cf[(jl - 1) * 2 * R + R + hrow];
+          m.rr[jl][hrow] = v[0] + cf[jl * 2 * R + hrow];
+          m.rr[jl][R + hrow] = v[1] + cf[jl * 2 * R + R + hrow];
         }
-        bar_arrive(jl == 1 ? kBarRA : kBarRA + 3, kMain);
+        bar_arrive(bar_ra(jl), kMain);
       }
     }
   }
@@ -489,8 +553,30 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
 }
 
 // ------------------------------------------------------------------ chain CTA, warpgroup X (aux)
-// For the coming sample n: queue write of x^(j-1)_{n-1}, queue read of x^(j-1)_{n-d},
-// pre = B + L^(j)_{n/hop} + W_prev x^(j-1)_{n-d}  (Fig. 2 aux threads).
+// Forward h of sample n-1 as A publishes it: layers l-1 and l-2 to the heads' slots 0 and 1,
+// every other layer's to its skip CTA (16 x 16 B per
+// destination; a DSMEM store holds its warp for about one hop, hence not on A).
+__device__ __forceinline__ void aux_forward(const ClusterPlan& pl, Mail& m, int first, int nl, int at, int p) {
+  for (int jl = 0; jl < nl; ++jl) {
+    const int j = first + jl;
+    ptx::bar_sync(kBarHX + jl, kMain);
+    if (j >= pl.L - 2) {
+      const int sl = pl.L - 1 - j;
+      if (at < 16 * NH) {
+        const int hh = at >> 4, e = at & 15, off = 20 * (e >> 2) + 4 * (e & 3);
+        ptx::st_async4(remote(&m.hbuf[sl][off], pl.nc + hh), lds4(&m.hs[p][jl][off]),
+                       remote(&m.bar_h[sl], pl.nc + hh));
+      }
+    } else if (at < 16) {
+      const int off = 20 * (at >> 2) + 4 * (at & 3);
+      const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
+      ptx::st_async4(remote(&m.hbuf[sl][off], kk), lds4(&m.hs[p][jl][off]), remote(&m.bar_h[sl], kk));
+    }
+  }
+}
+
+// For the coming sample n: queue write of x_j(n-1), queue read of x_j(n-d),
+// pre = B + L_j(n/hop) + W_prev x_j(n-d)  (Fig. 2 aux threads).
 template <bool TRACE>
 __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
@@ -503,27 +589,10 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
   const int L = A.L;
 
   for (int64_t n = 0; n < A.N; ++n) {
+    const int pp = (int)((n - 1) & 1);  // parity of sample n-1
     if (n > 0) {
-      // forward h^(j) of sample n-1, layer by layer as A publishes it: to its skip CTA, or
-      // (last two layers) to the four heads; 16 x 16 B per destination.  Kept off A
-      // because a DSMEM store holds its warp for about one hop.
-      for (int jl = 0; jl < nl; ++jl) {
-        const int j = first + jl;
-        ptx::bar_sync(kBarHX + jl, kMain);
-        if (j >= pl.L - 2) {
-          if (at < 16 * NH) {
-            const int hh = at >> 4, e = at & 15, off = 20 * (e >> 2) + 4 * (e & 3);
-            const int sl = pl.L - 1 - j;
-            ptx::st_async4(remote(&m.hbuf[sl][off], pl.nc + hh), lds4(&m.hs[jl][off]),
-                           remote(&m.bar_h[sl], pl.nc + hh));
-          }
-        } else if (at < 16) {
-          const int off = 20 * (at >> 2) + 4 * (at & 3);
-          const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
-          ptx::st_async4(remote(&m.hbuf[sl][off], kk), lds4(&m.hs[jl][off]), remote(&m.bar_h[sl], kk));
-        }
-      }
-      wait(cx, &m.bar_done, (uint32_t)((n - 1) & 1), 14);
+      aux_forward(pl, m, first, nl, at, pp);
+      wait(cx, &m.bar_done, (uint32_t)pp, 14);
     }
     const int64_t f = n / A.hop;
     for (int jl = 0; jl < nl; ++jl) {
@@ -532,7 +601,7 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       const float lv = __ldg(A.cond + (f * L + j) * 2 * R + at);
       if (at < R) {
         float* ring = A.ring + A.ring_off[j];
-        const float xc = (jl == 0) ? m.xsave0[at] : m.xs[jl][pad16(at)];  // x^(j-1)_{n-1}
+        const float xc = m.xs[pp][jl][pad16(at)];  // x_j(n-1) (unused when n = 0)
         float xpv = 0.0f;
         if (n - d >= 0) xpv = (d == 1) ? xc : ring[(int64_t)(n % d) * R + at];  // slot of n-d
         if (n > 0 && d >= 2) ring[(int64_t)((n - 1) % d) * R + at] = xc;
@@ -557,23 +626,7 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_pre));
     }
   }
-  if (A.N > 0) {  // forward the last sample's h (same as above)
-    for (int jl = 0; jl < nl; ++jl) {
-      const int j = first + jl;
-      ptx::bar_sync(kBarHX + jl, kMain);
-      if (j >= pl.L - 2) {
-        if (at < 16 * NH) {
-          const int hh = at >> 4, e = at & 15, off = 20 * (e >> 2) + 4 * (e & 3);
-          const int sl = pl.L - 1 - j;
-          ptx::st_async4(remote(&m.hbuf[sl][off], pl.nc + hh), lds4(&m.hs[jl][off]), remote(&m.bar_h[sl], pl.nc + hh));
-        }
-      } else if (at < 16) {
-        const int off = 20 * (at >> 2) + 4 * (at & 3);
-        const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
-        ptx::st_async4(remote(&m.hbuf[sl][off], kk), lds4(&m.hs[jl][off]), remote(&m.bar_h[sl], kk));
-      }
-    }
-  }
+  if (A.N > 0) aux_forward(pl, m, first, nl, at, (int)((A.N - 1) & 1));  // the last sample's h
 }
 
 // ------------------------------------------------------------------ head CTA (rows [64h, 64h+64))
@@ -591,11 +644,10 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
   constexpr int CZ = S / 16;         // z_s columns per thread
   // TMEM tiles (this thread's lane): W_skip^(l) [RQ*16], W_relu [4*CZ], W_out [64]
   const uint32_t tm = tmem_lane_addr(m) + (k < 128 ? 0 : 256);
-  constexpr int cRelu = RQ * 16, cOut = RQ * 16 + 4 * CZ;
+  constexpr int cRelu = RQ * 16, cOut = RQ * 16 + 4 * CZ, cSk2 = RQ * 16 + 4 * CZ + 64;
   const float* bskip = sw;          // [S]
   const float* brelu = sw + S;      // [64]
   const float* bout = sw + S + 64;  // [64]
-  const float* wsk2 = sw + S + 128; // W_skip^(l-1) in shared memory, [q/4][k][4]
   const bool has2 = pl.L >= 2;
   const int g = k >> 2, cc = k & 3;
   const int qrow = g + 64 * ((RQ == 4) ? cc : (cc >> 1));  // q row this lane finishes
@@ -618,23 +670,22 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
 
   for (int64_t n = 0; n < A.N; ++n) {
     const uint32_t par = (uint32_t)(n & 1);
-    ptx::tmem_load_async<RQ * 16>(tm, w);  // W_skip^(l) tile, hidden behind the waits
     // q = B_skip + sum_k partial_k + W_skip^(l-1) h^(l-1) + W_skip^(l) h^(l); z_s = relu(q)
-    // (PAPER.md:365-372).  W_skip^(l-1) is applied here, from shared memory, while the
-    // last layer runs, so no skip CTA sits between the chain and the head.
+    // (PAPER.md:365-372).  W_skip^(l-1) is applied here, from tensor memory, while the last
+    // layer runs, so no skip CTA sits between the chain and the head (and the head's shared
+    // memory stays free for the inbound DSMEM traffic).
     float d2 = 0.0f;
     if (has2) {
+      ptx::tmem_load_async<RQ * 16>(tm + cSk2, w);  // W_skip^(l-1) tile
       if (wait(cx, &m.bar_h[1], par, 24) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[1]), R * 4);
-      float wl[RQ * 16];
-#pragma unroll
-      for (int q = 0; q < RQ * 16; q += 4) {
-        const float4 x = lds4(wsk2 + (q / 4 * kMain + k) * 4);
-        wl[q] = x.x; wl[q + 1] = x.y; wl[q + 2] = x.z; wl[q + 3] = x.w;
-      }
+      if (k == 0) trace<TRACE>(A, n, 4);
+      ptx::tmem_wait_ld<RQ * 16>(w);
       float v2[RQ];
-      tile_dot<RQ, 16>(wl, &m.hbuf[1][20 * cc], v2);
+      tile_dot<RQ, 16>(w, &m.hbuf[1][20 * cc], v2);
       d2 = finish(v2);
+      if (k == 0) trace<TRACE>(A, n, 6);
     }
+    ptx::tmem_load_async<RQ * 16>(tm, w);  // W_skip^(l) tile, hidden behind the wait
     if (wait(cx, &m.bar_h[0], par, 21) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[0]), R * 4);
     if (k == 0) trace<TRACE>(A, n, 0);
     ptx::tmem_wait_ld<RQ * 16>(w);
@@ -654,6 +705,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
       m.zs[cpad<CZ>(qrow)] = fmaxf(qv, 0.0f);
     }
     ptx::bar_sync(kBarHS, kMain);
+    if (k == 0) trace<TRACE>(A, n, 7);
     // z_a = relu(W_relu z_s + B_relu)
     ptx::tmem_wait_ld<4 * CZ>(w);
     float za[4];
@@ -664,12 +716,12 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     za[0] += __shfl_xor_sync(0xffffffffu, za[0], 2);
     za[0] += __shfl_xor_sync(0xffffffffu, za[0], 1);
     const float zav = fmaxf(za[0] + brelu[orow], 0.0f);
-    if (owriter) {
+    {  // all four lanes of a quad hold z_a[orow]: lane k%4 sends it to head k%4 (one st.async
+       // per lane -- a st.async holds its warp for about one hop, so never several in a row)
       const int dst = pad16(64 * hidx + orow);
-#pragma unroll
-      for (int hh = 0; hh < NH; ++hh)
-        ptx::st_async(remote(&m.za_in[dst], pl.nc + hh), zav, remote(&m.bar_za, pl.nc + hh));
+      ptx::st_async(remote(&m.za_in[dst], pl.nc + (k & 3)), zav, remote(&m.bar_za, pl.nc + (k & 3)));
     }
+    if (k == 0) trace<TRACE>(A, n, 9);
     if (wait(cx, &m.bar_za, par, 23) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_za), kLevels * 4);
     if (k == 0) trace<TRACE>(A, n, 2);
     // logits = W_out z_a + B_out
@@ -765,6 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   if (t < 32) ptx::tmem_alloc(ptx::smem_u32(&mail->tmem_base), kTmemCols);
   if (t == 0) {
     mail->abort_flag = 0;
+    ptx::mbar_init(ptx::smem_u32(&mail->bar_hin), 1);
     ptx::mbar_init(ptx::smem_u32(&mail->bar_xin), 1);
     ptx::mbar_init(ptx::smem_u32(&mail->bar_logits), 1);
     ptx::mbar_init(ptx::smem_u32(&mail->bar_pre), 1);
@@ -775,6 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     for (int i = 0; i < kCMaxSlot; ++i) ptx::mbar_init(ptx::smem_u32(&mail->bar_h[i]), 1);
     ptx::fence_mbar_init();
     // arm phase 0 of every transaction barrier a role receives on
+    ptx::mbar_arm(ptx::smem_u32(&mail->bar_hin), R * 4);
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_xin), R * 4);
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_logits), kLevels * 4);
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_part), pl.nk * S * 4);
@@ -797,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     int c0 = 0, c1 = 0;
     if (role == kChain) {
       if (wg == 0) { c0 = kColA; c1 = kColC; }
-      else if (wg == 1) { c0 = kColB; c1 = kColB + 3 * 32; }
+      else if (wg == 1) { c0 = kColB; c1 = kColEnd; }
       else { c0 = kColC; c1 = kColB; }
     } else if (wg < 2) {
       c0 = 256 * wg;
@@ -924,7 +978,7 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
   for (int rank = 0; rank < p.size; ++rank) {
     int swf = 0;
     if (rank < p.nc) swf = smem_chain(rank);
-    else if (rank < p.nc + p.nh) swf = s + 128 + (L >= 2 ? qs * kMain : 0);
+    else if (rank < p.nc + p.nh) swf = s + 128;
     else swf = p.skip_nsm[rank - p.nc - p.nh] * lstride;
     p.pk_off[rank] = off;
     p.tm_cols[rank] = kTmemCols;
@@ -985,29 +1039,31 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
     auto put = [&](int col, int lane, float v) { img[(int64_t)col * 128 + lane] = v; };
     if (rank < p.nc) {
       const int first = p.chain_first[rank], nl = p.chain_nl[rank];
+      const int xb = (rank == 0) ? 1 : 0;  // CTA 0's layer 0 takes the embedding directly
+      // local layer jl (layer j = first + jl) with jl >= xb: M_j = W_cur_j W_res_{j-1}, c_j = W_cur_j B_res_{j-1}
       std::vector<std::vector<float>> M(LPC), cf(LPC);
-      for (int jl = 0; jl + 1 < nl; ++jl) fold(first + jl, M[jl], cf[jl]);
+      for (int jl = xb; jl < nl; ++jl) fold(first + jl - 1, M[jl], cf[jl]);
       for (int lane = 0; lane < 128; ++lane) {
-        const int g = lane >> 2, cc = lane & 3;
-        const int arow[4] = {g, R + g, 32 + g, R + 32 + g};  // tanh g, sigmoid g, tanh 32+g, sigmoid 32+g
-        const int brow[2] = {g, 32 + g};
+        const int g = lane >> 1, half = lane & 1;  // rows g (tanh), R + g (sigmoid); columns [32 half, +32)
         for (int jl = 0; jl < nl; ++jl)
           for (int q = 0; q < 64; ++q) {
-            const int row = arow[q / 16], col = 16 * cc + q % 16;
-            put(kColA + 64 * jl + q, lane, jl == 0 ? W(first, o.w_cur, row, col, R) : M[jl - 1][row * R + col]);
-            if (jl >= 1) put(kColC + 64 * (jl - 1) + q, lane, W(first + jl, o.w_cur, row, col, R));
+            const int row = (q < 32) ? g : R + g, col = 32 * half + (q & 31);
+            put(kColA + 64 * jl + q, lane, jl < xb ? W(first, o.w_cur, row, col, R) : M[jl][row * R + col]);
+            if (jl >= xb) put(kColC + 64 * jl + q, lane, W(first + jl, o.w_cur, row, col, R));
           }
-        for (int jl = 0; jl < nl; ++jl)
-          for (int q = 0; q < 32; ++q) put(kColB + 32 * jl + q, lane, W(first + jl, o.w_res, brow[q / 16], 16 * cc + q % 16, R));
+        for (int jl = xb; jl < nl; ++jl)
+          for (int q = 0; q < 32; ++q)
+            put(kColB + 32 * jl + q, lane, W(first + jl - 1, o.w_res, g, 32 * half + q, R));
       }
       for (int jl = 0; jl < nl; ++jl) {
         const int j = first + jl;
         for (int k = 0; k < R; ++k)
           for (int i = 0; i < 2 * R; ++i) sm[jl * R * 2 * R + k * 2 * R + i] = W(j, o.w_prev, i, k, R);
         for (int i = 0; i < 2 * R; ++i) sm[kSmB + jl * 2 * R + i] = w[(int64_t)j * o.layer_stride + o.b + i];
-        for (int i = 0; i < R; ++i) sm[kSmBres + jl * R + i] = w[(int64_t)j * o.layer_stride + o.b_res + i];
-        if (jl + 1 < nl)
+        if (jl >= xb) {
+          for (int i = 0; i < R; ++i) sm[kSmBres + jl * R + i] = w[(int64_t)(j - 1) * o.layer_stride + o.b_res + i];
           for (int i = 0; i < 2 * R; ++i) sm[kSmFold + jl * 2 * R + i] = cf[jl][i];
+        }
       }
       if (rank == 0) {
         float* we = sm + kSmEmb;
@@ -1035,17 +1091,14 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
         sm[s + i] = w[o.b_relu + 64 * hidx + i];
         sm[s + 64 + i] = w[o.b_out + 64 * hidx + i];
       }
-      if (p.L >= 2) {  // W_skip^(l-1), [q/4][k][4]
-        float* w2 = sm + s + 128;
+      if (p.L >= 2)  // W_skip^(l-1) in tensor memory after W_out
         for (int k = 0; k < kMain; ++k) {
+          const int lane = k & 127, cbase = (k < 128) ? 0 : 256;
           const int g = k >> 2, cc = k & 3;
           for (int mm = 0; mm < rq; ++mm)
-            for (int q = 0; q < 16; ++q) {
-              const int qq = mm * 16 + q;
-              w2[((qq / 4) * kMain + k) * 4 + (qq % 4)] = W(p.L - 2, o.w_skip, g + 64 * mm, 16 * cc + q, R);
-            }
+            for (int q = 0; q < 16; ++q)
+              put(cbase + rq * 16 + 4 * cz + 64 + mm * 16 + q, lane, W(p.L - 2, o.w_skip, g + 64 * mm, 16 * cc + q, R));
         }
-      }
     } else {
       const int k = rank - p.nc - p.nh;
       std::vector<int> layers;
