@@ -40,7 +40,7 @@ namespace dvw {
 namespace {
 
 constexpr int R = 64;       // residual channels the kernel is built for
-constexpr int LPC = 3;      // layers per chain CTA
+constexpr int LPC = 4;      // most layers per chain CTA (template LP = 3 or 4 per model)
 constexpr int NH = 4;       // head CTAs (64 output rows each)
 constexpr int kAux = 128;   // threads [0,128): warpgroup X, off-chain work
 constexpr int kMain = 256;  // head / skip math threads: warpgroups A and B, [128,384)
@@ -53,20 +53,20 @@ constexpr uint64_t kTimeoutNs = 2000000000ull;
 // within a sample, so it can never lap its consumer on one barrier.
 constexpr int kBarMath = 1;  // A + B + C, 384 threads (CTA 0 sampler hand-off, teardown)
 constexpr int kBarH = 2;     // chain: A and B sync (h of a non-final local layer ready), 256
-__device__ __forceinline__ constexpr int bar_xr(int jl) { return 3 + jl; }  // chain: B arrives x_{j0+jl}
-                                                                            // (jl = 0, 1), C syncs, 256
-constexpr int kBarAux = 5;   // X, 128
-constexpr int kBarHS = 6;    // head / skip: A + B, 256
-__device__ __forceinline__ constexpr int bar_ra(int jl) { return jl == 0 ? 7 : 10 + jl; }  // chain: C arrives
-                                                                            // R_{j0+jl}, A syncs, 256 (7, 11, 12)
-constexpr int kBarHX = 8;    // chain: A arrives (h of local layer jl in hs), X syncs and forwards it,
-                             // 256; one id per local layer (8, 9, 10)
+constexpr int kBarAux = 3;   // X, 128
+__device__ __forceinline__ constexpr int bar_xr(int jl) { return 4 + jl; }  // chain: B arrives x_{j0+jl}
+                                                                            // (jl = 0..2), C syncs, 256
+__device__ __forceinline__ constexpr int bar_ra(int jl) { return 7 + jl; }  // chain: C arrives R_{j0+jl}
+                                                                            // (jl = 0..3), A syncs, 256
+constexpr int kBarHX = 11;   // chain: A arrives (h of local layer jl in hs), X syncs and forwards it,
+                             // 256; one id per local layer (11..14)
+constexpr int kBarHS = 4;    // head / skip CTAs only (aliases a chain-only id): A + B, 256
 
-// chain TMEM columns (per lane), local layer jl = 0..2 of layers j0..j0+2:
-//   A [0,192)   : W_cur_0 (CTA 0, jl = 0) or M_j = W_cur_j W_res_{j-1}   (64 each)
-//   C [192,384) : W_cur_j                                                 (64 each)
-//   B [384,480) : W_res_{j-1}                                             (32 each)
-constexpr int kColA = 0, kColC = 192, kColB = 384, kColEnd = 480;
+// chain TMEM columns (per lane), local layer jl of layers j0..j0+LP-1:
+//   A [0, 64 LP)       : W_cur_0 (CTA 0, jl = 0) or M_j = W_cur_j W_res_{j-1}   (64 each)
+//   C [64 LP, 128 LP)  : W_cur_j                                                 (64 each)
+//   B [384, 480), LP = 3 only : W_res_{j-1}                                      (32 each)
+constexpr int kColA = 0;
 
 enum Role { kChain = 0, kHead = 1, kSkip = 2, kIdle = 3 };
 
@@ -132,13 +132,16 @@ __device__ __forceinline__ void raise_abort(const Ctx& cx, int code) {
 // hardware).  On the watchdog (2 s without progress) or a cluster-wide abort,
 // return false: the caller runs on without blocking so every CTA reaches the
 // final cluster barrier, and the host sees DVW_E_DEVICE_TIMEOUT.
+// CTA-scope acquire: every hand-off into this CTA is a st.async into its own shared memory,
+// tracked by the mbarrier's transaction count, so observing the phase makes the data visible;
+// a cluster-scope acquire would also invalidate L1 (CCTL.IVALL) on every wake-up.
 __device__ __forceinline__ bool wait(const Ctx& cx, uint64_t* bar, uint32_t parity, int code) {
   const uint32_t b = ptx::smem_u32(bar);
-  if (ptx::mbar_try_wait(b, parity)) return true;
+  if (ptx::mbar_try_wait_cta(b, parity)) return true;
   const uint64_t t0 = ptx::globaltimer();
 #pragma unroll 1
   for (uint32_t i = 1;; ++i) {
-    if (ptx::mbar_try_wait(b, parity)) return true;
+    if (ptx::mbar_try_wait_cta(b, parity)) return true;
     if ((i & 7) == 0) {
       if (*reinterpret_cast<volatile int*>(&cx.mail->abort_flag)) return false;
       if (ptx::globaltimer() - t0 > kTimeoutNs) {
@@ -340,12 +343,18 @@ __device__ __forceinline__ uint32_t tmem_lane_addr(const Mail& m) {
 }
 
 // Shared-memory image of a chain CTA (floats), local layer jl of layer j = j0 + jl:
-// W_prev_j [LPC][R (k)][2R (i)], B_j [LPC][2R], B_res_{j-1} [LPC][R], c_j = W_cur_j B_res_{j-1}
-// [LPC][2R]; CTA 0 adds W_emb_cur^T [256][R], B_emb [R].
-constexpr int kSmB = LPC * R * 2 * R;
-constexpr int kSmBres = kSmB + LPC * 2 * R;
-constexpr int kSmFold = kSmBres + LPC * R;
-constexpr int kSmEmb = kSmFold + LPC * 2 * R;
+// (LP = 4 only) W_res_{j-1} [LPC][8 (q/4)][128 (B thread)][4] (B's row-pair tiles, one
+// conflict-free LDS.128 per 4 columns), B_j [LPC][2R], B_res_{j-1} [LPC][R], c_j = W_cur_j B_res_{j-1} [LPC][2R]; CTA 0 adds
+// W_emb_cur^T [256][R], B_emb [R].  W_prev streams from L2 (the aux warps, off the chain).
+constexpr int kSmWres = 0;
+// LP = 4: W_res tiles; LP = 3: W_prev [3][16][128][4] (at LP = 4 it streams from L2)
+__host__ __device__ constexpr int sm_b(int lp) { return lp == 4 ? LPC * 32 * 128 : 3 * 16 * 128 * 4; }
+__host__ __device__ constexpr int sm_bres(int lp) { return sm_b(lp) + LPC * 2 * R; }
+__host__ __device__ constexpr int sm_fold(int lp) { return sm_bres(lp) + LPC * R; }
+__host__ __device__ constexpr int sm_emb(int lp) { return sm_fold(lp) + LPC * 2 * R; }
+// TMEM: A [0, 64 LP), C [64 LP, 128 LP); at LP = 3 B's W_res tiles sit in [384, 480)
+__host__ __device__ constexpr int col_c(int lp) { return 64 * lp; }
+constexpr int kColB3 = 384;
 
 // The chain, per chain CTA c with layers j0..j0+nl-1 (x_j = input of layer j, h_j = its gate
 // output, a_j = W_cur_j x_j + pre_j, x_{j+1} = x_j + W_res_j h_j + B_res_j):
@@ -363,7 +372,7 @@ constexpr int kSmEmb = kSmFold + LPC * 2 * R;
 // pair, where the gate runs.  B: row g of W_res, same columns.
 
 // ------------------------------------------------------------------ chain CTA, warpgroup A (the chain)
-template <bool TRACE>
+template <int LP, bool TRACE>
 __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -375,7 +384,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
   const int nl = pl.chain_nl[c];
   const bool last_cta = (c == pl.nc - 1);
   const uint32_t tm = tmem_lane_addr(m) + kColA;
-  const float* wembc = sw + kSmEmb;  // CTA 0: [256][R]
+  const float* wembc = sw + sm_emb(LP);  // CTA 0: [256][R]
   const float* bemb = wembc + kLevels * R;
   int y1 = kLevels / 2, y2 = kLevels / 2;
   float w[64];
@@ -392,7 +401,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
     wait(cx, &m.bar_pre, (uint32_t)p, 13);
     ptx::tmem_wait_ld<64>(w);
 #pragma unroll
-    for (int jl = 0; jl < LPC; ++jl) {
+    for (int jl = 0; jl < LP; ++jl) {
       if (jl < nl) {
         const bool direct = (c == 0 && jl == 0);  // a_0 = W_cur_0 x_0
         if (a == 0) trace_clk<TRACE>(A, n, 8 + 2 * jl);
@@ -436,7 +445,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
 // x_{j0+jl} = x_{j0+jl-1} + W_res_{j0+jl-1} h_{j0+jl-1} + B_res_{j0+jl-1} for
 // jl >= xb (CTA 0 starts from the embedding): for the dilation queues, for C, and (jl = nl-1)
 // for the next chain CTA.
-template <bool TRACE>
+template <int LP, bool TRACE>
 __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -449,9 +458,10 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
   const int nl = pl.chain_nl[c];
   const int xb = (c == 0) ? 1 : 0;
   const bool last_cta = (c == pl.nc - 1);
-  const uint32_t tm = tmem_lane_addr(m) + kColB;
-  const float* bres = sw + kSmBres;  // [LPC][R]: B_res_{j0+jl-1}
-  const float* wembc = sw + kSmEmb;
+  const float* wres = sw + kSmWres;  // LP = 4: [LPC][8][128][4] in shared memory
+  const uint32_t tmb = tmem_lane_addr(m) + kColB3;  // LP = 3: tensor memory
+  const float* bres = sw + sm_bres(LP);  // [LPC][R]: B_res_{j0+jl-1}
+  const float* wembc = sw + sm_emb(LP);
   const float* bemb = wembc + kLevels * R;
   int y1 = kLevels / 2, y2 = kLevels / 2;
   float wr[32];
@@ -460,9 +470,17 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
     const int p = (int)(n & 1);
     if (c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
 #pragma unroll
-    for (int jl = 0; jl < LPC; ++jl) {
+    for (int jl = 0; jl < LP; ++jl) {
       if (jl < nl && jl >= xb) {
-        ptx::tmem_load_async<32>(tm + 32 * jl, wr);
+        if constexpr (LP == 3) {
+          ptx::tmem_load_async<32>(tmb + 32 * jl, wr);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; q += 4) {  // W_res tile into registers before the wait
+            const float4 t4 = lds4(wres + ((jl * 8 + q / 4) * 128 + b) * 4);
+            wr[q] = t4.x; wr[q + 1] = t4.y; wr[q + 2] = t4.z; wr[q + 3] = t4.w;
+          }
+        }
         const float* hv;
         const float* xv;
         if (jl == 0) {  // inbound h_{j0-1}, x_{j0-1}
@@ -476,7 +494,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
           xv = m.xs[p][jl - 1];
         }
         const float xi = xv[pad16(row)];
-        ptx::tmem_wait_ld<32>(wr);
+        if constexpr (LP == 3) ptx::tmem_wait_ld<32>(wr);
         float v[1];
         tile_dot_half<1>(wr, hv + voff, v);
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
@@ -501,7 +519,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
 // ------------------------------------------------------------------ chain CTA, warpgroup C (R terms)
 // R_{j0+jl} = W_cur_{j0+jl} x_{j0+jl-1} + c_{j0+jl} for jl >= xb: jl = 0 from the inbound x_{j0-1},
 // jl >= 1 from x_{j0+jl-1} (B, or the embedding on CTA 0).
-template <bool TRACE>
+template <int LP, bool TRACE>
 __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -513,9 +531,9 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
   const int voff = 40 * half;
   const int nl = pl.chain_nl[c];
   const int xb = (c == 0) ? 1 : 0;
-  const uint32_t tm = tmem_lane_addr(m) + kColC;
-  const float* cf = sw + kSmFold;  // [LPC][2R]
-  const float* wembc = sw + kSmEmb;
+  const uint32_t tm = tmem_lane_addr(m) + col_c(LP);
+  const float* cf = sw + sm_fold(LP);  // [LPC][2R]
+  const float* wembc = sw + sm_emb(LP);
   const float* bemb = wembc + kLevels * R;
   int y1 = kLevels / 2, y2 = kLevels / 2;
   float w[64];
@@ -525,7 +543,7 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
     if (nl > xb) ptx::tmem_load_async<64>(tm + 64 * xb, w);
     if (c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
 #pragma unroll
-    for (int jl = 0; jl < LPC; ++jl) {
+    for (int jl = 0; jl < LP; ++jl) {
       if (jl < nl && jl >= xb) {
         const float* xv;
         if (jl == 0) {
@@ -567,7 +585,7 @@ __device__ __forceinline__ void aux_forward(const ClusterPlan& pl, Mail& m, int 
         ptx::st_async4(remote(&m.hbuf[sl][off], pl.nc + hh), lds4(&m.hs[p][jl][off]),
                        remote(&m.bar_h[sl], pl.nc + hh));
       }
-    } else if (at < 16) {
+    } else if (at < 16 && pl.layer_skip_cta[j] >= 0) {
       const int off = 20 * (at >> 2) + 4 * (at & 3);
       const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
       ptx::st_async4(remote(&m.hbuf[sl][off], kk), lds4(&m.hs[p][jl][off]), remote(&m.bar_h[sl], kk));
@@ -575,29 +593,89 @@ __device__ __forceinline__ void aux_forward(const ClusterPlan& pl, Mail& m, int 
   }
 }
 
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+// Chain-skip layers (those no skip CTA holds, j < nxs): this CTA's partial
+// sum_j W_skip_j h_j of sample n-1, W_skip streamed from L2 ([16][S][4], rows at and
+// at + 128), then sent to every head's partial slot.  Off the critical chain: these are the
+// earliest layers, at least two chain CTAs before the heads need the sum.
+template <int S>
+__device__ __forceinline__ void aux_chain_skip(const Params& P, const Ctx& cx, int c, int at, int pp) {
+  const ClusterPlan& pl = P.p;
+  Mail& m = *cx.mail;
+  const int first = pl.chain_first[c], nl = pl.chain_nl[c];
+  constexpr int RR = S / 128;  // rows per thread
+  float part[RR];
+#pragma unroll
+  for (int rr = 0; rr < RR; ++rr) part[rr] = 0.0f;
+  for (int jl = 0; jl < nl; ++jl) {
+    const int j = first + jl;
+    if (j >= pl.nxs) break;
+    const float* wsk = P.pk + pl.wskx_off + (int64_t)j * 16 * S * 4;
+    const float* h = m.hs[pp][jl];
+#pragma unroll
+    for (int rr = 0; rr < RR; ++rr) {
+      float4 wv[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) wv[q] = ldg4(wsk + ((int64_t)q * S + at + 128 * rr) * 4);
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const float4 x = lds4(h + pad16(4 * q));
+        s0 = fmaf(wv[q].x, x.x, s0);
+        s1 = fmaf(wv[q].y, x.y, s1);
+        s2 = fmaf(wv[q].z, x.z, s2);
+        s3 = fmaf(wv[q].w, x.w, s3);
+      }
+      part[rr] += (s0 + s1) + (s2 + s3);
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < RR; ++rr) m.zs[at + 128 * rr] = part[rr];
+  ptx::bar_sync(kBarAux, kAux);
+  const int slot = pl.xpart_slot[c];
+#pragma unroll
+  for (int i = at; i < (S / 4) * NH; i += kAux) {  // S / 4 float4 per head
+    const int hh = i / (S / 4), e = i % (S / 4);
+    ptx::st_async4(remote(&m.part[slot][4 * e], pl.nc + hh), lds4(&m.zs[4 * e]), remote(&m.bar_part, pl.nc + hh));
+  }
+}
+
 // For the coming sample n: queue write of x_j(n-1), queue read of x_j(n-d),
-// pre = B + L_j(n/hop) + W_prev x_j(n-d)  (Fig. 2 aux threads).
-template <bool TRACE>
+// pre = B + L_j(n/hop) + W_prev x_j(n-d)  (Fig. 2 aux threads),
+// W_prev streamed from L2 ([16][128][4]; thread at = row of a).
+template <int S, int LP, bool TRACE>
 __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
   const int at = threadIdx.x;  // 0..127 = row of a (2r rows)
   const int first = pl.chain_first[c], nl = pl.chain_nl[c];
-  const float* wprev = sw;                 // [LPC][R (k)][2R (i)]
-  const float* bj = sw + LPC * R * 2 * R;  // [LPC][2R]
+  const float* bj = sw + sm_b(LP);  // [LPC][2R]
   const int L = A.L;
+  const bool xskip = first < pl.nxs;
 
   for (int64_t n = 0; n < A.N; ++n) {
     const int pp = (int)((n - 1) & 1);  // parity of sample n-1
     if (n > 0) {
       aux_forward(pl, m, first, nl, at, pp);
       wait(cx, &m.bar_done, (uint32_t)pp, 14);
+      if (xskip) aux_chain_skip<S>(P, cx, c, at, pp);
     }
     const int64_t f = n / A.hop;
     for (int jl = 0; jl < nl; ++jl) {
       const int j = first + jl;
       const int d = A.dil[j];
+      float4 wv[16];
+      if constexpr (LP == 3) {
+        const float* wp = sw + jl * 16 * 128 * 4;  // shared memory
+#pragma unroll
+        for (int q = 0; q < 16; ++q) wv[q] = lds4(wp + (q * 128 + at) * 4);
+      } else {
+        const float* wp = P.pk + pl.wprev_off + (int64_t)j * 16 * 128 * 4;  // L2
+#pragma unroll
+        for (int q = 0; q < 16; ++q) wv[q] = ldg4(wp + (q * 128 + at) * 4);
+      }
       const float lv = __ldg(A.cond + (f * L + j) * 2 * R + at);
       if (at < R) {
         float* ring = A.ring + A.ring_off[j];
@@ -608,15 +686,14 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
         m.xp[at] = xpv;
       }
       ptx::bar_sync(kBarAux, kAux);
-      const float* w = wprev + jl * R * 2 * R;
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 4
-      for (int q = 0; q < R; q += 4) {
-        const float4 x = lds4(&m.xp[q]);
-        a0 = fmaf(w[q * 2 * R + at], x.x, a0);
-        a1 = fmaf(w[(q + 1) * 2 * R + at], x.y, a1);
-        a2 = fmaf(w[(q + 2) * 2 * R + at], x.z, a2);
-        a3 = fmaf(w[(q + 3) * 2 * R + at], x.w, a3);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const float4 x = lds4(&m.xp[4 * q]);
+        a0 = fmaf(wv[q].x, x.x, a0);
+        a1 = fmaf(wv[q].y, x.y, a1);
+        a2 = fmaf(wv[q].z, x.z, a2);
+        a3 = fmaf(wv[q].w, x.w, a3);
       }
       m.pre[jl][at] = (bj[jl * 2 * R + at] + lv) + ((a0 + a1) + (a2 + a3));
       ptx::bar_sync(kBarAux, kAux);
@@ -626,7 +703,14 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_pre));
     }
   }
-  if (A.N > 0) aux_forward(pl, m, first, nl, at, (int)((A.N - 1) & 1));  // the last sample's h
+  if (A.N > 0) {  // the last sample's h and chain-skip partial
+    const int pp = (int)((A.N - 1) & 1);
+    aux_forward(pl, m, first, nl, at, pp);
+    if (xskip) {
+      wait(cx, &m.bar_done, (uint32_t)pp, 14);
+      aux_chain_skip<S>(P, cx, c, at, pp);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ head CTA (rows [64h, 64h+64))
@@ -655,7 +739,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
   const int c16 = k & 15;
   const int orow = 4 * (k >> 4) + ((k >> 2) & 3);  // z_a / logits row (within the head) this lane finishes
   const bool owriter = (k & 3) == 0;
-  const int nk = pl.nk;
+  const int np = pl.npart;
   float w[64];
 
   auto finish = [&](float (&v)[RQ]) -> float {
@@ -693,13 +777,13 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     tile_dot<RQ, 16>(w, &m.hbuf[0][20 * cc], v);
     ptx::tmem_load_async<4 * CZ>(tm + cRelu, w);
     v[0] = finish(v);
-    if (nk > 0) {
-      if (wait(cx, &m.bar_part, par, 22) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_part), nk * S * 4);
+    if (np > 0) {
+      if (wait(cx, &m.bar_part, par, 22) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_part), np * S * 4);
     }
     if (k == 0) trace<TRACE>(A, n, 1);
     if (qwriter) {
       float qv = bskip[qrow];
-      for (int kk = 0; kk < nk; ++kk) qv += m.part[kk][qrow];
+      for (int kk = 0; kk < np; ++kk) qv += m.part[kk][qrow];
       qv += d2;
       qv += v[0];
       m.zs[cpad<CZ>(qrow)] = fmaxf(qv, 0.0f);
@@ -799,7 +883,7 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
   }
 }
 
-template <int S, bool TRACE>
+template <int S, int LP, bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Mail* mail = reinterpret_cast<Mail*>(smem_raw);
@@ -831,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_hin), R * 4);
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_xin), R * 4);
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_logits), kLevels * 4);
-    ptx::mbar_arm(ptx::smem_u32(&mail->bar_part), pl.nk * S * 4);
+    ptx::mbar_arm(ptx::smem_u32(&mail->bar_part), pl.npart * S * 4);
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_za), kLevels * 4);
     for (int i = 0; i < kCMaxSlot; ++i) ptx::mbar_arm(ptx::smem_u32(&mail->bar_h[i]), R * 4);
   }
@@ -850,9 +934,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     const int wg = (t - kAux) >> 7;  // 0 = A, 1 = B, 2 = C
     int c0 = 0, c1 = 0;
     if (role == kChain) {
-      if (wg == 0) { c0 = kColA; c1 = kColC; }
-      else if (wg == 1) { c0 = kColB; c1 = kColEnd; }
-      else { c0 = kColC; c1 = kColB; }
+      if (wg == 0) { c0 = kColA; c1 = col_c(LP); }
+      else if (wg == 2) { c0 = col_c(LP); c1 = 2 * col_c(LP); }
+      else if (LP == 3) { c0 = kColB3; c1 = kColB3 + 3 * 32; }
     } else if (wg < 2) {
       c0 = 256 * wg;
       c1 = c0 + 256;
@@ -876,9 +960,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
 
   if (t >= kAux) {
     if (role == kChain) {
-      if (t < kAux + 128) chain_A<TRACE>(P, cx, idx, sw);
-      else if (t < kAux + 256) chain_B<TRACE>(P, cx, idx, sw);
-      else chain_C<TRACE>(P, cx, idx, sw);
+      if (t < kAux + 128) chain_A<LP, TRACE>(P, cx, idx, sw);
+      else if (t < kAux + 256) chain_B<LP, TRACE>(P, cx, idx, sw);
+      else chain_C<LP, TRACE>(P, cx, idx, sw);
     } else if (role == kHead) {
       if (t < kAux + kMain) head_main<S, TRACE>(P, cx, idx, sw);
     } else if (role == kSkip) {
@@ -891,9 +975,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     ptx::cluster_sync();
     return;
   }
-  if (role == kChain) chain_aux<TRACE>(P, cx, idx, sw);
+  if (role == kChain) chain_aux<S, LP, TRACE>(P, cx, idx, sw);
   // Park until the math warps are done (try_wait suspends the warp), then free TMEM.
-  while (!ptx::mbar_try_wait(ptx::smem_u32(&mail->bar_exit), 0)) {
+  while (!ptx::mbar_try_wait_cta(ptx::smem_u32(&mail->bar_exit), 0)) {
   }
   ptx::tmem_fence_after();
   if (t < 32) ptx::tmem_dealloc(mail->tmem_base, kTmemCols);
@@ -901,17 +985,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   ptx::cluster_sync();
 }
 
-template <int S, bool TRACE>
+template <int S, int LP, bool TRACE>
 cudaError_t configure(int smem) {
-  cudaError_t e = cudaFuncSetAttribute(k_cluster<S, TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_cluster<S, TRACE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
-template <int S>
+template <int S, int LP>
 int max_active_clusters(int size, int smem) {
-  if (configure<S, false>(smem) != cudaSuccess || configure<S, true>(smem) != cudaSuccess) {
+  if (configure<S, LP, false>(smem) != cudaSuccess || configure<S, LP, true>(smem) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -927,45 +1011,63 @@ int max_active_clusters(int size, int smem) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, k_cluster<S, false>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, k_cluster<S, LP, false>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
   return n;
 }
 
-// floats of a chain CTA's shared-memory image (see kSm*)
-int smem_chain(int c) { return kSmEmb + (c == 0 ? kLevels * R + R : 0); }
+// floats of a chain CTA's shared-memory image (see sm_*)
+int smem_chain(int c, int lp) { return sm_emb(lp) + (c == 0 ? kLevels * R + R : 0); }
 
 }  // namespace
 
-ClusterPlan plan_cluster(int L, int r, int s, int device) {
+namespace {
+// One residency plan with `lp` layers per chain CTA.
+ClusterPlan plan_lp(int L, int r, int s, int device, int lp) {
   ClusterPlan p;
   p.L = L;
   p.r = r;
   p.s = s;
+  p.lpc = lp;
   if (r != R) { p.why = "cluster kernel is built for r = 64"; return p; }
   if (s != 128 && s != 256) { p.why = "cluster kernel needs s in {128, 256}"; return p; }
   if (L > kCMaxLayers) { p.why = "too many layers"; return p; }
-  p.nc = (L + LPC - 1) / LPC;
+  p.nc = (L + lp - 1) / lp;
   for (int c = 0; c < p.nc; ++c) {
-    p.chain_first[c] = c * LPC;
-    p.chain_nl[c] = std::min(LPC, L - c * LPC);
+    p.chain_first[c] = c * lp;
+    p.chain_nl[c] = std::min(lp, L - c * lp);
+    p.xpart_slot[c] = -1;
   }
   p.nh = NH;
+  if (p.nc + p.nh > kCMaxCta) { p.why = "model does not fit one 16-CTA cluster"; return p; }
   const int nskip = std::max(0, L - 2);  // W_skip^(l) and W_skip^(l-1) live in the head CTAs
   const int qs = s / 4;                   // floats of one skip layer's tile per thread
   const int maxtm = 256 / qs;             // skip layers in tensor memory per thread half
   const int lstride = qs * kMain;         // floats per shared-memory skip layer
   const int maxsm = std::min(kCMaxSlot - maxtm, (int)((190 * 1024) / (lstride * 4)));
   const int cap = maxtm + maxsm;
-  p.nk = nskip > 0 ? (nskip + cap - 1) / cap : 0;
-  if (p.nk > kCMaxSkip) { p.why = "too many skip CTAs"; return p; }
+  // skip CTAs take the latest layers; what they cannot hold (the earliest layers) is applied
+  // by each layer's own chain CTA from L2 after its pass
+  p.nk = nskip > 0 ? std::min(kCMaxCta - p.nc - p.nh, (nskip + cap - 1) / cap) : 0;
+  p.nxs = std::max(0, nskip - p.nk * cap);
+  if (p.nxs > 0 && p.nxs > nskip - 2 * lp) {
+    p.why = "model does not fit one 16-CTA cluster (chain-skip layers too close to the head)";
+    return p;
+  }
+  const int nxp = (p.nxs + lp - 1) / lp;  // chain CTAs that send a partial
+  p.npart = p.nk + nxp;
+  if (p.npart > kCMaxSkip) { p.why = "too many skip partials"; return p; }
+  for (int c = 0; c < nxp; ++c) p.xpart_slot[c] = p.nk + c;
   p.size = p.nc + p.nh + p.nk;
-  if (p.size > kCMaxCta) { p.why = "model does not fit one 16-CTA cluster"; return p; }
   for (int k = 0; k < p.nk; ++k) p.skip_n[k] = 0;
-  for (int j = 0; j < nskip; ++j) {  // round robin: consecutive layers go to different CTAs
-    const int k = j % p.nk;
+  for (int j = 0; j < p.nxs; ++j) {
+    p.layer_skip_cta[j] = -1;
+    p.layer_skip_slot[j] = 0;
+  }
+  for (int j = p.nxs; j < nskip; ++j) {  // round robin: consecutive layers go to different CTAs
+    const int k = (j - p.nxs) % p.nk;
     p.layer_skip_cta[j] = p.nc + p.nh + k;
     p.layer_skip_slot[j] = p.skip_n[k]++;
   }
@@ -977,7 +1079,7 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
   int max_sw = 0;
   for (int rank = 0; rank < p.size; ++rank) {
     int swf = 0;
-    if (rank < p.nc) swf = smem_chain(rank);
+    if (rank < p.nc) swf = smem_chain(rank, lp);
     else if (rank < p.nc + p.nh) swf = s + 128;
     else swf = p.skip_nsm[rank - p.nc - p.nh] * lstride;
     p.pk_off[rank] = off;
@@ -990,6 +1092,10 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
   }
   p.embp_off = off;
   off += (int64_t)kLevels * R;
+  p.wprev_off = off;
+  off += (int64_t)L * 16 * 128 * 4;
+  p.wskx_off = off;
+  off += (int64_t)p.nxs * 16 * s * 4;
   p.pk_total = off;
   p.smem_bytes = (int)(((sizeof(Mail) + 127) & ~size_t(127)) + (size_t)max_sw * 4);
   int dev_smem = 0;
@@ -998,13 +1104,24 @@ ClusterPlan plan_cluster(int L, int r, int s, int device) {
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  const int nclus = (s == 256) ? max_active_clusters<256>(p.size, p.smem_bytes)
-                               : max_active_clusters<128>(p.size, p.smem_bytes);
+  int nclus;
+  if (s == 256) nclus = lp == 3 ? max_active_clusters<256, 3>(p.size, p.smem_bytes) : max_active_clusters<256, 4>(p.size, p.smem_bytes);
+  else nclus = lp == 3 ? max_active_clusters<128, 3>(p.size, p.smem_bytes) : max_active_clusters<128, 4>(p.size, p.smem_bytes);
   if (prev >= 0) cudaSetDevice(prev);
   if (nclus < 1) { p.why = "cluster cannot be scheduled on this device"; return p; }
   p.ok = true;
   p.why = "ok";
   return p;
+}
+}  // namespace
+
+// 3 layers per chain CTA (every weight of the chain in tensor memory) when the model fits
+// one cluster that way with no chain-skip layers; else 4 (W_res in shared memory).
+ClusterPlan plan_cluster(int L, int r, int s, int device) {
+  ClusterPlan p3 = plan_lp(L, r, s, device, 3);
+  if (p3.ok && p3.nxs == 0) return p3;
+  ClusterPlan p4 = plan_lp(L, r, s, device, 4);
+  return p4.ok ? p4 : p3;
 }
 
 size_t packed_bytes(const ClusterPlan& p) { return sizeof(float) * (size_t)p.pk_total; }
@@ -1038,7 +1155,7 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
     float* sm = h.data() + p.pk_smem_off[rank];
     auto put = [&](int col, int lane, float v) { img[(int64_t)col * 128 + lane] = v; };
     if (rank < p.nc) {
-      const int first = p.chain_first[rank], nl = p.chain_nl[rank];
+      const int first = p.chain_first[rank], nl = p.chain_nl[rank], lp = p.lpc;
       const int xb = (rank == 0) ? 1 : 0;  // CTA 0's layer 0 takes the embedding directly
       // local layer jl (layer j = first + jl) with jl >= xb: M_j = W_cur_j W_res_{j-1}, c_j = W_cur_j B_res_{j-1}
       std::vector<std::vector<float>> M(LPC), cf(LPC);
@@ -1049,24 +1166,28 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
           for (int q = 0; q < 64; ++q) {
             const int row = (q < 32) ? g : R + g, col = 32 * half + (q & 31);
             put(kColA + 64 * jl + q, lane, jl < xb ? W(first, o.w_cur, row, col, R) : M[jl][row * R + col]);
-            if (jl >= xb) put(kColC + 64 * jl + q, lane, W(first + jl, o.w_cur, row, col, R));
+            if (jl >= xb) put(col_c(lp) + 64 * jl + q, lane, W(first + jl, o.w_cur, row, col, R));
           }
-        for (int jl = xb; jl < nl; ++jl)
-          for (int q = 0; q < 32; ++q)
-            put(kColB + 32 * jl + q, lane, W(first + jl - 1, o.w_res, g, 32 * half + q, R));
+        for (int jl = xb; jl < nl; ++jl)  // B's W_res_{j-1} row-pair tile: TMEM (LP 3) or shared memory (LP 4)
+          for (int q = 0; q < 32; ++q) {
+            const float v = W(first + jl - 1, o.w_res, g, 32 * half + q, R);
+            if (lp == 3) put(kColB3 + 32 * jl + q, lane, v);
+            else sm[kSmWres + ((jl * 8 + q / 4) * 128 + lane) * 4 + q % 4] = v;
+          }
       }
       for (int jl = 0; jl < nl; ++jl) {
         const int j = first + jl;
-        for (int k = 0; k < R; ++k)
-          for (int i = 0; i < 2 * R; ++i) sm[jl * R * 2 * R + k * 2 * R + i] = W(j, o.w_prev, i, k, R);
-        for (int i = 0; i < 2 * R; ++i) sm[kSmB + jl * 2 * R + i] = w[(int64_t)j * o.layer_stride + o.b + i];
+        if (lp == 3)  // W_prev_j [16][128][4] in shared memory
+          for (int i = 0; i < 2 * R; ++i)
+            for (int k = 0; k < R; ++k) sm[(jl * 16 * 128 + (k / 4) * 128 + i) * 4 + k % 4] = W(j, o.w_prev, i, k, R);
+        for (int i = 0; i < 2 * R; ++i) sm[sm_b(lp) + jl * 2 * R + i] = w[(int64_t)j * o.layer_stride + o.b + i];
         if (jl >= xb) {
-          for (int i = 0; i < R; ++i) sm[kSmBres + jl * R + i] = w[(int64_t)(j - 1) * o.layer_stride + o.b_res + i];
-          for (int i = 0; i < 2 * R; ++i) sm[kSmFold + jl * 2 * R + i] = cf[jl][i];
+          for (int i = 0; i < R; ++i) sm[sm_bres(lp) + jl * R + i] = w[(int64_t)(j - 1) * o.layer_stride + o.b_res + i];
+          for (int i = 0; i < 2 * R; ++i) sm[sm_fold(lp) + jl * 2 * R + i] = cf[jl][i];
         }
       }
       if (rank == 0) {
-        float* we = sm + kSmEmb;
+        float* we = sm + sm_emb(lp);
         for (int y = 0; y < kLevels; ++y)
           for (int i = 0; i < R; ++i) we[y * R + i] = w[o.emb_cur + (int64_t)i * kLevels + y];
         for (int i = 0; i < R; ++i) we[kLevels * R + i] = w[o.b_emb + i];
@@ -1124,6 +1245,16 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
   float* ep = h.data() + p.embp_off;
   for (int y = 0; y < kLevels; ++y)
     for (int i = 0; i < R; ++i) ep[y * R + i] = w[o.emb_prev + (int64_t)i * kLevels + y];
+  for (int j = 0; j < p.L; ++j) {  // W_prev_j [16][128][4] (streamed by the chain aux warps)
+    float* wp = h.data() + p.wprev_off + (int64_t)j * 16 * 128 * 4;
+    for (int i = 0; i < 2 * R; ++i)
+      for (int k = 0; k < R; ++k) wp[((k / 4) * 128 + i) * 4 + k % 4] = W(j, o.w_prev, i, k, R);
+  }
+  for (int j = 0; j < p.nxs; ++j) {  // chain-skip W_skip_j [16][s][4]
+    float* ws = h.data() + p.wskx_off + (int64_t)j * 16 * s * 4;
+    for (int i = 0; i < s; ++i)
+      for (int k = 0; k < R; ++k) ws[((k / 4) * s + i) * 4 + k % 4] = W(j, o.w_skip, i, k, R);
+  }
   return cudaMemcpy(packed, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice);
 }
 
@@ -1149,10 +1280,14 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaError_t e;
-  if (p.s == 256) {
-    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<256, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<256, false>, P);
+  if (p.s == 256 && p.lpc == 3) {
+    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<256, 3, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<256, 3, false>, P);
+  } else if (p.s == 256) {
+    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<256, 4, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<256, 4, false>, P);
+  } else if (p.lpc == 3) {
+    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<128, 3, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<128, 3, false>, P);
   } else {
-    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<128, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<128, false>, P);
+    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<128, 4, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<128, 4, false>, P);
   }
   info->grid = p.size;
   info->cluster = p.size;

@@ -244,3 +244,18 @@ def test_tc_batched_configs_teacher_forced_and_free_running(L, cfg):
         _, ref_lg, _ = oracle_tf(cfg, w, cond[i], hop, codes[i])
         err = float(np.max(np.abs(lg[i].astype(np.float64) - ref_lg)))
         assert err <= FP32_FAITHFUL, (i, err)
+
+
+def test_cluster_c3_deep_model_chain_skip(L):
+    """C3 (l = 40, r = 64, s = 256) on the batch-1 cluster kernel: 10 chain CTAs, and the
+    earliest skip layers applied by their chain CTAs from L2 (the skip CTAs cannot hold all
+    38) -- free-running codes bit-exact with the oracle for 1,600 samples, teacher-forced
+    logits fp32-faithful."""
+    cfg = synth.C3
+    N, hop = 1600, 64
+    w, cond, u, codes, lg = run_pair(L, cfg, "cluster", N, hop, utt=1)
+    ref_codes, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, N, uniforms=u)
+    first_bad = int(np.argmax(codes != ref_codes)) if np.any(codes != ref_codes) else N
+    assert first_bad == N, f"first divergence at n={first_bad}"
+    _, ref_lg, _ = oracle_tf(cfg, w, cond, hop, codes)
+    assert float(np.max(np.abs(lg.astype(np.float64) - ref_lg))) <= FP32_FAITHFUL
