@@ -128,12 +128,19 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "n_samples": len(self.samples)}
 
 
-def load_ncu_traffic(workload: str):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+def load_ncu_traffic(workload: str, stream_samples: int):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary
+    (profiles/ncu_summary.json): the captured launch's bytes, or -- for the batched
+    workloads, captured on a short launch -- bytes per stream-sample x this launch's
+    stream-samples (the queue traffic scales with it)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
-        d = json.load(open(p))
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+        d = json.load(open(p)).get(workload, {})
+        if d.get("dram_bytes_per_launch") is not None:
+            return d["dram_bytes_per_launch"]
+        if d.get("dram_bytes_per_stream_sample") is not None:
+            return d["dram_bytes_per_stream_sample"] * stream_samples
+        return None
     except Exception:
         return None
 
@@ -321,14 +328,14 @@ def main():
         if kname == "tc":
             peak, peak_src = tf32_peak_tflops()
             roof = {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved_tflops / peak, "traffic": load_ncu_traffic(args.workload),
+                    "frac": achieved_tflops / peak, "traffic": load_ncu_traffic(args.workload, n * S),
                     "note": "algorithmic FLOP (2 x MAC/sample x samples x streams) / launch time vs dense tf32 "
                             f"peak ({peak_src}); the 3-pass split issues ~3.2x these FLOPs on the tensor pipe; "
                             "the step is barrier/latency bound (DESIGN.md Batched kernel)"}
         else:
             roof = {"bound": "alu", "achieved": achieved_tflops, "peak": FP32_FMA_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": achieved_tflops / FP32_FMA_PEAK_TFLOPS,
-                    "traffic": load_ncu_traffic(args.workload),
+                    "traffic": load_ncu_traffic(args.workload, n * S),
                     "note": "batch-1 is latency-bound: algorithmic FLOP (2 x MAC/sample x samples) / "
                             "launch time vs FP32 FFMA peak of the whole chip (DESIGN.md Roofline)"}
         line = {
