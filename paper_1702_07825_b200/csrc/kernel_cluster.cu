@@ -653,14 +653,15 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
   const int first = pl.chain_first[c], nl = pl.chain_nl[c];
   const float* bj = sw + sm_b(LP);  // [LPC][2R]
   const int L = A.L;
-  const bool xskip = first < pl.nxs;
+  const bool xskip = LP == 4 && first < pl.nxs;  // LP = 3 plans never have chain-skip layers
 
   for (int64_t n = 0; n < A.N; ++n) {
     const int pp = (int)((n - 1) & 1);  // parity of sample n-1
     if (n > 0) {
       aux_forward(pl, m, first, nl, at, pp);
       wait(cx, &m.bar_done, (uint32_t)pp, 14);
-      if (xskip) aux_chain_skip<S>(P, cx, c, at, pp);
+      if constexpr (LP == 4)
+        if (xskip) aux_chain_skip<S>(P, cx, c, at, pp);
     }
     const int64_t f = n / A.hop;
     for (int jl = 0; jl < nl; ++jl) {
@@ -706,9 +707,11 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
   if (A.N > 0) {  // the last sample's h and chain-skip partial
     const int pp = (int)((A.N - 1) & 1);
     aux_forward(pl, m, first, nl, at, pp);
-    if (xskip) {
-      wait(cx, &m.bar_done, (uint32_t)pp, 14);
-      aux_chain_skip<S>(P, cx, c, at, pp);
+    if constexpr (LP == 4) {
+      if (xskip) {
+        wait(cx, &m.bar_done, (uint32_t)pp, 14);
+        aux_chain_skip<S>(P, cx, c, at, pp);
+      }
     }
   }
 }
