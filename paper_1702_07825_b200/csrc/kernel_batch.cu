@@ -15,13 +15,16 @@
 //       and stores it into layer j's dilation queue ("never recompute").
 //       Skip tile u accumulates q += W_skip^(j-1) h^(j-1) in TMEM.
 //   phase l    : skip tiles add W_skip^(l-1) h^(l-1); z_s = relu(q), q_0 = B_skip
-//   phase l+1  : head tile v: z_a = relu(W_relu z_s + B_relu), rows [32v, 32v+32)
+//   phase l+1  : head tile v: z_a = relu(W_relu z_s + B_relu), rows [64v, 64v+64)
 //   phase l+2  : head tile v: logits = W_out z_a + B_out
 //   phase l+3  : one warp per stream: inverse-CDF draw (R11), then the
 //                embedding x^(0)_{n+1} = W_emb_prev[:, y_{n-1}] + W_emb_cur[:, y_n] + B_emb
 //                 into x^(0) and layer 0's queue.
+// One thread-block cluster per stream block of 128 streams holds all of its tiles
+// (r/16 layer tiles + s/64 skip tiles + 4 head tiles <= 16 CTAs); the phases are
+// separated by a hardware cluster barrier, and stream blocks never wait for each other.
 // Operands: A = activations of 128 streams (M = 128, TMEM lane = stream), B = a weight
-// tile (N = 32 or 48 rows), K staged 32 channels at a time through a 3-deep ring of
+// tile (N = 48 or 64 rows), K staged 32 channels at a time through a 5-deep ring of
 // shared-memory stages filled by cp.async.bulk; every fp32 operand is split into
 // hi = x (the MMA reads its tf32 truncation) and lo = x - tf32(x), and each K-step
 // issues hi*hi + hi*lo + lo*hi (reading R22).
@@ -37,33 +40,34 @@ namespace dvw {
 namespace {
 
 constexpr int kBT = 256;  // 8 warps; warp w reads TMEM lanes [32(w%4), +32) = its streams, half w/4 of the columns
-constexpr int kStages = 5;
+constexpr int kStages = 4;
 constexpr int kChunk = 32;                   // K channels per staged chunk
 constexpr int kActChunk = 128 * kChunk;      // floats of one activation chunk (hi or lo)
-constexpr int kMaxN = 48;
+constexpr int kMaxN = 64;
 constexpr int kStageFloats = 2 * kActChunk + kMaxN * kChunk * 2;
-constexpr int kTmemCols = 256;
-// TMEM accumulator columns.  Each tile accumulates hi*hi + lo*hi in its first block
-// of columns and hi*lo in a second block (the stacked-B pass below):
+constexpr int kTmemCols = 128;
+// TMEM accumulator columns (a CTA has one role).  Each tile accumulates hi*hi + lo*hi in
+// its first block of columns and hi*lo in a second block (the stacked-B pass below):
 //   layer: [0,48) = tanh 16 | sigmoid 16 | residual 16, [48,96) the hi*lo partner
-//   skip : [96,128) and [128,160);  head: [160,192) and [192,224)
-constexpr uint32_t kColA = 0, kColA2 = 48, kColQ = 96, kColQ2 = 128, kColH = 160, kColH2 = 192;
+//   skip / head (64 rows): [0,64) and [64,128)
+constexpr uint32_t kColA = 0, kColA2 = 48, kColQ = 0, kColQ2 = 64, kColH = 0, kColH2 = 64;
+constexpr int kTileRows = 64;  // rows of a skip or head tile
+
 constexpr uint64_t kTimeoutNs = 4000000000ull;
 
 struct BParams {
   RunArgs a;
   const float* pk;
-  int L, r, s, TA, TQ, TH, per_sb, nsb, ncta;
+  int L, r, s, TA, TQ, TH, per_sb, nsb;
   int64_t la_off, la_floats, q_off, q_floats, hr_off, hr_floats, ho_off, ho_floats, bias_off;
-  float* xb[2];   // x^(k) in xb[k & 1]: [hi | lo], each nsb x [r/32][8][128][4]
+
   float* hb[2];   // h^(k) in hb[k & 1]
   float* zs;      // [hi | lo] nsb x [s/32][8][128][4]
   float* za;      // [hi | lo] nsb x [8][8][128][4]
   float* logits;  // [nsb*128][256]
   float* ring;    // per layer j: (d_j + 1) slots of [hi | lo] nsb x [r/32][8][128][4]
   int* yh;        // [nsb*128][2]: y_{n-1}, y_{n-2}
-  unsigned long long* ctr;
-  int* abort_flag;
+  int* abort_flag;  // [nsb]: per stream block (cluster)
   int32_t dil[kBMaxLayers];
   int64_t ring_off[kBMaxLayers];  // floats
 };
@@ -103,9 +107,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
+
+// The abort word of this CTA's stream block (one cluster); the host error word is shared.
+__device__ __forceinline__ int* abort_word(const BParams& P) { return P.abort_flag + blockIdx.x / P.per_sb; }
+
 __device__ __forceinline__ void raise_abort(const BParams& P, Ctl& c, int code) {
   c.abort = 1;
-  if (atomicExch(P.abort_flag, 1) == 0) *(volatile int*)P.a.err = code;  // mapped host word
+  if (atomicExch(abort_word(P), 1) == 0) *(volatile int*)P.a.err = code;  // mapped host word
 }
 
 // mbarrier wait with watchdog; false on abort / timeout.  The spin touches only the
@@ -118,7 +126,7 @@ __device__ __forceinline__ bool mwait(const BParams& P, Ctl& c, uint64_t* bar, u
   for (uint32_t it = 1;; ++it) {
     if (ptx::mbar_test_wait_cta(b, parity)) return true;
     if ((it & 255) == 0) {
-      if (*(volatile int*)&c.abort || *(volatile int*)P.abort_flag) {
+      if (*(volatile int*)&c.abort || *(volatile int*)abort_word(P)) {
         c.abort = 1;
         return false;
       }
@@ -130,37 +138,18 @@ __device__ __forceinline__ bool mwait(const BParams& P, Ctl& c, uint64_t* bar, u
   }
 }
 
-// Grid-wide barrier between phases: every CTA's generic stores are made visible to
-// the async proxy (bulk copies of the next phase) and released at GPU scope.
-__device__ __forceinline__ bool grid_sync(const BParams& P, Ctl& c, unsigned long long& target) {
+// Barrier between phases of one stream block: the hardware cluster barrier (release /
+// acquire at cluster scope), with every CTA's generic global stores made visible to the
+// async proxy (the next phase's bulk copies) on both sides.  Every CTA of the cluster
+// passes every barrier, aborted or not.
+__device__ __forceinline__ bool phase_sync(const BParams& P, Ctl& c) {
+  (void)P;
+  (void)c;
   fence_proxy_async_global();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    target += (unsigned long long)P.ncta;
-    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(P.ctr), "l"(1ull) : "memory");
-    const uint64_t t0 = ptx::globaltimer();
-    for (uint32_t it = 1;; ++it) {
-      unsigned long long v;
-      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(P.ctr) : "memory");
-      if (v >= target) {
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        break;
-      }
-      if ((it & 63) == 0) {
-        if (*(volatile int*)P.abort_flag) {
-          c.abort = 1;
-          break;
-        }
-        if (ptx::globaltimer() - t0 > kTimeoutNs) {
-          raise_abort(P, c, 41);
-          break;
-        }
-      }
-    }
-    fence_proxy_async_global();
-  }
-  __syncthreads();
-  return !*(volatile int*)&c.abort;
+  ptx::cluster_sync();
+  fence_proxy_async_global();
+  return true;
 }
 
 enum BRole { kLayer = 0, kSkipT = 1, kHeadT = 2 };
@@ -186,6 +175,14 @@ struct Chunk {
   uint32_t dcol;
   uint32_t acc;
 };
+
+// x^(j)_n (this step's input of layer j) lives in layer j's dilation queue, slot n mod (d_j + 1):
+// the epilogue of phase j (or the embedding, j = 0) writes it there once and phase j + 1 reads
+// it back from the same place.  [hi | lo] halves, stream block sb.
+__device__ __forceinline__ const float* x_now(const BParams& P, int j, int64_t n) {
+  const int d = P.dil[j];
+  return P.ring + P.ring_off[j] + (int64_t)(n % (d + 1)) * 2 * ((int64_t)P.nsb * P.r * 128);
+}
 
 __device__ __forceinline__ int job_chunks(const BParams& P, int role, int ph) {
   const int nR = P.r / kChunk;
@@ -222,7 +219,7 @@ __device__ __forceinline__ Chunk job_chunk(const BParams& P, int role, int idx, 
       k.N = 32;
       k.NS = 80;
     } else if (part == 1) {  // x^(j-1) (j >= 1) or x^(0) (j = 0)
-      src = P.xb[j >= 1 ? ((j - 1) & 1) : 0];
+      src = x_now(P, j >= 1 ? j - 1 : 0, n);
       k.w = wb + (int64_t)nR * 80 * 32 + (int64_t)kc * 80 * 32;
       k.N = 32;
       k.NS = 80;
@@ -241,9 +238,9 @@ __device__ __forceinline__ Chunk job_chunk(const BParams& P, int role, int idx, 
     const float* src = P.hb[j & 1];
     k.ah = src + ((int64_t)sb * r + c * kChunk) * 128;
     k.al = k.ah + actR;
-    k.w = P.pk + P.q_off + ((int64_t)j * P.TQ + idx) * P.q_floats + (int64_t)c * 64 * 32;
-    k.N = 32;
-    k.NS = 64;
+    k.w = P.pk + P.q_off + ((int64_t)j * P.TQ + idx) * P.q_floats + (int64_t)c * 2 * kTileRows * 32;
+    k.N = kTileRows;
+    k.NS = 2 * kTileRows;
     k.dcol = kColQ;
     k.acc = (j > 0 || c > 0);
   } else {
@@ -252,9 +249,10 @@ __device__ __forceinline__ Chunk job_chunk(const BParams& P, int role, int idx, 
     const float* src = relu ? P.zs : P.za;
     k.ah = src + ((int64_t)sb * C + c * kChunk) * 128;
     k.al = k.ah + (int64_t)P.nsb * C * 128;
-    k.w = P.pk + (relu ? P.hr_off + idx * P.hr_floats : P.ho_off + idx * P.ho_floats) + (int64_t)c * 64 * 32;
-    k.N = 32;
-    k.NS = 64;
+    k.w = P.pk + (relu ? P.hr_off + idx * P.hr_floats : P.ho_off + idx * P.ho_floats) +
+          (int64_t)c * 2 * kTileRows * 32;
+    k.N = kTileRows;
+    k.NS = 2 * kTileRows;
     k.dcol = kColH;
     k.acc = c > 0;
   }
@@ -375,7 +373,7 @@ __device__ __forceinline__ int sample_warp_g(const float* logits, float u, int l
 }
 
 // x^(0)_{n+1} = W_emb_prev[:, y_{n-1}] + W_emb_cur[:, y_n] + B_emb
-// into x^(0) and layer 0's queue slot (n+1) mod (d_0+1); one warp, stream g.
+// into layer 0's queue slot (n+1) mod (d_0+1) (where phase 0 reads it); one warp, stream g.
 __device__ __forceinline__ void embed(const BParams& P, int g, int64_t n1, int yprev, int ycur, int lane) {
   const RunArgs& A = P.a;
   const int r = P.r, sb = g >> 7, i = g & 127;
@@ -385,12 +383,9 @@ __device__ __forceinline__ void embed(const BParams& P, int g, int64_t n1, int y
   const float* be = A.w + A.off.b_emb;
   const int d = P.dil[0];
   float* q = P.ring + P.ring_off[0] + (int64_t)(n1 % (d + 1)) * 2 * half + (int64_t)sb * r * 128;
-  float* x = P.xb[0] + (int64_t)sb * r * 128;
   for (int c = lane; c < r; c += 32) {
     const float v = (__ldg(ep + (int64_t)c * kLevels + yprev) + __ldg(ec + (int64_t)c * kLevels + ycur)) + __ldg(be + c);
     const int o = canon(c, i);
-    __stcg(x + o, v);
-    __stcg(x + half + o, tf32_lo(v));
     __stcg(q + o, v);
     __stcg(q + half + o, tf32_lo(v));
   }
@@ -448,7 +443,7 @@ __device__ __forceinline__ void prefetch(const BParams& P, int role, int idx, in
     for (int q = 0; q < 16; ++q) pre.L[q] = 0.0f;
   }
   if (j >= 1) {
-    const float* xin = P.xb[(j - 1) & 1] + (int64_t)sb * r * 128;
+    const float* xin = x_now(P, j - 1, n) + (int64_t)sb * r * 128;
     const float* bres = A.w + A.off.b_res + (int64_t)(j - 1) * A.off.layer_stride + c0;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -501,7 +496,6 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
     }
     if (t == 0 && ph == 3) btrace(P, n, 17);
     if (j >= 1) {
-      float* xout = P.xb[j & 1] + (int64_t)sb * r * 128;
       const int d = P.dil[j];
       float* qd = P.ring + P.ring_off[j] + (int64_t)(n % (d + 1)) * 2 * half_f + (int64_t)sb * r * 128;
 #pragma unroll
@@ -509,58 +503,54 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
         float xv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) xv[e] = pre.x[4 * q + e] + ((Dx[4 * q + e] + Ex[4 * q + e]) + pre.br[4 * q + e]);
-        st_act(xout, half_f, c0 + 4 * q, i, xv);
         st_act(qd, half_f, c0 + 4 * q, i, xv);
       }
     }
-  } else if (role == kSkipT) {
-    if (ph != P.L) return;  // accumulation continues in TMEM
-    float D[16], E[16];
-    tmem_cols<16>(lane_base + kColQ + 16 * half, D);
-    tmem_cols<16>(lane_base + kColQ2 + 16 * half, E);
-    ptx::tmem_wait_ld<16>(D);
-    ptx::tmem_wait_ld<16>(E);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) D[q] += E[q];
-    const int c0 = 32 * idx + 16 * half;
-    const float* bsk = A.w + A.off.b_skip + c0;
-    const int64_t half_f = (int64_t)P.nsb * P.s * 128;
-    float* dst = P.zs + (int64_t)sb * P.s * 128;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float v[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = fmaxf(D[4 * q + e] + __ldg(bsk + 4 * q + e), 0.0f);
-      st_act(dst, half_f, c0 + 4 * q, i, v);
-    }
   } else {
-    float D[16], E[16];
-    tmem_cols<16>(lane_base + kColH + 16 * half, D);
-    tmem_cols<16>(lane_base + kColH2 + 16 * half, E);
-    ptx::tmem_wait_ld<16>(D);
-    ptx::tmem_wait_ld<16>(E);
+    if (role == kSkipT && ph != P.L) return;  // accumulation continues in TMEM
+    // 64-row tile: thread (stream i, half) finishes rows [64 idx + 32 half, +32)
+    float D[32], E[32];
+    const uint32_t c0t = kColQ + 32 * half, c1t = kColQ2 + 32 * half;  // kColQ == kColH
+    tmem_cols<16>(lane_base + c0t, *reinterpret_cast<float(*)[16]>(D));
+    tmem_cols<16>(lane_base + c0t + 16, *reinterpret_cast<float(*)[16]>(D + 16));
+    tmem_cols<16>(lane_base + c1t, *reinterpret_cast<float(*)[16]>(E));
+    tmem_cols<16>(lane_base + c1t + 16, *reinterpret_cast<float(*)[16]>(E + 16));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int q = 0; q < 16; ++q) D[q] += E[q];
-    const int c0 = 32 * idx + 16 * half;
-    if (ph == P.L + 1) {
-      const float* b = A.w + A.off.b_relu + c0;
+    for (int q = 0; q < 32; ++q) asm volatile("" : "+f"(D[q]), "+f"(E[q]));
+#pragma unroll
+    for (int q = 0; q < 32; ++q) D[q] += E[q];
+    const int c0 = kTileRows * idx + 32 * half;
+    if (role == kSkipT) {  // z_s = relu(q + B_skip)
+      const float* bsk = A.w + A.off.b_skip + c0;
+      const int64_t half_f = (int64_t)P.nsb * P.s * 128;
+      float* dst = P.zs + (int64_t)sb * P.s * 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = fmaxf(D[4 * q + e] + __ldg(bsk + 4 * q + e), 0.0f);
+        st_act(dst, half_f, c0 + 4 * q, i, v);
+      }
+    } else if (ph == P.L + 1) {  // z_a = relu(W_relu z_s + B_relu)
+      const float* bb = A.w + A.off.b_relu + c0;
       const int64_t half_f = (int64_t)P.nsb * kLevels * 128;
       float* dst = P.za + (int64_t)sb * kLevels * 128;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         float v[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) v[e] = fmaxf(D[4 * q + e] + __ldg(b + 4 * q + e), 0.0f);
+        for (int e = 0; e < 4; ++e) v[e] = fmaxf(D[4 * q + e] + __ldg(bb + 4 * q + e), 0.0f);
         st_act(dst, half_f, c0 + 4 * q, i, v);
       }
-    } else {
-      const float* b = A.w + A.off.b_out + c0;
+    } else {  // logits = W_out z_a + B_out
+      const float* bb = A.w + A.off.b_out + c0;
       float* lg = P.logits + (int64_t)g * kLevels + c0;
       float* ol = (A.forced && live) ? A.out_logits + ((int64_t)g * A.N + n) * kLevels + c0 : nullptr;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float4 v = make_float4(D[4 * q] + __ldg(b + 4 * q), D[4 * q + 1] + __ldg(b + 4 * q + 1),
-                               D[4 * q + 2] + __ldg(b + 4 * q + 2), D[4 * q + 3] + __ldg(b + 4 * q + 3));
+      for (int q = 0; q < 8; ++q) {
+        float4 v = make_float4(D[4 * q] + __ldg(bb + 4 * q), D[4 * q + 1] + __ldg(bb + 4 * q + 1),
+                               D[4 * q + 2] + __ldg(bb + 4 * q + 2), D[4 * q + 3] + __ldg(bb + 4 * q + 3));
         __stcg(reinterpret_cast<float4*>(lg) + q, v);
         if (ol) reinterpret_cast<float4*>(ol)[q] = v;
       }
@@ -595,28 +585,32 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
   __syncthreads();
   ptx::tmem_fence_after();
 
-  unsigned long long target = 0;
   uint32_t cseq = 0, jseq = 0;
-  const int nwarps = P.ncta * (kBT / 32);
-  const int gw = b * (kBT / 32) + w;
-  const int nst = min(A.n_streams, P.nsb * 128);
+  // the warps of this cluster serve the streams of its stream block (sampler, embedding)
+  const int nwarps = P.per_sb * (kBT / 32);
+  const int gw = k * (kBT / 32) + w;
+  const int g_end = min(A.n_streams, (sb + 1) * 128);
 
   // x^(0)_0 from y_{-1} = y_{-2} = 128 (R4)
-  for (int g = gw; g < nst; g += nwarps) {
+  for (int g = sb * 128 + gw; g < g_end; g += nwarps) {
     embed(P, g, 0, kLevels / 2, kLevels / 2, lane);
     if (lane == 0) {
       P.yh[2 * g] = kLevels / 2;
       P.yh[2 * g + 1] = kLevels / 2;
     }
   }
-  bool ok = grid_sync(P, cl, target);
+  phase_sync(P, cl);
+  // A CTA whose pipeline failed (watchdog) stops working but keeps passing every cluster
+  // barrier, so the other CTAs of its stream block never wait forever; the host sees the
+  // error word.
+  bool ok = true;
 
-  for (int64_t n = 0; ok && n < A.N; ++n) {
-    for (int ph = 0; ok && ph < P.L + 4; ++ph) {
+  for (int64_t n = 0; n < A.N; ++n) {
+    for (int ph = 0; ph < P.L + 4; ++ph) {
       const int tev = ph == 3 ? 0 : ph == P.L + 2 ? 8 : ph == P.L + 3 ? 4 : -1;
       if (t == 0 && tev >= 0) btrace(P, n, tev);
       if (ph < P.L + 3) {
-        const int nch = job_chunks(P, role, ph);
+        const int nch = ok ? job_chunks(P, role, ph) : 0;
         if (nch > 0) {
           bool good = true;
           if (t == 32) good = produce(P, cl, stages, role, idx, sb, ph, n, nch, cseq);
@@ -628,9 +622,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
           bool dn = true;
           if (lane == 0) dn = mwait(P, cl, &cl.done, jseq & 1, 44);
           dn = __shfl_sync(0xffffffffu, dn ? 1 : 0, 0) != 0;
-          if (!dn) {
-            ok = false;
-          } else {
+          if (dn) {
             if (t == 0 && tev >= 0) btrace(P, n, tev + 1);
             ptx::tmem_fence_after();
             if (t == 0 && ph == 3) btrace(P, n, 18);
@@ -641,9 +633,9 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
           cseq += nch;
           ++jseq;
         }
-      } else {
+      } else if (ok) {
         // sample y_n and embed x^(0)_{n+1}; one warp per stream
-        for (int g = gw; g < nst; g += nwarps) {
+        for (int g = sb * 128 + gw; g < g_end; g += nwarps) {
           const int y1 = __ldcg(P.yh + 2 * g);
           int y;
           if (A.forced) {
@@ -661,7 +653,9 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
         }
       }
       if (t == 0 && ph == P.L + 3) btrace(P, n, 5);
-      ok = grid_sync(P, cl, target) && ok;
+      __syncthreads();
+      ok = ok && !cl.abort;
+      phase_sync(P, cl);
       if (t == 0 && tev >= 0) btrace(P, n, tev == 4 ? 6 : tev + 3);
     }
   }
@@ -689,39 +683,58 @@ BatchPlan plan_batch(int L, int r, int s, int device) {
   p.s = s;
   if (L > kBMaxLayers) { p.why = "more than 64 layers"; return p; }
   if (r % kChunk != 0 || r > 128) { p.why = "residual channels must be 32, 64 or 128"; return p; }
-  if (s % kChunk != 0) { p.why = "skip channels must be a multiple of 32"; return p; }
+  if (s % kTileRows != 0) { p.why = "skip channels must be a multiple of 64"; return p; }
   p.TA = r / 16;
-  p.TQ = s / 32;
-  p.TH = kLevels / 32;
-  p.per_sb = p.TA + p.TQ + p.TH;
+  p.TQ = s / kTileRows;
+  p.TH = kLevels / kTileRows;
+  p.per_sb = p.TA + p.TQ + p.TH;  // one cluster per stream block
+  if (p.per_sb > 16) { p.why = "a stream block needs more than 16 CTAs"; return p; }
   const int nR = r / kChunk;
   int64_t off = 0;
   p.la_off = off;
   p.la_floats = (int64_t)nR * (80 * 32 + 80 * 32 + 96 * 32);
   off += (int64_t)L * p.TA * p.la_floats;
   p.q_off = off;
-  p.q_floats = (int64_t)nR * 64 * 32;
+  p.q_floats = (int64_t)nR * 2 * kTileRows * 32;
   off += (int64_t)L * p.TQ * p.q_floats;
   p.hr_off = off;
-  p.hr_floats = (int64_t)(s / kChunk) * 64 * 32;
+  p.hr_floats = (int64_t)(s / kChunk) * 2 * kTileRows * 32;
   off += (int64_t)p.TH * p.hr_floats;
   p.ho_off = off;
-  p.ho_floats = (int64_t)(kLevels / kChunk) * 64 * 32;
+  p.ho_floats = (int64_t)(kLevels / kChunk) * 2 * kTileRows * 32;
   off += (int64_t)p.TH * p.ho_floats;
   p.bias_off = off;
   off += (int64_t)L * 2 * r;
   p.total = off;
   p.smem_bytes = 128 + kStages * kStageFloats * 4;
-  int nsm = 0, coop = 0;
-  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
-      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device) != cudaSuccess) {
+  // stream blocks per launch = clusters that are co-resident (one wave)
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaError_t e = cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_batch, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  int ncl = 0;
+  if (e == cudaSuccess) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.per_sb);
+    cfg.blockDim = dim3(kBT);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p.per_sb;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaOccupancyMaxActiveClusters(&ncl, k_batch, &cfg);
+  }
+  if (prev >= 0) cudaSetDevice(prev);
+  if (e != cudaSuccess || ncl < 1) {
     cudaGetLastError();
-    p.why = "device query failed";
+    p.why = "a stream-block cluster cannot be scheduled on this device";
     return p;
   }
-  if (!coop) { p.why = "device lacks cooperative launch"; return p; }
-  p.max_sb = nsm / p.per_sb;
-  if (p.max_sb < 1) { p.why = "too few SMs for one stream block"; return p; }
+  p.max_sb = ncl;
   p.ok = true;
   p.why = "ok";
   return p;
@@ -788,27 +801,30 @@ cudaError_t pack_batch_weights(const BatchPlan& p, const float* w, const Offsets
     for (int u = 0; u < p.TQ; ++u) {
       float* blk = pk.data() + p.q_off + ((int64_t)j * p.TQ + u) * p.q_floats;
       for (int kc = 0; kc < nR; ++kc) {
-        rows.assign(32 * kChunk, 0.0f);
-        for (int rho = 0; rho < 32; ++rho)
-          for (int kk = 0; kk < kChunk; ++kk) rows[rho * kChunk + kk] = W(j, o.w_skip, 32 * u + rho, 32 * kc + kk, r);
-        put_block(blk + (int64_t)kc * 64 * 32, 32, 64, rows);
+        rows.assign(kTileRows * kChunk, 0.0f);
+        for (int rho = 0; rho < kTileRows; ++rho)
+          for (int kk = 0; kk < kChunk; ++kk)
+            rows[rho * kChunk + kk] = W(j, o.w_skip, kTileRows * u + rho, 32 * kc + kk, r);
+        put_block(blk + (int64_t)kc * 2 * kTileRows * 32, kTileRows, 2 * kTileRows, rows);
       }
     }
   }
   for (int v = 0; v < p.TH; ++v) {
     for (int kc = 0; kc < s / kChunk; ++kc) {
-      rows.assign(32 * kChunk, 0.0f);
-      for (int rho = 0; rho < 32; ++rho)
+      rows.assign(kTileRows * kChunk, 0.0f);
+      for (int rho = 0; rho < kTileRows; ++rho)
         for (int kk = 0; kk < kChunk; ++kk)
-          rows[rho * kChunk + kk] = w[o.w_relu + (int64_t)(32 * v + rho) * s + 32 * kc + kk];
-      put_block(pk.data() + p.hr_off + v * p.hr_floats + (int64_t)kc * 64 * 32, 32, 64, rows);
+          rows[rho * kChunk + kk] = w[o.w_relu + (int64_t)(kTileRows * v + rho) * s + 32 * kc + kk];
+      put_block(pk.data() + p.hr_off + v * p.hr_floats + (int64_t)kc * 2 * kTileRows * 32, kTileRows, 2 * kTileRows,
+                rows);
     }
     for (int kc = 0; kc < kLevels / kChunk; ++kc) {
-      rows.assign(32 * kChunk, 0.0f);
-      for (int rho = 0; rho < 32; ++rho)
+      rows.assign(kTileRows * kChunk, 0.0f);
+      for (int rho = 0; rho < kTileRows; ++rho)
         for (int kk = 0; kk < kChunk; ++kk)
-          rows[rho * kChunk + kk] = w[o.w_out + (int64_t)(32 * v + rho) * kLevels + 32 * kc + kk];
-      put_block(pk.data() + p.ho_off + v * p.ho_floats + (int64_t)kc * 64 * 32, 32, 64, rows);
+          rows[rho * kChunk + kk] = w[o.w_out + (int64_t)(kTileRows * v + rho) * kLevels + 32 * kc + kk];
+      put_block(pk.data() + p.ho_off + v * p.ho_floats + (int64_t)kc * 2 * kTileRows * 32, kTileRows, 2 * kTileRows,
+                rows);
     }
   }
   return cudaMemcpy(packed, pk.data(), sizeof(float) * pk.size(), cudaMemcpyHostToDevice);
@@ -816,7 +832,7 @@ cudaError_t pack_batch_weights(const BatchPlan& p, const float* w, const Offsets
 
 namespace {
 struct WsLayout {
-  int64_t xb[2], hb[2], zs, za, logits, ring, yh, ctr, total;  // byte offsets
+  int64_t hb[2], zs, za, logits, ring, yh, abort, total;  // byte offsets
   int64_t ring_off[kBMaxLayers];                                 // floats from ring
 };
 WsLayout ws_layout(const BatchPlan& p, const int32_t* dil, int nsb) {
@@ -828,15 +844,13 @@ WsLayout ws_layout(const BatchPlan& p, const int32_t* dil, int nsb) {
     return o;
   };
   const int64_t act = (int64_t)2 * nsb * p.r * 128 * 4;
-  l.xb[0] = take(act);
-  l.xb[1] = take(act);
   l.hb[0] = take(act);
   l.hb[1] = take(act);
   l.zs = take((int64_t)2 * nsb * p.s * 128 * 4);
   l.za = take((int64_t)2 * nsb * kLevels * 128 * 4);
   l.logits = take((int64_t)nsb * 128 * kLevels * 4);
   l.yh = take((int64_t)nsb * 128 * 2 * 4);
-  l.ctr = take(256);
+  l.abort = take((int64_t)nsb * 4);
   int64_t rf = 0;
   for (int j = 0; j < p.L; ++j) {
     l.ring_off[j] = rf;
@@ -855,12 +869,7 @@ size_t batch_workspace_bytes(const BatchPlan& p, const int32_t* dil, int nsb) {
 cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void* packed, void* ws, size_t ws_bytes,
                                 const int32_t* dil_host, cudaStream_t st, LaunchInfo* info) {
   if (!p.ok) return cudaErrorNotSupported;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  // (plan_batch set the kernel's shared-memory and cluster-size attributes)
   const int per_launch = p.max_sb * 128;
   int64_t launches = 0;
   int grid = 0;
@@ -883,7 +892,7 @@ cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void
     P.L = p.L; P.r = p.r; P.s = p.s;
     P.TA = p.TA; P.TQ = p.TQ; P.TH = p.TH; P.per_sb = p.per_sb;
     P.nsb = nsb;
-    P.ncta = nsb * p.per_sb;
+
     P.la_off = p.la_off; P.la_floats = p.la_floats;
     P.q_off = p.q_off; P.q_floats = p.q_floats;
     P.hr_off = p.hr_off; P.hr_floats = p.hr_floats;
@@ -891,7 +900,6 @@ cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void
     P.bias_off = p.bias_off;
     char* base = static_cast<char*>(ws);
     for (int q = 0; q < 2; ++q) {
-      P.xb[q] = reinterpret_cast<float*>(base + l.xb[q]);
       P.hb[q] = reinterpret_cast<float*>(base + l.hb[q]);
     }
     P.zs = reinterpret_cast<float*>(base + l.zs);
@@ -899,20 +907,30 @@ cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void
     P.logits = reinterpret_cast<float*>(base + l.logits);
     P.ring = reinterpret_cast<float*>(base + l.ring);
     P.yh = reinterpret_cast<int*>(base + l.yh);
-    P.ctr = reinterpret_cast<unsigned long long*>(base + l.ctr);
-    P.abort_flag = reinterpret_cast<int*>(base + l.ctr + 64);
+    P.abort_flag = reinterpret_cast<int*>(base + l.abort);
     for (int j = 0; j < p.L; ++j) {
       P.dil[j] = dil_host[j];
       P.ring_off[j] = l.ring_off[j];
     }
-    void* args[] = {&P};
-    e = cudaLaunchCooperativeKernel((const void*)k_batch, dim3(P.ncta), dim3(kBT), args, (size_t)p.smem_bytes, st);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nsb * p.per_sb);  // one cluster of per_sb CTAs per stream block
+    cfg.blockDim = dim3(kBT);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p.per_sb;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_batch, P);
     if (e != cudaSuccess) return e;
     ++launches;
-    grid = std::max(grid, P.ncta);
+    grid = std::max(grid, nsb * p.per_sb);
   }
   info->grid = grid;
-  info->cluster = 1;
+  info->cluster = p.per_sb;
   info->threads = kBT;
   info->launches = launches;
   return cudaSuccess;

@@ -10,9 +10,9 @@
 // in tensor memory; the epilogue warps own one stream each (TMEM lane = stream),
 // so the gate, residual update and sampler are thread-local per stream.
 //
-// One cooperative, persistent launch runs every step; the steps' phases
-// (one per layer, then z_s, z_a, logits, sample) are separated by a grid-wide
-// barrier.  Weight tiles and activations are staged into shared memory with
+// One persistent launch runs every step; a stream block of 128 streams is one
+// thread-block cluster holding all of its tiles, and the steps' phases (one per
+// layer, then z_s, z_a, logits, sample) are separated by the cluster barrier.  Weight tiles and activations are staged into shared memory with
 // 1-D bulk copies (cp.async.bulk) from global memory, where they are kept in the
 // K-major "core matrix" order the MMA descriptors read.
 #pragma once
@@ -26,9 +26,9 @@ struct BatchPlan {
   bool ok = false;
   const char* why = "not planned";
   int L = 0, r = 0, s = 0;
-  int TA = 0, TQ = 0, TH = 0;  // CTAs per stream block: layer tiles (16 channels), skip tiles, head tiles (32 rows)
-  int per_sb = 0;              // TA + TQ + TH
-  int max_sb = 0;              // stream blocks (128 streams each) per launch
+  int TA = 0, TQ = 0, TH = 0;  // CTAs per stream block: layer tiles (16 channels), skip tiles, head tiles (64 rows)
+  int per_sb = 0;              // TA + TQ + TH = the cluster size (<= 16)
+  int max_sb = 0;              // stream blocks (clusters, 128 streams each) per launch: one co-resident wave
   // packed weights (floats)
   int64_t la_off = 0, la_floats = 0;    // [L][TA] layer-tile blocks
   int64_t q_off = 0, q_floats = 0;      // [L][TQ] skip-tile blocks
