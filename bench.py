@@ -180,8 +180,10 @@ def run_reference(args, wl):
     return 0
 
 
-def cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, budget_samples):
-    """Oracle timed on this host (1 core) on the same utterance; plus parity on it."""
+def cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, budget_samples, gpu_tf_logits=None):
+    """Oracle timed on this host (1 core) on the same utterance; plus parity on it
+    (free-running codes, per-step mismatch rate, and -- when given -- the GPU's
+    teacher-forced logits on its own codes against the oracle's)."""
     import oracle
     nb = min(n, budget_samples)
     t0 = time.perf_counter()
@@ -191,14 +193,20 @@ def cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, budget_samples):
     diff = np.nonzero(ref_codes != gpu_codes[:nb])[0]
     first = int(diff[0]) if diff.size else None
     # per-step mismatch rate: oracle teacher-forced on the GPU's own codes, drawing with the same u
-    _, _, sampled = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, HOP, nb, uniforms=u[:nb],
-                               forced=gpu_codes[:nb], dilations=cfg.dilation_list(), want_logits=False,
-                               want_sampled=True)
+    _, ref_lg, sampled = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, HOP, nb, uniforms=u[:nb],
+                                    forced=gpu_codes[:nb], dilations=cfg.dilation_list(),
+                                    want_logits=gpu_tf_logits is not None, want_sampled=True)
     mism = int(np.sum(sampled != gpu_codes[:nb]))
     cpu = {"value": nb / sec, "unit": "samples/s", "cores": 1, "kind": "oracle",
            "sample": f"{nb} samples of the same utterance (utterance 0), fp64 scalar C oracle, 1 thread"}
     parity = {"checked_samples": nb, "bit_exact_first_1600": bool(first is None or first >= 1600),
               "first_divergence": first, "divergence_rate": mism / nb, "mismatches": mism}
+    if gpu_tf_logits is not None:
+        k = min(nb, len(gpu_tf_logits))
+        parity["teacher_forced_max_abs_dlogit"] = float(
+            np.max(np.abs(gpu_tf_logits[:k].astype(np.float64) - ref_lg[:k])))
+        parity["teacher_forced_samples"] = k
+        parity["teacher_forced_gate"] = 1e-3
     return cpu, parity
 
 
@@ -222,6 +230,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--kernel", default="auto", choices=["auto", "cluster", "stream", "tc"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32"],
+                    help="batched-kernel arithmetic (tf32 = one pass, SURVEY.md 8(f) f1)")
     ap.add_argument("--samples", type=int, default=0, help="override samples per utterance (0 = workload's)")
     ap.add_argument("--ref-samples", type=int, default=1600, help="samples per reference step")
     ap.add_argument("--cpu-samples", type=int, default=16000, help="oracle samples for cpu_baseline")
@@ -261,7 +271,7 @@ def main():
         d_u = torch.from_numpy(u_np)[None].to(dev)
     else:
         d_cond, d_u = device_inputs(cfg, n, utts, dev)
-    model = Model.from_config(cfg, device=dev.index).load(w).set_kernel(args.kernel)
+    model = Model.from_config(cfg, device=dev.index).load(w).set_kernel(args.kernel).set_precision(args.precision)
     stream = torch.cuda.current_stream(dev)
     out = torch.empty((S, n), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
@@ -325,13 +335,15 @@ def main():
         flop_launch = 2.0 * macs_per_sample(cfg) * n * S
         achieved_tflops = flop_launch / (kernel_ms / 1e3) / 1e12
         kname = info["last_kernel_name"]
+        fast = kname == "tc" and args.precision == "tf32"
         if kname == "tc":
             peak, peak_src = tf32_peak_tflops()
             roof = {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved_tflops / peak, "traffic": load_ncu_traffic(args.workload, n * S),
                     "note": "algorithmic FLOP (2 x MAC/sample x samples x streams) / launch time vs dense tf32 "
-                            f"peak ({peak_src}); the 3-pass split issues ~3.2x these FLOPs on the tensor pipe; "
-                            "the step is barrier/latency bound (DESIGN.md Batched kernel)"}
+                            f"peak ({peak_src}); " + ("one tf32 pass (DVW_PRECISION_TF32); " if fast else
+                            "the 3-pass split issues ~3.2x these FLOPs on the tensor pipe; ") +
+                            "the step is phase-latency bound (DESIGN.md Batched kernel)"}
         else:
             roof = {"bound": "alu", "achieved": achieved_tflops, "peak": FP32_FMA_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": achieved_tflops / FP32_FMA_PEAK_TFLOPS,
@@ -342,7 +354,9 @@ def main():
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True,
             "scaling": "strong" if wl["split"] else "weak",
-            "vs_baseline": None, "dtype": "f32" if kname != "tc" else "f32 (tf32 x3 tensor passes)",
+            "vs_baseline": None,
+            "dtype": "f32" if kname != "tc" else ("tf32 (1 tensor pass, inputs rounded to tf32)" if fast
+                                                  else "f32 (tf32 x3 tensor passes)"),
             "data": "synthetic",
             "config": {"workload": wl["desc"], "samples_per_step": n, "streams_per_gpu": S,
                        "streams_total": total_streams,
@@ -362,7 +376,10 @@ def main():
         if not args.no_cpu:
             cond0 = d_cond[0].cpu().numpy()
             u0 = d_u[0].cpu().numpy()
-            cpu, parity = cpu_baseline_and_parity(cfg, n, w, cond0, u0, gpu_codes0, args.cpu_samples)
+            k = min(n, 1600)
+            model.set_kernel(kname)  # the teacher-forced check runs on the kernel that was timed
+            tf = model.logits(d_cond[0:1].contiguous(), out[0:1, :k].contiguous(), HOP)[0].cpu().numpy()
+            cpu, parity = cpu_baseline_and_parity(cfg, n, w, cond0, u0, gpu_codes0, args.cpu_samples, tf)
             line["cpu_baseline"] = cpu
             line["parity"] = parity
         print(json.dumps(line), flush=True)

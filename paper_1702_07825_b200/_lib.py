@@ -30,8 +30,10 @@ KERNEL_AUTO, KERNEL_STREAM, KERNEL_CLUSTER, KERNEL_TC = 0, 1, 2, 3
 KERNEL_NAMES = {0: "auto", 1: "stream", 2: "cluster", 3: "tc"}
 
 EXPORTS = ("dvw_create", "dvw_weights_numel", "dvw_load_weights", "dvw_generate", "dvw_logits",
-           "dvw_generate_host", "dvw_set_kernel", "dvw_set_trace", "dvw_get_info", "dvw_sync",
-           "dvw_destroy", "dvw_last_error")
+           "dvw_generate_host", "dvw_set_kernel", "dvw_set_precision", "dvw_set_trace", "dvw_get_info",
+           "dvw_sync", "dvw_destroy", "dvw_last_error")
+PRECISION_FP32, PRECISION_TF32 = 0, 1
+PRECISION_NAMES = {0: "fp32", 1: "tf32"}
 
 
 class _Config(ctypes.Structure):
@@ -62,6 +64,8 @@ _lib.dvw_generate_host.argtypes = [_vp, _vp, _i64, _i32, _vp, _i64, _i32, _vp, _
 _lib.dvw_generate_host.restype = _i32
 _lib.dvw_set_kernel.argtypes = [_vp, _i32]
 _lib.dvw_set_kernel.restype = _i32
+_lib.dvw_set_precision.argtypes = [_vp, _i32]
+_lib.dvw_set_precision.restype = _i32
 _lib.dvw_set_trace.argtypes = [_vp, _vp, _i64, _i32]
 _lib.dvw_set_trace.restype = _i32
 _lib.dvw_get_info.argtypes = [_vp, ctypes.POINTER(_Info)]
@@ -160,6 +164,14 @@ class Model:
         if isinstance(kernel, str):
             kernel = {v: k for k, v in KERNEL_NAMES.items()}[kernel]
         _check(_lib.dvw_set_kernel(self._h, int(kernel)))
+        return self
+
+    def set_precision(self, precision):
+        """Batched-kernel arithmetic: "fp32" (default, 3-pass tf32 split, fp32-faithful)
+        or "tf32" (one pass; within the 1e-3 logit gate, not bit-exact)."""
+        if isinstance(precision, str):
+            precision = {v: k for k, v in PRECISION_NAMES.items()}[precision]
+        _check(_lib.dvw_set_precision(self._h, int(precision)))
         return self
 
     def set_trace(self, buf=None, first_sample: int = 0):

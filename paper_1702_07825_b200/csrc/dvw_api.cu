@@ -28,6 +28,7 @@ struct dvw_model {
   Offsets off{};
   bool loaded = false;
   int kernel = DVW_KERNEL_AUTO;
+  int precision = DVW_PRECISION_FP32;
   // device buffers
   float* d_w = nullptr;
   int32_t* d_dil = nullptr;
@@ -207,7 +208,8 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   } else if (kern == DVW_KERNEL_STREAM) {
     e = launch_stream_kernel(A, cs, &li);
   } else if (kern == DVW_KERNEL_TC) {
-    e = launch_batch_kernel(A, m->bplan, m->d_bpacked, m->d_bws, m->bws_bytes, m->dil.data(), cs, &li);
+    e = launch_batch_kernel(A, m->bplan, m->d_bpacked, m->d_bws, m->bws_bytes, m->dil.data(),
+                            m->precision == DVW_PRECISION_TF32, cs, &li);
   } else {
     return fail(DVW_E_UNSUPPORTED, "kernel %d is not available in this build", kern);
   }
@@ -383,6 +385,14 @@ DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel) {
   if (kernel == DVW_KERNEL_TC && !m->bplan.ok)
     return fail(DVW_E_UNSUPPORTED, "batched kernel cannot run this model: %s", m->bplan.why);
   m->kernel = kernel;
+  return DVW_OK;
+}
+
+DVW_API dvw_status dvw_set_precision(dvw_model* m, int32_t precision) {
+  if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
+  if (precision != DVW_PRECISION_FP32 && precision != DVW_PRECISION_TF32)
+    return fail(DVW_E_INVALID_ARG, "unknown precision %d", precision);
+  m->precision = precision;
   return DVW_OK;
 }
 

@@ -59,6 +59,7 @@ struct BParams {
   RunArgs a;
   const float* pk;
   int L, r, s, TA, TQ, TH, per_sb, nsb;
+  int fast;       // DVW_PRECISION_TF32: A_hi * W_hi only (no residual passes, no A_lo staging)
   int64_t la_off, la_floats, q_off, q_floats, hr_off, hr_floats, ho_off, ho_floats, bias_off;
 
   float* hb[2];   // h^(k) in hb[k & 1]
@@ -269,9 +270,9 @@ __device__ __forceinline__ bool produce(const BParams& P, Ctl& cl, float* stages
     float* sbase = stages + (int64_t)st * kStageFloats;
     const uint32_t bar = ptx::smem_u32(&cl.full[st]);
     const uint32_t wbytes = (uint32_t)k.NS * kChunk * 4;
-    ptx::mbar_arm(bar, 2 * kActChunk * 4 + wbytes);
+    ptx::mbar_arm(bar, (P.fast ? 1 : 2) * kActChunk * 4 + wbytes);
     bulk_g2s(ptx::smem_u32(sbase), k.ah, kActChunk * 4, bar);
-    bulk_g2s(ptx::smem_u32(sbase + kActChunk), k.al, kActChunk * 4, bar);
+    if (!P.fast) bulk_g2s(ptx::smem_u32(sbase + kActChunk), k.al, kActChunk * 4, bar);
     bulk_g2s(ptx::smem_u32(sbase + 2 * kActChunk), k.w, wbytes, bar);
   }
   if (ph == 3) btrace(P, n, 12);
@@ -298,8 +299,12 @@ __device__ __forceinline__ bool issue(const BParams& P, Ctl& cl, float* stages, 
       const uint32_t ao = ks * 2 * 128 * 16, bo = ks * 2 * k.NS * 16;
       const uint64_t dah = sdesc(a_hi + ao, 128 * 16, 128), dal = sdesc(a_lo + ao, 128 * 16, 128);
       const uint64_t db = sdesc(wb + bo, k.NS * 16, 128);
-      mma_tf32(d, dah, db, id2, (k.acc || ks > 0) ? 1u : 0u);
-      mma_tf32(d, dal, db, id1, 1u);
+      if (P.fast) {  // DVW_PRECISION_TF32: D[:, 0:N) += A_hi . W_hi^T only
+        mma_tf32(d, dah, db, id1, (k.acc || ks > 0) ? 1u : 0u);
+      } else {
+        mma_tf32(d, dah, db, id2, (k.acc || ks > 0) ? 1u : 0u);
+        mma_tf32(d, dal, db, id1, 1u);
+      }
     }
     mma_commit(ptx::smem_u32(&cl.freeb[st]));
   }
@@ -308,13 +313,17 @@ __device__ __forceinline__ bool issue(const BParams& P, Ctl& cl, float* stages, 
   return true;
 }
 
-__device__ __forceinline__ void st_act(float* base_hi, int64_t half, int c, int i, const float (&v)[4]) {
-  // 4 consecutive channels c..c+3 (c % 4 == 0) of stream row i
+__device__ __forceinline__ void st_act(float* base_hi, int64_t half, int c, int i, const float (&v)[4],
+                                       bool with_lo = true) {
+  // 4 consecutive channels c..c+3 (c % 4 == 0) of stream row i; the lo half is not read
+  // in the one-pass tf32 mode
   const int o = canon(c, i);
   float4 hi = make_float4(v[0], v[1], v[2], v[3]);
-  float4 lo = make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3]));
   __stcg(reinterpret_cast<float4*>(base_hi + o), hi);
-  __stcg(reinterpret_cast<float4*>(base_hi + half + o), lo);
+  if (with_lo) {
+    float4 lo = make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3]));
+    __stcg(reinterpret_cast<float4*>(base_hi + half + o), lo);
+  }
 }
 
 __device__ __forceinline__ float4 ld_act(const float* base_hi, int c, int i) {
@@ -481,6 +490,10 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       asm volatile("" : "+f"(Dt[q]), "+f"(Ds[q]), "+f"(Dx[q]), "+f"(Et[q]), "+f"(Es[q]), "+f"(Ex[q]));
+    if (P.fast) {  // the hi*lo partner columns were not written this phase
+#pragma unroll
+      for (int q = 0; q < 8; ++q) Et[q] = Es[q] = Ex[q] = 0.0f;
+    }
     if (t == 0 && ph == 3) btrace(P, n, 16);
     const int64_t half_f = (int64_t)P.nsb * r * 128;
     float* hdst = P.hb[j & 1] + (int64_t)sb * r * 128;
@@ -492,7 +505,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
         const int c = 4 * q + e;
         hv[e] = gate_fast(((Dt[c] + Et[c]) + pre.b[c]) + pre.L[c], ((Ds[c] + Es[c]) + pre.b[8 + c]) + pre.L[8 + c]);
       }
-      st_act(hdst, half_f, c0 + 4 * q, i, hv);
+      st_act(hdst, half_f, c0 + 4 * q, i, hv, !P.fast);
     }
     if (t == 0 && ph == 3) btrace(P, n, 17);
     if (j >= 1) {
@@ -503,7 +516,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
         float xv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) xv[e] = pre.x[4 * q + e] + ((Dx[4 * q + e] + Ex[4 * q + e]) + pre.br[4 * q + e]);
-        st_act(qd, half_f, c0 + 4 * q, i, xv);
+        st_act(qd, half_f, c0 + 4 * q, i, xv, !P.fast);
       }
     }
   } else {
@@ -518,8 +531,10 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int q = 0; q < 32; ++q) asm volatile("" : "+f"(D[q]), "+f"(E[q]));
+    if (!P.fast) {
 #pragma unroll
-    for (int q = 0; q < 32; ++q) D[q] += E[q];
+      for (int q = 0; q < 32; ++q) D[q] += E[q];
+    }
     const int c0 = kTileRows * idx + 32 * half;
     if (role == kSkipT) {  // z_s = relu(q + B_skip)
       const float* bsk = A.w + A.off.b_skip + c0;
@@ -530,7 +545,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
         float v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = fmaxf(D[4 * q + e] + __ldg(bsk + 4 * q + e), 0.0f);
-        st_act(dst, half_f, c0 + 4 * q, i, v);
+        st_act(dst, half_f, c0 + 4 * q, i, v, !P.fast);
       }
     } else if (ph == P.L + 1) {  // z_a = relu(W_relu z_s + B_relu)
       const float* bb = A.w + A.off.b_relu + c0;
@@ -541,7 +556,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
         float v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = fmaxf(D[4 * q + e] + __ldg(bb + 4 * q + e), 0.0f);
-        st_act(dst, half_f, c0 + 4 * q, i, v);
+        st_act(dst, half_f, c0 + 4 * q, i, v, !P.fast);
       }
     } else {  // logits = W_out z_a + B_out
       const float* bb = A.w + A.off.b_out + c0;
@@ -867,7 +882,7 @@ size_t batch_workspace_bytes(const BatchPlan& p, const int32_t* dil, int nsb) {
 }
 
 cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void* packed, void* ws, size_t ws_bytes,
-                                const int32_t* dil_host, cudaStream_t st, LaunchInfo* info) {
+                                const int32_t* dil_host, bool fast, cudaStream_t st, LaunchInfo* info) {
   if (!p.ok) return cudaErrorNotSupported;
   // (plan_batch set the kernel's shared-memory and cluster-size attributes)
   const int per_launch = p.max_sb * 128;
@@ -892,6 +907,7 @@ cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void
     P.L = p.L; P.r = p.r; P.s = p.s;
     P.TA = p.TA; P.TQ = p.TQ; P.TH = p.TH; P.per_sb = p.per_sb;
     P.nsb = nsb;
+    P.fast = fast ? 1 : 0;
 
     P.la_off = p.la_off; P.la_floats = p.la_floats;
     P.q_off = p.q_off; P.q_floats = p.q_floats;

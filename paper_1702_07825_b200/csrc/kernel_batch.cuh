@@ -44,7 +44,8 @@ cudaError_t pack_batch_weights(const BatchPlan& p, const float* host_blob, const
 // Workspace for `nsb` stream blocks with dilations `dil` (host array, length L).
 size_t batch_workspace_bytes(const BatchPlan& p, const int32_t* dil, int nsb);
 // Runs n_streams (any count; groups of max_sb * 128 run back to back on `st`).
+// fast: one tf32 pass (DVW_PRECISION_TF32) instead of the fp32-faithful split.
 cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void* packed, void* ws, size_t ws_bytes,
-                                const int32_t* dil_host, cudaStream_t st, LaunchInfo* info);
+                                const int32_t* dil_host, bool fast, cudaStream_t st, LaunchInfo* info);
 
 }  // namespace dvw

@@ -259,3 +259,32 @@ def test_cluster_c3_deep_model_chain_skip(L):
     assert first_bad == N, f"first divergence at n={first_bad}"
     _, ref_lg, _ = oracle_tf(cfg, w, cond, hop, codes)
     assert float(np.max(np.abs(lg.astype(np.float64) - ref_lg))) <= FP32_FAITHFUL
+
+
+@pytest.mark.parametrize("cfg", [synth.C4, synth.C5], ids=["C4", "C5"])
+def test_tc_fast_tf32_mode_within_gate(L, cfg):
+    """the one-pass tf32 batched mode.  Teacher-forced logits on the
+    oracle's own codes stay inside the north_star 1e-3 gate (but far above the fp32-faithful
+    bound); the free-running per-step mismatch rate against the oracle is measured and small.
+    The default (fp32) mode on the same handle stays fp32-faithful."""
+    N, hop = 400, 64
+    w = synth.make_weights(cfg, 2)
+    utts = [0, 7]
+    cond, u = synth.make_batch(cfg, N, utts, hop)
+    m = L.Model.from_config(cfg).load(w).set_kernel("tc").set_precision("tf32")
+    codes = m.generate(dev(cond), dev(u), hop)
+    lg = m.logits(dev(cond), codes, hop).cpu().numpy()
+    codes = codes.cpu().numpy()
+    worst, mism = 0.0, 0
+    for i in range(len(utts)):
+        _, ref_lg, sampled = oracle_tf(cfg, w, cond[i], hop, codes[i], u=u[i])
+        worst = max(worst, float(np.max(np.abs(lg[i].astype(np.float64) - ref_lg))))
+        mism += int(np.sum(sampled != codes[i]))
+    print(f"tf32 {cfg}: max|dlogit| = {worst:.2e}, per-step mismatches {mism}/{N * len(utts)}")
+    assert worst <= GATE
+    assert worst > FP32_FAITHFUL / 10  # it really is the reduced-precision path
+    assert mism <= 0.05 * N * len(utts)
+    m.set_precision("fp32")
+    lg32 = m.logits(dev(cond), dev(codes), hop).cpu().numpy()
+    _, ref_lg, _ = oracle_tf(cfg, w, cond[0], hop, codes[0])
+    assert float(np.max(np.abs(lg32[0].astype(np.float64) - ref_lg))) <= FP32_FAITHFUL
