@@ -59,7 +59,6 @@ struct BParams {
   RunArgs a;
   const float* pk;
   int L, r, s, TA, TQ, TH, per_sb, nsb;
-  int fast;       // DVW_PRECISION_TF32: A_hi * W_hi only (no residual passes, no A_lo staging)
   int64_t la_off, la_floats, q_off, q_floats, hr_off, hr_floats, ho_off, ho_floats, bias_off;
 
   float* hb[2];   // h^(k) in hb[k & 1]
@@ -261,6 +260,7 @@ __device__ __forceinline__ Chunk job_chunk(const BParams& P, int role, int idx, 
 }
 
 // Producer (warp 1, one lane): stage every chunk of the job through the ring.
+template <bool FAST>
 __device__ __forceinline__ bool produce(const BParams& P, Ctl& cl, float* stages, int role, int idx, int sb, int ph,
                                         int64_t n, int nch, uint32_t cseq) {
   for (int c = 0; c < nch; ++c) {
@@ -270,9 +270,9 @@ __device__ __forceinline__ bool produce(const BParams& P, Ctl& cl, float* stages
     float* sbase = stages + (int64_t)st * kStageFloats;
     const uint32_t bar = ptx::smem_u32(&cl.full[st]);
     const uint32_t wbytes = (uint32_t)k.NS * kChunk * 4;
-    ptx::mbar_arm(bar, (P.fast ? 1 : 2) * kActChunk * 4 + wbytes);
+    ptx::mbar_arm(bar, (FAST ? 1 : 2) * kActChunk * 4 + wbytes);
     bulk_g2s(ptx::smem_u32(sbase), k.ah, kActChunk * 4, bar);
-    if (!P.fast) bulk_g2s(ptx::smem_u32(sbase + kActChunk), k.al, kActChunk * 4, bar);
+    if (!FAST) bulk_g2s(ptx::smem_u32(sbase + kActChunk), k.al, kActChunk * 4, bar);
     bulk_g2s(ptx::smem_u32(sbase + 2 * kActChunk), k.w, wbytes, bar);
   }
   if (ph == 3) btrace(P, n, 12);
@@ -280,6 +280,7 @@ __device__ __forceinline__ bool produce(const BParams& P, Ctl& cl, float* stages
 }
 
 // MMA issuer (warp 0, one lane): 4 K-steps of 8 per chunk, 3 passes each.
+template <bool FAST>
 __device__ __forceinline__ bool issue(const BParams& P, Ctl& cl, float* stages, int role, int idx, int sb, int ph,
                                       int64_t n, int nch, uint32_t cseq) {
   for (int c = 0; c < nch; ++c) {
@@ -299,7 +300,7 @@ __device__ __forceinline__ bool issue(const BParams& P, Ctl& cl, float* stages, 
       const uint32_t ao = ks * 2 * 128 * 16, bo = ks * 2 * k.NS * 16;
       const uint64_t dah = sdesc(a_hi + ao, 128 * 16, 128), dal = sdesc(a_lo + ao, 128 * 16, 128);
       const uint64_t db = sdesc(wb + bo, k.NS * 16, 128);
-      if (P.fast) {  // DVW_PRECISION_TF32: D[:, 0:N) += A_hi . W_hi^T only
+      if constexpr (FAST) {  // DVW_PRECISION_TF32: D[:, 0:N) += A_hi . W_hi^T only
         mma_tf32(d, dah, db, id1, (k.acc || ks > 0) ? 1u : 0u);
       } else {
         mma_tf32(d, dah, db, id2, (k.acc || ks > 0) ? 1u : 0u);
@@ -465,6 +466,7 @@ __device__ __forceinline__ void prefetch(const BParams& P, int role, int idx, in
 }
 
 // Thread t: stream row i = t % 128 (its TMEM lane), column half t / 128 of the tile.
+template <bool FAST>
 __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, int ph, int64_t n, const Pre& pre) {
   const RunArgs& A = P.a;
   const int t = threadIdx.x, w = t >> 5, i = t & 127, half = t >> 7;
@@ -490,7 +492,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       asm volatile("" : "+f"(Dt[q]), "+f"(Ds[q]), "+f"(Dx[q]), "+f"(Et[q]), "+f"(Es[q]), "+f"(Ex[q]));
-    if (P.fast) {  // the hi*lo partner columns were not written this phase
+    if constexpr (FAST) {  // the hi*lo partner columns were not written this phase
 #pragma unroll
       for (int q = 0; q < 8; ++q) Et[q] = Es[q] = Ex[q] = 0.0f;
     }
@@ -505,7 +507,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
         const int c = 4 * q + e;
         hv[e] = gate_fast(((Dt[c] + Et[c]) + pre.b[c]) + pre.L[c], ((Ds[c] + Es[c]) + pre.b[8 + c]) + pre.L[8 + c]);
       }
-      st_act(hdst, half_f, c0 + 4 * q, i, hv, !P.fast);
+      st_act(hdst, half_f, c0 + 4 * q, i, hv, !FAST);
     }
     if (t == 0 && ph == 3) btrace(P, n, 17);
     if (j >= 1) {
@@ -516,7 +518,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
         float xv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) xv[e] = pre.x[4 * q + e] + ((Dx[4 * q + e] + Ex[4 * q + e]) + pre.br[4 * q + e]);
-        st_act(qd, half_f, c0 + 4 * q, i, xv, !P.fast);
+        st_act(qd, half_f, c0 + 4 * q, i, xv, !FAST);
       }
     }
   } else {
@@ -531,7 +533,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int q = 0; q < 32; ++q) asm volatile("" : "+f"(D[q]), "+f"(E[q]));
-    if (!P.fast) {
+    if constexpr (!FAST) {
 #pragma unroll
       for (int q = 0; q < 32; ++q) D[q] += E[q];
     }
@@ -545,7 +547,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
         float v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = fmaxf(D[4 * q + e] + __ldg(bsk + 4 * q + e), 0.0f);
-        st_act(dst, half_f, c0 + 4 * q, i, v, !P.fast);
+        st_act(dst, half_f, c0 + 4 * q, i, v, !FAST);
       }
     } else if (ph == P.L + 1) {  // z_a = relu(W_relu z_s + B_relu)
       const float* bb = A.w + A.off.b_relu + c0;
@@ -556,7 +558,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
         float v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = fmaxf(D[4 * q + e] + __ldg(bb + 4 * q + e), 0.0f);
-        st_act(dst, half_f, c0 + 4 * q, i, v, !P.fast);
+        st_act(dst, half_f, c0 + 4 * q, i, v, !FAST);
       }
     } else {  // logits = W_out z_a + B_out
       const float* bb = A.w + A.off.b_out + c0;
@@ -573,6 +575,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
   }
 }
 
+template <bool FAST>
 __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ctl& cl = *reinterpret_cast<Ctl*>(smem_raw);
@@ -628,8 +631,8 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
         const int nch = ok ? job_chunks(P, role, ph) : 0;
         if (nch > 0) {
           bool good = true;
-          if (t == 32) good = produce(P, cl, stages, role, idx, sb, ph, n, nch, cseq);
-          else if (t == 0) good = issue(P, cl, stages, role, idx, sb, ph, n, nch, cseq);
+          if (t == 32) good = produce<FAST>(P, cl, stages, role, idx, sb, ph, n, nch, cseq);
+          else if (t == 0) good = issue<FAST>(P, cl, stages, role, idx, sb, ph, n, nch, cseq);
           if (!good) cl.abort = 1;
           __syncwarp();
           Pre pre;
@@ -641,7 +644,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
             if (t == 0 && tev >= 0) btrace(P, n, tev + 1);
             ptx::tmem_fence_after();
             if (t == 0 && ph == 3) btrace(P, n, 18);
-            epilogue(P, cl, role, idx, sb, ph, n, pre);
+            epilogue<FAST>(P, cl, role, idx, sb, ph, n, pre);
             if (t == 0 && tev >= 0) btrace(P, n, tev + 2);
           }
           ptx::tmem_fence_before();
@@ -726,8 +729,11 @@ BatchPlan plan_batch(int L, int r, int s, int device) {
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  cudaError_t e = cudaFuncSetAttribute(k_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_batch, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaError_t e = cudaSuccess;
+  for (auto fn : {k_batch<false>, k_batch<true>}) {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_bytes);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
   int ncl = 0;
   if (e == cudaSuccess) {
     cudaLaunchConfig_t cfg{};
@@ -741,7 +747,7 @@ BatchPlan plan_batch(int L, int r, int s, int device) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    e = cudaOccupancyMaxActiveClusters(&ncl, k_batch, &cfg);
+    e = cudaOccupancyMaxActiveClusters(&ncl, k_batch<false>, &cfg);
   }
   if (prev >= 0) cudaSetDevice(prev);
   if (e != cudaSuccess || ncl < 1) {
@@ -907,7 +913,6 @@ cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void
     P.L = p.L; P.r = p.r; P.s = p.s;
     P.TA = p.TA; P.TQ = p.TQ; P.TH = p.TH; P.per_sb = p.per_sb;
     P.nsb = nsb;
-    P.fast = fast ? 1 : 0;
 
     P.la_off = p.la_off; P.la_floats = p.la_floats;
     P.q_off = p.q_off; P.q_floats = p.q_floats;
@@ -940,7 +945,7 @@ cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, k_batch, P);
+    e = fast ? cudaLaunchKernelEx(&cfg, k_batch<true>, P) : cudaLaunchKernelEx(&cfg, k_batch<false>, P);
     if (e != cudaSuccess) return e;
     ++launches;
     grid = std::max(grid, nsb * p.per_sb);
