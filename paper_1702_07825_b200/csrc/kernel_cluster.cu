@@ -168,6 +168,23 @@ __device__ __forceinline__ void trace(const RunArgs& A, int64_t n, int ev) {
   }
 }
 
+// Per-sample slot of this CTA in the trace buffer (nullptr outside the window), so an
+// event inside the chain costs one clock read and one store.
+template <bool TRACE>
+__device__ __forceinline__ uint64_t* trace_slot(const RunArgs& A, int64_t n) {
+  if constexpr (TRACE) {
+    const int64_t i = n - A.trace_n0;
+    if (i >= 0 && i < A.trace_count) return A.trace + (i * kCMaxCta + ptx::cluster_rank()) * 32;
+  }
+  return nullptr;
+}
+template <bool TRACE>
+__device__ __forceinline__ void stamp(uint64_t* tp, int ev) {
+  if constexpr (TRACE) {
+    if (tp) tp[ev] = clock64();
+  }
+}
+
 template <bool TRACE>
 __device__ __forceinline__ void trace_clk(const RunArgs& A, int64_t n, int ev) {
   if constexpr (TRACE) {
@@ -398,13 +415,14 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
       if (wait(cx, &m.bar_hin, (uint32_t)p, 12) && a == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_hin), R * 4);
     }
     if (a == 0) trace<TRACE>(A, n, 0);
+    uint64_t* tp = (a == 0) ? trace_slot<TRACE>(A, n) : nullptr;
     wait(cx, &m.bar_pre, (uint32_t)p, 13);
     ptx::tmem_wait_ld<64>(w);
 #pragma unroll
     for (int jl = 0; jl < LP; ++jl) {
       if (jl < nl) {
         const bool direct = (c == 0 && jl == 0);  // a_0 = W_cur_0 x_0
-        if (a == 0) trace_clk<TRACE>(A, n, 8 + 2 * jl);
+        stamp<TRACE>(tp, 8 + 2 * jl);
         const float pre0 = m.pre[jl][hrow], pre1 = m.pre[jl][R + hrow];
         float v[2];
         tile_dot_half<2>(w, (direct ? m.xs[p][0] : (jl == 0 ? m.hin : m.hs[p][jl - 1])) + voff, v);
@@ -412,12 +430,15 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);  // both lanes of the pair: full (tanh, sigmoid) rows
         v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
         if (!direct) {
+          stamp<TRACE>(tp, 14 + jl);
           ptx::bar_sync(bar_ra(jl), kMain);  // R_j from C
+          stamp<TRACE>(tp, 17 + jl);
           v[0] += m.rr[jl][hrow];
           v[1] += m.rr[jl][R + hrow];
         }
         // a = a_cur + (W_prev x_{n-d} + B + L); h = tanh(a_h) sigma(a_g)
         const float hv = gate_fast(v[0] + pre0, v[1] + pre1);
+        stamp<TRACE>(tp, 27 + jl);
         if (jl + 1 == nl) {
           // the CTA's last layer: h goes straight to the next chain CTA (or, for layer l, to the
           // four heads) -- the only hop on the critical chain between two CTAs
@@ -427,12 +448,12 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
             m.hs[p][jl][pad16(hrow)] = hv;
           }
           bar_arrive(kBarHX + jl, kMain);  // X forwards h_{L-1}, h_{L-2} / skip-layer h
-          if (a == 0) trace_clk<TRACE>(A, n, 9 + 2 * jl);
+          stamp<TRACE>(tp, 9 + 2 * jl);
         } else {
           if (writer) m.hs[p][jl][pad16(hrow)] = hv;
           ptx::bar_sync(kBarH, kMain);     // h_j complete for A (next layer) and B
           bar_arrive(kBarHX + jl, kMain);  // ... and for X, which forwards it to the skip / head CTAs
-          if (a == 0) trace_clk<TRACE>(A, n, 9 + 2 * jl);
+          stamp<TRACE>(tp, 9 + 2 * jl);
           ptx::tmem_wait_ld<64>(w);
         }
       }
@@ -489,6 +510,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
           hv = m.hin;
           xv = m.xin;
         } else {
+          if (b == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 24 + jl - 1);  // B arrives for h_{j0+jl-1}
           ptx::bar_sync(kBarH, kMain);  // h_{j0+jl-1} from A
           hv = m.hs[p][jl - 1];
           xv = m.xs[p][jl - 1];
@@ -563,6 +585,7 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
           m.rr[jl][hrow] = v[0] + cf[jl * 2 * R + hrow];
           m.rr[jl][R + hrow] = v[1] + cf[jl * 2 * R + R + hrow];
         }
+        if (ct == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 21 + jl);
         bar_arrive(bar_ra(jl), kMain);
       }
     }

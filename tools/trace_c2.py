@@ -63,6 +63,18 @@ for c in range(ncta):
         if np.all(a == 0):
             continue
         cyc.append(f"L{jl}:{np.median(b - a):.0f}")
+    if c < 7:
+        for jl in range(3):
+            st, bra, ara, gate, cra, bh = (t[:, c, e] for e in (8 + 2 * jl, 14 + jl, 17 + jl, 27 + jl, 21 + jl, 24 + jl))
+            if np.all(st == 0):
+                continue
+            parts = [f"L{jl}:"]
+            if not np.all(bra == 0):
+                parts.append(f"toRA={np.median(bra - st):.0f} waitRA={np.median(ara - bra):.0f} Carr={np.median(cra - st):.0f}")
+            parts.append(f"gate@{np.median(gate - st):.0f}")
+            if not np.all(bh == 0):
+                parts.append(f"Barr(prev h)={np.median(bh - st):.0f}")
+            cyc.append(" ".join(parts))
     gaps = []
     for jl in range(2):
         a, b = t[:, c, 9 + 2 * jl], t[:, c, 8 + 2 * (jl + 1)]
