@@ -64,6 +64,11 @@ def _load():
         ]
         lib.oracle_sample.restype = ctypes.c_int
         lib.oracle_sample.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_float]
+        lib.oracle_run_policy.restype = ctypes.c_int
+        lib.oracle_run_policy.argtypes = lib.oracle_run.argtypes + [ctypes.c_int, ctypes.c_double, ctypes.c_int]
+        lib.oracle_sample_policy.restype = ctypes.c_int
+        lib.oracle_sample_policy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                             ctypes.c_int, ctypes.c_float]
         _lib = lib
     return _lib
 
@@ -85,13 +90,15 @@ def run(n_layers: int, residual: int, skip: int, weights: np.ndarray, cond: np.n
         hop: int, n_samples: int, uniforms: Optional[np.ndarray] = None,
         forced: Optional[np.ndarray] = None, levels: int = 256,
         dilations: Optional[Sequence[int]] = None, want_logits: bool = True,
-        want_sampled: bool = False):
+        want_sampled: bool = False, sampler: Optional[tuple] = None):
     """One utterance through the fp64 ring-buffer oracle.
 
     Returns ``(codes uint8[N], logits float64[N][a] or None, sampled uint8[N] or None)``.
     ``codes[n]`` is the code fed back after step n: ``forced[n]`` when
     teacher-forced, else the inverse-CDF draw with ``uniforms[n]``.  ``sampled[n]``
     is always the draw with ``uniforms[n]`` (for the divergence rate).
+    ``sampler = (kind, temperature, top_k)`` selects the App. A.4 strategy (0 direct,
+    1 temperature, 2 mean, 3 mode, 4 top-k; see ``sample_policy``); default direct.
     """
     lib = _load()
     w = np.ascontiguousarray(weights, dtype=np.float32)
@@ -103,9 +110,10 @@ def run(n_layers: int, residual: int, skip: int, weights: np.ndarray, cond: np.n
     codes = np.zeros(n_samples, dtype=np.uint8)
     logits = np.zeros((n_samples, levels), dtype=np.float64) if want_logits else None
     sampled = np.zeros(n_samples, dtype=np.uint8) if (want_sampled and u is not None) else None
-    rc = lib.oracle_run(n_layers, residual, skip, levels, _ptr(d), _ptr(w), w.size, _ptr(c),
-                        c.shape[0], hop, _ptr(u), _ptr(f), n_samples, _ptr(codes),
-                        _ptr(logits), _ptr(sampled))
+    kind, temp, topk = sampler if sampler is not None else (0, 1.0, 1)
+    rc = lib.oracle_run_policy(n_layers, residual, skip, levels, _ptr(d), _ptr(w), w.size, _ptr(c),
+                               c.shape[0], hop, _ptr(u), _ptr(f), n_samples, _ptr(codes),
+                               _ptr(logits), _ptr(sampled), int(kind), float(temp), int(topk))
     if rc != 0:
         raise ValueError(f"oracle_run rejected its arguments (code {rc})")
     return codes, logits, sampled
@@ -115,3 +123,15 @@ def sample(logits: np.ndarray, u: float) -> int:
     """The oracle's inverse-CDF draw on one logit vector (reading R11)."""
     l = np.ascontiguousarray(logits, dtype=np.float64)
     return int(_load().oracle_sample(_ptr(l), l.size, float(np.float32(u))))
+
+
+DIRECT, TEMPERATURE, MEAN, MODE, TOP_K = 0, 1, 2, 3, 4
+
+
+def sample_policy(logits: np.ndarray, u: float, kind: int, temperature: float = 1.0, top_k: int = 1) -> int:
+    """The oracle's draw under App. A.4 strategy ``kind`` (readings R24-R27):
+    temperature P^(1/t)/Z, mean round(E_P[y]), mode argmax (lowest index), top-k (k largest,
+    ties by lower index, renormalised); -1 for invalid parameters."""
+    l = np.ascontiguousarray(logits, dtype=np.float64)
+    return int(_load().oracle_sample_policy(_ptr(l), l.size, int(kind), float(temperature), int(top_k),
+                                            float(np.float32(u))))

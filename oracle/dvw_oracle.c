@@ -66,9 +66,67 @@ static int sample_inverse_cdf(const double* logit, int a, double u, double* e) {
   return a - 1;
 }
 
+/* The draw under each of the paper's sampling strategies (App. A.4);
+ * kind: 0 direct, 1 temperature, 2 mean, 3 mode, 4 top-k.  Details the paper leaves open
+ * follow SPEC's sample() post-conditions (readings R24-R27):
+ *   temperature t : P_t(y) = P(y)^(1/t) / Z, i.e. e_k = exp((l_k - max l) / t), then the
+ *                   direct inverse-CDF rule with u (t = 1 is direct sampling)
+ *   mean          : round(sum_y y P(y)) = floor(E_P[y] + 0.5), clamped to [0, a-1]; no u
+ *   mode          : argmax_y P(y) = argmax l, lowest index on ties; no u
+ *   top-k         : keep the k largest P(y) (ties by lower index), zero the rest,
+ *                   renormalise (implicitly), then the direct rule with u */
+static int sample_policy(const double* logit, int a, int kind, double t, int topk, double u, double* e) {
+  if (kind == 0) return sample_inverse_cdf(logit, a, u, e);
+  double m = logit[0];
+  int am = 0;
+  for (int k = 1; k < a; ++k)
+    if (logit[k] > m) { m = logit[k]; am = k; }
+  if (kind == 3) return am;  /* first index reaching the max */
+  if (kind == 2) {
+    double S = 0.0, M = 0.0;
+    for (int k = 0; k < a; ++k) {
+      const double ek = exp(logit[k] - m);
+      S += ek;
+      M += (double)k * ek;
+    }
+    double y = floor(M / S + 0.5);
+    if (y < 0.0) y = 0.0;
+    if (y > a - 1) y = a - 1;
+    return (int)y;
+  }
+  for (int k = 0; k < a; ++k) {
+    if (kind == 1) {
+      e[k] = exp((logit[k] - m) / t);
+    } else { /* top-k: rank of k among all codes, larger first, ties by lower index */
+      int rank = 0;
+      for (int j = 0; j < a; ++j)
+        if (logit[j] > logit[k] || (logit[j] == logit[k] && j < k)) ++rank;
+      e[k] = rank < topk ? exp(logit[k] - m) : 0.0;
+    }
+  }
+  double S = 0.0;
+  for (int k = 0; k < a; ++k) S += e[k];
+  double thr = u * S, P = 0.0;
+  for (int k = 0; k < a; ++k) {
+    P += e[k];
+    if (thr < P) return k;
+  }
+  for (int k = a - 1; k >= 0; --k)
+    if (e[k] > 0.0) return k;
+  return a - 1;
+}
+
 ORACLE_API int oracle_sample(const double* logits, int a, float u) {
   double* e = (double*)malloc(sizeof(double) * a);
   int y = sample_inverse_cdf(logits, a, (double)u, e);
+  free(e);
+  return y;
+}
+
+ORACLE_API int oracle_sample_policy(const double* logits, int a, int kind, double t, int topk, float u) {
+  if (kind < 0 || kind > 4 || (kind == 1 && !(t > 0.0)) || (kind == 4 && (topk < 1 || topk > a))) return -1;
+  double* e = (double*)malloc(sizeof(double) * a);
+  int y = sample_policy(logits, a, kind, t, topk, (double)u, e);
   free(e);
   return y;
 }
@@ -95,12 +153,14 @@ static void matvec(const double* W, int rows, int cols, const double* x, double*
  *   out_logits  : double [N][a] pre-softmax logits (may be NULL)
  *   out_sampled : uint8 [N] the draw with u_n even when teacher-forced (may be NULL)
  */
-ORACLE_API int oracle_run(int L, int r, int s, int a, const int32_t* dilations,
-                          const float* weights, int64_t numel, const float* cond,
-                          int64_t n_frames, int hop, const float* uniforms,
-                          const uint8_t* forced, int64_t N, uint8_t* out_codes,
-                          double* out_logits, uint8_t* out_sampled) {
+ORACLE_API int oracle_run_policy(int L, int r, int s, int a, const int32_t* dilations,
+                                 const float* weights, int64_t numel, const float* cond,
+                                 int64_t n_frames, int hop, const float* uniforms,
+                                 const uint8_t* forced, int64_t N, uint8_t* out_codes,
+                                 double* out_logits, uint8_t* out_sampled, int kind, double temp,
+                                 int topk) {
   if (L < 1 || r < 1 || s < 1 || a < 2 || a > 256 || hop < 1 || N < 0) return -1;
+  if (kind < 0 || kind > 4 || (kind == 1 && !(temp > 0.0)) || (kind == 4 && (topk < 1 || topk > a))) return -5;
   if (numel != oracle_weights_numel(L, r, s, a)) return -2;
   if (N > 0 && n_frames < (N + hop - 1) / hop) return -3;
   if (!forced && !uniforms) return -4;
@@ -199,7 +259,7 @@ ORACLE_API int oracle_run(int L, int r, int s, int a, const int32_t* dilations,
     for (int i = 0; i < a; ++i) lg[i] += Bout[i];
     if (out_logits) memcpy(out_logits + n * a, lg, sizeof(double) * a);
     int drawn = -1;
-    if (uniforms) drawn = sample_inverse_cdf(lg, a, (double)uniforms[n], e);
+    if (uniforms) drawn = sample_policy(lg, a, kind, temp, topk, (double)uniforms[n], e);
     if (out_sampled) out_sampled[n] = (uint8_t)(drawn < 0 ? 0 : drawn);
     int y = forced ? (int)forced[n] : drawn;
     out_codes[n] = (uint8_t)y;
@@ -212,4 +272,12 @@ ORACLE_API int oracle_run(int L, int r, int s, int a, const int32_t* dilations,
   free(Wprev); free(Wcur); free(Bj); free(Wres); free(Bres); free(Wskip);
   free(W); free(d);
   return 0;
+}
+
+ORACLE_API int oracle_run(int L, int r, int s, int a, const int32_t* dilations, const float* weights,
+                          int64_t numel, const float* cond, int64_t n_frames, int hop, const float* uniforms,
+                          const uint8_t* forced, int64_t N, uint8_t* out_codes, double* out_logits,
+                          uint8_t* out_sampled) {
+  return oracle_run_policy(L, r, s, a, dilations, weights, numel, cond, n_frames, hop, uniforms, forced, N,
+                           out_codes, out_logits, out_sampled, 0, 1.0, 1);
 }

@@ -285,3 +285,97 @@ def test_argument_validation():
         oracle.run(2, 4, 4, w, cond, 4, 20, uniforms=synth.make_uniforms(20))
     with pytest.raises(ValueError):  # wrong blob length
         oracle.run(2, 4, 4, w[:-1], cond, 64, 20, uniforms=synth.make_uniforms(20))
+
+
+# ---------------------------------------------------------------- App. A.4 sampling strategies (row f3)
+# PAPER.md:496-516; readings R24-R27 fix what the paper leaves open.
+_rng_s = np.random.default_rng(24)
+
+
+def _draws(l, us, kind, t=1.0, k=1):
+    return np.array([oracle.sample_policy(l, u, kind, t, k) for u in us])
+
+
+def test_sampler_one_hot_is_fixed_under_every_strategy():
+    l = np.zeros(256)
+    l[42] = 60.0  # p(42) = 1 - 255 e^-60
+    us = _rng_s.random(50, dtype=np.float32)
+    for kind, t, k in [(0, 1, 1), (1, 0.5, 1), (1, 3.0, 1), (2, 1, 1), (3, 1, 1), (4, 1, 1), (4, 1, 7)]:
+        assert np.all(_draws(l, us, kind, t, k) == 42), (kind, t, k)
+
+
+def test_temperature_special_cases_pin_the_formula():
+    """P^(1/t)/Z: t = 1 is direct sampling; t -> 0 is the mode; t -> inf is uniform."""
+    for _ in range(20):
+        l = _rng_s.normal(0, 2, 256)
+        us = _rng_s.random(20, dtype=np.float32)
+        assert np.array_equal(_draws(l, us, 1, 1.0), np.array([oracle.sample(l, u) for u in us]))
+        assert np.all(_draws(l, us, 1, 1e-4) == int(np.argmax(l)))
+    grid = ((np.arange(256) + 0.5) / 256).astype(np.float32)
+    assert np.array_equal(_draws(_rng_s.normal(0, 2, 256), grid, 1, 1e12), np.arange(256))
+
+
+def test_mode_is_argmax_lowest_index():
+    l = _rng_s.normal(0, 1, 256)
+    assert oracle.sample_policy(l, 0.9, 3) == int(np.argmax(l))
+    l[[17, 99, 200]] = l.max() + 1.0  # three-way tie
+    assert oracle.sample_policy(l, 0.1, 3) == 17
+    assert oracle.sample_policy(np.zeros(256), 0.5, 3) == 0
+
+
+def test_mean_rounds_the_expectation():
+    assert oracle.sample_policy(np.zeros(256), 0.3, 2) == 128  # E = 127.5 -> 128
+    l = np.zeros(256)
+    l[[10, 20]] = 80.0
+    assert oracle.sample_policy(l, 0.3, 2) == 15
+    l = np.zeros(256)
+    l[[10, 21]] = 80.0
+    assert oracle.sample_policy(l, 0.3, 2) == 16  # 15.5 rounds up
+    l = np.zeros(256)
+    l[[0, 3]] = [80.0, 80.0 + np.log(3.0)]  # E = (0 + 3 * 3) / 4 = 2.25
+    assert oracle.sample_policy(l, 0.3, 2) == 2
+
+
+def test_top_k_special_cases_and_support():
+    for _ in range(20):
+        l = _rng_s.normal(0, 2, 256)
+        us = _rng_s.random(20, dtype=np.float32)
+        assert np.array_equal(_draws(l, us, 4, 1, 256), np.array([oracle.sample(l, u) for u in us]))
+        assert np.all(_draws(l, us, 4, 1, 1) == int(np.argmax(l)))
+    l = _rng_s.normal(0, 1, 256)
+    top5 = set(np.argsort(-l, kind="stable")[:5].tolist())
+    grid = ((np.arange(4096) + 0.5) / 4096).astype(np.float32)
+    d = _draws(l, grid, 4, 1, 5)
+    assert set(d.tolist()) <= top5
+    # frequencies over a uniform u grid = the renormalised top-5 distribution (inverse CDF)
+    p = np.exp(l - l.max())
+    for kk in top5:
+        assert abs(np.mean(d == kk) - p[kk] / sum(p[j] for j in top5)) <= 2.0 / 4096
+    l2 = np.zeros(256)
+    l2[[5, 9, 30]] = 3.0  # ties at the cut: k = 2 keeps the two lower indices
+    assert set(_draws(l2, grid[::64], 4, 1, 2).tolist()) == {5, 9}
+
+
+def test_sampler_rejects_bad_parameters():
+    l = np.zeros(256)
+    assert oracle.sample_policy(l, 0.5, 1, 0.0) == -1
+    assert oracle.sample_policy(l, 0.5, 1, -1.0) == -1
+    assert oracle.sample_policy(l, 0.5, 4, 1.0, 0) == -1
+    assert oracle.sample_policy(l, 0.5, 4, 1.0, 257) == -1
+    assert oracle.sample_policy(l, 0.5, 7) == -1
+
+
+def test_run_with_strategies_zero_weights_closed_form():
+    """All-zero weights give all-zero logits: mode -> 0, mean -> 128 every step; direct and
+    temperature draw floor(256 u) (uniform distribution); top-k (k = 256) likewise."""
+    cfg = synth.C1
+    w = np.zeros(synth.weights_numel(cfg), np.float32)
+    N = 64
+    cond = synth.make_cond(cfg, synth.n_frames_for(N, 64), 0)
+    u = synth.make_uniforms(N, 5)
+    floor256 = np.floor(256 * u.astype(np.float64)).astype(np.uint8)
+    for sampler, expect in [((3, 1.0, 1), np.zeros(N, np.uint8)), ((2, 1.0, 1), np.full(N, 128, np.uint8)),
+                            ((1, 0.7, 1), floor256), ((4, 1.0, 256), floor256)]:
+        codes, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, 64, N, uniforms=u,
+                                 sampler=sampler, want_logits=False)
+        assert np.array_equal(codes, expect), sampler
