@@ -166,6 +166,28 @@ DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel);
 typedef enum { DVW_PRECISION_FP32 = 0, DVW_PRECISION_TF32 = 1 } dvw_precision;
 DVW_API dvw_status dvw_set_precision(dvw_model* m, int32_t precision);
 
+/* Sampling strategy for dvw_generate (App. A.4).
+ * Details the paper leaves open follow DESIGN.md readings R24-R27:
+ *   DVW_SAMPLER_DIRECT      (default) inverse-CDF draw from P with u_n (reading R11)
+ *   DVW_SAMPLER_TEMPERATURE from P_t = P^(1/t) / Z, same inverse-CDF rule with u_n
+ *   DVW_SAMPLER_MEAN        round(E_P[y]) = floor(sum_y y P(y) + 0.5); u_n unused
+ *   DVW_SAMPLER_MODE        argmax P (lowest code on ties); u_n unused
+ *   DVW_SAMPLER_TOP_K       the k largest P(y) kept (ties by lower code), renormalised,
+ *                           inverse-CDF rule with u_n
+ * temperature must be finite and > 0 (used by TEMPERATURE only), 1 <= top_k <= 256 (TOP_K
+ * only); otherwise DVW_E_INVALID_ARG.  The batched (TC) and STREAM kernels implement every
+ * strategy; the batch-1 CLUSTER kernel only DIRECT (pinning CLUSTER with another strategy
+ * makes generate return DVW_E_UNSUPPORTED; AUTO then runs STREAM for a single stream).
+ * dvw_logits is unaffected. */
+typedef enum {
+  DVW_SAMPLER_DIRECT = 0,
+  DVW_SAMPLER_TEMPERATURE = 1,
+  DVW_SAMPLER_MEAN = 2,
+  DVW_SAMPLER_MODE = 3,
+  DVW_SAMPLER_TOP_K = 4
+} dvw_sampler;
+DVW_API dvw_status dvw_set_sampler(dvw_model* m, int32_t kind, float temperature, int32_t top_k);
+
 /* Tracing: when device_buf != NULL, persistent kernels record %globaltimer (ns)
  * at fixed events of samples [first_sample, first_sample + n_samples) into
  * device_buf, uint64 [n_samples][16 cluster ranks][32 events] (unwritten slots keep

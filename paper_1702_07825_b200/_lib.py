@@ -30,8 +30,9 @@ KERNEL_AUTO, KERNEL_STREAM, KERNEL_CLUSTER, KERNEL_TC = 0, 1, 2, 3
 KERNEL_NAMES = {0: "auto", 1: "stream", 2: "cluster", 3: "tc"}
 
 EXPORTS = ("dvw_create", "dvw_weights_numel", "dvw_load_weights", "dvw_generate", "dvw_logits",
-           "dvw_generate_host", "dvw_set_kernel", "dvw_set_precision", "dvw_set_trace", "dvw_get_info",
-           "dvw_sync", "dvw_destroy", "dvw_last_error")
+           "dvw_generate_host", "dvw_set_kernel", "dvw_set_precision", "dvw_set_sampler", "dvw_set_trace",
+           "dvw_get_info", "dvw_sync", "dvw_destroy", "dvw_last_error")
+SAMPLERS = {"direct": 0, "temperature": 1, "mean": 2, "mode": 3, "top_k": 4}
 PRECISION_FP32, PRECISION_TF32 = 0, 1
 PRECISION_NAMES = {0: "fp32", 1: "tf32"}
 
@@ -66,6 +67,8 @@ _lib.dvw_set_kernel.argtypes = [_vp, _i32]
 _lib.dvw_set_kernel.restype = _i32
 _lib.dvw_set_precision.argtypes = [_vp, _i32]
 _lib.dvw_set_precision.restype = _i32
+_lib.dvw_set_sampler.argtypes = [_vp, _i32, ctypes.c_float, _i32]
+_lib.dvw_set_sampler.restype = _i32
 _lib.dvw_set_trace.argtypes = [_vp, _vp, _i64, _i32]
 _lib.dvw_set_trace.restype = _i32
 _lib.dvw_get_info.argtypes = [_vp, ctypes.POINTER(_Info)]
@@ -172,6 +175,13 @@ class Model:
         if isinstance(precision, str):
             precision = {v: k for k, v in PRECISION_NAMES.items()}[precision]
         _check(_lib.dvw_set_precision(self._h, int(precision)))
+        return self
+
+    def set_sampler(self, kind="direct", temperature: float = 1.0, top_k: int = 256):
+        """App. A.4 strategy for generate(): "direct", "temperature", "mean", "mode", "top_k"."""
+        if isinstance(kind, str):
+            kind = SAMPLERS[kind]
+        _check(_lib.dvw_set_sampler(self._h, int(kind), float(temperature), int(top_k)))
         return self
 
     def set_trace(self, buf=None, first_sample: int = 0):

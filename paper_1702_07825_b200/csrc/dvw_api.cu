@@ -29,6 +29,9 @@ struct dvw_model {
   bool loaded = false;
   int kernel = DVW_KERNEL_AUTO;
   int precision = DVW_PRECISION_FP32;
+  int samp_kind = DVW_SAMPLER_DIRECT;
+  float samp_inv_t = 1.0f;
+  int samp_topk = kLevels;
   // device buffers
   float* d_w = nullptr;
   int32_t* d_dil = nullptr;
@@ -155,8 +158,11 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   dvw_status st = check_device_error(m);
   if (st != DVW_OK) return st;
   int kern = m->kernel;
+  const bool direct = forced != nullptr || m->samp_kind == DVW_SAMPLER_DIRECT;
+  if (kern == DVW_KERNEL_CLUSTER && !direct)
+    return fail(DVW_E_UNSUPPORTED, "the cluster kernel samples directly only (dvw_set_sampler)");
   if (kern == DVW_KERNEL_AUTO) {
-    if (n_streams == 1 && m->cplan.ok) kern = DVW_KERNEL_CLUSTER;
+    if (n_streams == 1 && m->cplan.ok && direct) kern = DVW_KERNEL_CLUSTER;
     else if (n_streams > 1 && m->bplan.ok) kern = DVW_KERNEL_TC;
     else kern = DVW_KERNEL_STREAM;
   }
@@ -196,6 +202,9 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   A.out_logits = out_logits;
   A.ring = m->d_ring;
   A.err = m->d_err;
+  A.samp_kind = forced ? DVW_SAMPLER_DIRECT : m->samp_kind;
+  A.samp_inv_t = m->samp_inv_t;
+  A.samp_topk = m->samp_topk;
   A.trace = m->trace;
   A.trace_n0 = m->trace_n0;
   A.trace_count = m->trace_count;
@@ -393,6 +402,19 @@ DVW_API dvw_status dvw_set_precision(dvw_model* m, int32_t precision) {
   if (precision != DVW_PRECISION_FP32 && precision != DVW_PRECISION_TF32)
     return fail(DVW_E_INVALID_ARG, "unknown precision %d", precision);
   m->precision = precision;
+  return DVW_OK;
+}
+
+DVW_API dvw_status dvw_set_sampler(dvw_model* m, int32_t kind, float temperature, int32_t top_k) {
+  if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
+  if (kind < DVW_SAMPLER_DIRECT || kind > DVW_SAMPLER_TOP_K) return fail(DVW_E_INVALID_ARG, "unknown sampler %d", kind);
+  if (kind == DVW_SAMPLER_TEMPERATURE && !(std::isfinite(temperature) && temperature > 0.0f))
+    return fail(DVW_E_INVALID_ARG, "temperature must be finite and > 0 (got %g)", (double)temperature);
+  if (kind == DVW_SAMPLER_TOP_K && (top_k < 1 || top_k > kLevels))
+    return fail(DVW_E_INVALID_ARG, "top_k must be in [1, 256] (got %d)", top_k);
+  m->samp_kind = kind;
+  m->samp_inv_t = kind == DVW_SAMPLER_TEMPERATURE ? 1.0f / temperature : 1.0f;
+  m->samp_topk = kind == DVW_SAMPLER_TOP_K ? top_k : kLevels;
   return DVW_OK;
 }
 

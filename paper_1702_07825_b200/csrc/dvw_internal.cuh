@@ -64,6 +64,9 @@ struct RunArgs {
   float* out_logits;     // [S][N][256] or nullptr
   float* ring;           // [S][ring_floats] workspace
   int* err;              // device error word (0 = ok)
+  int samp_kind;         // App. A.4 strategy (dvw_sampler): 0 direct, 1 temperature, 2 mean, 3 mode, 4 top-k
+  float samp_inv_t;      // 1 / temperature
+  int samp_topk;         // k of top-k
   uint64_t* trace;       // optional %globaltimer trace [trace_count][16 CTAs][32 events] (dvw_set_trace)
   int64_t trace_n0;
   int trace_count;
@@ -167,5 +170,130 @@ struct LaunchInfo {
 };
 
 cudaError_t launch_stream_kernel(const RunArgs& a, cudaStream_t st, LaunchInfo* info);
+
+#ifdef __CUDACC__
+// ---------------------------------------------------------------- App. A.4 strategies (row f3)
+// One warp draws from 256 logits, lane owns codes 8 lane .. 8 lane + 7 (l[i] = code 8 lane + i).
+// fp64 running sums of e in ascending code order, then an fp64 warp scan of the lane totals;
+// y = #{k : P_k <= u * P_255}; fallback the largest k with e_k > 0 (reading R11).
+__device__ __forceinline__ int warp_cdf_draw(const float (&e)[8], float u, int lane) {
+  double p[8];
+  p[0] = (double)e[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) p[i] = p[i - 1] + (double)e[i];
+  double incl = p[7];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const double base = incl - p[7];
+  const double S = __shfl_sync(0xffffffffu, incl, 31);
+  const double thr = (double)u * S;
+  int cnt = 0, lastpos = -1;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    cnt += (base + p[i] <= thr) ? 1 : 0;
+    if (e[i] > 0.0f) lastpos = 8 * lane + i;
+  }
+  const int y = __reduce_add_sync(0xffffffffu, cnt);
+  return y < kLevels ? y : (int)__reduce_max_sync(0xffffffffu, (unsigned)(lastpos + 1)) - 1;
+}
+
+// float -> unsigned key with the same order (larger float, larger key)
+__device__ __forceinline__ unsigned ordered_key(float v) {
+  const unsigned b = __float_as_uint(v);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// The draw under strategy `kind` (readings R24-R27, as the oracle):
+// direct: e = exp(l - max l); temperature: e = exp((l - max l) / t); top-k: e = exp(l - max l)
+// on the k largest logits (ties by lower code), 0 elsewhere -- each then drawn with u by
+// warp_cdf_draw; mode: argmax (lowest code on ties); mean: floor(sum k e_k / sum e_k + 0.5).
+// Every reduction has a fixed order (bitwise deterministic).
+__device__ __forceinline__ int warp_sample_policy(const float (&l)[8], float u, int kind, float inv_t, int topk,
+                                                  int lane) {
+  float mx = fmaxf(fmaxf(fmaxf(l[0], l[1]), fmaxf(l[2], l[3])), fmaxf(fmaxf(l[4], l[5]), fmaxf(l[6], l[7])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float e[8];
+  if (kind == 3) {  // mode
+    float bv = l[0];
+    int bi = 8 * lane;
+#pragma unroll
+    for (int i = 1; i < 8; ++i)
+      if (l[i] > bv) { bv = l[i]; bi = 8 * lane + i; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    return bi;
+  }
+  if (kind == 2) {  // mean
+    double S = 0.0, M = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double ei = (double)expf(l[i] - mx);
+      S += ei;
+      M += (double)(8 * lane + i) * ei;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      S += __shfl_xor_sync(0xffffffffu, S, o);
+      M += __shfl_xor_sync(0xffffffffu, M, o);
+    }
+    const double y = floor(M / S + 0.5);
+    return y < 0.0 ? 0 : (y > kLevels - 1 ? kLevels - 1 : (int)y);
+  }
+  if (kind == 1) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) e[i] = expf((l[i] - mx) * inv_t);
+    return warp_cdf_draw(e, u, lane);
+  }
+  if (kind == 4) {  // top-k: the k-th largest key by bisection on the ordered key, then ties by code
+    unsigned key[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) key[i] = ordered_key(l[i]);
+    unsigned T = 0;
+#pragma unroll 1
+    for (int bit = 31; bit >= 0; --bit) {
+      const unsigned cand = T | (1u << bit);
+      int c = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c += key[i] >= cand ? 1 : 0;
+      if ((int)__reduce_add_sync(0xffffffffu, (unsigned)c) >= topk) T = cand;
+    }
+    int gt = 0, eq = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      gt += key[i] > T ? 1 : 0;
+      eq += key[i] == T ? 1 : 0;
+    }
+    const int need = topk - (int)__reduce_add_sync(0xffffffffu, (unsigned)gt);  // equal keys to keep
+    int eq_before = eq;  // exclusive prefix of equal keys over lower lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, eq_before, o);
+      if (lane >= o) eq_before += t;
+    }
+    eq_before -= eq;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      bool keep = key[i] > T;
+      if (key[i] == T) {
+        keep = eq_before < need;
+        ++eq_before;
+      }
+      e[i] = keep ? expf(l[i] - mx) : 0.0f;
+    }
+    return warp_cdf_draw(e, u, lane);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) e[i] = expf(l[i] - mx);
+  return warp_cdf_draw(e, u, lane);
+}
+#endif
 
 }  // namespace dvw

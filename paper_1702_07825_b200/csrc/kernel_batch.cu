@@ -344,42 +344,14 @@ __device__ __forceinline__ float4 ld4_early_cg(const float* p) {
   return v;
 }
 
-// Inverse-CDF draw over 256 logits by one warp (same arithmetic as the cluster
-// kernel's sampler: fp32 exp, fp64 running sums in ascending k; reading R11).
-__device__ __forceinline__ int sample_warp_g(const float* logits, float u, int lane) {
+// The draw for one stream by one warp (App. A.4 strategy of RunArgs; direct sampling is the
+// cluster kernel's sampler arithmetic: fp32 exp, fp64 running sums in ascending k; R11).
+__device__ __forceinline__ int sample_warp_g(const RunArgs& A, const float* logits, float u, int lane) {
   float l[8];
-  {
-    const float4 a = __ldcg(reinterpret_cast<const float4*>(logits + 8 * lane));
-    const float4 b = __ldcg(reinterpret_cast<const float4*>(logits + 8 * lane + 4));
-    l[0] = a.x; l[1] = a.y; l[2] = a.z; l[3] = a.w; l[4] = b.x; l[5] = b.y; l[6] = b.z; l[7] = b.w;
-  }
-  float mx = fmaxf(fmaxf(fmaxf(l[0], l[1]), fmaxf(l[2], l[3])), fmaxf(fmaxf(l[4], l[5]), fmaxf(l[6], l[7])));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float e[8];
-  double p[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) e[i] = expf(l[i] - mx);
-  p[0] = (double)e[0];
-#pragma unroll
-  for (int i = 1; i < 8; ++i) p[i] = p[i - 1] + (double)e[i];
-  double incl = p[7];
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  const double base = incl - p[7];
-  const double S = __shfl_sync(0xffffffffu, incl, 31);
-  const double thr = (double)u * S;
-  int cnt = 0, lastpos = -1;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    cnt += (base + p[i] <= thr) ? 1 : 0;
-    if (e[i] > 0.0f) lastpos = 8 * lane + i;
-  }
-  const int y = __reduce_add_sync(0xffffffffu, cnt);
-  return y < kLevels ? y : __reduce_max_sync(0xffffffffu, (unsigned)(lastpos + 1)) - 1;
+  const float4 a = __ldcg(reinterpret_cast<const float4*>(logits + 8 * lane));
+  const float4 b = __ldcg(reinterpret_cast<const float4*>(logits + 8 * lane + 4));
+  l[0] = a.x; l[1] = a.y; l[2] = a.z; l[3] = a.w; l[4] = b.x; l[5] = b.y; l[6] = b.z; l[7] = b.w;
+  return warp_sample_policy(l, u, A.samp_kind, A.samp_inv_t, A.samp_topk, lane);
 }
 
 // x^(0)_{n+1} = W_emb_prev[:, y_{n-1}] + W_emb_cur[:, y_n] + B_emb
@@ -659,7 +631,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
           if (A.forced) {
             y = __ldg(A.forced + (int64_t)g * A.N + n);
           } else {
-            y = sample_warp_g(P.logits + (int64_t)g * kLevels, __ldg(A.uniforms + (int64_t)g * A.N + n), lane);
+            y = sample_warp_g(A, P.logits + (int64_t)g * kLevels, __ldg(A.uniforms + (int64_t)g * A.N + n), lane);
             if (lane == 0) A.out_codes[(int64_t)g * A.N + n] = (uint8_t)y;
           }
           if (n + 1 < A.N) embed(P, g, n + 1, y1, y, lane);

@@ -168,7 +168,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(RunArgs A) {
       A.out_logits[((int64_t)st * A.N + n) * kLevels + tid] = l;
       y = forced[n];
     } else {
-      y = sample_256(l, uni[n], dscr, fscr, iscr, tid, 1);
+      if (A.samp_kind == 0) {
+        y = sample_256(l, uni[n], dscr, fscr, iscr, tid, 1);
+      } else {  // App. A.4 strategies: one warp (row f3)
+        if (tid < 32) {
+          float lv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) lv[i] = lg[8 * tid + i];
+          const int yy = warp_sample_policy(lv, uni[n], A.samp_kind, A.samp_inv_t, A.samp_topk, tid);
+          if (tid == 0) iscr[0] = yy;
+        }
+        __syncthreads();
+        y = iscr[0];
+      }
       if (tid == 0) A.out_codes[(int64_t)st * A.N + n] = (uint8_t)y;
     }
     y2 = y1;

@@ -288,3 +288,49 @@ def test_tc_fast_tf32_mode_within_gate(L, cfg):
     lg32 = m.logits(dev(cond), dev(codes), hop).cpu().numpy()
     _, ref_lg, _ = oracle_tf(cfg, w, cond[0], hop, codes[0])
     assert float(np.max(np.abs(lg32[0].astype(np.float64) - ref_lg))) <= FP32_FAITHFUL
+
+
+STRATEGIES = [("temperature", 0.7, 256), ("mean", 1.0, 256), ("mode", 1.0, 256), ("top_k", 1.0, 5)]
+KIND = {"direct": 0, "temperature": 1, "mean": 2, "mode": 3, "top_k": 4}
+
+
+@pytest.mark.parametrize("kernel", ["stream", "tc"])
+@pytest.mark.parametrize("policy", STRATEGIES, ids=[p[0] for p in STRATEGIES])
+def test_sampler_strategies_match_oracle(L, kernel, policy):
+    """Row f3: free-running codes under each App. A.4 strategy equal the
+    fp64 oracle's under the same strategy (peaky weights: decisions far from ties)."""
+    cfg = synth.C1
+    N, hop = 300, 64
+    w = synth.make_weights(cfg, 3, "peaky")
+    cond = synth.make_cond(cfg, synth.n_frames_for(N, hop), 2)
+    u = synth.make_uniforms(N, 2)
+    name, t, k = policy
+    m = model(L, cfg, w, kernel).set_sampler(name, t, k)
+    codes = m.generate(dev(cond)[None], dev(u)[None], hop).cpu().numpy()[0]
+    assert m.info()["last_kernel_name"] == kernel
+    ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, N, uniforms=u,
+                           sampler=(KIND[name], t, k), want_logits=False)
+    first_bad = int(np.argmax(codes != ref)) if np.any(codes != ref) else N
+    assert first_bad == N, f"{name}: first divergence at n={first_bad}"
+
+
+def test_sampler_routing_and_validation(L):
+    cfg = synth.C1
+    w = synth.make_weights(cfg, 0)
+    N = 64
+    cond = dev(synth.make_cond(cfg, synth.n_frames_for(N, 64), 0))[None]
+    u = dev(synth.make_uniforms(N, 0))[None]
+    m = L.Model.from_config(cfg).load(w).set_sampler("mode")
+    m.generate(cond, u, 64)
+    assert m.info()["last_kernel_name"] == "stream"  # AUTO: the cluster kernel samples directly only
+    m.set_kernel("cluster")
+    with pytest.raises(L.DvwError) as e:
+        m.generate(cond, u, 64)
+    assert e.value.name == "DVW_E_UNSUPPORTED"
+    m.set_sampler("direct")
+    m.generate(cond, u, 64)
+    assert m.info()["last_kernel_name"] == "cluster"
+    for bad in [("temperature", 0.0, 1), ("temperature", float("inf"), 1), ("top_k", 1.0, 0), ("top_k", 1.0, 257)]:
+        with pytest.raises(L.DvwError) as e:
+            m.set_sampler(*bad)
+        assert e.value.name == "DVW_E_INVALID_ARG"
