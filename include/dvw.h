@@ -208,6 +208,41 @@ DVW_API void dvw_destroy(dvw_model* m);
 /* Thread-local text for the last non-OK status ("" if none). */
 DVW_API const char* dvw_last_error(void);
 
+/* ---------------------------------------------------------------------------------------
+ * Conditioning network (App. A.2): features at
+ * frame rate -> the per-layer conditioning `cond` dvw_generate consumes.  Two bidirectional
+ * QRNN layers with fo-pooling and 2x1 convolutions,
+ *   h~ = tanh(W_h * x + B_h), o = sigma(W_o * x + B_o), f = sigma(W_f * x + B_f),
+ *   h_t = f_t h_{t-1} + (1 - f_t) h~_t, z_t = o_t h_t, h_0 = 0,
+ * the backward QRNN running on the reversed sequence (its taps are x_{t+1}, x_t; reading
+ * R28), channels stacked [forward | backward] per layer, interleaved after the second layer
+ * (channel 2i forward i, 2i+1 backward i; R29), then one projection per WaveNet layer,
+ * L^(j)_t = P^(j) out_t + B^(j) (R30).  Upsampling by repetition happens inside
+ * dvw_generate (hop).  fp32, bitwise deterministic.
+ *
+ * Weight blob (fp32, this order): for QRNN layer q = 1, 2 (C_in = in_channels, then
+ * 2 hidden), for the forward then the backward direction: W [3 gates h,o,f][2 taps: older,
+ * current][hidden][C_in], B [3][hidden]; then P [n_layers][2 residual][2 hidden] and
+ * B_P [n_layers][2 residual].
+ * dvwc_run: features fp32 [n_streams][n_frames][in_channels] (device), out_cond fp32
+ * [n_streams][n_frames][n_layers][2 residual] (device) -- exactly dvw_generate's cond layout.
+ * Same conventions as the generator: stream-ordered, asynchronous, caller owns buffers,
+ * errors via dvw_last_error(). */
+typedef struct dvwc_model dvwc_model;
+typedef struct {
+  int32_t in_channels;  /* feature channels per frame (>= 1) */
+  int32_t hidden;       /* QRNN channels per direction (1..1024) */
+  int32_t n_layers;     /* l of the WaveNet it conditions */
+  int32_t residual;     /* r of the WaveNet it conditions */
+  int32_t device;
+} dvwc_config;
+DVW_API dvw_status dvwc_create(const dvwc_config* cfg, dvwc_model** out);
+DVW_API int64_t dvwc_weights_numel(const dvwc_config* cfg);
+DVW_API dvw_status dvwc_load_weights(dvwc_model* m, const float* blob, int64_t numel, int32_t blob_on_device);
+DVW_API dvw_status dvwc_run(dvwc_model* m, const float* features, int64_t n_frames, int32_t n_streams,
+                            float* out_cond, void* cuda_stream);
+DVW_API void dvwc_destroy(dvwc_model* m);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,7 +31,8 @@ KERNEL_NAMES = {0: "auto", 1: "stream", 2: "cluster", 3: "tc"}
 
 EXPORTS = ("dvw_create", "dvw_weights_numel", "dvw_load_weights", "dvw_generate", "dvw_logits",
            "dvw_generate_host", "dvw_set_kernel", "dvw_set_precision", "dvw_set_sampler", "dvw_set_trace",
-           "dvw_get_info", "dvw_sync", "dvw_destroy", "dvw_last_error")
+           "dvw_get_info", "dvw_sync", "dvw_destroy", "dvw_last_error",
+           "dvwc_create", "dvwc_weights_numel", "dvwc_load_weights", "dvwc_run", "dvwc_destroy")
 SAMPLERS = {"direct": 0, "temperature": 1, "mean": 2, "mode": 3, "top_k": 4}
 PRECISION_FP32, PRECISION_TF32 = 0, 1
 PRECISION_NAMES = {0: "fp32", 1: "tf32"}
@@ -67,6 +68,22 @@ _lib.dvw_set_kernel.argtypes = [_vp, _i32]
 _lib.dvw_set_kernel.restype = _i32
 _lib.dvw_set_precision.argtypes = [_vp, _i32]
 _lib.dvw_set_precision.restype = _i32
+class _CConfig(ctypes.Structure):
+    _fields_ = [("in_channels", ctypes.c_int32), ("hidden", ctypes.c_int32), ("n_layers", ctypes.c_int32),
+                ("residual", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+
+_lib.dvwc_create.argtypes = [ctypes.POINTER(_CConfig), ctypes.POINTER(ctypes.c_void_p)]
+_lib.dvwc_create.restype = ctypes.c_int32
+_lib.dvwc_weights_numel.argtypes = [ctypes.POINTER(_CConfig)]
+_lib.dvwc_weights_numel.restype = ctypes.c_int64
+_lib.dvwc_load_weights.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32]
+_lib.dvwc_load_weights.restype = ctypes.c_int32
+_lib.dvwc_run.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+                          ctypes.c_void_p]
+_lib.dvwc_run.restype = ctypes.c_int32
+_lib.dvwc_destroy.argtypes = [ctypes.c_void_p]
+_lib.dvwc_destroy.restype = None
 _lib.dvw_set_sampler.argtypes = [_vp, _i32, ctypes.c_float, _i32]
 _lib.dvw_set_sampler.restype = _i32
 _lib.dvw_set_trace.argtypes = [_vp, _vp, _i64, _i32]
@@ -248,3 +265,50 @@ def raw_call(name: str, *args) -> int:
 
 def last_error() -> str:
     return (_lib.dvw_last_error() or b"").decode()
+
+
+def conditioner_numel(in_channels: int, hidden: int, n_layers: int, residual: int) -> int:
+    cfg = _CConfig(in_channels, hidden, n_layers, residual, 0)
+    return int(_lib.dvwc_weights_numel(ctypes.byref(cfg)))
+
+
+class Conditioner:
+    """Handle on the GPU conditioning network (dvwc_*, include/dvw.h; App. A.2):
+    features [S][T][in_channels] (CUDA fp32) -> cond [S][T][n_layers][2 residual] for
+    Model.generate."""
+
+    def __init__(self, in_channels: int, hidden: int, n_layers: int, residual: int, device: int = 0):
+        cfg = _CConfig(in_channels, hidden, n_layers, residual, device)
+        h = _vp()
+        _check(_lib.dvwc_create(ctypes.byref(cfg), ctypes.byref(h)))
+        self._h = h
+        self.in_channels, self.hidden, self.n_layers, self.residual = in_channels, hidden, n_layers, residual
+        self.numel = int(_lib.dvwc_weights_numel(ctypes.byref(cfg)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.dvwc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load(self, blob):
+        if isinstance(blob, np.ndarray):
+            b = np.ascontiguousarray(blob, dtype=np.float32)
+            _check(_lib.dvwc_load_weights(self._h, b.ctypes.data, b.size, 0))
+        else:
+            _check(_lib.dvwc_load_weights(self._h, _dptr(blob, blob.dtype, "blob"), blob.numel(), 1))
+        return self
+
+    def run(self, features, out=None, stream=None):
+        import torch
+        S, T = int(features.shape[0]), int(features.shape[1])
+        if out is None:
+            out = torch.empty((S, T, self.n_layers, 2 * self.residual), dtype=torch.float32, device=features.device)
+        _check(_lib.dvwc_run(self._h, _dptr(features, torch.float32, "features"), T, S,
+                             _dptr(out, torch.float32, "out"), _stream_handle(stream)))
+        return out

@@ -72,6 +72,12 @@ dvw_status fail(dvw_status st, const char* fmt, ...) {
   return st;
 }
 
+}  // namespace
+
+void dvw::note_error(const char* text) { g_err = text; }
+
+namespace {
+
 dvw_status cuda_fail(cudaError_t e, const char* what) {
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();

@@ -45,6 +45,9 @@ inline Offsets make_offsets(int L, int r, int s) {
   return o;
 }
 
+// Records the thread-local text dvw_last_error() returns (dvw_api.cu).
+void note_error(const char* text);
+
 // Arguments common to every generation kernel.  All pointers are device pointers.
 struct RunArgs {
   const float* w;        // raw roster-order weights

@@ -141,3 +141,61 @@ def make_codes(n_samples: int, utt: int = 0, levels: int = LEVELS) -> np.ndarray
     """Random uint8 code history for teacher-forced runs (role key 3)."""
     rng = np.random.default_rng([3, utt])
     return rng.integers(0, levels, n_samples, dtype=np.int64).astype(np.uint8)
+
+
+# ---------------------------------------------------------------- conditioning network (row f2)
+# Features: 227 channels per 256 Hz frame (one-hot phoneme with two previous and two next
+# phonemes, voiced flag, normalised log F0 -- PAPER.md:485-489 App. A.3, SPEC's featurizer
+# count); QRNN hidden width 64 per direction (the paper does not state it; reading R30).
+COND_FEATURES = 227
+COND_HIDDEN = 64
+
+
+def conditioner_numel(in_channels: int, hidden: int, n_layers: int, residual: int) -> int:
+    """Length of the conditioner blob in include/dvw.h's order (dvwc_load_weights)."""
+    n = 0
+    for cin in (in_channels, 2 * hidden):
+        n += 2 * (3 * 2 * hidden * cin + 3 * hidden)
+    return n + n_layers * 2 * residual * 2 * hidden + n_layers * 2 * residual
+
+
+def make_conditioner_weights(in_channels: int, hidden: int, n_layers: int, residual: int,
+                             seed: int = 0) -> np.ndarray:
+    """uniform(+-1/sqrt(fan_in)) per tensor in blob order: fan_in = 2 C_in for the QRNN taps and
+    biases (2x1 convolution), 2 hidden for the projections."""
+    rng = np.random.default_rng([3, seed])
+    parts = []
+    for cin in (in_channels, 2 * hidden):
+        b = 1.0 / math.sqrt(2 * cin)
+        for _ in range(2):  # forward, backward
+            parts.append(rng.uniform(-b, b, 3 * 2 * hidden * cin))
+            parts.append(rng.uniform(-b, b, 3 * hidden))
+    b = 1.0 / math.sqrt(2 * hidden)
+    parts.append(rng.uniform(-b, b, n_layers * 2 * residual * 2 * hidden))
+    parts.append(rng.uniform(-b, b, n_layers * 2 * residual))
+    out = np.concatenate(parts).astype(np.float32)
+    assert out.size == conditioner_numel(in_channels, hidden, n_layers, residual)
+    return out
+
+
+def make_features(n_frames: int, in_channels: int = COND_FEATURES, utt: int = 0) -> np.ndarray:
+    """Frame-rate features of utterance u: ``default_rng([4, u])``; a one-hot-like phoneme block
+    (5 x 45 channels, one active per phoneme slot, held for a random 8-40 frame duration) plus
+    a voiced flag and a normalised log-F0 in [-1, 1], padded/truncated to in_channels."""
+    rng = np.random.default_rng([4, utt])
+    f = np.zeros((n_frames, in_channels), np.float32)
+    t = 0
+    while t < n_frames:
+        d = int(rng.integers(8, 41))
+        ph = rng.integers(0, 45, 5)
+        voiced = float(rng.random() < 0.7)
+        f0 = rng.uniform(-1, 1)
+        for k in range(5):
+            if 45 * k + ph[k] < in_channels:
+                f[t:t + d, 45 * k + ph[k]] = 1.0
+        if in_channels > 225:
+            f[t:t + d, 225] = voiced
+        if in_channels > 226:
+            f[t:t + d, 226] = f0 * voiced
+        t += d
+    return f

@@ -21,12 +21,12 @@ def lib():
 
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "dvw.h")).read()
-    return sorted(set(re.findall(r"DVW_API\s+[\w\s\*]+?\b(dvw_\w+)\s*\(", text)))
+    return sorted(set(re.findall(r"DVW_API\s+[\w\s\*]+?\b(dvwc?_\w+)\s*\(", text)))
 
 
 def test_exports_every_declared_symbol(lib):
     names = declared_symbols()
-    assert len(names) == 14, names
+    assert len(names) == 19, names
     raw = ctypes.CDLL(lib.LIB_PATH)
     for n in names:
         assert hasattr(raw, n), n
@@ -76,3 +76,11 @@ def test_product_path_has_no_oracle_dependency():
                 assert not re.search(r"^\s*(import|from)\s+oracle", text, re.M), f
                 assert not re.search(r'#include\s*[<"][^>"]*oracle', text), f
                 assert "liboracle" not in text, f
+
+
+def test_conditioner_abi_without_gpu(lib):
+    assert lib.conditioner_numel(227, 64, 20, 64) > 0
+    assert lib.raw_call("dvwc_create", None, None) == 1
+    assert lib.raw_call("dvwc_load_weights", None, None, 0, 0) == 1
+    assert lib.raw_call("dvwc_run", None, None, 1, 1, None, None) == 1
+    lib._lib.dvwc_destroy(None)

@@ -334,3 +334,33 @@ def test_sampler_routing_and_validation(L):
         with pytest.raises(L.DvwError) as e:
             m.set_sampler(*bad)
         assert e.value.name == "DVW_E_INVALID_ARG"
+
+
+def test_conditioner_matches_oracle_and_feeds_generation(L):
+    """Row f2 (App. A.2): the GPU QRNN conditioner's L^(j) against the fp64
+    oracle (fp32-faithful), and generation from it code-for-code with the oracle run on the same
+    conditioning (the layouts line up end to end)."""
+    from oracle import qrnn
+    cfg = synth.C1
+    T, hop, N = 40, 16, 600
+    cw = synth.make_conditioner_weights(synth.COND_FEATURES, synth.COND_HIDDEN, cfg.n_layers, cfg.residual, 1)
+    feats = np.stack([synth.make_features(T, utt=u) for u in (0, 3)])
+    c = L.Conditioner(synth.COND_FEATURES, synth.COND_HIDDEN, cfg.n_layers, cfg.residual).load(cw)
+    cond = c.run(dev(feats))
+    torch.cuda.synchronize()
+    got = cond.cpu().numpy()
+    for i in range(2):
+        ref = qrnn.condition(feats[i], cw, synth.COND_HIDDEN, cfg.n_layers, cfg.residual)
+        err = float(np.max(np.abs(got[i].astype(np.float64) - ref)))
+        assert err <= 2e-5, err
+        assert np.max(np.abs(ref)) > 0.05  # not trivially small
+    assert np.array_equal(c.run(dev(feats)).cpu().numpy(), got)  # deterministic
+    w = synth.make_weights(cfg, 0)
+    u = synth.make_uniforms(N, 0)
+    m = L.Model.from_config(cfg).load(w)
+    codes = m.generate(cond[0:1].contiguous(), dev(u)[None], hop).cpu().numpy()[0]
+    ref_codes, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, got[0], hop, N, uniforms=u)
+    assert np.array_equal(codes, ref_codes)
+    with pytest.raises(L.DvwError) as e:
+        c.load(cw[:-1])
+    assert e.value.name == "DVW_E_SHAPE"
