@@ -69,11 +69,11 @@ __global__ void __launch_bounds__(kGThreads) k_gates(const float* __restrict__ x
     xs[i] = (tt >= 0 && tt < T) ? xsrc[(int64_t)tt * C + c] : 0.0f;  // x_{-1} = x_T = 0 (h_0 = 0 start)
   }
   __syncthreads();
-  const int rows = 2 * 3 * H;  // (direction, gate, channel)
-  for (int job = threadIdx.x; job < rows * kTT; job += blockDim.x) {
-    const int row = job % rows, tl = job / rows, t = t0 + tl;
+  const int d = blockIdx.z / 3, gate = blockIdx.z % 3;  // this block's direction and gate
+  for (int job = threadIdx.x; job < H * kTT; job += blockDim.x) {
+    const int ch = job % H, tl = job / H, t = t0 + tl;
     if (t >= T) continue;
-    const int d = row / (3 * H), gh = row % (3 * H);  // gh = gate * H + channel
+    const int gh = gate * H + ch;
     const float* w = W + (d == 0 ? wf : wb);
     const float* w_old = w + (int64_t)(gh / H) * 2 * H * C + (int64_t)(gh % H) * C;  // tap 0: x_{t-1} / x_{t+1}
     const float* w_now = w_old + (int64_t)H * C;                                       // tap 1: x_t
@@ -105,12 +105,22 @@ __global__ void k_pool(const float* __restrict__ gates, int S, int T, int H, flo
   const int s = id / (2 * H), d = (id / H) % 2, c = id % H;
   const float* g = gates + ((int64_t)s * 2 + d) * T * 3 * H;
   float h = 0.0f;
-  for (int k = 0; k < T; ++k) {
-    const int t = d == 0 ? k : T - 1 - k;
-    const float* gt = g + (int64_t)t * 3 * H;
-    const float ht = gt[c], o = gt[H + c], f = gt[2 * H + c];
+  int t = d == 0 ? 0 : T - 1;
+  const int step = d == 0 ? 1 : -1;
+  float ht = g[(int64_t)t * 3 * H + c], o = g[(int64_t)t * 3 * H + H + c], f = g[(int64_t)t * 3 * H + 2 * H + c];
+  for (int k = 0; k < T; ++k, t += step) {
+    float nht = 0.f, no = 0.f, nf = 0.f;
+    if (k + 1 < T) {  // next frame's gates in flight while this one is pooled
+      const float* gn = g + (int64_t)(t + step) * 3 * H;
+      nht = gn[c];
+      no = gn[H + c];
+      nf = gn[2 * H + c];
+    }
     h = f * h + (1.0f - f) * ht;
     z[((int64_t)s * T + t) * 2 * H + d * H + c] = o * h;
+    ht = nht;
+    o = no;
+    f = nf;
   }
 }
 
@@ -126,9 +136,9 @@ __global__ void __launch_bounds__(kGThreads) k_proj(const float* __restrict__ z,
     zs[i] = t < T ? z[((int64_t)s * T + t) * 2 * H + src] : 0.0f;
   }
   __syncthreads();
-  const int rows = L * r2;
-  for (int job = threadIdx.x; job < rows * kTT; job += blockDim.x) {
-    const int row = job % rows, tl = job / rows, t = t0 + tl;
+  const int rows = L * r2, j = blockIdx.z;  // this block's WaveNet layer
+  for (int job = threadIdx.x; job < r2 * kTT; job += blockDim.x) {
+    const int row = j * r2 + job % r2, tl = job / r2, t = t0 + tl;
     if (t >= T) continue;
     const float* p = P + (int64_t)row * 2 * H;
     const float* v = zs + tl * 2 * H;
@@ -253,11 +263,12 @@ DVW_API dvw_status dvwc_run(dvwc_model* m, const float* features, int64_t n_fram
     const float* in = features;
     int C = m->cin;
     const dim3 grid((T + kTT - 1) / kTT, S);
+    const dim3 ggrid((T + kTT - 1) / kTT, S, 6);  // x (direction, gate)
     for (int q = 0; q < 2 && e == cudaSuccess; ++q) {
       const size_t sm = sizeof(float) * (kTT + 2) * C;
       if (sm > 48 * 1024) e = cudaFuncSetAttribute(k_gates, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) break;
-      k_gates<<<grid, kGThreads, sm, st>>>(in, T, C, H, m->d_w, m->off.w[q][0], m->off.b[q][0], m->off.w[q][1],
+      k_gates<<<ggrid, kGThreads, sm, st>>>(in, T, C, H, m->d_w, m->off.w[q][0], m->off.b[q][0], m->off.w[q][1],
                                            m->off.b[q][1], g);
       k_pool<<<(S * 2 * H + 127) / 128, 128, 0, st>>>(g, S, T, H, z[q]);
       e = cudaGetLastError();
@@ -268,7 +279,7 @@ DVW_API dvw_status dvwc_run(dvwc_model* m, const float* features, int64_t n_fram
       const size_t sm = sizeof(float) * kTT * 2 * H;
       if (sm > 48 * 1024) e = cudaFuncSetAttribute(k_proj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e == cudaSuccess) {
-        k_proj<<<grid, kGThreads, sm, st>>>(z[1], T, H, m->L, 2 * m->r, m->d_w + m->off.P, m->d_w + m->off.BP,
+        k_proj<<<dim3(grid.x, grid.y, m->L), kGThreads, sm, st>>>(z[1], T, H, m->L, 2 * m->r, m->d_w + m->off.P, m->d_w + m->off.BP,
                                             out_cond);
         e = cudaGetLastError();
       }
