@@ -230,8 +230,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--kernel", default="auto", choices=["auto", "cluster", "stream", "tc"])
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32"],
-                    help="batched-kernel arithmetic (tf32 = one pass, SURVEY.md 8(f) f1)")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "approx"],
+                    help="tf32: one-pass batched kernel (SURVEY.md 8(f) f1); approx: hardware tanh in the "
+                         "batch-1 gates (f4)")
     ap.add_argument("--samples", type=int, default=0, help="override samples per utterance (0 = workload's)")
     ap.add_argument("--ref-samples", type=int, default=1600, help="samples per reference step")
     ap.add_argument("--cpu-samples", type=int, default=16000, help="oracle samples for cpu_baseline")
@@ -355,7 +356,7 @@ def main():
         flop_launch = 2.0 * macs_per_sample(cfg) * n * S
         achieved_tflops = flop_launch / (kernel_ms / 1e3) / 1e12
         kname = info["last_kernel_name"]
-        fast = kname == "tc" and args.precision == "tf32"
+        fast = kname == "tc" and args.precision != "fp32"
         if kname == "tc":
             peak, peak_src = tf32_peak_tflops()
             roof = {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
@@ -375,8 +376,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True,
             "scaling": "strong" if wl["split"] else "weak",
             "vs_baseline": None,
-            "dtype": "f32" if kname != "tc" else ("tf32 (1 tensor pass, inputs rounded to tf32)" if fast
-                                                  else "f32 (tf32 x3 tensor passes)"),
+            "dtype": (("f32 (hardware tanh.approx gate)" if args.precision == "approx" else "f32") if kname != "tc"
+                      else ("tf32 (1 tensor pass, inputs rounded to tf32)" if fast else "f32 (tf32 x3 tensor passes)")),
             "data": "synthetic",
             "config": {"workload": wl["desc"], "samples_per_step": n, "streams_per_gpu": S,
                        "streams_total": total_streams,

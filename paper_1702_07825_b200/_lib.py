@@ -34,8 +34,8 @@ EXPORTS = ("dvw_create", "dvw_weights_numel", "dvw_load_weights", "dvw_generate"
            "dvw_get_info", "dvw_sync", "dvw_destroy", "dvw_last_error",
            "dvwc_create", "dvwc_weights_numel", "dvwc_load_weights", "dvwc_run", "dvwc_destroy")
 SAMPLERS = {"direct": 0, "temperature": 1, "mean": 2, "mode": 3, "top_k": 4}
-PRECISION_FP32, PRECISION_TF32 = 0, 1
-PRECISION_NAMES = {0: "fp32", 1: "tf32"}
+PRECISION_FP32, PRECISION_TF32, PRECISION_APPROX = 0, 1, 2
+PRECISION_NAMES = {0: "fp32", 1: "tf32", 2: "approx"}
 
 
 class _Config(ctypes.Structure):

@@ -208,6 +208,7 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   A.out_logits = out_logits;
   A.ring = m->d_ring;
   A.err = m->d_err;
+  A.approx = m->precision == DVW_PRECISION_APPROX ? 1 : 0;
   A.samp_kind = forced ? DVW_SAMPLER_DIRECT : m->samp_kind;
   A.samp_inv_t = m->samp_inv_t;
   A.samp_topk = m->samp_topk;
@@ -224,7 +225,7 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
     e = launch_stream_kernel(A, cs, &li);
   } else if (kern == DVW_KERNEL_TC) {
     e = launch_batch_kernel(A, m->bplan, m->d_bpacked, m->d_bws, m->bws_bytes, m->dil.data(),
-                            m->precision == DVW_PRECISION_TF32, cs, &li);
+                            m->precision != DVW_PRECISION_FP32, cs, &li);
   } else {
     return fail(DVW_E_UNSUPPORTED, "kernel %d is not available in this build", kern);
   }
@@ -405,7 +406,7 @@ DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel) {
 
 DVW_API dvw_status dvw_set_precision(dvw_model* m, int32_t precision) {
   if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
-  if (precision != DVW_PRECISION_FP32 && precision != DVW_PRECISION_TF32)
+  if (precision != DVW_PRECISION_FP32 && precision != DVW_PRECISION_TF32 && precision != DVW_PRECISION_APPROX)
     return fail(DVW_E_INVALID_ARG, "unknown precision %d", precision);
   m->precision = precision;
   return DVW_OK;

@@ -67,6 +67,7 @@ struct RunArgs {
   float* out_logits;     // [S][N][256] or nullptr
   float* ring;           // [S][ring_floats] workspace
   int* err;              // device error word (0 = ok)
+  int approx;            // DVW_PRECISION_APPROX: hardware tanh in the batch-1 kernels' gates
   int samp_kind;         // App. A.4 strategy (dvw_sampler): 0 direct, 1 temperature, 2 mean, 3 mode, 4 top-k
   float samp_inv_t;      // 1 / temperature
   int samp_topk;         // k of top-k
@@ -106,6 +107,18 @@ __device__ __forceinline__ float gate_fast(float a, float g) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(ea + 1.0f));
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rg) : "f"(eg + 1.0f));
   return fmaf(-2.0f, ra, 1.0f) * rg;
+}
+
+// The approximate tier (DVW_PRECISION_APPROX; the GPU analogue of the paper's App. C
+// approximations): the hardware tanh unit (tanh.approx.f32, relative
+// error ~2^-11) for both halves, sigma(g) = 0.5 tanh(g / 2) + 0.5.  Two MUFU operations in
+// parallel instead of two dependent pairs: a shorter gate on the critical chain, at the
+// price of bit-exact sampling (measured per-step mismatch rate reported by bench.py).
+__device__ __forceinline__ float gate_approx(float a, float g) {
+  float ta, tg;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(ta) : "f"(a));
+  asm("tanh.approx.f32 %0, %1;" : "=f"(tg) : "f"(0.5f * g));
+  return ta * fmaf(0.5f, tg, 0.5f);
 }
 
 // Inverse-CDF direct sampling over a = 256 logits held one per thread by a

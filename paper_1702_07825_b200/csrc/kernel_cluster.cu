@@ -389,7 +389,7 @@ constexpr int kColB3 = 384;
 // pair, where the gate runs.  B: row g of W_res, same columns.
 
 // ------------------------------------------------------------------ chain CTA, warpgroup A (the chain)
-template <int LP, bool TRACE>
+template <int LP, bool TRACE, bool APPROX>
 __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -437,7 +437,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
           v[1] += m.rr[jl][R + hrow];
         }
         // a = a_cur + (W_prev x_{n-d} + B + L); h = tanh(a_h) sigma(a_g)
-        const float hv = gate_fast(v[0] + pre0, v[1] + pre1);
+        const float hv = APPROX ? gate_approx(v[0] + pre0, v[1] + pre1) : gate_fast(v[0] + pre0, v[1] + pre1);
         stamp<TRACE>(tp, 27 + jl);
         if (jl + 1 == nl) {
           // the CTA's last layer: h goes straight to the next chain CTA (or, for layer l, to the
@@ -909,7 +909,7 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
   }
 }
 
-template <int S, int LP, bool TRACE>
+template <int S, int LP, bool TRACE, bool APPROX = false>
 __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Mail* mail = reinterpret_cast<Mail*>(smem_raw);
@@ -986,7 +986,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
 
   if (t >= kAux) {
     if (role == kChain) {
-      if (t < kAux + 128) chain_A<LP, TRACE>(P, cx, idx, sw);
+      if (t < kAux + 128) chain_A<LP, TRACE, APPROX>(P, cx, idx, sw);
       else if (t < kAux + 256) chain_B<LP, TRACE>(P, cx, idx, sw);
       else chain_C<LP, TRACE>(P, cx, idx, sw);
     } else if (role == kHead) {
@@ -1011,17 +1011,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   ptx::cluster_sync();
 }
 
-template <int S, int LP, bool TRACE>
+template <int S, int LP, bool TRACE, bool APPROX = false>
 cudaError_t configure(int smem) {
-  cudaError_t e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e =
+      cudaFuncSetAttribute(k_cluster<S, LP, TRACE, APPROX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, APPROX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
 template <int S, int LP>
 int max_active_clusters(int size, int smem) {
-  if (configure<S, LP, false>(smem) != cudaSuccess || configure<S, LP, true>(smem) != cudaSuccess) {
+  if (configure<S, LP, false>(smem) != cudaSuccess || configure<S, LP, true>(smem) != cudaSuccess ||
+      configure<S, LP, false, true>(smem) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -1306,15 +1308,22 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaError_t e;
+  // variants: production (exact gate), TRACE (exact gate + timestamps), APPROX (hardware tanh)
+  const bool ap = a.approx != 0 && !tr;
+#define DVW_LAUNCH(S_, LP_)                                                   \
+  e = tr   ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, true>, P)           \
+      : ap ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, true>, P)    \
+           : cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false>, P)
   if (p.s == 256 && p.lpc == 3) {
-    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<256, 3, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<256, 3, false>, P);
+    DVW_LAUNCH(256, 3);
   } else if (p.s == 256) {
-    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<256, 4, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<256, 4, false>, P);
+    DVW_LAUNCH(256, 4);
   } else if (p.lpc == 3) {
-    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<128, 3, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<128, 3, false>, P);
+    DVW_LAUNCH(128, 3);
   } else {
-    e = tr ? cudaLaunchKernelEx(&cfg, k_cluster<128, 4, true>, P) : cudaLaunchKernelEx(&cfg, k_cluster<128, 4, false>, P);
+    DVW_LAUNCH(128, 4);
   }
+#undef DVW_LAUNCH
   info->grid = p.size;
   info->cluster = p.size;
   info->threads = kThreads;

@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(RunArgs A) {
                            [&](int row, float acc) { av[row] = acc + Wl[o.b + row] + Lj[row]; });
       }
       __syncthreads();
-      for (int i = tid; i < R; i += kThreads) h[i] = gate(av[i], av[R + i]);
+      for (int i = tid; i < R; i += kThreads) h[i] = A.approx ? gate_approx(av[i], av[R + i]) : gate(av[i], av[R + i]);
       __syncthreads();
       {
         Vec<R> vh;

@@ -364,3 +364,28 @@ def test_conditioner_matches_oracle_and_feeds_generation(L):
     with pytest.raises(L.DvwError) as e:
         c.load(cw[:-1])
     assert e.value.name == "DVW_E_SHAPE"
+
+
+@pytest.mark.parametrize("kernel", ["cluster", "stream"])
+def test_approx_gate_tier_within_gate(L, kernel):
+    """Row f4 (the GPU analogue of App. C's approximate nonlinearities): DVW_PRECISION_APPROX
+    evaluates the gate with the hardware tanh unit.  Teacher-forced logits stay inside the
+    north_star 1e-3 gate; the per-step mismatch rate against the fp64 oracle is measured."""
+    cfg = synth.C1
+    N, hop = 1600, 64
+    w = synth.make_weights(cfg, 0)
+    cond = synth.make_cond(cfg, synth.n_frames_for(N, hop), 0)
+    u = synth.make_uniforms(N, 0)
+    m = model(L, cfg, w, kernel).set_precision("approx")
+    codes = m.generate(dev(cond)[None], dev(u)[None], hop)
+    lg = m.logits(dev(cond)[None], codes, hop).cpu().numpy()[0]
+    codes = codes.cpu().numpy()[0]
+    _, ref_lg, sampled = oracle_tf(cfg, w, cond, hop, codes, u=u)
+    err = float(np.max(np.abs(lg.astype(np.float64) - ref_lg)))
+    mism = int(np.sum(sampled != codes))
+    print(f"approx {kernel}: max|dlogit| = {err:.2e}, per-step mismatches {mism}/{N}")
+    assert err <= GATE
+    assert mism <= 0.01 * N
+    m.set_precision("fp32")
+    lg32 = m.logits(dev(cond)[None], dev(codes)[None], hop).cpu().numpy()[0]
+    assert float(np.max(np.abs(lg32.astype(np.float64) - ref_lg))) <= FP32_FAITHFUL
