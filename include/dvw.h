@@ -75,13 +75,15 @@ typedef struct {
   int32_t device;
 } dvw_config;
 
-/* Kernel selection.  AUTO picks CLUSTER for n_streams == 1
- * when the model fits its residency plan, else STREAM. */
+/* Kernel selection.  AUTO: dvw_generate picks CLUSTER for
+ * n_streams == 1 when the model fits its residency plan (and the sampler is direct), TC for
+ * n_streams > 1, else STREAM; dvw_logits picks PARALLEL. */
 typedef enum {
   DVW_KERNEL_AUTO = 0,
-  DVW_KERNEL_STREAM = 1,  /* one CTA per stream, weights read from L2 every sample */
-  DVW_KERNEL_CLUSTER = 2, /* batch-1 persistent cluster kernel, weights on chip */
-  DVW_KERNEL_TC = 3       /* batched streams, tcgen05 projections (when built) */
+  DVW_KERNEL_STREAM = 1,   /* one CTA per stream, weights read from L2 every sample */
+  DVW_KERNEL_CLUSTER = 2,  /* batch-1 persistent cluster kernel, weights on chip */
+  DVW_KERNEL_TC = 3,       /* batched streams, tcgen05 projections */
+  DVW_KERNEL_PARALLEL = 4  /* dvw_logits only: all timesteps of a layer at once (codes known) */
 } dvw_kernel;
 
 typedef struct {

@@ -26,8 +26,8 @@ _lib = ctypes.CDLL(LIB_PATH)
 DVW_OK = 0
 STATUS = {0: "DVW_OK", 1: "DVW_E_INVALID_ARG", 2: "DVW_E_SHAPE", 3: "DVW_E_UNSUPPORTED",
           4: "DVW_E_STATE", 5: "DVW_E_OOM", 6: "DVW_E_CUDA", 7: "DVW_E_DEVICE_TIMEOUT"}
-KERNEL_AUTO, KERNEL_STREAM, KERNEL_CLUSTER, KERNEL_TC = 0, 1, 2, 3
-KERNEL_NAMES = {0: "auto", 1: "stream", 2: "cluster", 3: "tc"}
+KERNEL_AUTO, KERNEL_STREAM, KERNEL_CLUSTER, KERNEL_TC, KERNEL_PARALLEL = 0, 1, 2, 3, 4
+KERNEL_NAMES = {0: "auto", 1: "stream", 2: "cluster", 3: "tc", 4: "parallel"}
 
 EXPORTS = ("dvw_create", "dvw_weights_numel", "dvw_load_weights", "dvw_generate", "dvw_logits",
            "dvw_generate_host", "dvw_set_kernel", "dvw_set_precision", "dvw_set_sampler", "dvw_set_trace",

@@ -48,6 +48,8 @@ struct dvw_model {
   size_t bpacked_bytes = 0;
   void* d_bws = nullptr;      // batched-kernel workspace (activations, queues, barrier)
   size_t bws_bytes = 0;
+  void* d_pws = nullptr;      // parallel teacher-forced workspace (x, x', q for a group of streams)
+  size_t pws_bytes = 0;
   // host-call staging
   void* d_stage = nullptr;
   size_t stage_bytes = 0;
@@ -167,12 +169,28 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   const bool direct = forced != nullptr || m->samp_kind == DVW_SAMPLER_DIRECT;
   if (kern == DVW_KERNEL_CLUSTER && !direct)
     return fail(DVW_E_UNSUPPORTED, "the cluster kernel samples directly only (dvw_set_sampler)");
+  if (kern == DVW_KERNEL_PARALLEL && !forced)
+    return fail(DVW_E_UNSUPPORTED, "the parallel kernel computes teacher-forced logits only (dvw_logits)");
+  if (kern == DVW_KERNEL_AUTO && forced) kern = DVW_KERNEL_PARALLEL;
   if (kern == DVW_KERNEL_AUTO) {
     if (n_streams == 1 && m->cplan.ok && direct) kern = DVW_KERNEL_CLUSTER;
     else if (n_streams > 1 && m->bplan.ok) kern = DVW_KERNEL_TC;
     else kern = DVW_KERNEL_STREAM;
   }
-  if (kern == DVW_KERNEL_TC) {
+  int pgroup = 0;  // parallel kernel: streams per workspace group
+  if (kern == DVW_KERNEL_PARALLEL) {
+    const size_t per = parallel_workspace_bytes(m->r, m->s, n_samples, 1);
+    const size_t cap = std::max(per, (size_t)2 << 30);  // bound the workspace to ~2 GiB
+    pgroup = (int)std::min<size_t>((size_t)n_streams, cap / per);
+    const size_t need = per * pgroup;
+    if (m->pws_bytes < need) {
+      if (m->d_pws) cudaFree(m->d_pws);
+      m->d_pws = nullptr;
+      m->pws_bytes = 0;
+      DVW_CUDA(cudaMalloc(&m->d_pws, need), "allocating parallel workspace");
+      m->pws_bytes = need;
+    }
+  } else if (kern == DVW_KERNEL_TC) {
     const int nsb = std::min(m->bplan.max_sb, (n_streams + 127) / 128);
     const size_t need = batch_workspace_bytes(m->bplan, m->dil.data(), nsb);
     if (m->bws_bytes < need) {
@@ -223,6 +241,19 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
     e = launch_cluster_kernel(A, m->cplan, m->d_packed, cs, &li);
   } else if (kern == DVW_KERNEL_STREAM) {
     e = launch_stream_kernel(A, cs, &li);
+  } else if (kern == DVW_KERNEL_PARALLEL) {
+    e = cudaSuccess;
+    int64_t launches = 0;
+    for (int g0 = 0; g0 < n_streams && e == cudaSuccess; g0 += pgroup) {
+      RunArgs G = A;
+      G.n_streams = std::min(pgroup, n_streams - g0);
+      G.cond = cond + (int64_t)g0 * n_frames * m->L * 2 * m->r;
+      G.forced = forced + (int64_t)g0 * n_samples;
+      G.out_logits = out_logits + (int64_t)g0 * n_samples * kLevels;
+      e = launch_parallel_logits(G, m->d_pws, cs, &li);
+      launches += li.launches;
+    }
+    li.launches = launches;
   } else if (kern == DVW_KERNEL_TC) {
     e = launch_batch_kernel(A, m->bplan, m->d_bpacked, m->d_bws, m->bws_bytes, m->dil.data(),
                             m->precision != DVW_PRECISION_FP32, cs, &li);
@@ -395,7 +426,7 @@ DVW_API dvw_status dvw_generate_host(dvw_model* m, const float* cond_host, int64
 
 DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel) {
   if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
-  if (kernel < DVW_KERNEL_AUTO || kernel > DVW_KERNEL_TC) return fail(DVW_E_INVALID_ARG, "unknown kernel %d", kernel);
+  if (kernel < DVW_KERNEL_AUTO || kernel > DVW_KERNEL_PARALLEL) return fail(DVW_E_INVALID_ARG, "unknown kernel %d", kernel);
   if (kernel == DVW_KERNEL_CLUSTER && !m->cplan.ok)
     return fail(DVW_E_UNSUPPORTED, "cluster kernel cannot hold this model: %s", m->cplan.why);
   if (kernel == DVW_KERNEL_TC && !m->bplan.ok)
@@ -458,6 +489,7 @@ DVW_API void dvw_destroy(dvw_model* m) {
   cudaFree(m->d_packed);
   cudaFree(m->d_bpacked);
   cudaFree(m->d_bws);
+  cudaFree(m->d_pws);
   cudaFree(m->d_stage);
   delete m;
 }

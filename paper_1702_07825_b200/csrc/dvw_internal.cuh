@@ -186,6 +186,10 @@ struct LaunchInfo {
 };
 
 cudaError_t launch_stream_kernel(const RunArgs& a, cudaStream_t st, LaunchInfo* info);
+// Teacher-forced logits in parallel over time (kernel_parallel.cu): workspace for a group of
+// streams, then one call per group.
+size_t parallel_workspace_bytes(int r, int s, int64_t n_samples, int n_streams);
+cudaError_t launch_parallel_logits(const RunArgs& a, void* ws, cudaStream_t st, LaunchInfo* info);
 
 #ifdef __CUDACC__
 // ---------------------------------------------------------------- App. A.4 strategies (row f3)

@@ -389,3 +389,28 @@ def test_approx_gate_tier_within_gate(L, kernel):
     m.set_precision("fp32")
     lg32 = m.logits(dev(cond)[None], dev(codes)[None], hop).cpu().numpy()[0]
     assert float(np.max(np.abs(lg32.astype(np.float64) - ref_lg))) <= FP32_FAITHFUL
+
+
+@pytest.mark.parametrize("shape", [(20, 64, 256), (5, 32, 128), (3, 128, 256), (40, 64, 256)])
+def test_parallel_teacher_forced_logits(L, shape):
+    """dvw_logits computed all timesteps of a layer at once (DVW_KERNEL_PARALLEL, AUTO for
+    dvw_logits): equal to the fp64 oracle within the fp32-faithful bound on ragged lengths,
+    two streams, dilations beyond the 64-timestep tile; bitwise deterministic."""
+    cfg = synth.Config(*shape)
+    N, hop = 1000, 7
+    w = synth.make_weights(cfg, 4)
+    cond, _ = synth.make_batch(cfg, N, [0, 5], hop)
+    codes = np.stack([synth.make_codes(N, 0), synth.make_codes(N, 5)])
+    m = L.Model.from_config(cfg).load(w)
+    lg = m.logits(dev(cond), dev(codes), hop)
+    assert m.info()["last_kernel_name"] == "parallel"
+    lg2 = m.logits(dev(cond), dev(codes), hop)
+    assert torch.equal(lg, lg2)
+    lg = lg.cpu().numpy()
+    for i in range(2):
+        _, ref, _ = oracle_tf(cfg, w, cond[i], hop, codes[i])
+        err = float(np.max(np.abs(lg[i].astype(np.float64) - ref)))
+        assert err <= FP32_FAITHFUL, (i, err)
+    with pytest.raises(L.DvwError) as e:  # generation cannot run in parallel over time
+        m.set_kernel("parallel").generate(dev(cond), dev(synth.make_uniforms(N, 0))[None].repeat(2, 1), hop)
+    assert e.value.name == "DVW_E_UNSUPPORTED"
