@@ -258,7 +258,7 @@ def main():
     dev = torch.device("cuda", local if ws > 1 else 0)
     torch.cuda.set_device(dev)
     from paper_1702_07825_b200._lib import Conditioner, Model
-    from paper_1702_07825_b200.shard import shard_range
+    from paper_1702_07825_b200.shard import gather_codes, shard_range
 
     cfg, n = wl["cfg"], wl["n"]
     if wl["split"]:
@@ -341,7 +341,20 @@ def main():
     # max over ranks
     t_max, e_max = kernel_ms, (e2e_step if e2e_step is not None else -1.0)
     total_streams = S
+    gather = None
     if ws > 1:
+        # results to rank 0 after the timed work: the only collective (NCCL all_gather of uint8 codes)
+        n_utts = wl["streams"] if wl["split"] else S * ws
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        torch.distributed.barrier()
+        g0.record(stream)
+        full = gather_codes(out, n_utts)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        gather = {"ms": g0.elapsed_time(g1), "bytes": int(n_utts * n), "utterances": n_utts,
+                  "ok": (full is None) or (tuple(full.shape) == (n_utts, n) and bool(torch.equal(full[start:start + S],
+                                                                                              out)))}
         import torch.distributed as dist
         t = torch.tensor([kernel_ms, e_max], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -397,6 +410,8 @@ def main():
             "gpu_launches": (int(info["last_launches"]) + (5 if cond_net is not None else 0)) * args.steps,
             "roofline": roof,
         }
+        if gather is not None:
+            line["gather_results"] = gather
         if not args.no_cpu:
             cond0 = d_cond[0].cpu().numpy()
             u0 = d_u[0].cpu().numpy()
