@@ -150,6 +150,28 @@ DVW_API dvw_status dvw_generate_host(dvw_model* m, const float* cond_host, int64
                                      int32_t n_streams, uint8_t* out_codes_host,
                                      void* cuda_stream);
 
+/* Streaming (stateful) generation: one utterance in consecutive chunks, the output of the
+ * chunks bitwise equal to a single dvw_generate over their concatenation (SURVEY.md §8(f)
+ * "streaming/stateful generation across calls").  The session owns the state a one-shot call
+ * rebuilds from zero (reading R4): every stream's dilation queues and its last two codes.
+ *   dvw_session_create   : state for n_streams utterances of model m (queues zero, codes 128)
+ *   dvw_session_generate : the next n_samples of every stream.  cond covers the WHOLE
+ *                          utterance, fp32 [n_streams][n_frames][l][2r] with
+ *                          n_frames >= ceil((position + n_samples) / hop); uniforms and
+ *                          out_codes are the chunk's, [n_streams][n_samples].  hop must not
+ *                          change within a session.  Runs on the CLUSTER (one stream, direct
+ *                          sampler) or STREAM kernel; a pinned TC kernel -> DVW_E_UNSUPPORTED.
+ *                          Calls on one session must be ordered (same CUDA stream).
+ *   dvw_session_position : samples generated so far (-1 for NULL)
+ * The session is bound to the model's device and dilation schedule. */
+typedef struct dvw_session dvw_session;
+DVW_API dvw_status dvw_session_create(dvw_model* m, int32_t n_streams, dvw_session** out);
+DVW_API dvw_status dvw_session_generate(dvw_model* m, dvw_session* s, const float* cond, int64_t n_frames,
+                                        int32_t hop, const float* uniforms, int64_t n_samples,
+                                        uint8_t* out_codes, void* cuda_stream);
+DVW_API int64_t dvw_session_position(const dvw_session* s);
+DVW_API void dvw_session_destroy(dvw_session* s);
+
 /* Pin the kernel used by later calls (DVW_KERNEL_AUTO restores the default).
  * DVW_E_UNSUPPORTED if that kernel cannot run this model. */
 DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel);

@@ -32,6 +32,7 @@ KERNEL_NAMES = {0: "auto", 1: "stream", 2: "cluster", 3: "tc", 4: "parallel"}
 EXPORTS = ("dvw_create", "dvw_weights_numel", "dvw_load_weights", "dvw_generate", "dvw_logits",
            "dvw_generate_host", "dvw_set_kernel", "dvw_set_precision", "dvw_set_sampler", "dvw_set_trace",
            "dvw_get_info", "dvw_sync", "dvw_destroy", "dvw_last_error",
+           "dvw_session_create", "dvw_session_generate", "dvw_session_position", "dvw_session_destroy",
            "dvwc_create", "dvwc_weights_numel", "dvwc_load_weights", "dvwc_run", "dvwc_destroy")
 SAMPLERS = {"direct": 0, "temperature": 1, "mean": 2, "mode": 3, "top_k": 4}
 PRECISION_FP32, PRECISION_TF32, PRECISION_APPROX = 0, 1, 2
@@ -84,6 +85,14 @@ _lib.dvwc_run.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctyp
 _lib.dvwc_run.restype = ctypes.c_int32
 _lib.dvwc_destroy.argtypes = [ctypes.c_void_p]
 _lib.dvwc_destroy.restype = None
+_lib.dvw_session_create.argtypes = [_vp, _i32, ctypes.POINTER(_vp)]
+_lib.dvw_session_create.restype = _i32
+_lib.dvw_session_generate.argtypes = [_vp, _vp, _vp, _i64, _i32, _vp, _i64, _vp, _vp]
+_lib.dvw_session_generate.restype = _i32
+_lib.dvw_session_position.argtypes = [_vp]
+_lib.dvw_session_position.restype = _i64
+_lib.dvw_session_destroy.argtypes = [_vp]
+_lib.dvw_session_destroy.restype = None
 _lib.dvw_set_sampler.argtypes = [_vp, _i32, ctypes.c_float, _i32]
 _lib.dvw_set_sampler.restype = _i32
 _lib.dvw_set_trace.argtypes = [_vp, _vp, _i64, _i32]
@@ -201,6 +210,10 @@ class Model:
         _check(_lib.dvw_set_sampler(self._h, int(kind), float(temperature), int(top_k)))
         return self
 
+    def session(self, n_streams: int = 1) -> "Session":
+        """A streaming session: generate one utterance chunk by chunk (dvw_session_*)."""
+        return Session(self, n_streams)
+
     def set_trace(self, buf=None, first_sample: int = 0):
         """Record per-event %globaltimer stamps into a CUDA uint64/int64 tensor
         [n][16][32] (see include/dvw.h dvw_set_trace); None disables."""
@@ -312,3 +325,39 @@ class Conditioner:
         _check(_lib.dvwc_run(self._h, _dptr(features, torch.float32, "features"), T, S,
                              _dptr(out, torch.float32, "out"), _stream_handle(stream)))
         return out
+
+
+class Session:
+    """dvw_session_*: consecutive chunks of the same utterances, bitwise equal to one call."""
+
+    def __init__(self, model: "Model", n_streams: int = 1):
+        h = _vp()
+        _check(_lib.dvw_session_create(model._h, int(n_streams), ctypes.byref(h)))
+        self._h, self.model, self.n_streams = h, model, n_streams
+
+    @property
+    def position(self) -> int:
+        return int(_lib.dvw_session_position(self._h))
+
+    def generate(self, cond, uniforms, hop: int, out=None, stream=None):
+        """cond: the WHOLE utterance's conditioning [S][F][l][2r]; uniforms: this chunk's [S][n]."""
+        import torch
+        S, F = int(cond.shape[0]), int(cond.shape[1])
+        n = int(uniforms.shape[-1])
+        if out is None:
+            out = torch.empty((S, n), dtype=torch.uint8, device=cond.device)
+        _check(_lib.dvw_session_generate(self.model._h, self._h, _dptr(cond, torch.float32, "cond"), F, hop,
+                                         _dptr(uniforms, torch.float32, "uniforms"), n,
+                                         _dptr(out, torch.uint8, "out"), _stream_handle(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.dvw_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

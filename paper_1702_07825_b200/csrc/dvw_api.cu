@@ -19,6 +19,18 @@
 
 using namespace dvw;
 
+// A streaming session (include/dvw.h dvw_session_*): the state one-shot calls rebuild from
+// zero -- the dilation queues of every stream and the last two codes -- kept between calls.
+struct dvw_session {
+  int device = 0;
+  int n_streams = 0;
+  int64_t ring_floats = 0;
+  float* d_ring = nullptr;  // [S][ring_floats]
+  int* d_y = nullptr;       // [S][2]: y_{n-1}, y_{n-2}
+  int64_t n_done = 0;
+  int hop = 0;
+};
+
 struct dvw_model {
   int device = 0;
   int L = 0, r = 0, s = 0, a = 0;
@@ -145,15 +157,16 @@ dvw_status check_device_error(dvw_model* m) {
 
 dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, const float* uniforms,
                const uint8_t* forced, int64_t n_samples, int32_t n_streams, uint8_t* out_codes,
-               float* out_logits, void* stream) {
+               float* out_logits, void* stream, dvw_session* sess = nullptr) {
   if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
   if (!m->loaded) return fail(DVW_E_STATE, "weights not loaded (call dvw_load_weights first)");
   if (n_samples < 0) return fail(DVW_E_SHAPE, "n_samples must be >= 0");
   if (n_streams < 1) return fail(DVW_E_SHAPE, "n_streams must be >= 1 (got %d)", n_streams);
   if (hop < 1) return fail(DVW_E_SHAPE, "hop must be >= 1 (got %d)", hop);
-  if (n_samples > 0 && n_frames < (n_samples + hop - 1) / hop)
-    return fail(DVW_E_SHAPE, "n_frames = %lld < ceil(n_samples / hop) = %lld", (long long)n_frames,
-                (long long)((n_samples + hop - 1) / hop));
+  const int64_t n0 = sess ? sess->n_done : 0;  // sessions: cond holds the whole utterance
+  if (n_samples > 0 && n_frames < (n0 + n_samples + hop - 1) / hop)
+    return fail(DVW_E_SHAPE, "n_frames = %lld < ceil(%s / hop) = %lld", (long long)n_frames,
+                sess ? "(samples so far + n_samples)" : "n_samples", (long long)((n0 + n_samples + hop - 1) / hop));
   if (n_samples == 0) return DVW_OK;
   if (!cond) return fail(DVW_E_INVALID_ARG, "cond is NULL");
   if (forced) {
@@ -172,6 +185,10 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   if (kern == DVW_KERNEL_PARALLEL && !forced)
     return fail(DVW_E_UNSUPPORTED, "the parallel kernel computes teacher-forced logits only (dvw_logits)");
   if (kern == DVW_KERNEL_AUTO && forced) kern = DVW_KERNEL_PARALLEL;
+  if (sess) {  // sessions run on the batch-1 kernels, whose queues are laid out per stream
+    if (kern == DVW_KERNEL_TC) return fail(DVW_E_UNSUPPORTED, "streaming sessions run on the CLUSTER or STREAM kernel");
+    if (kern == DVW_KERNEL_AUTO) kern = (n_streams == 1 && m->cplan.ok && direct) ? DVW_KERNEL_CLUSTER : DVW_KERNEL_STREAM;
+  }
   if (kern == DVW_KERNEL_AUTO) {
     if (n_streams == 1 && m->cplan.ok && direct) kern = DVW_KERNEL_CLUSTER;
     else if (n_streams > 1 && m->bplan.ok) kern = DVW_KERNEL_TC;
@@ -201,7 +218,7 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
       m->bws_bytes = need;
       m->info.workspace_bytes = (int64_t)need;
     }
-  } else {
+  } else if (!sess) {
     st = ensure_ring(m, n_streams);
     if (st != DVW_OK) return st;
   }
@@ -224,7 +241,9 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   A.n_streams = n_streams;
   A.out_codes = out_codes;
   A.out_logits = out_logits;
-  A.ring = m->d_ring;
+  A.ring = sess ? sess->d_ring : m->d_ring;
+  A.n0 = n0;
+  A.ystate = sess ? sess->d_y : nullptr;
   A.err = m->d_err;
   A.approx = m->precision == DVW_PRECISION_APPROX ? 1 : 0;
   A.samp_kind = forced ? DVW_SAMPLER_DIRECT : m->samp_kind;
@@ -422,6 +441,58 @@ DVW_API dvw_status dvw_generate_host(dvw_model* m, const float* cond_host, int64
   DVW_CUDA(cudaMemcpyAsync(out_codes_host, dout, ob, cudaMemcpyDeviceToHost, cs), "D2H codes");
   DVW_CUDA(cudaStreamSynchronize(cs), "synchronizing");
   return check_device_error(m);
+}
+
+DVW_API dvw_status dvw_session_create(dvw_model* m, int32_t n_streams, dvw_session** out) {
+  if (!m || !out) return fail(DVW_E_INVALID_ARG, "NULL argument");
+  if (n_streams < 1) return fail(DVW_E_SHAPE, "n_streams must be >= 1 (got %d)", n_streams);
+  DeviceGuard g(m->device);
+  dvw_session* s = new (std::nothrow) dvw_session();
+  if (!s) return fail(DVW_E_OOM, "host allocation failed");
+  s->device = m->device;
+  s->n_streams = n_streams;
+  s->ring_floats = m->ring_floats;
+  cudaError_t e = cudaMalloc(&s->d_ring, sizeof(float) * (size_t)m->ring_floats * n_streams);
+  if (e == cudaSuccess) e = cudaMemset(s->d_ring, 0, sizeof(float) * (size_t)m->ring_floats * n_streams);
+  if (e == cudaSuccess) e = cudaMalloc(&s->d_y, sizeof(int) * 2 * n_streams);
+  if (e == cudaSuccess) {
+    std::vector<int> y(2 * (size_t)n_streams, kLevels / 2);  // codes at negative times: 128 (R4)
+    e = cudaMemcpy(s->d_y, y.data(), sizeof(int) * y.size(), cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    cudaFree(s->d_ring);
+    cudaFree(s->d_y);
+    delete s;
+    return cuda_fail(e, "creating session");
+  }
+  *out = s;
+  return DVW_OK;
+}
+
+DVW_API dvw_status dvw_session_generate(dvw_model* m, dvw_session* s, const float* cond, int64_t n_frames,
+                                        int32_t hop, const float* uniforms, int64_t n_samples, uint8_t* out_codes,
+                                        void* cuda_stream) {
+  if (!m || !s) return fail(DVW_E_INVALID_ARG, "NULL argument");
+  if (s->device != m->device || s->ring_floats != m->ring_floats)
+    return fail(DVW_E_INVALID_ARG, "session belongs to another model");
+  if (s->hop != 0 && hop != s->hop) return fail(DVW_E_SHAPE, "hop changed within a session (%d -> %d)", s->hop, hop);
+  dvw_status st = run(m, cond, n_frames, hop, uniforms, nullptr, n_samples, s->n_streams, out_codes, nullptr,
+                      cuda_stream, s);
+  if (st == DVW_OK) {
+    s->hop = hop;
+    s->n_done += n_samples;
+  }
+  return st;
+}
+
+DVW_API int64_t dvw_session_position(const dvw_session* s) { return s ? s->n_done : -1; }
+
+DVW_API void dvw_session_destroy(dvw_session* s) {
+  if (!s) return;
+  DeviceGuard g(s->device);
+  cudaFree(s->d_ring);
+  cudaFree(s->d_y);
+  delete s;
 }
 
 DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel) {

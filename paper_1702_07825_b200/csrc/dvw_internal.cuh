@@ -63,6 +63,9 @@ struct RunArgs {
   const uint8_t* forced; // [S][N] (teacher forced) or nullptr
   int64_t N;
   int n_streams;
+  int64_t n0;            // streaming sessions: global index of this call's first sample (0 otherwise)
+  int* ystate;           // streaming sessions: [S][2] codes y_{n0-1}, y_{n0-2} in, y_{n0+N-1}, y_{n0+N-2}
+                         // out; the dilation queues are flushed at the end (nullptr: one-shot call)
   uint8_t* out_codes;    // [S][N] or nullptr
   float* out_logits;     // [S][N][256] or nullptr
   float* ring;           // [S][ring_floats] workspace

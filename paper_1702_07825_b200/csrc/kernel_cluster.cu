@@ -336,22 +336,24 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
   ptx::bar_sync(kBarMath, kMath);
 }
 
-// The final draw (sample N-1) after the last layer pass (first warp of A).
-__device__ __forceinline__ void final_draw(const Params& P, const Ctx& cx, int k) {
+// The final draw (sample N-1) after the last layer pass (first warp of A); returns it.
+__device__ __forceinline__ int final_draw(const Params& P, const Ctx& cx, int k) {
   const RunArgs& A = P.a;
   Mail& m = *cx.mail;
-  if (k >= 32) return;
+  if (k >= 32) return 0;
   const int64_t n = A.N;
   const float u = A.uniforms ? __ldg(A.uniforms + n - 1) : 0.0f;
   wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11);
+  int y = 0;
   if (A.forced) {
     float4* o = reinterpret_cast<float4*>(A.out_logits + (n - 1) * kLevels) + 2 * k;
     o[0] = lds4(m.logits_in + 8 * k);
     o[1] = lds4(m.logits_in + 8 * k + 4);
   } else {
-    const int y = sample_warp(m.logits_in, u, k);
+    y = sample_warp(m.logits_in, u, k);
     if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
   }
+  return y;
 }
 
 // TMEM address of this thread's lane (warp w of a warpgroup owns lanes 32w..32w+31)
@@ -389,7 +391,7 @@ constexpr int kColB3 = 384;
 // pair, where the gate runs.  B: row g of W_res, same columns.
 
 // ------------------------------------------------------------------ chain CTA, warpgroup A (the chain)
-template <int LP, bool TRACE, bool APPROX>
+template <int LP, bool TRACE, bool APPROX, bool SESS>
 __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -403,7 +405,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
   const uint32_t tm = tmem_lane_addr(m) + kColA;
   const float* wembc = sw + sm_emb(LP);  // CTA 0: [256][R]
   const float* bemb = wembc + kLevels * R;
-  int y1 = kLevels / 2, y2 = kLevels / 2;
+  int y1 = SESS ? A.ystate[0] : kLevels / 2, y2 = SESS ? A.ystate[1] : kLevels / 2;
   float w[64];
 
   for (int64_t n = 0; n < A.N; ++n) {
@@ -459,14 +461,20 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
       }
     }
   }
-  if (c == 0 && A.N > 0) final_draw(P, cx, a);
+  if (c == 0 && A.N > 0) {
+    const int y = final_draw(P, cx, a);
+    if (SESS && a == 0 && !A.forced) {  // streaming session: the code history for the next call
+      A.ystate[0] = y;
+      A.ystate[1] = y1;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ chain CTA, warpgroup B (x updates)
 // x_{j0+jl} = x_{j0+jl-1} + W_res_{j0+jl-1} h_{j0+jl-1} + B_res_{j0+jl-1} for
 // jl >= xb (CTA 0 starts from the embedding): for the dilation queues, for C, and (jl = nl-1)
 // for the next chain CTA.
-template <int LP, bool TRACE>
+template <int LP, bool TRACE, bool SESS>
 __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -484,7 +492,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
   const float* bres = sw + sm_bres(LP);  // [LPC][R]: B_res_{j0+jl-1}
   const float* wembc = sw + sm_emb(LP);
   const float* bemb = wembc + kLevels * R;
-  int y1 = kLevels / 2, y2 = kLevels / 2;
+  int y1 = SESS ? A.ystate[0] : kLevels / 2, y2 = SESS ? A.ystate[1] : kLevels / 2;
   float wr[32];
 
   for (int64_t n = 0; n < A.N; ++n) {
@@ -541,7 +549,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
 // ------------------------------------------------------------------ chain CTA, warpgroup C (R terms)
 // R_{j0+jl} = W_cur_{j0+jl} x_{j0+jl-1} + c_{j0+jl} for jl >= xb: jl = 0 from the inbound x_{j0-1},
 // jl >= 1 from x_{j0+jl-1} (B, or the embedding on CTA 0).
-template <int LP, bool TRACE>
+template <int LP, bool TRACE, bool SESS>
 __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -557,7 +565,7 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
   const float* cf = sw + sm_fold(LP);  // [LPC][2R]
   const float* wembc = sw + sm_emb(LP);
   const float* bemb = wembc + kLevels * R;
-  int y1 = kLevels / 2, y2 = kLevels / 2;
+  int y1 = SESS ? A.ystate[0] : kLevels / 2, y2 = SESS ? A.ystate[1] : kLevels / 2;
   float w[64];
 
   for (int64_t n = 0; n < A.N; ++n) {
@@ -667,7 +675,7 @@ __device__ __forceinline__ void aux_chain_skip(const Params& P, const Ctx& cx, i
 // For the coming sample n: queue write of x_j(n-1), queue read of x_j(n-d),
 // pre = B + L_j(n/hop) + W_prev x_j(n-d)  (Fig. 2 aux threads),
 // W_prev streamed from L2 ([16][128][4]; thread at = row of a).
-template <int S, int LP, bool TRACE>
+template <int S, int LP, bool TRACE, bool SESS>
 __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -686,7 +694,8 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       if constexpr (LP == 4)
         if (xskip) aux_chain_skip<S>(P, cx, c, at, pp);
     }
-    const int64_t f = n / A.hop;
+    const int64_t ng = SESS ? A.n0 + n : n;  // global sample index (streaming sessions continue at n0)
+    const int64_t f = ng / A.hop;
     for (int jl = 0; jl < nl; ++jl) {
       const int j = first + jl;
       const int d = A.dil[j];
@@ -703,10 +712,12 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       const float lv = __ldg(A.cond + (f * L + j) * 2 * R + at);
       if (at < R) {
         float* ring = A.ring + A.ring_off[j];
-        const float xc = m.xs[pp][jl][pad16(at)];  // x_j(n-1) (unused when n = 0)
+        const float xc = m.xs[pp][jl][pad16(at)];  // x_j(n-1) of this call (unused when n = 0)
         float xpv = 0.0f;
-        if (n - d >= 0) xpv = (d == 1) ? xc : ring[(int64_t)(n % d) * R + at];  // slot of n-d
-        if (n > 0 && d >= 2) ring[(int64_t)((n - 1) % d) * R + at] = xc;
+        // x_j(ng - d): slot (ng - d) mod d = ng mod d; at n = 0 of a continued session x_j(ng - 1)
+        // was flushed to the queue by the previous call
+        if (ng - d >= 0) xpv = (d == 1 && n > 0) ? xc : ring[(int64_t)(ng % d) * R + at];
+        if (n > 0 && d >= 2) ring[(int64_t)((ng - 1) % d) * R + at] = xc;
         m.xp[at] = xpv;
       }
       ptx::bar_sync(kBarAux, kAux);
@@ -730,10 +741,15 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
   if (A.N > 0) {  // the last sample's h and chain-skip partial
     const int pp = (int)((A.N - 1) & 1);
     aux_forward(pl, m, first, nl, at, pp);
+    if (xskip || SESS) wait(cx, &m.bar_done, (uint32_t)pp, 14);
     if constexpr (LP == 4) {
-      if (xskip) {
-        wait(cx, &m.bar_done, (uint32_t)pp, 14);
-        aux_chain_skip<S>(P, cx, c, at, pp);
+      if (xskip) aux_chain_skip<S>(P, cx, c, at, pp);
+    }
+    if (SESS && at < R) {  // streaming session: x_j of the last sample into its queue slot
+      const int64_t ng = A.n0 + A.N - 1;
+      for (int jl = 0; jl < nl; ++jl) {
+        const int d = A.dil[first + jl];
+        A.ring[A.ring_off[first + jl] + (int64_t)(ng % d) * R + at] = m.xs[pp][jl][pad16(at)];
       }
     }
   }
@@ -909,7 +925,7 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
   }
 }
 
-template <int S, int LP, bool TRACE, bool APPROX = false>
+template <int S, int LP, bool TRACE, bool APPROX = false, bool SESS = false>
 __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Mail* mail = reinterpret_cast<Mail*>(smem_raw);
@@ -986,9 +1002,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
 
   if (t >= kAux) {
     if (role == kChain) {
-      if (t < kAux + 128) chain_A<LP, TRACE, APPROX>(P, cx, idx, sw);
-      else if (t < kAux + 256) chain_B<LP, TRACE>(P, cx, idx, sw);
-      else chain_C<LP, TRACE>(P, cx, idx, sw);
+      if (t < kAux + 128) chain_A<LP, TRACE, APPROX, SESS>(P, cx, idx, sw);
+      else if (t < kAux + 256) chain_B<LP, TRACE, SESS>(P, cx, idx, sw);
+      else chain_C<LP, TRACE, SESS>(P, cx, idx, sw);
     } else if (role == kHead) {
       if (t < kAux + kMain) head_main<S, TRACE>(P, cx, idx, sw);
     } else if (role == kSkip) {
@@ -1001,7 +1017,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     ptx::cluster_sync();
     return;
   }
-  if (role == kChain) chain_aux<S, LP, TRACE>(P, cx, idx, sw);
+  if (role == kChain) chain_aux<S, LP, TRACE, SESS>(P, cx, idx, sw);
   // Park until the math warps are done (try_wait suspends the warp), then free TMEM.
   while (!ptx::mbar_try_wait_cta(ptx::smem_u32(&mail->bar_exit), 0)) {
   }
@@ -1011,19 +1027,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   ptx::cluster_sync();
 }
 
-template <int S, int LP, bool TRACE, bool APPROX = false>
+template <int S, int LP, bool TRACE, bool APPROX = false, bool SESS = false>
 cudaError_t configure(int smem) {
-  cudaError_t e =
-      cudaFuncSetAttribute(k_cluster<S, LP, TRACE, APPROX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, APPROX, SESS>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, APPROX>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, APPROX, SESS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
 template <int S, int LP>
 int max_active_clusters(int size, int smem) {
   if (configure<S, LP, false>(smem) != cudaSuccess || configure<S, LP, true>(smem) != cudaSuccess ||
-      configure<S, LP, false, true>(smem) != cudaSuccess) {
+      configure<S, LP, false, true>(smem) != cudaSuccess || configure<S, LP, false, false, true>(smem) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -1308,11 +1324,14 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaError_t e;
-  // variants: production (exact gate), TRACE (exact gate + timestamps), APPROX (hardware tanh)
-  const bool ap = a.approx != 0 && !tr;
-#define DVW_LAUNCH(S_, LP_)                                                   \
-  e = tr   ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, true>, P)           \
-      : ap ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, true>, P)    \
+  // variants: production (exact gate), TRACE (exact gate + timestamps), APPROX (hardware tanh),
+  // SESS (streaming session: continues the queues and code history; exact gate)
+  const bool ss = a.ystate != nullptr;
+  const bool ap = a.approx != 0 && !tr && !ss;
+#define DVW_LAUNCH(S_, LP_)                                                         \
+  e = ss   ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, false, true>, P)   \
+      : tr ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, true>, P)                 \
+      : ap ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, true>, P)          \
            : cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false>, P)
   if (p.s == 256 && p.lpc == 3) {
     DVW_LAUNCH(256, 3);

@@ -105,9 +105,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(RunArgs A) {
   const float* uni = A.uniforms ? A.uniforms + (int64_t)st * A.N : nullptr;
   const uint8_t* forced = A.forced ? A.forced + (int64_t)st * A.N : nullptr;
 
-  int y1 = kLevels / 2, y2 = kLevels / 2;  // codes at negative times: mu-law(0) = 128 (R4)
+  // codes at negative times: mu-law(0) = 128 (R4); a streaming session continues its history
+  int y1 = A.ystate ? A.ystate[2 * st] : kLevels / 2, y2 = A.ystate ? A.ystate[2 * st + 1] : kLevels / 2;
   for (int64_t n = 0; n < A.N; ++n) {
-    const int64_t f = n / A.hop;
+    const int64_t ng = A.n0 + n;  // global sample index (queues, conditioning frame)
+    const int64_t f = ng / A.hop;
     for (int i = tid; i < R; i += kThreads)
       x[i] = W[o.emb_prev + (int64_t)i * kLevels + y2] + W[o.emb_cur + (int64_t)i * kLevels + y1] +
              W[o.b_emb + i];
@@ -117,8 +119,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(RunArgs A) {
     for (int j = 0; j < L; ++j) {
       const float* Wl = W + (int64_t)j * o.layer_stride;
       const int d = A.dil[j];
-      float* slot = ring + A.ring_off[j] + (int64_t)(n % d) * R;
-      for (int i = tid; i < R; i += kThreads) xp[i] = (n >= d) ? slot[i] : 0.0f;
+      float* slot = ring + A.ring_off[j] + (int64_t)(ng % d) * R;
+      for (int i = tid; i < R; i += kThreads) xp[i] = (ng >= d) ? slot[i] : 0.0f;
       __syncthreads();
       for (int i = tid; i < R; i += kThreads) slot[i] = x[i];
       const float* Lj = cond + (f * L + j) * 2 * R;
@@ -186,6 +188,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(RunArgs A) {
     y2 = y1;
     y1 = y;
     __syncthreads();
+  }
+  if (A.ystate && !forced && tid == 0) {  // the code history for the session's next call
+    A.ystate[2 * st] = y1;
+    A.ystate[2 * st + 1] = y2;
   }
 }
 

@@ -26,7 +26,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol(lib):
     names = declared_symbols()
-    assert len(names) == 19, names
+    assert len(names) == 23, names
     raw = ctypes.CDLL(lib.LIB_PATH)
     for n in names:
         assert hasattr(raw, n), n
@@ -84,3 +84,7 @@ def test_conditioner_abi_without_gpu(lib):
     assert lib.raw_call("dvwc_load_weights", None, None, 0, 0) == 1
     assert lib.raw_call("dvwc_run", None, None, 1, 1, None, None) == 1
     lib._lib.dvwc_destroy(None)
+    assert lib.raw_call("dvw_session_create", None, 1, None) == 1
+    assert lib.raw_call("dvw_session_generate", None, None, None, 0, 1, None, 0, None, None) == 1
+    assert lib.raw_call("dvw_session_position", None) == -1
+    lib._lib.dvw_session_destroy(None)

@@ -414,3 +414,30 @@ def test_parallel_teacher_forced_logits(L, shape):
     with pytest.raises(L.DvwError) as e:  # generation cannot run in parallel over time
         m.set_kernel("parallel").generate(dev(cond), dev(synth.make_uniforms(N, 0))[None].repeat(2, 1), hop)
     assert e.value.name == "DVW_E_UNSUPPORTED"
+
+
+@pytest.mark.parametrize("kernel,cfg", [("cluster", synth.C2), ("stream", synth.C1), ("cluster", synth.C3)],
+                         ids=["cluster-C2", "stream-C1", "cluster-C3"])
+def test_streaming_session_chunks_equal_one_shot(L, kernel, cfg):
+    """Streaming sessions: chunks of 1, 63, 200, 500 and the rest (chunk edges across hop frames
+    and across every dilation) give bitwise the codes of one dvw_generate -- and the oracle's."""
+    N, hop = 1600, 64
+    w = synth.make_weights(cfg, 0)
+    cond = dev(synth.make_cond(cfg, synth.n_frames_for(N, hop), 6))[None]
+    u = dev(synth.make_uniforms(N, 6))[None]
+    m = L.Model.from_config(cfg).load(w).set_kernel(kernel)
+    one = m.generate(cond, u, hop).cpu().numpy()[0]
+    sess = m.session()
+    parts, pos = [], 0
+    for n in (1, 63, 200, 500, N - 764):
+        parts.append(sess.generate(cond, u[:, pos:pos + n].contiguous(), hop).cpu().numpy()[0])
+        pos += n
+        assert sess.position == pos
+    assert m.info()["last_kernel_name"] == kernel
+    assert np.array_equal(np.concatenate(parts), one)
+    ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond.cpu().numpy()[0], hop, N,
+                           uniforms=u.cpu().numpy()[0], want_logits=False)
+    assert np.array_equal(one, ref)
+    with pytest.raises(L.DvwError) as e:  # cond must cover the session's position + n
+        sess.generate(cond, u[:, :200].contiguous(), hop)
+    assert e.value.name == "DVW_E_SHAPE"
