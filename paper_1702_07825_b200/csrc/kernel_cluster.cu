@@ -255,22 +255,18 @@ __device__ __forceinline__ void xpose_level(float (&v)[N], int lane, int bit) {
 
 // ------------------------------------------------------------------ chain CTA 0: sample + embed
 // Inverse-CDF direct sampling (reading R11) by ONE warp, 8 logits per
-// lane, no block barriers: m = max l; e_k = exp(l_k - m) (fp32); P_k = fp64 running
-// sums (lane-sequential, then an fp64 warp scan of the lane totals; P is
-// non-decreasing); y = #{k : P_k <= u * P_255}; fallback the largest k with e_k > 0.
-__device__ __forceinline__ int sample_warp(const float* logits, float u, int lane) {
-  float l[8];
-  {
-    const float4 a = lds4(logits + 8 * lane), b = lds4(logits + 8 * lane + 4);
-    l[0] = a.x; l[1] = a.y; l[2] = a.z; l[3] = a.w; l[4] = b.x; l[5] = b.y; l[6] = b.z; l[7] = b.w;
-  }
-  float mx = fmaxf(fmaxf(fmaxf(l[0], l[1]), fmaxf(l[2], l[3])), fmaxf(fmaxf(l[4], l[5]), fmaxf(l[6], l[7])));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float e[8];
+// lane, no block barriers: m = max l; e_k = exp(l_k - m) (fp32); P_k = running sums in
+// ascending k; y = #{k : P_k <= u * P_255}; fallback the largest k with e_k > 0.
+// The decision is defined by fp64 running sums (R11).  It is first taken with fp32 sums:
+// each fp32 P_k, and u * S, is within 28 * 2^-24 * S of its fp64 value (at most 13 fp32 adds
+// on any P_k, values <= S), so when no P_k lies within M = 32 * 2^-24 * S of the threshold
+// the fp32 count equals the fp64 count exactly; otherwise (about 2 * 256 * M / S ~ 0.1 % of
+// draws) the fp64 sums decide.  Bitwise the same codes as the fp64-only sampler.
+// The fp64 decision (reading R11): out of line, it runs for ~0.1 % of draws only.
+__device__ __noinline__ int sample_fp64(float e0, float e1, float e2, float e3, float e4, float e5, float e6,
+                                        float e7, float u, int lane) {
+  const float e[8] = {e0, e1, e2, e3, e4, e5, e6, e7};
   double p[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) e[i] = expf(l[i] - mx);
   p[0] = (double)e[0];
 #pragma unroll
   for (int i = 1; i < 8; ++i) p[i] = p[i - 1] + (double)e[i];
@@ -293,6 +289,46 @@ __device__ __forceinline__ int sample_warp(const float* logits, float u, int lan
   return y < kLevels ? y : __reduce_max_sync(0xffffffffu, (unsigned)(lastpos + 1)) - 1;
 }
 
+__device__ __forceinline__ int sample_warp(const float* logits, float u, int lane) {
+  float l[8];
+  {
+    const float4 a = lds4(logits + 8 * lane), b = lds4(logits + 8 * lane + 4);
+    l[0] = a.x; l[1] = a.y; l[2] = a.z; l[3] = a.w; l[4] = b.x; l[5] = b.y; l[6] = b.z; l[7] = b.w;
+  }
+  float mx = fmaxf(fmaxf(fmaxf(l[0], l[1]), fmaxf(l[2], l[3])), fmaxf(fmaxf(l[4], l[5]), fmaxf(l[6], l[7])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float e[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) e[i] = expf(l[i] - mx);
+  // fp32 pass
+  float q[8];
+  q[0] = e[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) q[i] = q[i - 1] + e[i];
+  float inc = q[7];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  const float fbase = inc - q[7];
+  const float fS = __shfl_sync(0xffffffffu, inc, 31);
+  const float fthr = u * fS;
+  const float M = 1.9073486e-06f * fS;  // 32 * 2^-24 * S
+  int fcnt = 0;
+  bool near = false;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float P = fbase + q[i];
+    fcnt += (P <= fthr) ? 1 : 0;
+    near |= fabsf(P - fthr) <= M;
+  }
+  const int fy = __reduce_add_sync(0xffffffffu, fcnt);
+  if (!__any_sync(0xffffffffu, near) && fy < kLevels) return fy;
+  return sample_fp64(e[0], e[1], e[2], e[3], e[4], e[5], e[6], e[7], u, lane);
+}
+
 // Draw y_{n-1} from the inbound logits (App. A.4) and write x^(0)_n (step 1) into xs[n&1][0]
 // with the first warp of warpgroup A; warpgroups A, B, C wait at the closing barrier.
 template <bool TRACE>
@@ -308,8 +344,10 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
       const int yf = A.forced ? (int)__ldg(A.forced + n - 1) : 0;
       ep0 = __ldg(embp_g + y1 * R + k);  // W_emb_prev[:, y_{n-2}] (= y1 before the update)
       ep1 = __ldg(embp_g + y1 * R + k + 32);
+      uint64_t* tp = (k == 0) ? trace_slot<TRACE>(A, n) : nullptr;
       if (wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11) && k == 0)
         ptx::mbar_arm(ptx::smem_u32(&m.bar_logits), kLevels * 4);
+      stamp<TRACE>(tp, 1);
       if (k == 0) trace<TRACE>(A, n - 1, 3);
       int y;
       if (A.forced) {
@@ -318,7 +356,9 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
         o[1] = lds4(m.logits_in + 8 * k + 4);
         y = yf;
       } else {
+        stamp<TRACE>(tp, 4);
         y = sample_warp(m.logits_in, u, k);
+        stamp<TRACE>(tp, 6);
         if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
       }
       if (k == 0) trace<TRACE>(A, n, 20);
@@ -332,8 +372,10 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
     float* x0 = m.xs[n & 1][0];
     x0[pad16(k)] = (ep0 + wembc[y1 * R + k]) + bemb[k];
     x0[pad16(k + 32)] = (ep1 + wembc[y1 * R + k + 32]) + bemb[k + 32];
+    if (k == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 7);
   }
   ptx::bar_sync(kBarMath, kMath);
+  if (k == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 30);
 }
 
 // The final draw (sample N-1) after the last layer pass (first warp of A); returns it.

@@ -48,6 +48,11 @@ ncta = info["last_cluster"]
 base = t[:, 0, 0].copy()  # chain CTA 0, event 0: start of the sample's first layer
 period = np.diff(base)
 print(f"sample period {np.median(period):.0f} ns (median), min {period.min()} max {period.max()}")
+c0 = t[:, 0, :]
+if not np.all(c0[:, 1] == 0):
+    d = lambda a, b: np.median(c0[:, b] - c0[:, a])  # noqa: E731
+    print(f"CTA 0 sampler (cycles): logits-in -> call {d(1, 4):.0f}, sample_warp {d(4, 6):.0f}, "
+          f"-> embed stored {d(6, 7):.0f}, -> barrier passed {d(7, 30):.0f}, -> layer 0 start {d(30, 8):.0f}")
 names = {0: "start/recv", 1: "q/partial", 2: "za/done", 3: "logits", 4: "h[l-1] in", 5: "pre ready", 6: "d2 done", 7: "zs sync", 9: "za sent", 20: "sampled"}
 for c in range(ncta):
     row = []
