@@ -257,11 +257,13 @@ __device__ __forceinline__ void xpose_level(float (&v)[N], int lane, int bit) {
 // Inverse-CDF direct sampling (reading R11) by ONE warp, 8 logits per
 // lane, no block barriers: m = max l; e_k = exp(l_k - m) (fp32); P_k = running sums in
 // ascending k; y = #{k : P_k <= u * P_255}; fallback the largest k with e_k > 0.
-// The decision is defined by fp64 running sums (R11).  It is first taken with fp32 sums:
-// each fp32 P_k, and u * S, is within 28 * 2^-24 * S of its fp64 value (at most 13 fp32 adds
-// on any P_k, values <= S), so when no P_k lies within M = 32 * 2^-24 * S of the threshold
-// the fp32 count equals the fp64 count exactly; otherwise (about 2 * 256 * M / S ~ 0.1 % of
-// draws) the fp64 sums decide.  Bitwise the same codes as the fp64-only sampler.
+// The decision is defined by fp64 running sums (R11).  It is first taken with fp32 sums
+// (d = 2^-24): a lane's prefix sums carry <= 7 d T_lane, the 5-level scan <= 5 d S (each
+// level's adds cover disjoint lanes), so the fp32 lane base is within 20 d S and each fp32
+// P_k within 28 d S of its exact value, and u * S within 13 d S; when no P_k lies within
+// M = 64 d S > 41 d S of the threshold the fp32 count equals the fp64 count exactly;
+// otherwise (about 2 * 256 * M / S ~ 0.2 % of draws) the fp64 sums decide.  Bitwise the
+// same codes as the fp64-only sampler.
 // The fp64 decision (reading R11): out of line, it runs for ~0.1 % of draws only.
 __device__ __noinline__ int sample_fp64(float e0, float e1, float e2, float e3, float e4, float e5, float e6,
                                         float e7, float u, int lane) {
@@ -315,7 +317,7 @@ __device__ __forceinline__ int sample_warp(const float* logits, float u, int lan
   const float fbase = inc - q[7];
   const float fS = __shfl_sync(0xffffffffu, inc, 31);
   const float fthr = u * fS;
-  const float M = 1.9073486e-06f * fS;  // 32 * 2^-24 * S
+  const float M = 3.8146973e-06f * fS;  // 64 * 2^-24 * S
   int fcnt = 0;
   bool near = false;
 #pragma unroll
