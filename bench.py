@@ -338,6 +338,30 @@ def main():
         e2e_step = float(np.mean(e2e_ms))
         assert np.array_equal(h_out[0].numpy(), gpu_codes0), "host-buffer path disagrees with device path"
 
+    # batch 1: per-sample latency at 1,000-sample granularity -- the same
+    # utterance through a streaming session in 1,000-sample chunks, CUDA events per chunk
+    latency = None
+    if S == 1 and cond_net is None and info["last_kernel_name"] in ("cluster", "stream") and n >= 2000:
+        sess = model.session(1)
+        chunk = 1000
+        cev = []
+        for c0 in range(0, n, chunk):
+            k = min(chunk, n - c0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sess.generate(d_cond, d_u[:, c0:c0 + k].contiguous(), HOP, out=out[:, c0:c0 + k])
+            b.record(stream)
+            cev.append((a, b, k))
+        torch.cuda.synchronize(dev)
+        per = np.array([a.elapsed_time(b) * 1e3 / k for a, b, k in cev])  # us per sample, per chunk
+        assert np.array_equal(out[0].cpu().numpy(), gpu_codes0), "chunked session disagrees with one call"
+        latency = {"us_per_sample_mean": float(per.mean()), "us_per_sample_p50": float(np.percentile(per, 50)),
+                   "us_per_sample_p99": float(np.percentile(per, 99)), "chunks": len(per), "chunk_samples": chunk,
+                   "first_chunk_ms": cev[0][0].elapsed_time(cev[0][1]),
+                   "note": "streaming session (dvw_session_generate), 1,000-sample chunks incl. one launch each; "
+                           "codes equal to the one-call run"}
+        sess.close()
+
     # max over ranks
     t_max, e_max = kernel_ms, (e2e_step if e2e_step is not None else -1.0)
     total_streams = S
@@ -412,6 +436,8 @@ def main():
         }
         if gather is not None:
             line["gather_results"] = gather
+        if latency is not None:
+            line["latency"] = latency
         if not args.no_cpu:
             cond0 = d_cond[0].cpu().numpy()
             u0 = d_u[0].cpu().numpy()
