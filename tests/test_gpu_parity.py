@@ -441,3 +441,31 @@ def test_streaming_session_chunks_equal_one_shot(L, kernel, cfg):
     with pytest.raises(L.DvwError) as e:  # cond must cover the session's position + n
         sess.generate(cond, u[:, :200].contiguous(), hop)
     assert e.value.name == "DVW_E_SHAPE"
+
+
+@pytest.mark.parametrize("kernel", ["stream", "cluster", "tc", "parallel"])
+@pytest.mark.parametrize("case", [
+    dict(shape=(1, 64, 256), dil=None, N=70, hop=1),          # a single layer, upsampled cond (hop 1)
+    dict(shape=(6, 64, 128), dil=(1, 1, 1, 1, 1, 1), N=129, hop=5),  # d = 1 everywhere
+    dict(shape=(4, 32, 256), dil=(3, 70, 1, 2), N=65, hop=64),  # a dilation beyond N and the 64 tile
+    dict(shape=(2, 128, 128), dil=None, N=1, hop=3),          # one sample
+])
+def test_edge_shapes_teacher_forced_all_kernels(L, kernel, case):
+    """Teacher-forced logits of every kernel on edge shapes against the oracle (fp32-faithful);
+    for the generating kernels, free-running codes too."""
+    l, r, s = case["shape"]
+    cfg = synth.Config(l, r, s, dilations=case["dil"])
+    N, hop = case["N"], case["hop"]
+    w = synth.make_weights(cfg, 9, "peaky")
+    cond = synth.make_cond(cfg, synth.n_frames_for(N, hop), 1)
+    u = synth.make_uniforms(N, 1)
+    m = model(L, cfg, w, kernel)
+    codes_in = synth.make_codes(N, 1)
+    lg = m.logits(dev(cond)[None], dev(codes_in)[None], hop).cpu().numpy()[0]
+    assert m.info()["last_kernel_name"] == kernel
+    _, ref_lg, _ = oracle_tf(cfg, w, cond, hop, codes_in)
+    assert float(np.max(np.abs(lg.astype(np.float64) - ref_lg))) <= FP32_FAITHFUL * 30
+    if kernel != "parallel":
+        codes = m.generate(dev(cond)[None], dev(u)[None], hop).cpu().numpy()[0]
+        ref, _, _ = oracle.run(l, r, s, w, cond, hop, N, uniforms=u, dilations=cfg.dilation_list(), want_logits=False)
+        assert np.array_equal(codes, ref)
