@@ -24,13 +24,25 @@ constexpr int kTile = 64;  // timesteps per block
 constexpr int kPT = 256;   // threads per block
 constexpr int kKC = 32;    // K chunk of the staged weights
 
-// Stage W rows [n0, n0 + N) x columns [k0, k0 + kKC) of a row-major matrix (leading dim ld)
-// into Bs[kk][n] (k-major).
+// Stage W rows [0, N) x columns [k0, k0 + kKC) of a row-major matrix (leading dim ld) into
+// Bs[kk][n] (k-major).  Thread -> (row n, 4 consecutive k): one 16-byte read per thread and
+// four shared-memory writes in which consecutive threads hit consecutive n (conflict-free).
 template <int N>
 __device__ __forceinline__ void stage_w(float* Bs, const float* W, int ld, int k0, int kmax) {
-  for (int i = threadIdx.x; i < N * kKC; i += kPT) {
-    const int n = i / kKC, kk = i % kKC;
-    Bs[kk * N + n] = (k0 + kk < kmax) ? __ldg(W + (int64_t)n * ld + k0 + kk) : 0.0f;
+  for (int i = threadIdx.x; i < N * (kKC / 4); i += kPT) {
+    const int n = i % N, kq = i / N, k = k0 + 4 * kq;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k + 3 < kmax) {
+      v = __ldg(reinterpret_cast<const float4*>(W + (int64_t)n * ld + k));
+    } else {
+      if (k < kmax) v.x = __ldg(W + (int64_t)n * ld + k);
+      if (k + 1 < kmax) v.y = __ldg(W + (int64_t)n * ld + k + 1);
+      if (k + 2 < kmax) v.z = __ldg(W + (int64_t)n * ld + k + 2);
+    }
+    Bs[(4 * kq) * N + n] = v.x;
+    Bs[(4 * kq + 1) * N + n] = v.y;
+    Bs[(4 * kq + 2) * N + n] = v.z;
+    Bs[(4 * kq + 3) * N + n] = v.w;
   }
 }
 
@@ -53,10 +65,17 @@ __device__ __forceinline__ void fma_chunk(const float* At, int kbase, const floa
 }
 
 // Load rows [t0 - shift, t0 - shift + 64) (zero outside [0, T)) of X [T][C] into At[koff + c][t].
+// Thread -> (timestep t, 4 consecutive channels): a 16-byte read, and writes in which
+// consecutive threads hit consecutive t (conflict-free).  C is a multiple of 4.
 __device__ __forceinline__ void load_act(float* At, int koff, const float* X, int C, int T, int t0, int shift) {
-  for (int i = threadIdx.x; i < kTile * C; i += kPT) {
-    const int t = i / C, c = i % C, tg = t0 - shift + t;
-    At[(koff + c) * kTile + t] = (tg >= 0 && tg < T) ? X[(int64_t)tg * C + c] : 0.0f;
+  for (int i = threadIdx.x; i < kTile * (C / 4); i += kPT) {
+    const int t = i % kTile, c = 4 * (i / kTile), tg = t0 - shift + t;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tg >= 0 && tg < T) v = *reinterpret_cast<const float4*>(X + (int64_t)tg * C + c);
+    At[(koff + c) * kTile + t] = v.x;
+    At[(koff + c + 1) * kTile + t] = v.y;
+    At[(koff + c + 2) * kTile + t] = v.z;
+    At[(koff + c + 3) * kTile + t] = v.w;
   }
 }
 
@@ -193,7 +212,7 @@ __global__ void __launch_bounds__(kPT) k_head(RunArgs A, const float* Q) {
   const int T = (int)A.N;
   const float* q = Q + (int64_t)st * T * S;
   for (int i = threadIdx.x; i < kTile * S; i += kPT) {
-    const int t = i / S, c = i % S;
+    const int t = i % kTile, c = i / kTile;  // consecutive threads: consecutive t (conflict-free)
     Zs[c * kTile + t] = (t0 + t < T) ? fmaxf(q[(int64_t)(t0 + t) * S + c], 0.0f) : 0.0f;
   }
   const int cg = threadIdx.x % 16, tg = threadIdx.x / 16;
