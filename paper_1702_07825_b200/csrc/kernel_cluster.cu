@@ -193,27 +193,33 @@ __device__ __forceinline__ void trace_clk(const RunArgs& A, int64_t n, int ev) {
   }
 }
 
+// Packed fp32 FMA (FFMA2, sm_100): {c.x + a.x b.x, c.y + a.y b.y}, each rounded exactly
+// like fmaf -- the same results as two scalar FMAs at ~1.4x the issue rate (measured
+// 118 vs 85 FMA/clk/SM, tools/ffma2_probe.cu), so every matvec below pairs its two
+// independent accumulator chains into one FFMA2.
+__device__ __forceinline__ float2 ffma2(float a0, float a1, float b0, float b1, float2 c) {
+  return __ffma2_rn(make_float2(a0, a1), make_float2(b0, b1), c);
+}
+
 // Register tile x vector chunk: acc[m] = sum_c w[m*C + c] * v[c] for RQ rows and a
 // C-float chunk of a shared vector; two accumulators per row (even/odd c) for ILP.
 // Summation order is fixed (bitwise deterministic).
 template <int RQ, int C>
 __device__ __forceinline__ void tile_dot(const float* w, const float* v, float (&acc)[RQ]) {
-  float e[RQ], o[RQ];
+  float2 eo[RQ];  // (even, odd) accumulators
 #pragma unroll
-  for (int m = 0; m < RQ; ++m) e[m] = o[m] = 0.0f;
+  for (int m = 0; m < RQ; ++m) eo[m] = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int c = 0; c < C; c += 4) {
     const float4 x = lds4(v + c);
 #pragma unroll
     for (int m = 0; m < RQ; ++m) {
-      e[m] = fmaf(w[m * C + c], x.x, e[m]);
-      o[m] = fmaf(w[m * C + c + 1], x.y, o[m]);
-      e[m] = fmaf(w[m * C + c + 2], x.z, e[m]);
-      o[m] = fmaf(w[m * C + c + 3], x.w, o[m]);
+      eo[m] = ffma2(w[m * C + c], w[m * C + c + 1], x.x, x.y, eo[m]);
+      eo[m] = ffma2(w[m * C + c + 2], w[m * C + c + 3], x.z, x.w, eo[m]);
     }
   }
 #pragma unroll
-  for (int m = 0; m < RQ; ++m) acc[m] = e[m] + o[m];
+  for (int m = 0; m < RQ; ++m) acc[m] = eo[m].x + eo[m].y;
 }
 
 // Register tile x one 32-column half of a padded 64-vector (two 16-float chunks at v and
@@ -221,22 +227,20 @@ __device__ __forceinline__ void tile_dot(const float* w, const float* v, float (
 // combined in a fixed order (bitwise deterministic).
 template <int RQ>
 __device__ __forceinline__ void tile_dot_half(const float* w, const float* v, float (&acc)[RQ]) {
-  float s[RQ][4];
+  float2 s01[RQ], s23[RQ];
 #pragma unroll
-  for (int m = 0; m < RQ; ++m) s[m][0] = s[m][1] = s[m][2] = s[m][3] = 0.0f;
+  for (int m = 0; m < RQ; ++m) s01[m] = s23[m] = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int c = 0; c < 32; c += 4) {
     const float4 x = lds4(v + c + ((c >> 4) << 2));
 #pragma unroll
     for (int m = 0; m < RQ; ++m) {
-      s[m][0] = fmaf(w[m * 32 + c], x.x, s[m][0]);
-      s[m][1] = fmaf(w[m * 32 + c + 1], x.y, s[m][1]);
-      s[m][2] = fmaf(w[m * 32 + c + 2], x.z, s[m][2]);
-      s[m][3] = fmaf(w[m * 32 + c + 3], x.w, s[m][3]);
+      s01[m] = ffma2(w[m * 32 + c], w[m * 32 + c + 1], x.x, x.y, s01[m]);
+      s23[m] = ffma2(w[m * 32 + c + 2], w[m * 32 + c + 3], x.z, x.w, s23[m]);
     }
   }
 #pragma unroll
-  for (int m = 0; m < RQ; ++m) acc[m] = (s[m][0] + s[m][1]) + (s[m][2] + s[m][3]);
+  for (int m = 0; m < RQ; ++m) acc[m] = (s01[m].x + s01[m].y) + (s23[m].x + s23[m].y);
 }
 
 // One transposing level of a butterfly reduction: lanes whose `bit` is set keep
@@ -693,16 +697,14 @@ __device__ __forceinline__ void aux_chain_skip(const Params& P, const Ctx& cx, i
       float4 wv[16];
 #pragma unroll
       for (int q = 0; q < 16; ++q) wv[q] = ldg4(wsk + ((int64_t)q * S + at + 128 * rr) * 4);
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const float4 x = lds4(h + pad16(4 * q));
-        s0 = fmaf(wv[q].x, x.x, s0);
-        s1 = fmaf(wv[q].y, x.y, s1);
-        s2 = fmaf(wv[q].z, x.z, s2);
-        s3 = fmaf(wv[q].w, x.w, s3);
+        s01 = ffma2(wv[q].x, wv[q].y, x.x, x.y, s01);
+        s23 = ffma2(wv[q].z, wv[q].w, x.z, x.w, s23);
       }
-      part[rr] += (s0 + s1) + (s2 + s3);
+      part[rr] += (s01.x + s01.y) + (s23.x + s23.y);
     }
   }
 #pragma unroll
@@ -765,16 +767,14 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
         m.xp[at] = xpv;
       }
       ptx::bar_sync(kBarAux, kAux);
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const float4 x = lds4(&m.xp[4 * q]);
-        a0 = fmaf(wv[q].x, x.x, a0);
-        a1 = fmaf(wv[q].y, x.y, a1);
-        a2 = fmaf(wv[q].z, x.z, a2);
-        a3 = fmaf(wv[q].w, x.w, a3);
+        a01 = ffma2(wv[q].x, wv[q].y, x.x, x.y, a01);
+        a23 = ffma2(wv[q].z, wv[q].w, x.z, x.w, a23);
       }
-      m.pre[jl][at] = (bj[jl * 2 * R + at] + lv) + ((a0 + a1) + (a2 + a3));
+      m.pre[jl][at] = (bj[jl * 2 * R + at] + lv) + ((a01.x + a01.y) + (a23.x + a23.y));
       ptx::bar_sync(kBarAux, kAux);
     }
     if (at == 0) {
