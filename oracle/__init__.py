@@ -66,6 +66,11 @@ def _load():
         lib.oracle_sample.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_float]
         lib.oracle_run_policy.restype = ctypes.c_int
         lib.oracle_run_policy.argtypes = lib.oracle_run.argtypes + [ctypes.c_int, ctypes.c_double, ctypes.c_int]
+        lib.oracle_run_nl.restype = ctypes.c_int
+        lib.oracle_run_nl.argtypes = lib.oracle_run_policy.argtypes + [ctypes.c_int]
+        for fn in ("oracle_appc_tanh", "oracle_appc_sigmoid", "oracle_appc_exp"):
+            getattr(lib, fn).restype = ctypes.c_double
+            getattr(lib, fn).argtypes = [ctypes.c_double]
         lib.oracle_sample_policy.restype = ctypes.c_int
         lib.oracle_sample_policy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                              ctypes.c_int, ctypes.c_float]
@@ -90,7 +95,7 @@ def run(n_layers: int, residual: int, skip: int, weights: np.ndarray, cond: np.n
         hop: int, n_samples: int, uniforms: Optional[np.ndarray] = None,
         forced: Optional[np.ndarray] = None, levels: int = 256,
         dilations: Optional[Sequence[int]] = None, want_logits: bool = True,
-        want_sampled: bool = False, sampler: Optional[tuple] = None):
+        want_sampled: bool = False, sampler: Optional[tuple] = None, nonlin: str = "exact"):
     """One utterance through the fp64 ring-buffer oracle.
 
     Returns ``(codes uint8[N], logits float64[N][a] or None, sampled uint8[N] or None)``.
@@ -99,6 +104,8 @@ def run(n_layers: int, residual: int, skip: int, weights: np.ndarray, cond: np.n
     is always the draw with ``uniforms[n]`` (for the divergence rate).
     ``sampler = (kind, temperature, top_k)`` selects the App. A.4 strategy (0 direct,
     1 temperature, 2 mean, 3 mode, 4 top-k; see ``sample_policy``); default direct.
+    ``nonlin="appc"`` evaluates every tanh, sigma and softmax exp with App. C's
+    approximations (PAPER.md:549-592; ``appc_tanh`` / ``appc_sigmoid`` / ``appc_exp``).
     """
     lib = _load()
     w = np.ascontiguousarray(weights, dtype=np.float32)
@@ -111,9 +118,10 @@ def run(n_layers: int, residual: int, skip: int, weights: np.ndarray, cond: np.n
     logits = np.zeros((n_samples, levels), dtype=np.float64) if want_logits else None
     sampled = np.zeros(n_samples, dtype=np.uint8) if (want_sampled and u is not None) else None
     kind, temp, topk = sampler if sampler is not None else (0, 1.0, 1)
-    rc = lib.oracle_run_policy(n_layers, residual, skip, levels, _ptr(d), _ptr(w), w.size, _ptr(c),
-                               c.shape[0], hop, _ptr(u), _ptr(f), n_samples, _ptr(codes),
-                               _ptr(logits), _ptr(sampled), int(kind), float(temp), int(topk))
+    nl = {"exact": 0, "appc": 1}[nonlin]
+    rc = lib.oracle_run_nl(n_layers, residual, skip, levels, _ptr(d), _ptr(w), w.size, _ptr(c),
+                           c.shape[0], hop, _ptr(u), _ptr(f), n_samples, _ptr(codes),
+                           _ptr(logits), _ptr(sampled), int(kind), float(temp), int(topk), nl)
     if rc != 0:
         raise ValueError(f"oracle_run rejected its arguments (code {rc})")
     return codes, logits, sampled
@@ -135,3 +143,20 @@ def sample_policy(logits: np.ndarray, u: float, kind: int, temperature: float = 
     l = np.ascontiguousarray(logits, dtype=np.float64)
     return int(_load().oracle_sample_policy(_ptr(l), l.size, int(kind), float(temperature), int(top_k),
                                             float(np.float32(u))))
+
+
+def appc_tanh(x: float) -> float:
+    """App. C tanh: sign(x) (e~ - 1/e~) / (e~ + 1/e~), e~ = 1 + |x| + 0.5658 x^2 + 0.143 x^4
+    (PAPER.md:556, 567)."""
+    return float(_load().oracle_appc_tanh(float(x)))
+
+
+def appc_sigmoid(x: float) -> float:
+    """App. C sigma: e~ / (1 + e~) for x >= 0, 1 / (1 + e~) for x <= 0."""
+    return float(_load().oracle_appc_sigmoid(float(x)))
+
+
+def appc_exp(x: float) -> float:
+    """App. C.2 e^x (x <= 0): the fp32 bit pattern I = (x/ln2 + 126 + g(z)) 2^23 with the
+    rational g (reading R31)."""
+    return float(_load().oracle_appc_exp(float(x)))

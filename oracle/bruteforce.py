@@ -50,8 +50,34 @@ def _split(blob: np.ndarray, L: int, r: int, s: int, a: int) -> dict:
     return out
 
 
+# App. C's approximations, vectorised independently of dvw_oracle.c.
+def _etilde(x):
+    return 1.0 + np.abs(x) + 0.5658 * x ** 2 + 0.143 * x ** 4
+
+
+def _tanh_appc(x):
+    e = _etilde(x)
+    return np.sign(x) * (e - 1.0 / e) / (e + 1.0 / e)
+
+
+def _sigmoid_appc(x):
+    e = _etilde(x)
+    return np.where(x >= 0.0, e / (1.0 + e), 1.0 / (1.0 + e))
+
+
+def _exp_appc(x):
+    """2^(x/ln2) through the fp32 bit pattern (x + 126 + g(z)) 2^23."""
+    xl = np.asarray(x, dtype=np.float64) / np.log(2.0)
+    z = xl - np.floor(xl)
+    g = -4.7259162 + 27.7280233 / (4.84252568 - z) - 1.49012907 * z
+    ok = xl >= -126.0
+    bits = np.trunc(np.where(ok, (xl + 126.0 + g) * 2.0 ** 23, 0.0)).astype(np.int32)
+    return np.where(ok, bits.view(np.float32).astype(np.float64), 0.0)
+
+
 def forward_logits(blob, L: int, r: int, s: int, codes_in: np.ndarray, cond: np.ndarray,
-                   hop: int, a: int = 256, dilations: Optional[Sequence[int]] = None) -> np.ndarray:
+                   hop: int, a: int = 256, dilations: Optional[Sequence[int]] = None,
+                   nonlin: str = "exact") -> np.ndarray:
     """Logits for t = 0..T-1 given the code history.
 
     ``codes_in[t]`` is the code emitted at step t (only t < T-1 matter for the
@@ -71,7 +97,10 @@ def forward_logits(blob, L: int, r: int, s: int, codes_in: np.ndarray, cond: np.
         if d[j] < T:
             xs[d[j]:] = x[:T - d[j]]
         hp = xs @ P[("W_prev", j)].T + x @ P[("W_cur", j)].T + P[("B", j)] + c[frames, j, :]
-        h = np.tanh(hp[:, :r]) * (1.0 / (1.0 + np.exp(-hp[:, r:])))
+        if nonlin == "appc":
+            h = _tanh_appc(hp[:, :r]) * _sigmoid_appc(hp[:, r:])
+        else:
+            h = np.tanh(hp[:, :r]) * (1.0 / (1.0 + np.exp(-hp[:, r:])))
         x = x + h @ P[("W_res", j)].T + P[("B_res", j)]
         hs.append(h)
     Hcat = np.concatenate(hs, axis=1)  # [T][l r], layer-major like App. A.1's stacked h
@@ -81,10 +110,10 @@ def forward_logits(blob, L: int, r: int, s: int, codes_in: np.ndarray, cond: np.
     return za @ P["W_out"].T + P["B_out"]
 
 
-def draw(logits: np.ndarray, u: float) -> int:
+def draw(logits: np.ndarray, u: float, nonlin: str = "exact") -> int:
     """Inverse-CDF draw (reading R11) written with numpy primitives."""
     l = np.asarray(logits, dtype=np.float64)
-    e = np.exp(l - l.max())
+    e = _exp_appc(l - l.max()) if nonlin == "appc" else np.exp(l - l.max())
     cdf = np.cumsum(e)
     k = int(np.searchsorted(cdf, float(np.float32(u)) * cdf[-1], side="right"))
     if k >= l.size:
@@ -93,10 +122,10 @@ def draw(logits: np.ndarray, u: float) -> int:
 
 
 def generate(blob, L: int, r: int, s: int, cond: np.ndarray, hop: int, uniforms: np.ndarray,
-             n_samples: int, a: int = 256, dilations=None) -> np.ndarray:
+             n_samples: int, a: int = 256, dilations=None, nonlin: str = "exact") -> np.ndarray:
     """Free-running generation by full recomputation at every step (O(N^2))."""
     codes = np.zeros(n_samples, dtype=np.int64)
     for n in range(n_samples):
-        lg = forward_logits(blob, L, r, s, codes[:n + 1], cond, hop, a, dilations)[n]
-        codes[n] = draw(lg, uniforms[n])
+        lg = forward_logits(blob, L, r, s, codes[:n + 1], cond, hop, a, dilations, nonlin)[n]
+        codes[n] = draw(lg, uniforms[n], nonlin)
     return codes.astype(np.uint8)

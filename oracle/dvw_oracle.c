@@ -20,7 +20,8 @@
  *     for j = 1 .. l:
  *       xp  = ring_j[n mod d_j]          (x^{(j-1)}_{n-d_j}, 0 if n < d_j)   (step 2a)
  *       a   = W_prev xp + W_cur x + B + L^{(j)}_n               (steps 2a-2c)
- *       h   = tanh(a[0:r]) * sigmoid(a[r:2r])                   (step 2c)
+ *       h   = tanh(a[0:r]) * sigmoid(a[r:2r])                   (step 2c;
+ *             oracle_run_nl with nl = 1: App. C's approximations, also for the softmax exp)
  *       ring_j[n mod d_j] = x            (store x^{(j-1)}_n after reading)
  *       x   = x + W_res h + B_res                               (App. A.1; R1)
  *       q   = q + W_skip^{(j)} h                                (step 2d)
@@ -44,16 +45,57 @@ ORACLE_API int64_t oracle_weights_numel(int L, int r, int s, int a) {
   return L * per_layer + (int64_t)2 * r * a + r + s + (int64_t)a * s + a + (int64_t)a * a + a;
 }
 
+/* ---- App. C: the paper's approximate nonlinearities (R31) ----
+ * The oracle of the DVW_PRECISION_APPC tier, written as the paper prints it:
+ *   e~(x)    = 1 + |x| + 0.5658 x^2 + 0.143 x^4
+ *   tanh(x) ~ sign(x) (e~(x) - 1/e~(x)) / (e~(x) + 1/e~(x))
+ *   sigma(x) ~ e~(x) / (1 + e~(x)) for x >= 0, 1 / (1 + e~(x)) for x <= 0
+ *   e^x = 2^(x / ln 2); for x' = x / ln 2 the fp32 bit pattern of 2^x' is
+ *     I = (x' + 126 + g(z)) 2^23, z = x' - floor(x'),
+ *     g(z) ~ -4.7259162 + 27.7280233 / (4.84252568 - z) - 1.49012907 z
+ *   I is truncated to an integer and read back as a 32-bit float; x' < -126 (no normal
+ *   fp32 pattern) gives 0 (reading R31).  Double arithmetic up to the bit pattern. */
+static double appc_etilde(double x) { return 1.0 + fabs(x) + 0.5658 * x * x + 0.143 * x * x * x * x; }
+
+static double appc_tanh(double x) {
+  const double e = appc_etilde(x);
+  const double v = (e - 1.0 / e) / (e + 1.0 / e);
+  return x > 0.0 ? v : (x < 0.0 ? -v : 0.0);
+}
+
+static double appc_sigmoid(double x) {
+  const double e = appc_etilde(x);
+  return x >= 0.0 ? e / (1.0 + e) : 1.0 / (1.0 + e);
+}
+
+static double appc_exp(double x) {
+  const double xl = x / log(2.0);
+  if (!(xl >= -126.0)) return 0.0;
+  const double z = xl - floor(xl);
+  const double g = -4.7259162 + 27.7280233 / (4.84252568 - z) - 1.49012907 * z;
+  const int32_t bits = (int32_t)((xl + 126.0 + g) * 8388608.0);  /* truncation toward zero */
+  float f;
+  memcpy(&f, &bits, sizeof f);
+  return (double)f;
+}
+
+ORACLE_API double oracle_appc_tanh(double x) { return appc_tanh(x); }
+ORACLE_API double oracle_appc_sigmoid(double x) { return appc_sigmoid(x); }
+ORACLE_API double oracle_appc_exp(double x) { return appc_exp(x); }
+
+/* the nonlinearity set: nl = 0 exact (reading R13), nl = 1 App. C */
+static double nl_exp(int nl, double x) { return nl ? appc_exp(x) : exp(x); }
+
 /* Inverse-CDF direct sampling (App. A.4 "Sample randomly from P(y)";
  * reading R11): e_k = exp(l_k - max l); P_k = sum_{i<=k} e_i in ascending k;
  * y = min{k : u * P_{a-1} < P_k}; fallback the largest k with e_k > 0. */
-static int sample_inverse_cdf(const double* logit, int a, double u, double* e) {
+static int sample_inverse_cdf(const double* logit, int a, double u, double* e, int nl) {
   double m = logit[0];
   for (int k = 1; k < a; ++k)
     if (logit[k] > m) m = logit[k];
   double S = 0.0;
   for (int k = 0; k < a; ++k) {
-    e[k] = exp(logit[k] - m);
+    e[k] = nl_exp(nl, logit[k] - m);
     S += e[k];
   }
   double t = u * S, P = 0.0;
@@ -75,8 +117,8 @@ static int sample_inverse_cdf(const double* logit, int a, double u, double* e) {
  *   mode          : argmax_y P(y) = argmax l, lowest index on ties; no u
  *   top-k         : keep the k largest P(y) (ties by lower index), zero the rest,
  *                   renormalise (implicitly), then the direct rule with u */
-static int sample_policy(const double* logit, int a, int kind, double t, int topk, double u, double* e) {
-  if (kind == 0) return sample_inverse_cdf(logit, a, u, e);
+static int sample_policy(const double* logit, int a, int kind, double t, int topk, double u, double* e, int nl) {
+  if (kind == 0) return sample_inverse_cdf(logit, a, u, e, nl);
   double m = logit[0];
   int am = 0;
   for (int k = 1; k < a; ++k)
@@ -85,7 +127,7 @@ static int sample_policy(const double* logit, int a, int kind, double t, int top
   if (kind == 2) {
     double S = 0.0, M = 0.0;
     for (int k = 0; k < a; ++k) {
-      const double ek = exp(logit[k] - m);
+      const double ek = nl_exp(nl, logit[k] - m);
       S += ek;
       M += (double)k * ek;
     }
@@ -96,12 +138,12 @@ static int sample_policy(const double* logit, int a, int kind, double t, int top
   }
   for (int k = 0; k < a; ++k) {
     if (kind == 1) {
-      e[k] = exp((logit[k] - m) / t);
+      e[k] = nl_exp(nl, (logit[k] - m) / t);
     } else { /* top-k: rank of k among all codes, larger first, ties by lower index */
       int rank = 0;
       for (int j = 0; j < a; ++j)
         if (logit[j] > logit[k] || (logit[j] == logit[k] && j < k)) ++rank;
-      e[k] = rank < topk ? exp(logit[k] - m) : 0.0;
+      e[k] = rank < topk ? nl_exp(nl, logit[k] - m) : 0.0;
     }
   }
   double S = 0.0;
@@ -118,7 +160,7 @@ static int sample_policy(const double* logit, int a, int kind, double t, int top
 
 ORACLE_API int oracle_sample(const double* logits, int a, float u) {
   double* e = (double*)malloc(sizeof(double) * a);
-  int y = sample_inverse_cdf(logits, a, (double)u, e);
+  int y = sample_inverse_cdf(logits, a, (double)u, e, 0);
   free(e);
   return y;
 }
@@ -126,7 +168,7 @@ ORACLE_API int oracle_sample(const double* logits, int a, float u) {
 ORACLE_API int oracle_sample_policy(const double* logits, int a, int kind, double t, int topk, float u) {
   if (kind < 0 || kind > 4 || (kind == 1 && !(t > 0.0)) || (kind == 4 && (topk < 1 || topk > a))) return -1;
   double* e = (double*)malloc(sizeof(double) * a);
-  int y = sample_policy(logits, a, kind, t, topk, (double)u, e);
+  int y = sample_policy(logits, a, kind, t, topk, (double)u, e, 0);
   free(e);
   return y;
 }
@@ -153,12 +195,13 @@ static void matvec(const double* W, int rows, int cols, const double* x, double*
  *   out_logits  : double [N][a] pre-softmax logits (may be NULL)
  *   out_sampled : uint8 [N] the draw with u_n even when teacher-forced (may be NULL)
  */
-ORACLE_API int oracle_run_policy(int L, int r, int s, int a, const int32_t* dilations,
-                                 const float* weights, int64_t numel, const float* cond,
-                                 int64_t n_frames, int hop, const float* uniforms,
-                                 const uint8_t* forced, int64_t N, uint8_t* out_codes,
-                                 double* out_logits, uint8_t* out_sampled, int kind, double temp,
-                                 int topk) {
+ORACLE_API int oracle_run_nl(int L, int r, int s, int a, const int32_t* dilations,
+                             const float* weights, int64_t numel, const float* cond,
+                             int64_t n_frames, int hop, const float* uniforms,
+                             const uint8_t* forced, int64_t N, uint8_t* out_codes,
+                             double* out_logits, uint8_t* out_sampled, int kind, double temp,
+                             int topk, int nl) {
+  if (nl < 0 || nl > 1) return -6;
   if (L < 1 || r < 1 || s < 1 || a < 2 || a > 256 || hop < 1 || N < 0) return -1;
   if (kind < 0 || kind > 4 || (kind == 1 && !(temp > 0.0)) || (kind == 4 && (topk < 1 || topk > a))) return -5;
   if (numel != oracle_weights_numel(L, r, s, a)) return -2;
@@ -239,7 +282,7 @@ ORACLE_API int oracle_run_policy(int L, int r, int s, int a, const int32_t* dila
       for (int i = 0; i < r; ++i) {
         double ah = ap[i] + ac[i] + Bj[j][i] + (double)Lj[i];
         double ag = ap[r + i] + ac[r + i] + Bj[j][r + i] + (double)Lj[r + i];
-        h[i] = tanh(ah) * sigmoid(ag);
+        h[i] = nl ? appc_tanh(ah) * appc_sigmoid(ag) : tanh(ah) * sigmoid(ag);
       }
       memcpy(slot, x, sizeof(double) * r);
       matvec(Wres[j], r, r, h, rh);
@@ -259,7 +302,7 @@ ORACLE_API int oracle_run_policy(int L, int r, int s, int a, const int32_t* dila
     for (int i = 0; i < a; ++i) lg[i] += Bout[i];
     if (out_logits) memcpy(out_logits + n * a, lg, sizeof(double) * a);
     int drawn = -1;
-    if (uniforms) drawn = sample_policy(lg, a, kind, temp, topk, (double)uniforms[n], e);
+    if (uniforms) drawn = sample_policy(lg, a, kind, temp, topk, (double)uniforms[n], e, nl);
     if (out_sampled) out_sampled[n] = (uint8_t)(drawn < 0 ? 0 : drawn);
     int y = forced ? (int)forced[n] : drawn;
     out_codes[n] = (uint8_t)y;
@@ -272,6 +315,16 @@ ORACLE_API int oracle_run_policy(int L, int r, int s, int a, const int32_t* dila
   free(Wprev); free(Wcur); free(Bj); free(Wres); free(Bres); free(Wskip);
   free(W); free(d);
   return 0;
+}
+
+ORACLE_API int oracle_run_policy(int L, int r, int s, int a, const int32_t* dilations,
+                                 const float* weights, int64_t numel, const float* cond,
+                                 int64_t n_frames, int hop, const float* uniforms,
+                                 const uint8_t* forced, int64_t N, uint8_t* out_codes,
+                                 double* out_logits, uint8_t* out_sampled, int kind, double temp,
+                                 int topk) {
+  return oracle_run_nl(L, r, s, a, dilations, weights, numel, cond, n_frames, hop, uniforms, forced, N,
+                       out_codes, out_logits, out_sampled, kind, temp, topk, 0);
 }
 
 ORACLE_API int oracle_run(int L, int r, int s, int a, const int32_t* dilations, const float* weights,
