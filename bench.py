@@ -180,7 +180,7 @@ def run_reference(args, wl):
     return 0
 
 
-def cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, budget_samples, gpu_tf_logits=None):
+def cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, budget_samples, gpu_tf_logits=None, nonlin="exact"):
     """Oracle timed on this host (1 core) on the same utterance; plus parity on it
     (free-running codes, per-step mismatch rate, and -- when given -- the GPU's
     teacher-forced logits on its own codes against the oracle's)."""
@@ -188,14 +188,14 @@ def cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, budget_samples, gpu_t
     nb = min(n, budget_samples)
     t0 = time.perf_counter()
     ref_codes, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, HOP, nb, uniforms=u[:nb],
-                                 dilations=cfg.dilation_list(), want_logits=False)
+                                 dilations=cfg.dilation_list(), want_logits=False, nonlin=nonlin)
     sec = time.perf_counter() - t0
     diff = np.nonzero(ref_codes != gpu_codes[:nb])[0]
     first = int(diff[0]) if diff.size else None
     # per-step mismatch rate: oracle teacher-forced on the GPU's own codes, drawing with the same u
     _, ref_lg, sampled = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, HOP, nb, uniforms=u[:nb],
                                     forced=gpu_codes[:nb], dilations=cfg.dilation_list(),
-                                    want_logits=gpu_tf_logits is not None, want_sampled=True)
+                                    want_logits=gpu_tf_logits is not None, want_sampled=True, nonlin=nonlin)
     mism = int(np.sum(sampled != gpu_codes[:nb]))
     cpu = {"value": nb / sec, "unit": "samples/s", "cores": 1, "kind": "oracle",
            "sample": f"{nb} samples of the same utterance (utterance 0), fp64 scalar C oracle, 1 thread"}
@@ -230,9 +230,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
     ap.add_argument("--kernel", default="auto", choices=["auto", "cluster", "stream", "tc"])
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "approx"],
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "approx", "appc"],
                     help="tf32: one-pass batched kernel (SURVEY.md 8(f) f1); approx: hardware tanh in the "
-                         "batch-1 gates (f4)")
+                         "batch-1 gates (f4); appc: the paper's App. C approximations (f4; parity against "
+                         "the oracle's App. C mode)")
     ap.add_argument("--samples", type=int, default=0, help="override samples per utterance (0 = workload's)")
     ap.add_argument("--ref-samples", type=int, default=1600, help="samples per reference step")
     ap.add_argument("--cpu-samples", type=int, default=16000, help="oracle samples for cpu_baseline")
@@ -413,7 +414,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True,
             "scaling": "strong" if wl["split"] else "weak",
             "vs_baseline": None,
-            "dtype": (("f32 (hardware tanh.approx gate)" if args.precision == "approx" else "f32") if kname != "tc"
+            "dtype": ({"approx": "f32 (hardware tanh.approx gate)",
+                       "appc": "f32 (App. C tanh/sigma/exp approximations)"}.get(args.precision, "f32") if kname != "tc"
                       else ("tf32 (1 tensor pass, inputs rounded to tf32)" if fast else "f32 (tf32 x3 tensor passes)")),
             "data": "synthetic",
             "config": {"workload": wl["desc"], "samples_per_step": n, "streams_per_gpu": S,
@@ -444,7 +446,8 @@ def main():
             k = min(n, 1600)
             model.set_kernel(kname)  # the teacher-forced check runs on the kernel that was timed
             tf = model.logits(d_cond[0:1].contiguous(), out[0:1, :k].contiguous(), HOP)[0].cpu().numpy()
-            cpu, parity = cpu_baseline_and_parity(cfg, n, w, cond0, u0, gpu_codes0, args.cpu_samples, tf)
+            cpu, parity = cpu_baseline_and_parity(cfg, n, w, cond0, u0, gpu_codes0, args.cpu_samples, tf,
+                                                  nonlin="appc" if args.precision == "appc" else "exact")
             line["cpu_baseline"] = cpu
             line["parity"] = parity
         print(json.dumps(line), flush=True)

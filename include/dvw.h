@@ -193,7 +193,18 @@ DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel);
  *     relative error ~2^-11; sigma(g) = (1 + tanh(g/2)) / 2) -- a shorter gate on the
  *     critical chain; logits within the 1e-3 gate, codes not bit-exact (measured rate
  *     reported).  The batched kernel runs as DVW_PRECISION_TF32 under this setting. */
-typedef enum { DVW_PRECISION_FP32 = 0, DVW_PRECISION_TF32 = 1, DVW_PRECISION_APPROX = 2 } dvw_precision;
+/*   DVW_PRECISION_APPC           : the paper's own approximations (App. C, PAPER.md:551-592;
+ *     reading R31): tanh and sigma from e~(x) = 1 + |x| + 0.5658 x^2 + 0.143 x^4 in every
+ *     gate, and the softmax's e^x by the 2^x bit-pattern construction with the rational
+ *     g(z) in the sampler (all strategies).  CLUSTER, STREAM (generation, sessions) and
+ *     PARALLEL (logits) kernels; TC -> DVW_E_UNSUPPORTED (AUTO picks STREAM for batches).
+ *     Parity is with the oracle's App. C mode (oracle.run(..., nonlin="appc")). */
+typedef enum {
+  DVW_PRECISION_FP32 = 0,
+  DVW_PRECISION_TF32 = 1,
+  DVW_PRECISION_APPROX = 2,
+  DVW_PRECISION_APPC = 3
+} dvw_precision;
 DVW_API dvw_status dvw_set_precision(dvw_model* m, int32_t precision);
 
 /* Sampling strategy for dvw_generate (App. A.4).

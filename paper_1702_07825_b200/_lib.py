@@ -35,8 +35,8 @@ EXPORTS = ("dvw_create", "dvw_weights_numel", "dvw_load_weights", "dvw_generate"
            "dvw_session_create", "dvw_session_generate", "dvw_session_position", "dvw_session_destroy",
            "dvwc_create", "dvwc_weights_numel", "dvwc_load_weights", "dvwc_run", "dvwc_destroy")
 SAMPLERS = {"direct": 0, "temperature": 1, "mean": 2, "mode": 3, "top_k": 4}
-PRECISION_FP32, PRECISION_TF32, PRECISION_APPROX = 0, 1, 2
-PRECISION_NAMES = {0: "fp32", 1: "tf32", 2: "approx"}
+PRECISION_FP32, PRECISION_TF32, PRECISION_APPROX, PRECISION_APPC = 0, 1, 2, 3
+PRECISION_NAMES = {0: "fp32", 1: "tf32", 2: "approx", 3: "appc"}
 
 
 class _Config(ctypes.Structure):
@@ -196,8 +196,10 @@ class Model:
         return self
 
     def set_precision(self, precision):
-        """Batched-kernel arithmetic: "fp32" (default, 3-pass tf32 split, fp32-faithful)
-        or "tf32" (one pass; within the 1e-3 logit gate, not bit-exact)."""
+        """Arithmetic tier (include/dvw.h dvw_precision): "fp32" (default; batched kernel as a
+        3-pass tf32 split, fp32-faithful), "tf32" (batched one pass; within the 1e-3 logit
+        gate, not bit-exact), "approx" (hardware tanh gate, batch-1 kernels) or "appc" (the
+        paper's App. C tanh / sigma / exp approximations; cluster, stream, parallel)."""
         if isinstance(precision, str):
             precision = {v: k for k, v in PRECISION_NAMES.items()}[precision]
         _check(_lib.dvw_set_precision(self._h, int(precision)))

@@ -187,11 +187,18 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   if (kern == DVW_KERNEL_AUTO && forced) kern = DVW_KERNEL_PARALLEL;
   if (sess) {  // sessions run on the batch-1 kernels, whose queues are laid out per stream
     if (kern == DVW_KERNEL_TC) return fail(DVW_E_UNSUPPORTED, "streaming sessions run on the CLUSTER or STREAM kernel");
-    if (kern == DVW_KERNEL_AUTO) kern = (n_streams == 1 && m->cplan.ok && direct) ? DVW_KERNEL_CLUSTER : DVW_KERNEL_STREAM;
+    // the cluster kernel's session variant evaluates the exact gate only
+    const bool exact = m->precision == DVW_PRECISION_FP32 || m->precision == DVW_PRECISION_TF32;
+    if (kern == DVW_KERNEL_CLUSTER && !exact)
+      return fail(DVW_E_UNSUPPORTED, "cluster-kernel sessions run the exact gate (use the STREAM kernel)");
+    if (kern == DVW_KERNEL_AUTO)
+      kern = (n_streams == 1 && m->cplan.ok && direct && exact) ? DVW_KERNEL_CLUSTER : DVW_KERNEL_STREAM;
   }
+  if (kern == DVW_KERNEL_TC && m->precision == DVW_PRECISION_APPC)
+    return fail(DVW_E_UNSUPPORTED, "the App. C tier runs on the CLUSTER, STREAM and PARALLEL kernels");
   if (kern == DVW_KERNEL_AUTO) {
     if (n_streams == 1 && m->cplan.ok && direct) kern = DVW_KERNEL_CLUSTER;
-    else if (n_streams > 1 && m->bplan.ok) kern = DVW_KERNEL_TC;
+    else if (n_streams > 1 && m->bplan.ok && m->precision != DVW_PRECISION_APPC) kern = DVW_KERNEL_TC;
     else kern = DVW_KERNEL_STREAM;
   }
   int pgroup = 0;  // parallel kernel: streams per workspace group
@@ -245,7 +252,7 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   A.n0 = n0;
   A.ystate = sess ? sess->d_y : nullptr;
   A.err = m->d_err;
-  A.approx = m->precision == DVW_PRECISION_APPROX ? 1 : 0;
+  A.approx = m->precision == DVW_PRECISION_APPROX ? 1 : m->precision == DVW_PRECISION_APPC ? 2 : 0;
   A.samp_kind = forced ? DVW_SAMPLER_DIRECT : m->samp_kind;
   A.samp_inv_t = m->samp_inv_t;
   A.samp_topk = m->samp_topk;
@@ -508,7 +515,8 @@ DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel) {
 
 DVW_API dvw_status dvw_set_precision(dvw_model* m, int32_t precision) {
   if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
-  if (precision != DVW_PRECISION_FP32 && precision != DVW_PRECISION_TF32 && precision != DVW_PRECISION_APPROX)
+  if (precision != DVW_PRECISION_FP32 && precision != DVW_PRECISION_TF32 && precision != DVW_PRECISION_APPROX &&
+      precision != DVW_PRECISION_APPC)
     return fail(DVW_E_INVALID_ARG, "unknown precision %d", precision);
   m->precision = precision;
   return DVW_OK;

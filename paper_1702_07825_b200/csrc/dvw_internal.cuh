@@ -70,7 +70,7 @@ struct RunArgs {
   float* out_logits;     // [S][N][256] or nullptr
   float* ring;           // [S][ring_floats] workspace
   int* err;              // device error word (0 = ok)
-  int approx;            // DVW_PRECISION_APPROX: hardware tanh in the batch-1 kernels' gates
+  int approx;            // 1: DVW_PRECISION_APPROX (hardware tanh gate); 2: DVW_PRECISION_APPC (App. C)
   int samp_kind;         // App. A.4 strategy (dvw_sampler): 0 direct, 1 temperature, 2 mean, 3 mode, 4 top-k
   float samp_inv_t;      // 1 / temperature
   int samp_topk;         // k of top-k
@@ -122,6 +122,44 @@ __device__ __forceinline__ float gate_approx(float a, float g) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(ta) : "f"(a));
   asm("tanh.approx.f32 %0, %1;" : "=f"(tg) : "f"(0.5f * g));
   return ta * fmaf(0.5f, tg, 0.5f);
+}
+
+// The paper's own approximations (DVW_PRECISION_APPC; App. C, row f4;
+// reading R31).  e~(x) = 1 + |x| + 0.5658 x^2 + 0.143 x^4;
+//   tanh(x) ~ sign(x) (e~ - 1/e~) / (e~ + 1/e~), evaluated as
+//             sign(x) (1 - r^2) / (1 + r^2) with r = 1/e~ (the same value; no inf/inf)
+//   sigma(x) ~ e~ / (1 + e~) (x >= 0), 1 / (1 + e~) (x <= 0), i.e.
+//             1 / (1 + r) and r / (1 + r)
+// IEEE division throughout (the approximation's own error is 1.5e-3 / 2.5e-3; the GPU
+// evaluates the same formula as the oracle to ~1e-7).
+__device__ __forceinline__ float appc_etilde(float x) {
+  const float x2 = x * x;
+  return fmaf(0.143f * x2, x2, fmaf(0.5658f, x2, 1.0f + fabsf(x)));
+}
+__device__ __forceinline__ float tanh_appc(float x) {
+  const float r = __fdiv_rn(1.0f, appc_etilde(x)), r2 = r * r;
+  return copysignf(__fdiv_rn(1.0f - r2, 1.0f + r2), x);
+}
+__device__ __forceinline__ float sigmoid_appc(float x) {
+  const float r = __fdiv_rn(1.0f, appc_etilde(x));
+  return x >= 0.0f ? __fdiv_rn(1.0f, 1.0f + r) : __fdiv_rn(r, 1.0f + r);
+}
+__device__ __forceinline__ float gate_appc(float a, float g) { return tanh_appc(a) * sigmoid_appc(g); }
+
+// e^x for x <= 0 by App. C.2: 2^x' with x' = x / ln 2 written straight
+// into an fp32 bit pattern, I = (x' + 126 + g(z)) 2^23, z = x' - floor(x'),
+// g(z) ~ -4.7259162 + 27.7280233 / (4.84252568 - z) - 1.49012907 z.  Evaluated as
+// (floor(x') + 127) 2^23 + trunc((z + g(z) - 1) 2^23) so the integer part is exact (a carry
+// out of the fraction near z -> 1 moves into the exponent, as in the paper's formula);
+// x' < -126 (below the normal range) -> 0 (reading R31).
+__device__ __forceinline__ float appc_exp(float x) {
+  const float xl = x * 1.44269504f;
+  if (!(xl >= -126.0f)) return 0.0f;
+  const float fl = floorf(xl);
+  const float z = xl - fl;
+  const float g = __fsub_rn(__fadd_rn(-4.7259162f, __fdiv_rn(27.7280233f, 4.84252568f - z)), __fmul_rn(1.49012907f, z));
+  const float t = __fsub_rn(__fadd_rn(z, g), 1.0f);
+  return __int_as_float(((int)fl + 127) * 8388608 + (int)(t * 8388608.0f));
 }
 
 // Inverse-CDF direct sampling over a = 256 logits held one per thread by a
@@ -235,7 +273,8 @@ __device__ __forceinline__ unsigned ordered_key(float v) {
 // warp_cdf_draw; mode: argmax (lowest code on ties); mean: floor(sum k e_k / sum e_k + 0.5).
 // Every reduction has a fixed order (bitwise deterministic).
 __device__ __forceinline__ int warp_sample_policy(const float (&l)[8], float u, int kind, float inv_t, int topk,
-                                                  int lane) {
+                                                  int lane, bool appc = false) {
+  auto ex = [appc](float v) { return appc ? appc_exp(v) : expf(v); };  // App. C.2 under DVW_PRECISION_APPC
   float mx = fmaxf(fmaxf(fmaxf(l[0], l[1]), fmaxf(l[2], l[3])), fmaxf(fmaxf(l[4], l[5]), fmaxf(l[6], l[7])));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -258,7 +297,7 @@ __device__ __forceinline__ int warp_sample_policy(const float (&l)[8], float u, 
     double S = 0.0, M = 0.0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const double ei = (double)expf(l[i] - mx);
+      const double ei = (double)ex(l[i] - mx);
       S += ei;
       M += (double)(8 * lane + i) * ei;
     }
@@ -272,7 +311,7 @@ __device__ __forceinline__ int warp_sample_policy(const float (&l)[8], float u, 
   }
   if (kind == 1) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) e[i] = expf((l[i] - mx) * inv_t);
+    for (int i = 0; i < 8; ++i) e[i] = ex((l[i] - mx) * inv_t);
     return warp_cdf_draw(e, u, lane);
   }
   if (kind == 4) {  // top-k: the k-th largest key by bisection on the ordered key, then ties by code
@@ -309,12 +348,12 @@ __device__ __forceinline__ int warp_sample_policy(const float (&l)[8], float u, 
         keep = eq_before < need;
         ++eq_before;
       }
-      e[i] = keep ? expf(l[i] - mx) : 0.0f;
+      e[i] = keep ? ex(l[i] - mx) : 0.0f;
     }
     return warp_cdf_draw(e, u, lane);
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) e[i] = expf(l[i] - mx);
+  for (int i = 0; i < 8; ++i) e[i] = ex(l[i] - mx);
   return warp_cdf_draw(e, u, lane);
 }
 #endif

@@ -295,6 +295,7 @@ __device__ __noinline__ int sample_fp64(float e0, float e1, float e2, float e3, 
   return y < kLevels ? y : __reduce_max_sync(0xffffffffu, (unsigned)(lastpos + 1)) - 1;
 }
 
+template <int NL>
 __device__ __forceinline__ int sample_warp(const float* logits, float u, int lane) {
   float l[8];
   {
@@ -306,7 +307,7 @@ __device__ __forceinline__ int sample_warp(const float* logits, float u, int lan
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   float e[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) e[i] = expf(l[i] - mx);
+  for (int i = 0; i < 8; ++i) e[i] = NL == 2 ? appc_exp(l[i] - mx) : expf(l[i] - mx);  // App. C.2 (R31)
   // fp32 pass
   float q[8];
   q[0] = e[0];
@@ -337,7 +338,7 @@ __device__ __forceinline__ int sample_warp(const float* logits, float u, int lan
 
 // Draw y_{n-1} from the inbound logits (App. A.4) and write x^(0)_n (step 1) into xs[n&1][0]
 // with the first warp of warpgroup A; warpgroups A, B, C wait at the closing barrier.
-template <bool TRACE>
+template <bool TRACE, int NL = 0>
 __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx, int64_t n, int k, int& y1,
                                                  int& y2, const float* wembc, const float* bemb) {
   const RunArgs& A = P.a;
@@ -363,7 +364,7 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
         y = yf;
       } else {
         stamp<TRACE>(tp, 4);
-        y = sample_warp(m.logits_in, u, k);
+        y = sample_warp<NL>(m.logits_in, u, k);
         stamp<TRACE>(tp, 6);
         if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
       }
@@ -385,6 +386,7 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
 }
 
 // The final draw (sample N-1) after the last layer pass (first warp of A); returns it.
+template <int NL = 0>
 __device__ __forceinline__ int final_draw(const Params& P, const Ctx& cx, int k) {
   const RunArgs& A = P.a;
   Mail& m = *cx.mail;
@@ -398,7 +400,7 @@ __device__ __forceinline__ int final_draw(const Params& P, const Ctx& cx, int k)
     o[0] = lds4(m.logits_in + 8 * k);
     o[1] = lds4(m.logits_in + 8 * k + 4);
   } else {
-    y = sample_warp(m.logits_in, u, k);
+    y = sample_warp<NL>(m.logits_in, u, k);
     if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
   }
   return y;
@@ -439,7 +441,7 @@ constexpr int kColB3 = 384;
 // pair, where the gate runs.  B: row g of W_res, same columns.
 
 // ------------------------------------------------------------------ chain CTA, warpgroup A (the chain)
-template <int LP, bool TRACE, bool APPROX, bool SESS>
+template <int LP, bool TRACE, int NL, bool SESS>
 __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -460,7 +462,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
     const int p = (int)(n & 1);
     ptx::tmem_load_async<64>(tm, w);  // layer j0's tile, hidden behind the waits
     if (c == 0) {
-      sample_and_embed<TRACE>(P, cx, n, a, y1, y2, wembc, bemb);
+      sample_and_embed<TRACE, NL>(P, cx, n, a, y1, y2, wembc, bemb);
     } else {
       if (wait(cx, &m.bar_hin, (uint32_t)p, 12) && a == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_hin), R * 4);
     }
@@ -487,7 +489,9 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
           v[1] += m.rr[jl][R + hrow];
         }
         // a = a_cur + (W_prev x_{n-d} + B + L); h = tanh(a_h) sigma(a_g)
-        const float hv = APPROX ? gate_approx(v[0] + pre0, v[1] + pre1) : gate_fast(v[0] + pre0, v[1] + pre1);
+        const float hv = NL == 1   ? gate_approx(v[0] + pre0, v[1] + pre1)
+                         : NL == 2 ? gate_appc(v[0] + pre0, v[1] + pre1)
+                                   : gate_fast(v[0] + pre0, v[1] + pre1);
         stamp<TRACE>(tp, 27 + jl);
         if (jl + 1 == nl) {
           // the CTA's last layer: h goes straight to the next chain CTA (or, for layer l, to the
@@ -510,7 +514,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
     }
   }
   if (c == 0 && A.N > 0) {
-    const int y = final_draw(P, cx, a);
+    const int y = final_draw<NL>(P, cx, a);
     if (SESS && a == 0 && !A.forced) {  // streaming session: the code history for the next call
       A.ystate[0] = y;
       A.ystate[1] = y1;
@@ -969,7 +973,7 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
   }
 }
 
-template <int S, int LP, bool TRACE, bool APPROX = false, bool SESS = false>
+template <int S, int LP, bool TRACE, int NL = 0, bool SESS = false>
 __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Mail* mail = reinterpret_cast<Mail*>(smem_raw);
@@ -1046,7 +1050,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
 
   if (t >= kAux) {
     if (role == kChain) {
-      if (t < kAux + 128) chain_A<LP, TRACE, APPROX, SESS>(P, cx, idx, sw);
+      if (t < kAux + 128) chain_A<LP, TRACE, NL, SESS>(P, cx, idx, sw);
       else if (t < kAux + 256) chain_B<LP, TRACE, SESS>(P, cx, idx, sw);
       else chain_C<LP, TRACE, SESS>(P, cx, idx, sw);
     } else if (role == kHead) {
@@ -1071,19 +1075,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   ptx::cluster_sync();
 }
 
-template <int S, int LP, bool TRACE, bool APPROX = false, bool SESS = false>
+template <int S, int LP, bool TRACE, int NL = 0, bool SESS = false>
 cudaError_t configure(int smem) {
-  cudaError_t e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, APPROX, SESS>,
+  cudaError_t e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, NL, SESS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, APPROX, SESS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, NL, SESS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
 template <int S, int LP>
 int max_active_clusters(int size, int smem) {
   if (configure<S, LP, false>(smem) != cudaSuccess || configure<S, LP, true>(smem) != cudaSuccess ||
-      configure<S, LP, false, true>(smem) != cudaSuccess || configure<S, LP, false, false, true>(smem) != cudaSuccess) {
+      configure<S, LP, false, 1>(smem) != cudaSuccess || configure<S, LP, false, 2>(smem) != cudaSuccess ||
+      configure<S, LP, false, 0, true>(smem) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -1368,14 +1373,17 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaError_t e;
-  // variants: production (exact gate), TRACE (exact gate + timestamps), APPROX (hardware tanh),
-  // SESS (streaming session: continues the queues and code history; exact gate)
+  // variants: production (exact gate), TRACE (exact gate + timestamps), NL = 1 (hardware tanh),
+  // NL = 2 (App. C gate and exp), SESS (streaming session: continues the queues and code
+  // history; exact gate -- the API routes approximate-tier sessions to the stream kernel)
   const bool ss = a.ystate != nullptr;
-  const bool ap = a.approx != 0 && !tr && !ss;
+  const bool ap = a.approx == 1 && !tr && !ss;
+  const bool pc = a.approx == 2 && !tr && !ss;
 #define DVW_LAUNCH(S_, LP_)                                                         \
-  e = ss   ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, false, true>, P)   \
+  e = ss   ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, 0, true>, P)       \
       : tr ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, true>, P)                 \
-      : ap ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, true>, P)          \
+      : ap ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, 1>, P)             \
+      : pc ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, 2>, P)             \
            : cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false>, P)
   if (p.s == 256 && p.lpc == 3) {
     DVW_LAUNCH(256, 3);

@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kPT, 2) k_layer(RunArgs A, int j, const float*
       const int c = 4 * og + q;
       const float ah = acc[i][q] + __ldg(bj + c) + (t < T ? __ldg(L + c) : 0.0f);
       const float ag = acc[i][4 + q] + __ldg(bj + R + c) + (t < T ? __ldg(L + R + c) : 0.0f);
-      Ht[c * kTile + tb + i] = gate(ah, ag);
+      Ht[c * kTile + tb + i] = A.approx == 0 ? gate(ah, ag) : A.approx == 1 ? gate_approx(ah, ag) : gate_appc(ah, ag);
     }
   }
   // ---- x_{j+1} = x_j + W_res h + B_res: same (tg, og) map, 4 channels

@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(RunArgs A) {
                            [&](int row, float acc) { av[row] = acc + Wl[o.b + row] + Lj[row]; });
       }
       __syncthreads();
-      for (int i = tid; i < R; i += kThreads) h[i] = A.approx ? gate_approx(av[i], av[R + i]) : gate(av[i], av[R + i]);
+      for (int i = tid; i < R; i += kThreads) h[i] = A.approx == 0 ? gate(av[i], av[R + i])
+                  : A.approx == 1 ? gate_approx(av[i], av[R + i]) : gate_appc(av[i], av[R + i]);
       __syncthreads();
       {
         Vec<R> vh;
@@ -170,14 +171,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(RunArgs A) {
       A.out_logits[((int64_t)st * A.N + n) * kLevels + tid] = l;
       y = forced[n];
     } else {
-      if (A.samp_kind == 0) {
+      if (A.samp_kind == 0 && A.approx != 2) {
         y = sample_256(l, uni[n], dscr, fscr, iscr, tid, 1);
-      } else {  // App. A.4 strategies: one warp (row f3)
+      } else {  // App. A.4 strategies (row f3) and App. C.2's exp (row f4): one warp
         if (tid < 32) {
           float lv[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) lv[i] = lg[8 * tid + i];
-          const int yy = warp_sample_policy(lv, uni[n], A.samp_kind, A.samp_inv_t, A.samp_topk, tid);
+          const int yy = warp_sample_policy(lv, uni[n], A.samp_kind, A.samp_inv_t, A.samp_topk, tid, A.approx == 2);
           if (tid == 0) iscr[0] = yy;
         }
         __syncthreads();

@@ -391,6 +391,55 @@ def test_approx_gate_tier_within_gate(L, kernel):
     assert float(np.max(np.abs(lg32.astype(np.float64) - ref_lg))) <= FP32_FAITHFUL
 
 
+@pytest.mark.parametrize("kernel", ["cluster", "stream", "parallel"])
+@pytest.mark.parametrize("cfg", [synth.C1, synth.C2], ids=["C1", "C2"])
+def test_appc_tier_matches_oracle_appc(L, kernel, cfg):
+    """Row f4, the paper's own approximations (DVW_PRECISION_APPC, App. C): every gate uses
+    e~-based tanh / sigma and the sampler's exp is App. C.2's bit-pattern construction.
+    Parity is with the oracle's App. C mode: teacher-forced logits within the fp32-faithful
+    bound; free-running codes equal the oracle's draws at a per-step rate <= 0.5 %."""
+    N, hop = 1600, 64
+    w = synth.make_weights(cfg, 0)
+    cond = synth.make_cond(cfg, synth.n_frames_for(N, hop), 0)
+    u = synth.make_uniforms(N, 0)
+    m = model(L, cfg, w, kernel).set_precision("appc")
+    if kernel == "parallel":
+        codes = synth.make_codes(N, 0)
+    else:
+        codes = m.generate(dev(cond)[None], dev(u)[None], hop).cpu().numpy()[0]
+    lg = m.logits(dev(cond)[None], dev(codes)[None], hop).cpu().numpy()[0]
+    _, ref_lg, sampled = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, N, uniforms=u,
+                                    forced=codes, want_sampled=True, nonlin="appc")
+    err = float(np.max(np.abs(lg.astype(np.float64) - ref_lg)))
+    _, ex_lg, _ = oracle_tf(cfg, w, cond, hop, codes)
+    dex = float(np.max(np.abs(ref_lg - ex_lg)))
+    print(f"appc {kernel} {cfg}: max|dlogit| vs oracle(appc) = {err:.2e} (appc vs exact: {dex:.2e})")
+    assert err <= FP32_FAITHFUL
+    assert dex > 10 * FP32_FAITHFUL  # the tier really is a different function
+    if kernel != "parallel":
+        mism = int(np.sum(sampled != codes))
+        print(f"  free-running per-step mismatches {mism}/{N}")
+        assert mism <= 0.005 * N
+
+
+def test_appc_tier_routing(L):
+    """App. C runs on CLUSTER / STREAM / PARALLEL; the batched TC kernel refuses it, and AUTO
+    sends a multi-stream batch to the stream kernel."""
+    cfg = synth.C1
+    N, hop = 64, 8
+    w = synth.make_weights(cfg, 0)
+    cond = np.stack([synth.make_cond(cfg, synth.n_frames_for(N, hop), s) for s in range(2)])
+    u = np.stack([synth.make_uniforms(N, s) for s in range(2)])
+    m = L.Model.from_config(cfg).load(w).set_precision("appc")
+    codes = m.generate(dev(cond), dev(u), hop)
+    assert m.info()["last_kernel_name"] == "stream"
+    ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[1], hop, N, uniforms=u[1], nonlin="appc")
+    assert np.array_equal(codes.cpu().numpy()[1], ref)
+    m.set_kernel("tc")
+    with pytest.raises(L.DvwError):
+        m.generate(dev(cond), dev(u), hop)
+
+
 @pytest.mark.parametrize("shape", [(20, 64, 256), (5, 32, 128), (3, 128, 256), (40, 64, 256)])
 def test_parallel_teacher_forced_logits(L, shape):
     """dvw_logits computed all timesteps of a layer at once (DVW_KERNEL_PARALLEL, AUTO for
