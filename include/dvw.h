@@ -207,6 +207,18 @@ typedef enum {
 } dvw_precision;
 DVW_API dvw_status dvw_set_precision(dvw_model* m, int32_t precision);
 
+/* Weight quantisation ("inference with weight matrices quantized to int16";
+ * SURVEY.md §8(f) row f4; reading R32).  bits = 16 or 8: at the NEXT
+ * dvw_load_weights every weight matrix (W_prev, W_cur, W_res, W_skip per layer; W_emb_prev,
+ * W_emb_cur, W_relu, W_out) is quantised symmetrically per row, in fp32 arithmetic:
+ *   s = max_c |W[row][c]| / (2^(bits-1) - 1),  q = rint(W / s) (half to even),  W := q s
+ * (rows of zeros stay zero); biases stay fp32.  Every kernel then runs on the quantised
+ * values (fp32 storage: the weights are resident on chip, so the batch-1 path gains no
+ * bandwidth from narrower storage -- the tier measures what the quantisation costs in
+ * accuracy).  bits = 0 (default) loads the blob unchanged.  Other values ->
+ * DVW_E_INVALID_ARG. */
+DVW_API dvw_status dvw_set_weight_bits(dvw_model* m, int32_t bits);
+
 /* Sampling strategy for dvw_generate (App. A.4).
  * Details the paper leaves open follow DESIGN.md readings R24-R27:
  *   DVW_SAMPLER_DIRECT      (default) inverse-CDF draw from P with u_n (reading R11)

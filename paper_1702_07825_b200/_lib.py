@@ -30,7 +30,8 @@ KERNEL_AUTO, KERNEL_STREAM, KERNEL_CLUSTER, KERNEL_TC, KERNEL_PARALLEL = 0, 1, 2
 KERNEL_NAMES = {0: "auto", 1: "stream", 2: "cluster", 3: "tc", 4: "parallel"}
 
 EXPORTS = ("dvw_create", "dvw_weights_numel", "dvw_load_weights", "dvw_generate", "dvw_logits",
-           "dvw_generate_host", "dvw_set_kernel", "dvw_set_precision", "dvw_set_sampler", "dvw_set_trace",
+           "dvw_generate_host", "dvw_set_kernel", "dvw_set_precision", "dvw_set_weight_bits",
+           "dvw_set_sampler", "dvw_set_trace",
            "dvw_get_info", "dvw_sync", "dvw_destroy", "dvw_last_error",
            "dvw_session_create", "dvw_session_generate", "dvw_session_position", "dvw_session_destroy",
            "dvwc_create", "dvwc_weights_numel", "dvwc_load_weights", "dvwc_run", "dvwc_destroy")
@@ -69,6 +70,8 @@ _lib.dvw_set_kernel.argtypes = [_vp, _i32]
 _lib.dvw_set_kernel.restype = _i32
 _lib.dvw_set_precision.argtypes = [_vp, _i32]
 _lib.dvw_set_precision.restype = _i32
+_lib.dvw_set_weight_bits.argtypes = [_vp, _i32]
+_lib.dvw_set_weight_bits.restype = _i32
 class _CConfig(ctypes.Structure):
     _fields_ = [("in_channels", ctypes.c_int32), ("hidden", ctypes.c_int32), ("n_layers", ctypes.c_int32),
                 ("residual", ctypes.c_int32), ("device", ctypes.c_int32)]
@@ -203,6 +206,12 @@ class Model:
         if isinstance(precision, str):
             precision = {v: k for k, v in PRECISION_NAMES.items()}[precision]
         _check(_lib.dvw_set_precision(self._h, int(precision)))
+        return self
+
+    def set_weight_bits(self, bits: int):
+        """Quantise every weight matrix per row to `bits` (16 or 8; 0 = off) at the next
+        load() (include/dvw.h dvw_set_weight_bits)."""
+        _check(_lib.dvw_set_weight_bits(self._h, int(bits)))
         return self
 
     def set_sampler(self, kind="direct", temperature: float = 1.0, top_k: int = 256):

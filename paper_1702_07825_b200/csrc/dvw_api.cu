@@ -41,6 +41,7 @@ struct dvw_model {
   bool loaded = false;
   int kernel = DVW_KERNEL_AUTO;
   int precision = DVW_PRECISION_FP32;
+  int weight_bits = 0;  // dvw_set_weight_bits: applied by dvw_load_weights
   int samp_kind = DVW_SAMPLER_DIRECT;
   float samp_inv_t = 1.0f;
   int samp_topk = kLevels;
@@ -295,6 +296,34 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   return DVW_OK;
 }
 
+// Symmetric per-row quantisation of one row-major matrix to `bits`-bit integers and back
+// (reading R32): s = max|row| / (2^(bits-1) - 1), W := rint(W / s) * s, fp32.
+void quantize_rows(float* w, int64_t rows, int64_t cols, int bits) {
+  const float qmax = (float)((1 << (bits - 1)) - 1);
+  for (int64_t i = 0; i < rows; ++i) {
+    float* row = w + i * cols;
+    float mx = 0.0f;
+    for (int64_t c = 0; c < cols; ++c) mx = std::max(mx, std::fabs(row[c]));
+    if (mx == 0.0f) continue;
+    const float sc = mx / qmax;
+    for (int64_t c = 0; c < cols; ++c) row[c] = std::rint(row[c] / sc) * sc;
+  }
+}
+
+void quantize_matrices(float* w, const Offsets& o, int L, int r, int s, int bits) {
+  for (int j = 0; j < L; ++j) {
+    float* lw = w + (int64_t)j * o.layer_stride;
+    quantize_rows(lw + o.w_prev, 2 * r, r, bits);
+    quantize_rows(lw + o.w_cur, 2 * r, r, bits);
+    quantize_rows(lw + o.w_res, r, r, bits);
+    quantize_rows(lw + o.w_skip, s, r, bits);
+  }
+  quantize_rows(w + o.emb_prev, r, kLevels, bits);
+  quantize_rows(w + o.emb_cur, r, kLevels, bits);
+  quantize_rows(w + o.w_relu, kLevels, s, bits);
+  quantize_rows(w + o.w_out, kLevels, kLevels, bits);
+}
+
 }  // namespace
 
 extern "C" {
@@ -371,6 +400,11 @@ DVW_API dvw_status dvw_load_weights(dvw_model* m, const float* blob, int64_t num
   }
   for (int64_t i = 0; i < numel; ++i)
     if (!std::isfinite(hp[i])) return fail(DVW_E_INVALID_ARG, "weight %lld is not finite", (long long)i);
+  if (m->weight_bits != 0) {  // row f4: quantise the matrices (include/dvw.h dvw_set_weight_bits)
+    if (host.empty()) host.assign(blob, blob + numel);
+    quantize_matrices(host.data(), m->off, m->L, m->r, m->s, m->weight_bits);
+    hp = host.data();
+  }
   if (!m->d_w) DVW_CUDA(cudaMalloc(&m->d_w, sizeof(float) * numel), "allocating weights");
   DVW_CUDA(cudaMemcpy(m->d_w, hp, sizeof(float) * numel, cudaMemcpyHostToDevice), "uploading weights");
   int64_t wb = sizeof(float) * numel;
@@ -510,6 +544,13 @@ DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel) {
   if (kernel == DVW_KERNEL_TC && !m->bplan.ok)
     return fail(DVW_E_UNSUPPORTED, "batched kernel cannot run this model: %s", m->bplan.why);
   m->kernel = kernel;
+  return DVW_OK;
+}
+
+DVW_API dvw_status dvw_set_weight_bits(dvw_model* m, int32_t bits) {
+  if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
+  if (bits != 0 && bits != 8 && bits != 16) return fail(DVW_E_INVALID_ARG, "weight bits must be 0, 8 or 16 (got %d)", bits);
+  m->weight_bits = bits;
   return DVW_OK;
 }
 

@@ -440,6 +440,48 @@ def test_appc_tier_routing(L):
         m.generate(dev(cond), dev(u), hop)
 
 
+@pytest.mark.parametrize("kernel", ["cluster", "stream", "tc", "parallel"])
+@pytest.mark.parametrize("bits", [16, 8])
+def test_quantized_weights_match_oracle_on_quantized_blob(L, kernel, bits):
+    """Row f4, int16 / int8 weights (reading R32): dvw_set_weight_bits quantises
+    every matrix per row at load; each kernel then equals the fp64 oracle run on the blob the
+    oracle's own quantiser produces -- teacher-forced logits fp32-faithful, codes at a per-step
+    mismatch rate <= 0.5 %."""
+    from oracle import quant
+    cfg = synth.C1
+    S = 2 if kernel == "tc" else 1
+    N, hop = 1000, 64
+    w = synth.make_weights(cfg, 0)
+    wq = quant.quantize_weights(w, cfg.n_layers, cfg.residual, cfg.skip, bits)
+    cond = np.stack([synth.make_cond(cfg, synth.n_frames_for(N, hop), s) for s in range(S)])
+    u = np.stack([synth.make_uniforms(N, s) for s in range(S)])
+    m = L.Model.from_config(cfg).set_weight_bits(bits).load(w)
+    try:
+        m.set_kernel(kernel)
+    except L.DvwError as e:
+        pytest.skip(str(e))
+    if kernel == "parallel":
+        codes = np.stack([synth.make_codes(N, s) for s in range(S)])
+    else:
+        codes = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    lg = m.logits(dev(cond), dev(codes), hop).cpu().numpy()
+    for st in range(S):
+        _, ref, sampled = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, wq, cond[st], hop, N, uniforms=u[st],
+                                     forced=codes[st], want_sampled=True)
+        err = float(np.max(np.abs(lg[st].astype(np.float64) - ref)))
+        print(f"int{bits} {kernel} stream {st}: max|dlogit| vs oracle(quantised) {err:.2e}")
+        assert err <= FP32_FAITHFUL
+        if kernel != "parallel":
+            assert int(np.sum(sampled != codes[st])) <= 0.005 * N
+    # quantisation applies at load: switching it off and reloading restores the fp32 model
+    m.set_weight_bits(0).load(w).set_kernel("stream")
+    lg0 = m.logits(dev(cond[:1]), dev(codes[:1]), hop).cpu().numpy()[0]
+    _, ref0, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[0], hop, N, forced=codes[0])
+    assert float(np.max(np.abs(lg0.astype(np.float64) - ref0))) <= FP32_FAITHFUL
+    with pytest.raises(L.DvwError):
+        m.set_weight_bits(12)
+
+
 @pytest.mark.parametrize("shape", [(20, 64, 256), (5, 32, 128), (3, 128, 256), (40, 64, 256)])
 def test_parallel_teacher_forced_logits(L, shape):
     """dvw_logits computed all timesteps of a layer at once (DVW_KERNEL_PARALLEL, AUTO for
