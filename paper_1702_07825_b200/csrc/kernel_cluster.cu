@@ -302,9 +302,11 @@ __device__ __forceinline__ int sample_warp(const float* logits, float u, int lan
     const float4 a = lds4(logits + 8 * lane), b = lds4(logits + 8 * lane + 4);
     l[0] = a.x; l[1] = a.y; l[2] = a.z; l[3] = a.w; l[4] = b.x; l[5] = b.y; l[6] = b.z; l[7] = b.w;
   }
-  float mx = fmaxf(fmaxf(fmaxf(l[0], l[1]), fmaxf(l[2], l[3])), fmaxf(fmaxf(l[4], l[5]), fmaxf(l[6], l[7])));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float lmx = fmaxf(fmaxf(fmaxf(l[0], l[1]), fmaxf(l[2], l[3])), fmaxf(fmaxf(l[4], l[5]), fmaxf(l[6], l[7])));
+  // warp max in one redux.sync on order-preserving integer keys (exact: the key map is a
+  // bijection that keeps the order of finite floats), instead of five shuffle + max steps
+  const unsigned kmx = __reduce_max_sync(0xffffffffu, ordered_key(lmx));
+  const float mx = __uint_as_float((kmx & 0x80000000u) ? (kmx & 0x7fffffffu) : ~kmx);
   float e[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) e[i] = NL == 2 ? appc_exp(l[i] - mx) : expf(l[i] - mx);  // App. C.2 (R31)
