@@ -159,9 +159,13 @@ DVW_API dvw_status dvw_generate_host(dvw_model* m, const float* cond_host, int64
  *                          utterance, fp32 [n_streams][n_frames][l][2r] with
  *                          n_frames >= ceil((position + n_samples) / hop); uniforms and
  *                          out_codes are the chunk's, [n_streams][n_samples].  hop must not
- *                          change within a session.  Runs on the CLUSTER (one stream, direct
- *                          sampler) or STREAM kernel; a pinned TC kernel -> DVW_E_UNSUPPORTED.
- *                          Calls on one session must be ordered (same CUDA stream).
+ *                          change within a session.  AUTO runs one stream on the CLUSTER
+ *                          kernel (direct sampler, exact gate), several on the batched TC
+ *                          kernel (the session then keeps its workspace: queues, x^(0) and
+ *                          codes of every launch group), else the STREAM kernel.  The kernel of
+ *                          the first call is kept; a later call pinned to a kernel with another
+ *                          state layout -> DVW_E_STATE.  Calls on one session must be ordered
+ *                          (same CUDA stream).
  *   dvw_session_position : samples generated so far (-1 for NULL)
  * The session is bound to the model's device and dilation schedule. */
 typedef struct dvw_session dvw_session;

@@ -29,6 +29,9 @@ struct dvw_session {
   int* d_y = nullptr;       // [S][2]: y_{n-1}, y_{n-2}
   int64_t n_done = 0;
   int hop = 0;
+  int kernel = 0;             // the kernel the session's first call ran on (state layouts differ)
+  void* d_bws = nullptr;      // TC kernel: every launch group's workspace (queues, x^(0), codes)
+  size_t bws_bytes = 0;
 };
 
 struct dvw_model {
@@ -186,14 +189,23 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   if (kern == DVW_KERNEL_PARALLEL && !forced)
     return fail(DVW_E_UNSUPPORTED, "the parallel kernel computes teacher-forced logits only (dvw_logits)");
   if (kern == DVW_KERNEL_AUTO && forced) kern = DVW_KERNEL_PARALLEL;
-  if (sess) {  // sessions run on the batch-1 kernels, whose queues are laid out per stream
-    if (kern == DVW_KERNEL_TC) return fail(DVW_E_UNSUPPORTED, "streaming sessions run on the CLUSTER or STREAM kernel");
+  if (sess) {
     // the cluster kernel's session variant evaluates the exact gate only
     const bool exact = m->precision == DVW_PRECISION_FP32 || m->precision == DVW_PRECISION_TF32;
     if (kern == DVW_KERNEL_CLUSTER && !exact)
       return fail(DVW_E_UNSUPPORTED, "cluster-kernel sessions run the exact gate (use the STREAM kernel)");
-    if (kern == DVW_KERNEL_AUTO)
-      kern = (n_streams == 1 && m->cplan.ok && direct && exact) ? DVW_KERNEL_CLUSTER : DVW_KERNEL_STREAM;
+    if (kern == DVW_KERNEL_AUTO) {
+      if (sess->kernel != 0) kern = sess->kernel;
+      else if (n_streams == 1 && m->cplan.ok && direct && exact) kern = DVW_KERNEL_CLUSTER;
+      else if (n_streams > 1 && m->bplan.ok && m->precision != DVW_PRECISION_APPC) kern = DVW_KERNEL_TC;
+      else kern = DVW_KERNEL_STREAM;
+    }
+    // a session's state (queues, code history) is laid out by the kernel that started it
+    if (sess->kernel != 0 && kern != sess->kernel &&
+        !((kern == DVW_KERNEL_CLUSTER || kern == DVW_KERNEL_STREAM) &&
+          (sess->kernel == DVW_KERNEL_CLUSTER || sess->kernel == DVW_KERNEL_STREAM)))
+      return fail(DVW_E_STATE, "this session was started on kernel %d and cannot continue on kernel %d",
+                  sess->kernel, kern);
   }
   if (kern == DVW_KERNEL_TC && m->precision == DVW_PRECISION_APPC)
     return fail(DVW_E_UNSUPPORTED, "the App. C tier runs on the CLUSTER, STREAM and PARALLEL kernels");
@@ -214,6 +226,12 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
       m->pws_bytes = 0;
       DVW_CUDA(cudaMalloc(&m->d_pws, need), "allocating parallel workspace");
       m->pws_bytes = need;
+    }
+  } else if (kern == DVW_KERNEL_TC && sess) {
+    if (!sess->d_bws) {
+      const size_t need = batch_session_bytes(m->bplan, m->dil.data(), n_streams);
+      DVW_CUDA(cudaMalloc(&sess->d_bws, need), "allocating the session's batched workspace");
+      sess->bws_bytes = need;
     }
   } else if (kern == DVW_KERNEL_TC) {
     const int nsb = std::min(m->bplan.max_sb, (n_streams + 127) / 128);
@@ -282,12 +300,15 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
     }
     li.launches = launches;
   } else if (kern == DVW_KERNEL_TC) {
-    e = launch_batch_kernel(A, m->bplan, m->d_bpacked, m->d_bws, m->bws_bytes, m->dil.data(),
-                            m->precision != DVW_PRECISION_FP32, cs, &li);
+    e = sess ? launch_batch_kernel(A, m->bplan, m->d_bpacked, sess->d_bws, sess->bws_bytes, m->dil.data(),
+                                   m->precision != DVW_PRECISION_FP32, cs, &li, true)
+             : launch_batch_kernel(A, m->bplan, m->d_bpacked, m->d_bws, m->bws_bytes, m->dil.data(),
+                                   m->precision != DVW_PRECISION_FP32, cs, &li);
   } else {
     return fail(DVW_E_UNSUPPORTED, "kernel %d is not available in this build", kern);
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  if (sess) sess->kernel = kern;
   m->info.last_kernel = kern;
   m->info.last_grid = li.grid;
   m->info.last_cluster = li.cluster;
@@ -533,6 +554,7 @@ DVW_API void dvw_session_destroy(dvw_session* s) {
   DeviceGuard g(s->device);
   cudaFree(s->d_ring);
   cudaFree(s->d_y);
+  cudaFree(s->d_bws);
   delete s;
 }
 

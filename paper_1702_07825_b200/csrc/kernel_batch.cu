@@ -535,7 +535,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
     } else {  // logits = W_out z_a + B_out
       const float* bb = A.w + A.off.b_out + c0;
       float* lg = P.logits + (int64_t)g * kLevels + c0;
-      float* ol = (A.forced && live) ? A.out_logits + ((int64_t)g * A.N + n) * kLevels + c0 : nullptr;
+      float* ol = (A.forced && live) ? A.out_logits + ((int64_t)g * A.N + (n - A.n0)) * kLevels + c0 : nullptr;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float4 v = make_float4(D[4 * q] + __ldg(bb + 4 * q), D[4 * q + 1] + __ldg(bb + 4 * q + 1),
@@ -581,12 +581,15 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
   const int gw = k * (kBT / 32) + w;
   const int g_end = min(A.n_streams, (sb + 1) * 128);
 
-  // x^(0)_0 from y_{-1} = y_{-2} = 128 (R4)
-  for (int g = sb * 128 + gw; g < g_end; g += nwarps) {
-    embed(P, g, 0, kLevels / 2, kLevels / 2, lane);
-    if (lane == 0) {
-      P.yh[2 * g] = kLevels / 2;
-      P.yh[2 * g + 1] = kLevels / 2;
+  // x^(0)_0 from y_{-1} = y_{-2} = 128 (R4).  A streaming session (n0 > 0) continues from
+  // the queues, x^(0)_{n0} and the code history its previous call left in the workspace.
+  if (A.n0 == 0) {
+    for (int g = sb * 128 + gw; g < g_end; g += nwarps) {
+      embed(P, g, 0, kLevels / 2, kLevels / 2, lane);
+      if (lane == 0) {
+        P.yh[2 * g] = kLevels / 2;
+        P.yh[2 * g + 1] = kLevels / 2;
+      }
     }
   }
   phase_sync(P, cl);
@@ -595,7 +598,10 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
   // error word.
   bool ok = true;
 
-  for (int64_t n = 0; n < A.N; ++n) {
+  // n: the global sample index (queue slots, conditioning frames); n - n0 indexes this call's
+  // uniforms, codes and logits
+  for (int64_t n = A.n0; n < A.n0 + A.N; ++n) {
+    const int64_t nl = n - A.n0;
     for (int ph = 0; ph < P.L + 4; ++ph) {
       const int tev = ph == 3 ? 0 : ph == P.L + 2 ? 8 : ph == P.L + 3 ? 4 : -1;
       if (t == 0 && tev >= 0) btrace(P, n, tev);
@@ -629,12 +635,13 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
           const int y1 = __ldcg(P.yh + 2 * g);
           int y;
           if (A.forced) {
-            y = __ldg(A.forced + (int64_t)g * A.N + n);
+            y = __ldg(A.forced + (int64_t)g * A.N + nl);
           } else {
-            y = sample_warp_g(A, P.logits + (int64_t)g * kLevels, __ldg(A.uniforms + (int64_t)g * A.N + n), lane);
-            if (lane == 0) A.out_codes[(int64_t)g * A.N + n] = (uint8_t)y;
+            y = sample_warp_g(A, P.logits + (int64_t)g * kLevels, __ldg(A.uniforms + (int64_t)g * A.N + nl), lane);
+            if (lane == 0) A.out_codes[(int64_t)g * A.N + nl] = (uint8_t)y;
           }
-          if (n + 1 < A.N) embed(P, g, n + 1, y1, y, lane);
+          // x^(0)_{n+1}, also after the call's last sample (a session's next call starts from it)
+          embed(P, g, n + 1, y1, y, lane);
           __syncwarp();
           if (lane == 0) {
             __stcg(P.yh + 2 * g, y);
@@ -859,19 +866,33 @@ size_t batch_workspace_bytes(const BatchPlan& p, const int32_t* dil, int nsb) {
   return (size_t)ws_layout(p, dil, nsb).total;
 }
 
+size_t batch_session_bytes(const BatchPlan& p, const int32_t* dil, int n_streams) {
+  size_t total = 0;
+  for (int g0 = 0; g0 < n_streams; g0 += p.max_sb * 128) {
+    const int ns = std::min(p.max_sb * 128, n_streams - g0);
+    total += (size_t)ws_layout(p, dil, (ns + 127) / 128).total;
+  }
+  return total;
+}
+
 cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void* packed, void* ws, size_t ws_bytes,
-                                const int32_t* dil_host, bool fast, cudaStream_t st, LaunchInfo* info) {
+                                const int32_t* dil_host, bool fast, cudaStream_t st, LaunchInfo* info,
+                                bool session) {
   if (!p.ok) return cudaErrorNotSupported;
   // (plan_batch set the kernel's shared-memory and cluster-size attributes)
   const int per_launch = p.max_sb * 128;
   int64_t launches = 0;
   int grid = 0;
+  size_t wsoff = 0;  // a session keeps every launch group's workspace (queues, x^(0), codes)
   for (int g0 = 0; g0 < a.n_streams; g0 += per_launch) {
     const int ns = std::min(per_launch, a.n_streams - g0);
     const int nsb = (ns + 127) / 128;
     const WsLayout l = ws_layout(p, dil_host, nsb);
-    if ((size_t)l.total > ws_bytes) return cudaErrorInvalidValue;
-    cudaError_t e = cudaMemsetAsync(ws, 0, (size_t)l.total, st);
+    if (wsoff + (size_t)l.total > ws_bytes) return cudaErrorInvalidValue;
+    char* gws = static_cast<char*>(ws) + wsoff;
+    if (session) wsoff += (size_t)l.total;
+    cudaError_t e = cudaSuccess;
+    if (!session || a.n0 == 0) e = cudaMemsetAsync(gws, 0, (size_t)l.total, st);
     if (e != cudaSuccess) return e;
     BParams P{};
     P.a = a;
@@ -891,7 +912,7 @@ cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void
     P.hr_off = p.hr_off; P.hr_floats = p.hr_floats;
     P.ho_off = p.ho_off; P.ho_floats = p.ho_floats;
     P.bias_off = p.bias_off;
-    char* base = static_cast<char*>(ws);
+    char* base = gws;
     for (int q = 0; q < 2; ++q) {
       P.hb[q] = reinterpret_cast<float*>(base + l.hb[q]);
     }

@@ -43,9 +43,15 @@ BatchPlan plan_batch(int L, int r, int s, int device);
 cudaError_t pack_batch_weights(const BatchPlan& p, const float* host_blob, const Offsets& o, void* packed);
 // Workspace for `nsb` stream blocks with dilations `dil` (host array, length L).
 size_t batch_workspace_bytes(const BatchPlan& p, const int32_t* dil, int nsb);
+// Workspace a streaming session keeps for n_streams: one region per launch group.
+size_t batch_session_bytes(const BatchPlan& p, const int32_t* dil, int n_streams);
 // Runs n_streams (any count; groups of max_sb * 128 run back to back on `st`).
 // fast: one tf32 pass (DVW_PRECISION_TF32) instead of the fp32-faithful split.
+// session: `ws` holds every group's region (batch_session_bytes), zeroed only when a.n0 == 0,
+// and the kernel continues from the queues and code history left there (global index a.n0 + n);
+// otherwise all groups share one region, zeroed per launch.
 cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void* packed, void* ws, size_t ws_bytes,
-                                const int32_t* dil_host, bool fast, cudaStream_t st, LaunchInfo* info);
+                                const int32_t* dil_host, bool fast, cudaStream_t st, LaunchInfo* info,
+                                bool session = false);
 
 }  // namespace dvw

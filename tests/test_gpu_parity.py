@@ -534,6 +534,48 @@ def test_streaming_session_chunks_equal_one_shot(L, kernel, cfg):
     assert e.value.name == "DVW_E_SHAPE"
 
 
+@pytest.mark.parametrize("cfg,S,N", [(synth.C1, 3, 1600), (synth.Config(2, 64, 128), 2100, 160)],
+                         ids=["C1x3", "l2x2100-two-launch-groups"])
+def test_tc_streaming_session_chunks_equal_one_shot(L, cfg, S, N):
+    """Batched (TC) streaming sessions: the session keeps every launch group's workspace
+    (queues, x^(0), code history); chunks give bitwise the codes of one call, and the oracle's."""
+    hop = 64
+    w = synth.make_weights(cfg, 0)
+    cond = dev(np.stack([synth.make_cond(cfg, synth.n_frames_for(N, hop), s) for s in (0, 1, S - 1)]))
+    cond = cond[torch.tensor([0] + [1] * (S - 2) + [2], device=cond.device)].contiguous()
+    u = dev(np.stack([synth.make_uniforms(N, s) for s in range(S)]))
+    m = L.Model.from_config(cfg).load(w)
+    try:
+        m.set_kernel("tc")
+    except L.DvwError as e:
+        pytest.skip(str(e))
+    one = m.generate(cond, u, hop).cpu().numpy()
+    m.set_kernel("auto")
+    sess = m.session(S)
+    cuts = [1, 63, N // 3, N - 64 - N // 3]
+    cuts.append(N - sum(cuts))
+    parts, pos = [], 0
+    for i, n in enumerate(cuts):
+        parts.append(sess.generate(cond, u[:, pos:pos + n].contiguous(), hop).cpu().numpy())
+        pos += n
+        assert sess.position == pos
+        if i == 1:  # the session's state is laid out for the TC kernel
+            m.set_kernel("stream")
+            with pytest.raises(L.DvwError) as e:
+                sess.generate(cond, u[:, pos:pos + 1].contiguous(), hop)
+            assert e.value.name == "DVW_E_STATE"
+            assert sess.position == pos
+            m.set_kernel("auto")
+    info = m.info()
+    assert info["last_kernel_name"] == "tc"
+    print(f"TC session {S} streams: {info['last_launches']} launch group(s) per call")
+    assert np.array_equal(np.concatenate(parts, axis=1), one)
+    for st in (0, S - 1):
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[st].cpu().numpy(), hop, N,
+                               uniforms=u[st].cpu().numpy(), want_logits=False)
+        assert np.array_equal(one[st], ref), st
+
+
 @pytest.mark.parametrize("kernel", ["stream", "cluster", "tc", "parallel"])
 @pytest.mark.parametrize("case", [
     dict(shape=(1, 64, 256), dil=None, N=70, hop=1),          # a single layer, upsampled cond (hop 1)
