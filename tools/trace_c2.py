@@ -13,7 +13,7 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("DVW_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1702_07825_b200 import synth  # noqa: E402
 from paper_1702_07825_b200._lib import Model  # noqa: E402
 
