@@ -602,3 +602,47 @@ def test_edge_shapes_teacher_forced_all_kernels(L, kernel, case):
         codes = m.generate(dev(cond)[None], dev(u)[None], hop).cpu().numpy()[0]
         ref, _, _ = oracle.run(l, r, s, w, cond, hop, N, uniforms=u, dilations=cfg.dilation_list(), want_logits=False)
         assert np.array_equal(codes, ref)
+
+
+# ------------------------------------------------------------------ BASELINE.json full sizes
+def test_c2_full_utterance_cluster_bench_config(L):
+    """C2 at the bench's full size (16,000 samples = 1 s, one cluster launch): every code equal
+    to the oracle's (the bench reports the same), teacher-forced logits fp32-faithful on a
+    window at the end of the utterance (oracle teacher-forced over the whole prefix)."""
+    cfg = synth.C2
+    N, hop = 16000, 64
+    w = synth.make_weights(cfg, 0)
+    cond = synth.make_cond(cfg, synth.n_frames_for(N, hop), 0)
+    u = synth.make_uniforms(N, 0)
+    m = L.Model.from_config(cfg).load(w).set_kernel("cluster")
+    codes = m.generate(dev(cond)[None], dev(u)[None], hop).cpu().numpy()[0]
+    _, ref_lg, sampled = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, N, uniforms=u,
+                                    forced=codes, want_sampled=True)
+    mism = int(np.sum(sampled != codes))
+    print(f"C2 16,000 samples: per-step mismatches {mism}")
+    assert np.array_equal(sampled[:1600], codes[:1600]) and mism <= 16
+    lg = m.set_kernel("parallel").logits(dev(cond)[None], dev(codes)[None], hop).cpu().numpy()[0]
+    win = slice(N - 64, N)
+    assert float(np.max(np.abs(lg[win].astype(np.float64) - ref_lg[win]))) <= FP32_FAITHFUL
+    assert float(np.max(np.abs(lg.astype(np.float64) - ref_lg))) <= FP32_FAITHFUL
+
+
+@pytest.mark.parametrize("cfg,S,N,check", [(synth.C4, 256, 2000, (0, 129, 255)),
+                                           (synth.C5, 2048, 600, (0, 895, 896, 2047))],
+                         ids=["C4-256-streams", "C5-2048-streams"])
+def test_tc_full_stream_counts_bench_launch_config(L, cfg, S, N, check):
+    """The batched workloads at BASELINE.json's stream counts, in the launch configuration the
+    bench times (C4: 2 clusters of 16 CTAs; C5: 896 streams per launch, 3 launch groups):
+    sampled streams equal the oracle code for code (free running)."""
+    hop = 64
+    w = synth.make_weights(cfg, 0)
+    cond, u = synth.make_batch(cfg, N, list(range(S)), hop)
+    m = L.Model.from_config(cfg).load(w)
+    codes = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    info = m.info()
+    assert info["last_kernel_name"] == "tc"
+    print(f"{cfg}: {S} streams, grid {info['last_grid']} x cluster {info['last_cluster']}, "
+          f"{info['last_launches']} launch(es)")
+    for i in check:
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[i], hop, N, uniforms=u[i])
+        assert np.array_equal(codes[i], ref), i
