@@ -33,6 +33,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cstdlib>
+
 #include "kernel_cluster.cuh"
 #include "ptx.cuh"
 
@@ -1213,6 +1215,11 @@ ClusterPlan plan_lp(int L, int r, int s, int device, int lp) {
 // 3 layers per chain CTA (every weight of the chain in tensor memory) when the model fits
 // one cluster that way with no chain-skip layers; else 4 (W_res in shared memory).
 ClusterPlan plan_cluster(int L, int r, int s, int device) {
+  // tuning override for A/B measurements (tools/sweep_layers.py): DVW_CLUSTER_LP=3|4
+  if (const char* e = std::getenv("DVW_CLUSTER_LP")) {
+    const int lp = std::atoi(e);
+    if (lp == 3 || lp == 4) return plan_lp(L, r, s, device, lp);
+  }
   ClusterPlan p3 = plan_lp(L, r, s, device, 3);
   if (p3.ok && p3.nxs == 0) return p3;
   ClusterPlan p4 = plan_lp(L, r, s, device, 4);
