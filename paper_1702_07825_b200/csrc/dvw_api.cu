@@ -65,6 +65,8 @@ struct dvw_model {
   void* d_bws = nullptr;      // batched-kernel workspace (activations, queues, barrier)
   size_t bws_bytes = 0;
   void* d_pws = nullptr;      // parallel teacher-forced workspace (x, x', q for a group of streams)
+  void* d_ptc = nullptr;      // parallel teacher-forced: tensor-core layer images (r = 64)
+  size_t ptc_bytes = 0;
   size_t pws_bytes = 0;
   // host-call staging
   void* d_stage = nullptr;
@@ -295,7 +297,7 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
       G.cond = cond + (int64_t)g0 * n_frames * m->L * 2 * m->r;
       G.forced = forced + (int64_t)g0 * n_samples;
       G.out_logits = out_logits + (int64_t)g0 * n_samples * kLevels;
-      e = launch_parallel_logits(G, m->d_pws, cs, &li);
+      e = launch_parallel_logits(G, m->d_pws, cs, &li, static_cast<const float*>(m->d_ptc));
       launches += li.launches;
     }
     li.launches = launches;
@@ -440,6 +442,19 @@ DVW_API dvw_status dvw_load_weights(dvw_model* m, const float* blob, int64_t num
       m->packed_bytes = need;
     }
     DVW_CUDA(pack_cluster_weights(m->cplan, hp, m->off, m->d_packed), "packing weights");
+    wb += (int64_t)need;
+  }
+  if (m->r == 64) {  // tensor-core images for the parallel teacher-forced layers
+    const size_t need = sizeof(float) * (size_t)parallel_tc_packed_floats(m->L, m->s);
+    if (m->d_ptc && m->ptc_bytes < need) {
+      cudaFree(m->d_ptc);
+      m->d_ptc = nullptr;
+    }
+    if (!m->d_ptc) {
+      DVW_CUDA(cudaMalloc(&m->d_ptc, need), "allocating tensor-core layer images");
+      m->ptc_bytes = need;
+    }
+    DVW_CUDA(pack_parallel_tc(hp, m->off, m->L, m->r, m->s, m->d_ptc), "packing tensor-core layer images");
     wb += (int64_t)need;
   }
   if (m->bplan.ok) {
@@ -632,6 +647,7 @@ DVW_API void dvw_destroy(dvw_model* m) {
   cudaFree(m->d_bpacked);
   cudaFree(m->d_bws);
   cudaFree(m->d_pws);
+  cudaFree(m->d_ptc);
   cudaFree(m->d_stage);
   delete m;
 }

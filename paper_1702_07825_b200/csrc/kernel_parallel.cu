@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kPT, 2) k_head(RunArgs A, const float* Q) {
 }
 
 template <int R, int S>
-cudaError_t run_rs(const RunArgs& a, float* ws, cudaStream_t st, LaunchInfo* info) {
+cudaError_t run_rs(const RunArgs& a, float* ws, cudaStream_t st, LaunchInfo* info, const float* pk_tc) {
   const int64_t T = a.N, nS = a.n_streams;
   float* X[2] = {ws, ws + nS * T * R};
   float* Q = ws + 2 * nS * T * R;
@@ -295,8 +295,10 @@ cudaError_t run_rs(const RunArgs& a, float* ws, cudaStream_t st, LaunchInfo* inf
   const dim3 grid((unsigned)((T + kTile - 1) / kTile), (unsigned)nS);
   const int lsm = (int)sizeof(float) * (3 * R * kTile + kKC * std::max(2 * R, S));
   cudaError_t e = cudaFuncSetAttribute(k_layer<R, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, lsm);
-  for (int j = 0; e == cudaSuccess && j < a.L; ++j)
-    k_layer<R, S><<<grid, kPT, lsm, st>>>(a, j, X[j & 1], X[(j + 1) & 1], Q);
+  for (int j = 0; e == cudaSuccess && j < a.L; ++j) {
+    if (R == 64 && pk_tc) e = launch_parallel_layer_tc(a, j, X[j & 1], X[(j + 1) & 1], Q, pk_tc, st);
+    else k_layer<R, S><<<grid, kPT, lsm, st>>>(a, j, X[j & 1], X[(j + 1) & 1], Q);
+  }
   const int hsm = (int)sizeof(float) * ((S + kLevels) * kTile + kKC * kLevels);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_head<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
   if (e == cudaSuccess) k_head<S><<<grid, kPT, hsm, st>>>(a, Q);
@@ -314,14 +316,15 @@ size_t parallel_workspace_bytes(int r, int s, int64_t n_samples, int n_streams) 
   return sizeof(float) * (size_t)n_streams * (size_t)n_samples * (size_t)(2 * r + s);
 }
 
-cudaError_t launch_parallel_logits(const RunArgs& a, void* ws, cudaStream_t st, LaunchInfo* info) {
+cudaError_t launch_parallel_logits(const RunArgs& a, void* ws, cudaStream_t st, LaunchInfo* info,
+                                   const float* pk_tc) {
   float* w = static_cast<float*>(ws);
-  if (a.r == 32 && a.s == 128) return run_rs<32, 128>(a, w, st, info);
-  if (a.r == 32 && a.s == 256) return run_rs<32, 256>(a, w, st, info);
-  if (a.r == 64 && a.s == 128) return run_rs<64, 128>(a, w, st, info);
-  if (a.r == 64 && a.s == 256) return run_rs<64, 256>(a, w, st, info);
-  if (a.r == 128 && a.s == 128) return run_rs<128, 128>(a, w, st, info);
-  if (a.r == 128 && a.s == 256) return run_rs<128, 256>(a, w, st, info);
+  if (a.r == 32 && a.s == 128) return run_rs<32, 128>(a, w, st, info, nullptr);
+  if (a.r == 32 && a.s == 256) return run_rs<32, 256>(a, w, st, info, nullptr);
+  if (a.r == 64 && a.s == 128) return run_rs<64, 128>(a, w, st, info, pk_tc);
+  if (a.r == 64 && a.s == 256) return run_rs<64, 256>(a, w, st, info, pk_tc);
+  if (a.r == 128 && a.s == 128) return run_rs<128, 128>(a, w, st, info, nullptr);
+  if (a.r == 128 && a.s == 256) return run_rs<128, 256>(a, w, st, info, nullptr);
   return cudaErrorNotSupported;
 }
 

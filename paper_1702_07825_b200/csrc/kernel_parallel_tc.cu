@@ -1,0 +1,298 @@
+// kernel_parallel_tc.cu -- the teacher-forced layer pass of dvw_logits on the tensor cores
+// (r = 64; the SIMT k_layer in kernel_parallel.cu serves the other widths).
+//
+// Same arithmetic as k_layer (SURVEY.md §8(a) a3-a7 for all timesteps
+// of a layer at once, codes given), per 128-timestep tile (M = 128, TMEM lane = timestep):
+//   GEMM 1  a[t][0:2r] = [W_prev | W_cur] [x_j(t-d); x_j(t)]       K = 2r = 128 in two 64-chunks
+//   gate    h = tanh(a_0:r + B + L) sigma(a_r:2r + B + L)            (epilogue, thread = timestep)
+//   GEMM 2  [x_{j+1} - x_j - B_res ; dq] = [W_res ; W_skip] h        K = r = 64, N = r + s rows in
+//                                                                      chunks of <= 128 rows
+// fp32-faithful on the tf32 pipe (reading R23): each operand x is split into x (the MMA reads
+// its tf32 head) and lo = x - tf32(x); per K-step of 8: D[:, 0:2N) += A_hi [W_hi; W_lo]^T and
+// D[:, 0:N) += A_lo W_hi^T, the epilogue adds column c and c + N (the dropped lo lo term is
+// <= 2^-22 relative).  Operands in shared memory in the K-major core-matrix order (umma.cuh):
+// activations written by the threads (with their lo halves), weight chunks pre-packed at load
+// time and fetched with one bulk copy each.  One elected thread issues the MMAs.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "dvw_internal.cuh"
+#include "ptx.cuh"
+#include "umma.cuh"
+
+namespace dvw {
+namespace {
+
+constexpr int R = 64;            // residual channels this kernel is built for
+constexpr int kTM = 128;         // timesteps per tile (= MMA M = TMEM lanes)
+constexpr int kThr = 128;        // one thread per timestep
+constexpr int kActF = 16 * kTM * 4;  // one 64-channel activation operand [16][128][4] (floats)
+constexpr int kW1F = 16 * 256 * 4;   // one GEMM-1 weight chunk: 64 K x (128 hi + 128 lo rows)
+
+// floats of one layer's packed weights: two GEMM-1 chunks, then GEMM-2 chunks of [16][2n][4]
+__host__ __device__ constexpr int64_t tc_layer_floats(int s) { return 2 * kW1F + 128 * (R + s); }
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// mbarrier wait with a 2 s watchdog: a lost completion traps (the launch fails with an error
+// the host reports) instead of hanging the device.
+__device__ __forceinline__ void wait_bar(uint32_t bar, uint32_t parity) {
+  if (ptx::mbar_try_wait_cta(bar, parity)) return;
+  const uint64_t t0 = ptx::globaltimer();
+  while (!ptx::mbar_try_wait_cta(bar, parity))
+    if (ptx::globaltimer() - t0 > 2000000000ull) asm volatile("trap;");
+}
+
+// Rows t0 - shift + i (zero outside [0, T)) of X [T][64] into the operand pair (hi, lo).
+__device__ __forceinline__ void stage_rows(float* hi, float* lo, const float* X, int T, int t0, int shift) {
+  for (int idx = threadIdx.x; idx < kTM * 16; idx += kThr) {
+    const int i = idx % kTM, g = idx / kTM, tg = t0 - shift + i;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tg >= 0 && tg < T) v = __ldg(reinterpret_cast<const float4*>(X + (int64_t)tg * R + 4 * g));
+    const int o = (g * kTM + i) * 4;
+    *reinterpret_cast<float4*>(hi + o) = v;
+    *reinterpret_cast<float4*>(lo + o) = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+  }
+}
+
+struct Sync {
+  uint32_t bar_w, bar_m;
+  uint32_t ph_w = 0, ph_m = 0;
+};
+
+// D[:, 0:2n) = / += A (K = 64, operand pair at a_hi/a_lo) times the staged weight chunk
+// (n real rows + their n lo rows), then wait for it.  Thread 0 issues; everybody waits.
+__device__ __forceinline__ void mma_chunk(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t wsm, int n, bool acc,
+                                          Sync& sy) {
+  if (threadIdx.x == 0) {
+    wait_bar(sy.bar_w, sy.ph_w);
+    ptx::tmem_fence_after();
+    const uint32_t id2 = idesc_tf32(2 * n), id1 = idesc_tf32(n);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const uint32_t ao = ks * 2 * kTM * 16, bo = ks * 2 * (2 * n) * 16;
+      const uint64_t dah = sdesc(a_hi + ao, kTM * 16, 128), dal = sdesc(a_lo + ao, kTM * 16, 128);
+      const uint64_t db = sdesc(wsm + bo, 2 * n * 16, 128);
+      mma_tf32(d, dah, db, id2, (acc || ks > 0) ? 1u : 0u);
+      mma_tf32(d, dal, db, id1, 1u);
+    }
+    mma_commit(sy.bar_m);
+  }
+  sy.ph_w ^= 1;
+  wait_bar(sy.bar_m, sy.ph_m);
+  sy.ph_m ^= 1;
+  ptx::tmem_fence_after();
+}
+
+__device__ __forceinline__ void fetch_w(uint32_t wsm, const float* src, int floats, const Sync& sy) {
+  if (threadIdx.x == 0) {
+    ptx::mbar_arm(sy.bar_w, (uint32_t)floats * 4);
+    bulk_g2s(wsm, src, (uint32_t)floats * 4, sy.bar_w);
+  }
+}
+
+// TMEM reads of this thread's lane must be complete before the next MMA overwrites D.
+__device__ __forceinline__ void release_tmem() {
+  ptx::tmem_fence_before();
+  __syncthreads();
+}
+
+template <int S>
+__global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const float* Xin, float* Xout, float* Q,
+                                                      const float* pk) {
+  extern __shared__ __align__(1024) float sm[];
+  float* a_hi = sm;            // [16][128][4]
+  float* a_lo = sm + kActF;    // [16][128][4]
+  float* wsm = sm + 2 * kActF; // one weight chunk, <= [16][256][4]
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ uint32_t tmem_base;
+  const int t = threadIdx.x, st = blockIdx.y, t0 = blockIdx.x * kTM;
+  const int T = (int)A.N;
+  const int tg = t0 + t;
+  const int64_t lo = (int64_t)j * A.off.layer_stride;
+  const float* xin = Xin + (int64_t)st * T * R;
+  const float* pl = pk + (int64_t)j * tc_layer_floats(S);
+  if (t < 32) ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 256);
+  Sync sy;
+  sy.bar_w = ptx::smem_u32(&bars[0]);
+  sy.bar_m = ptx::smem_u32(&bars[1]);
+  if (t == 0) {
+    ptx::mbar_init(sy.bar_w, 1);
+    ptx::mbar_init(sy.bar_m, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  ptx::tmem_fence_before();
+  __syncthreads();
+  ptx::tmem_fence_after();
+  const uint32_t d = tmem_base;
+  const uint32_t s_hi = ptx::smem_u32(a_hi), s_lo = ptx::smem_u32(a_lo), s_w = ptx::smem_u32(wsm);
+  const uint32_t lane_addr = d + ((uint32_t)(32 * (t >> 5)) << 16);
+
+  // ---- GEMM 1: chunk 0 = W_prev with x_j(t - d), chunk 1 = W_cur with x_j(t); each weight
+  //      bulk copy overlaps the staging of the activations
+  const float* w2 = pl + 2 * kW1F;
+  for (int kc = 0; kc < 2; ++kc) {
+    fetch_w(s_w, pl + kc * kW1F, kW1F, sy);
+    stage_rows(a_hi, a_lo, xin, T, t0, kc == 0 ? A.dil[j] : 0);
+    fence_proxy_async_smem();
+    __syncthreads();
+    mma_chunk(d, s_hi, s_lo, s_w, 128, kc > 0, sy);
+  }
+  fetch_w(s_w, w2, 16 * 2 * 128 * 4, sy);  // GEMM 2's first chunk, during the gate
+  // ---- gate: + B + L(t / hop); h -> operand pair for GEMM 2
+  const float* bj = A.w + lo + A.off.b;
+  const float* L = A.cond + (((int64_t)st * A.n_frames + (tg < T ? tg : 0) / A.hop) * A.L + j) * 2 * R;
+#pragma unroll 1
+  for (int cc = 0; cc < 4; ++cc) {  // channels 16 cc .. 16 cc + 15
+    float ah[16], ah2[16], ag[16], ag2[16];
+    ptx::tmem_ld16(lane_addr + 16 * cc, ah);
+    ptx::tmem_ld16(lane_addr + 128 + 16 * cc, ah2);
+    ptx::tmem_ld16(lane_addr + 64 + 16 * cc, ag);
+    ptx::tmem_ld16(lane_addr + 192 + 16 * cc, ag2);
+    ptx::tmem_wait_ld<16>(ah);
+    ptx::tmem_wait_ld<16>(ah2);
+    ptx::tmem_wait_ld<16>(ag);
+    ptx::tmem_wait_ld<16>(ag2);
+    float h[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int c = 16 * cc + e;
+      const float lh = tg < T ? __ldg(L + c) : 0.0f, lg = tg < T ? __ldg(L + R + c) : 0.0f;
+      const float xh = (ah[e] + ah2[e]) + __ldg(bj + c) + lh;
+      const float xg = (ag[e] + ag2[e]) + __ldg(bj + R + c) + lg;
+      h[e] = A.approx == 0 ? gate(xh, xg) : A.approx == 1 ? gate_approx(xh, xg) : gate_appc(xh, xg);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int o = ((4 * cc + q) * kTM + t) * 4;
+      const float4 v = make_float4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+      *reinterpret_cast<float4*>(a_hi + o) = v;
+      *reinterpret_cast<float4*>(a_lo + o) = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+    }
+  }
+  ptx::tmem_fence_before();  // GEMM 2 overwrites D after every lane has read it
+  fence_proxy_async_smem();
+  __syncthreads();
+  // ---- GEMM 2: rows [W_res (64); W_skip (S)] in chunks of <= 128 rows; the next chunk's
+  //      bulk copy overlaps this chunk's epilogue
+  const float* bres = A.w + lo + A.off.b_res;
+  float* xout = Xout + (int64_t)st * T * R;
+  float* q = Q + (int64_t)st * T * S;
+  int r0 = 0;
+#pragma unroll 1
+  for (int ci = 0; r0 < R + S; ++ci) {
+    const int n = std::min(128, R + S - r0);
+    mma_chunk(d, s_hi, s_lo, s_w, n, false, sy);
+    if (r0 + n < R + S) fetch_w(s_w, w2 + 16 * 2 * n * 4, 16 * 2 * std::min(128, R + S - r0 - n) * 4, sy);
+#pragma unroll 1
+    for (int nb = 0; nb < n; nb += 16) {
+      float v[16], v2[16];
+      ptx::tmem_ld16(lane_addr + nb, v);
+      ptx::tmem_ld16(lane_addr + n + nb, v2);
+      ptx::tmem_wait_ld<16>(v);
+      ptx::tmem_wait_ld<16>(v2);
+      if (tg < T) {
+        const int row = r0 + nb;  // 16 rows, all on one side of R (R and 128 are multiples of 16)
+        if (row < R) {  // x_{j+1} = x_j + W_res h + B_res
+          const float* xr = xin + (int64_t)tg * R + row;
+          float* xo = xout + (int64_t)tg * R + row;
+#pragma unroll
+          for (int e = 0; e < 16; e += 4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(xr + e));
+            *reinterpret_cast<float4*>(xo + e) =
+                make_float4(x.x + ((v[e] + v2[e]) + __ldg(bres + row + e)),
+                            x.y + ((v[e + 1] + v2[e + 1]) + __ldg(bres + row + e + 1)),
+                            x.z + ((v[e + 2] + v2[e + 2]) + __ldg(bres + row + e + 2)),
+                            x.w + ((v[e + 3] + v2[e + 3]) + __ldg(bres + row + e + 3)));
+          }
+        } else {  // q += W_skip h
+          float* qq = q + (int64_t)tg * S + (row - R);
+#pragma unroll
+          for (int e = 0; e < 16; e += 4) {
+            float4 a = *reinterpret_cast<float4*>(qq + e);
+            a.x += v[e] + v2[e];
+            a.y += v[e + 1] + v2[e + 1];
+            a.z += v[e + 2] + v2[e + 2];
+            a.w += v[e + 3] + v2[e + 3];
+            *reinterpret_cast<float4*>(qq + e) = a;
+          }
+        }
+      }
+    }
+    release_tmem();
+    w2 += 16 * 2 * n * 4;
+    r0 += n;
+  }
+  if (t < 32) ptx::tmem_dealloc(d, 256);
+}
+
+}  // namespace
+
+int64_t parallel_tc_packed_floats(int L, int s) { return (int64_t)L * tc_layer_floats(s); }
+
+// [K/4][rows][4] operand images of every layer (host, once per dvw_load_weights): GEMM-1
+// chunks kc = 0 (W_prev) and 1 (W_cur), each 128 rows of the weight and 128 rows of its
+// tf32 residual; then GEMM-2 chunks of <= 128 rows of [W_res; W_skip] and their residuals.
+cudaError_t pack_parallel_tc(const float* w, const Offsets& o, int L, int r, int s, void* dst) {
+  if (r != R) return cudaErrorInvalidValue;
+  auto lo_of = [](float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u &= 0xFFFFE000u;
+    float h;
+    std::memcpy(&h, &u, 4);
+    return x - h;
+  };
+  const int64_t per = tc_layer_floats(s);
+  std::vector<float> h((size_t)(L * per), 0.0f);
+  for (int j = 0; j < L; ++j) {
+    const float* lw = w + (int64_t)j * o.layer_stride;
+    float* out = h.data() + (int64_t)j * per;
+    for (int kc = 0; kc < 2; ++kc) {
+      const float* W = lw + (kc == 0 ? o.w_prev : o.w_cur);  // [2R][R]
+      float* c = out + kc * kW1F;
+      for (int k = 0; k < R; ++k)
+        for (int n = 0; n < 2 * R; ++n) {
+          const float v = W[(int64_t)n * R + k];
+          c[((k / 4) * 256 + n) * 4 + k % 4] = v;
+          c[((k / 4) * 256 + 128 + n) * 4 + k % 4] = lo_of(v);
+        }
+    }
+    float* c = out + 2 * kW1F;
+    for (int r0 = 0; r0 < R + s;) {
+      const int n = std::min(128, R + s - r0);
+      for (int k = 0; k < R; ++k)
+        for (int i = 0; i < n; ++i) {
+          const int row = r0 + i;
+          const float v = row < R ? lw[o.w_res + (int64_t)row * R + k] : lw[o.w_skip + (int64_t)(row - R) * R + k];
+          c[((k / 4) * 2 * n + i) * 4 + k % 4] = v;
+          c[((k / 4) * 2 * n + n + i) * 4 + k % 4] = lo_of(v);
+        }
+      c += 16 * 2 * n * 4;
+      r0 += n;
+    }
+  }
+  return cudaMemcpy(dst, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice);
+}
+
+cudaError_t launch_parallel_layer_tc(const RunArgs& a, int j, const float* xin, float* xout, float* q,
+                                     const float* pk, cudaStream_t st) {
+  const dim3 grid((unsigned)((a.N + kTM - 1) / kTM), (unsigned)a.n_streams);
+  const int smem = (int)sizeof(float) * (2 * kActF + kW1F);
+  cudaError_t e;
+  if (a.s == 256) {
+    e = cudaFuncSetAttribute(k_layer_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) k_layer_tc<256><<<grid, kThr, smem, st>>>(a, j, xin, xout, q, pk);
+  } else if (a.s == 128) {
+    e = cudaFuncSetAttribute(k_layer_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) k_layer_tc<128><<<grid, kThr, smem, st>>>(a, j, xin, xout, q, pk);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
+}  // namespace dvw
