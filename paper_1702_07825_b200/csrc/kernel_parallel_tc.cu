@@ -29,6 +29,8 @@ constexpr int kTM = 128;         // timesteps per tile (= MMA M = TMEM lanes)
 constexpr int kThr = 128;        // one thread per timestep
 constexpr int kActF = 16 * kTM * 4;  // one 64-channel activation operand [16][128][4] (floats)
 constexpr int kW1F = 16 * 256 * 4;   // one GEMM-1 weight chunk: 64 K x (128 hi + 128 lo rows)
+constexpr int kLBP = 2 * R + 1;      // padded row of the per-timestep (L + B) table
+constexpr int kSmemF = 2 * kActF + kW1F + kTM * kLBP;
 
 // floats of one layer's packed weights: two GEMM-1 chunks, then GEMM-2 chunks of [16][2n][4]
 __host__ __device__ constexpr int64_t tc_layer_floats(int s) { return 2 * kW1F + 128 * (R + s); }
@@ -47,14 +49,20 @@ __device__ __forceinline__ void wait_bar(uint32_t bar, uint32_t parity) {
 }
 
 // Rows t0 - shift + i (zero outside [0, T)) of X [T][64] into the operand pair (hi, lo).
+// Thread i loads its own row (16 float4, all in flight at once), then writes the 16 groups.
 __device__ __forceinline__ void stage_rows(float* hi, float* lo, const float* X, int T, int t0, int shift) {
-  for (int idx = threadIdx.x; idx < kTM * 16; idx += kThr) {
-    const int i = idx % kTM, g = idx / kTM, tg = t0 - shift + i;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (tg >= 0 && tg < T) v = __ldg(reinterpret_cast<const float4*>(X + (int64_t)tg * R + 4 * g));
+  const int i = threadIdx.x, tg = t0 - shift + i;
+  float4 v[16];
+  const bool in = tg >= 0 && tg < T;
+  const float4* src = reinterpret_cast<const float4*>(X + (int64_t)(in ? tg : 0) * R);
+#pragma unroll
+  for (int g = 0; g < 16; ++g) v[g] = in ? __ldg(src + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int g = 0; g < 16; ++g) {
     const int o = (g * kTM + i) * 4;
-    *reinterpret_cast<float4*>(hi + o) = v;
-    *reinterpret_cast<float4*>(lo + o) = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+    *reinterpret_cast<float4*>(hi + o) = v[g];
+    *reinterpret_cast<float4*>(lo + o) =
+        make_float4(tf32_lo(v[g].x), tf32_lo(v[g].y), tf32_lo(v[g].z), tf32_lo(v[g].w));
   }
 }
 
@@ -107,6 +115,7 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
   float* a_hi = sm;            // [16][128][4]
   float* a_lo = sm + kActF;    // [16][128][4]
   float* wsm = sm + 2 * kActF; // one weight chunk, <= [16][256][4]
+  float* lb = wsm + kW1F;      // [128][2R + 1]: L^(j)(t / hop) + B for this thread's timestep
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ uint32_t tmem_base;
   const int t = threadIdx.x, st = blockIdx.y, t0 = blockIdx.x * kTM;
@@ -130,6 +139,20 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
   const uint32_t d = tmem_base;
   const uint32_t s_hi = ptx::smem_u32(a_hi), s_lo = ptx::smem_u32(a_lo), s_w = ptx::smem_u32(wsm);
   const uint32_t lane_addr = d + ((uint32_t)(32 * (t >> 5)) << 16);
+  const float* bj = A.w + lo + A.off.b;
+  {  // the gate's addend row, loaded while GEMM 1 runs (each thread reads back only its own row)
+    const float* Lr = A.cond + (((int64_t)st * A.n_frames + (tg < T ? tg : 0) / A.hop) * A.L + j) * 2 * R;
+#pragma unroll 8
+    for (int c = 0; c < 2 * R; c += 4) {
+      const float4 lv = tg < T ? __ldg(reinterpret_cast<const float4*>(Lr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 bv = __ldg(reinterpret_cast<const float4*>(bj + c));
+      float* o = lb + t * kLBP + c;
+      o[0] = bv.x + lv.x;
+      o[1] = bv.y + lv.y;
+      o[2] = bv.z + lv.z;
+      o[3] = bv.w + lv.w;
+    }
+  }
 
   // ---- GEMM 1: chunk 0 = W_prev with x_j(t - d), chunk 1 = W_cur with x_j(t); each weight
   //      bulk copy overlaps the staging of the activations
@@ -143,8 +166,6 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
   }
   fetch_w(s_w, w2, 16 * 2 * 128 * 4, sy);  // GEMM 2's first chunk, during the gate
   // ---- gate: + B + L(t / hop); h -> operand pair for GEMM 2
-  const float* bj = A.w + lo + A.off.b;
-  const float* L = A.cond + (((int64_t)st * A.n_frames + (tg < T ? tg : 0) / A.hop) * A.L + j) * 2 * R;
 #pragma unroll 1
   for (int cc = 0; cc < 4; ++cc) {  // channels 16 cc .. 16 cc + 15
     float ah[16], ah2[16], ag[16], ag2[16];
@@ -160,9 +181,8 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       const int c = 16 * cc + e;
-      const float lh = tg < T ? __ldg(L + c) : 0.0f, lg = tg < T ? __ldg(L + R + c) : 0.0f;
-      const float xh = (ah[e] + ah2[e]) + __ldg(bj + c) + lh;
-      const float xg = (ag[e] + ag2[e]) + __ldg(bj + R + c) + lg;
+      const float xh = (ah[e] + ah2[e]) + lb[t * kLBP + c];
+      const float xg = (ag[e] + ag2[e]) + lb[t * kLBP + R + c];
       h[e] = A.approx == 0 ? gate(xh, xg) : A.approx == 1 ? gate_approx(xh, xg) : gate_appc(xh, xg);
     }
 #pragma unroll
@@ -185,39 +205,51 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
 #pragma unroll 1
   for (int ci = 0; r0 < R + S; ++ci) {
     const int n = std::min(128, R + S - r0);
+    const bool live = tg < T;
+    const int tr = live ? tg : 0;
+    // the addends of this chunk's rows (x_j for rows < R, the running q above), in flight
+    // while the MMAs run
+    float4 base[8][4];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      if (16 * g < n) {
+        const int row = r0 + 16 * g;  // 16 rows, all on one side of R
+        const float4* src = row < R ? reinterpret_cast<const float4*>(xin + (int64_t)tr * R + row)
+                                    : reinterpret_cast<const float4*>(q + (int64_t)tr * S + (row - R));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) base[g][e] = row < R ? __ldg(src + e) : src[e];
+      }
+    }
     mma_chunk(d, s_hi, s_lo, s_w, n, false, sy);
     if (r0 + n < R + S) fetch_w(s_w, w2 + 16 * 2 * n * 4, 16 * 2 * std::min(128, R + S - r0 - n) * 4, sy);
-#pragma unroll 1
-    for (int nb = 0; nb < n; nb += 16) {
-      float v[16], v2[16];
-      ptx::tmem_ld16(lane_addr + nb, v);
-      ptx::tmem_ld16(lane_addr + n + nb, v2);
-      ptx::tmem_wait_ld<16>(v);
-      ptx::tmem_wait_ld<16>(v2);
-      if (tg < T) {
-        const int row = r0 + nb;  // 16 rows, all on one side of R (R and 128 are multiples of 16)
-        if (row < R) {  // x_{j+1} = x_j + W_res h + B_res
-          const float* xr = xin + (int64_t)tg * R + row;
-          float* xo = xout + (int64_t)tg * R + row;
 #pragma unroll
-          for (int e = 0; e < 16; e += 4) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(xr + e));
-            *reinterpret_cast<float4*>(xo + e) =
-                make_float4(x.x + ((v[e] + v2[e]) + __ldg(bres + row + e)),
-                            x.y + ((v[e + 1] + v2[e + 1]) + __ldg(bres + row + e + 1)),
-                            x.z + ((v[e + 2] + v2[e + 2]) + __ldg(bres + row + e + 2)),
-                            x.w + ((v[e + 3] + v2[e + 3]) + __ldg(bres + row + e + 3)));
-          }
-        } else {  // q += W_skip h
-          float* qq = q + (int64_t)tg * S + (row - R);
+    for (int g = 0; g < 8; ++g) {
+      if (16 * g < n) {
+        const int row = r0 + 16 * g;
+        float v[16], v2[16];
+        ptx::tmem_ld16(lane_addr + 16 * g, v);
+        ptx::tmem_ld16(lane_addr + n + 16 * g, v2);
+        ptx::tmem_wait_ld<16>(v);
+        ptx::tmem_wait_ld<16>(v2);
+        if (live) {
+          float4* dst = row < R ? reinterpret_cast<float4*>(xout + (int64_t)tg * R + row)
+                                : reinterpret_cast<float4*>(q + (int64_t)tg * S + (row - R));
 #pragma unroll
-          for (int e = 0; e < 16; e += 4) {
-            float4 a = *reinterpret_cast<float4*>(qq + e);
-            a.x += v[e] + v2[e];
-            a.y += v[e + 1] + v2[e + 1];
-            a.z += v[e + 2] + v2[e + 2];
-            a.w += v[e + 3] + v2[e + 3];
-            *reinterpret_cast<float4*>(qq + e) = a;
+          for (int e = 0; e < 4; ++e) {
+            float4 o = base[g][e];
+            if (row < R) {  // x_{j+1} = x_j + W_res h + B_res
+              const float4 br = __ldg(reinterpret_cast<const float4*>(bres + row) + e);
+              o.x += (v[4 * e] + v2[4 * e]) + br.x;
+              o.y += (v[4 * e + 1] + v2[4 * e + 1]) + br.y;
+              o.z += (v[4 * e + 2] + v2[4 * e + 2]) + br.z;
+              o.w += (v[4 * e + 3] + v2[4 * e + 3]) + br.w;
+            } else {  // q += W_skip h
+              o.x += v[4 * e] + v2[4 * e];
+              o.y += v[4 * e + 1] + v2[4 * e + 1];
+              o.z += v[4 * e + 2] + v2[4 * e + 2];
+              o.w += v[4 * e + 3] + v2[4 * e + 3];
+            }
+            dst[e] = o;
           }
         }
       }
@@ -281,7 +313,7 @@ cudaError_t pack_parallel_tc(const float* w, const Offsets& o, int L, int r, int
 cudaError_t launch_parallel_layer_tc(const RunArgs& a, int j, const float* xin, float* xout, float* q,
                                      const float* pk, cudaStream_t st) {
   const dim3 grid((unsigned)((a.N + kTM - 1) / kTM), (unsigned)a.n_streams);
-  const int smem = (int)sizeof(float) * (2 * kActF + kW1F);
+  const int smem = (int)sizeof(float) * kSmemF;
   cudaError_t e;
   if (a.s == 256) {
     e = cudaFuncSetAttribute(k_layer_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
