@@ -244,6 +244,7 @@ int64_t parallel_tc_packed_floats(int L, int s);
 cudaError_t pack_parallel_tc(const float* w, const Offsets& o, int L, int r, int s, void* dst);
 cudaError_t launch_parallel_layer_tc(const RunArgs& a, int j, const float* xin, float* xout, float* q,
                                      const float* pk, cudaStream_t st);
+cudaError_t launch_parallel_head_tc(const RunArgs& a, const float* q, const float* pk, cudaStream_t st);
 
 #ifdef __CUDACC__
 // ---------------------------------------------------------------- App. A.4 strategies (row f3)

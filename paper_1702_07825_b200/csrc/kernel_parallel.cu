@@ -301,7 +301,10 @@ cudaError_t run_rs(const RunArgs& a, float* ws, cudaStream_t st, LaunchInfo* inf
   }
   const int hsm = (int)sizeof(float) * ((S + kLevels) * kTile + kKC * kLevels);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_head<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
-  if (e == cudaSuccess) k_head<S><<<grid, kPT, hsm, st>>>(a, Q);
+  if (e == cudaSuccess) {
+    if (R == 64 && pk_tc) e = launch_parallel_head_tc(a, Q, pk_tc, st);
+    else k_head<S><<<grid, kPT, hsm, st>>>(a, Q);
+  }
   if (e == cudaSuccess) e = cudaGetLastError();
   info->grid = (int)(grid.x * grid.y);
   info->cluster = 1;

@@ -261,9 +261,144 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
   if (t < 32) ptx::tmem_dealloc(d, 256);
 }
 
+// ---------------------------------------------------------------------------- the head
+// z_s = relu(q); z_a = relu(W_relu z_s + B_relu); logits = W_out z_a + B_out
+// per 128-timestep tile: two K = s and K = 256 GEMMs with N = 256.  Here the three tf32 passes
+// are three MMAs into the same columns (A_hi W_hi, A_hi W_lo, A_lo W_hi), so z_a and the
+// logits each take 256 TMEM columns and both fit; weight chunks are [16][256][4] hi images
+// followed by their lo images, 128 KB, one bulk copy each.
+constexpr int kHW = 16 * 256 * 4;  // floats of one 64-K x 256-row image
+
+__device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t w_hi, uint32_t w_lo,
+                                     bool acc, Sync& sy) {
+  if (threadIdx.x == 0) {
+    wait_bar(sy.bar_w, sy.ph_w);
+    ptx::tmem_fence_after();
+    const uint32_t id = idesc_tf32(256);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const uint32_t ao = ks * 2 * kTM * 16, bo = ks * 2 * 256 * 16;
+      const uint64_t dah = sdesc(a_hi + ao, kTM * 16, 128), dal = sdesc(a_lo + ao, kTM * 16, 128);
+      const uint64_t dbh = sdesc(w_hi + bo, 256 * 16, 128), dbl = sdesc(w_lo + bo, 256 * 16, 128);
+      mma_tf32(d, dah, dbh, id, (acc || ks > 0) ? 1u : 0u);
+      mma_tf32(d, dah, dbl, id, 1u);
+      mma_tf32(d, dal, dbh, id, 1u);
+    }
+    mma_commit(sy.bar_m);
+  }
+  sy.ph_w ^= 1;
+  wait_bar(sy.bar_m, sy.ph_m);
+  sy.ph_m ^= 1;
+  ptx::tmem_fence_after();
+}
+
+// 64 values of this thread's row into the operand pair (hi, lo), column group base g0 = 0.
+__device__ __forceinline__ void put_row64(float* hi, float* lo, const float (&v)[64]) {
+  const int i = threadIdx.x;
+#pragma unroll
+  for (int g = 0; g < 16; ++g) {
+    const int o = (g * kTM + i) * 4;
+    *reinterpret_cast<float4*>(hi + o) = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+    *reinterpret_cast<float4*>(lo + o) = make_float4(tf32_lo(v[4 * g]), tf32_lo(v[4 * g + 1]),
+                                                     tf32_lo(v[4 * g + 2]), tf32_lo(v[4 * g + 3]));
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(kThr, 1) k_head_tc(RunArgs A, const float* Q, const float* ph) {
+  extern __shared__ __align__(1024) float sm[];
+  float* a_hi = sm;
+  float* a_lo = sm + kActF;
+  float* w = sm + 2 * kActF;  // [hi image | lo image]
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ uint32_t tmem_base;
+  const int t = threadIdx.x, st = blockIdx.y, t0 = blockIdx.x * kTM;
+  const int T = (int)A.N;
+  const int tg = t0 + t;
+  const bool live = tg < T;
+  if (t < 32) ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 512);
+  Sync sy;
+  sy.bar_w = ptx::smem_u32(&bars[0]);
+  sy.bar_m = ptx::smem_u32(&bars[1]);
+  if (t == 0) {
+    ptx::mbar_init(sy.bar_w, 1);
+    ptx::mbar_init(sy.bar_m, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  ptx::tmem_fence_before();
+  __syncthreads();
+  ptx::tmem_fence_after();
+  const uint32_t d_za = tmem_base, d_lg = tmem_base + 256;
+  const uint32_t lane = (uint32_t)(32 * (t >> 5)) << 16;
+  const uint32_t s_hi = ptx::smem_u32(a_hi), s_lo = ptx::smem_u32(a_lo), s_w = ptx::smem_u32(w);
+  const float* qrow = Q + ((int64_t)st * T + (live ? tg : 0)) * S;
+  // ---- z_a pre-activation = W_relu relu(q), K = s in 64-chunks
+#pragma unroll 1
+  for (int kc = 0; kc < S / 64; ++kc) {
+    fetch_w(s_w, ph + (int64_t)kc * 2 * kHW, 2 * kHW, sy);
+    float v[64];
+#pragma unroll
+    for (int g = 0; g < 16; ++g) {
+      const float4 x = live ? *reinterpret_cast<const float4*>(qrow + 64 * kc + 4 * g) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[4 * g] = fmaxf(x.x, 0.0f);
+      v[4 * g + 1] = fmaxf(x.y, 0.0f);
+      v[4 * g + 2] = fmaxf(x.z, 0.0f);
+      v[4 * g + 3] = fmaxf(x.w, 0.0f);
+    }
+    put_row64(a_hi, a_lo, v);
+    fence_proxy_async_smem();
+    __syncthreads();
+    mma3(d_za, s_hi, s_lo, s_w, s_w + kHW * 4, kc > 0, sy);
+  }
+  // ---- logits = W_out z_a, K = 256 in 64-chunks; z_a = relu(pre + B_relu) chunk by chunk
+  const float* wout = ph + (int64_t)(S / 64) * 2 * kHW;
+  const float* brelu = A.w + A.off.b_relu;
+#pragma unroll 1
+  for (int kc = 0; kc < 4; ++kc) {
+    fetch_w(s_w, wout + (int64_t)kc * 2 * kHW, 2 * kHW, sy);
+    float v[64];
+#pragma unroll
+    for (int c = 0; c < 64; c += 16) ptx::tmem_ld16(d_za + lane + 64 * kc + c, v + c);
+    ptx::tmem_wait_ld<64>(v);
+#pragma unroll
+    for (int c = 0; c < 64; c += 4) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(brelu + 64 * kc + c));
+      v[c] = fmaxf(v[c] + b.x, 0.0f);
+      v[c + 1] = fmaxf(v[c + 1] + b.y, 0.0f);
+      v[c + 2] = fmaxf(v[c + 2] + b.z, 0.0f);
+      v[c + 3] = fmaxf(v[c + 3] + b.w, 0.0f);
+    }
+    put_row64(a_hi, a_lo, v);
+    ptx::tmem_fence_before();
+    fence_proxy_async_smem();
+    __syncthreads();
+    mma3(d_lg, s_hi, s_lo, s_w, s_w + kHW * 4, kc > 0, sy);
+  }
+  const float* bout = A.w + A.off.b_out;
+  float* out = A.out_logits + ((int64_t)st * T + (live ? tg : 0)) * kLevels;
+#pragma unroll 1
+  for (int c = 0; c < kLevels; c += 16) {
+    float v[16];
+    ptx::tmem_ld16(d_lg + lane + c, v);
+    ptx::tmem_wait_ld<16>(v);
+    if (live) {
+#pragma unroll
+      for (int e = 0; e < 16; e += 4) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(bout + c + e));
+        *reinterpret_cast<float4*>(out + c + e) = make_float4(v[e] + b.x, v[e + 1] + b.y, v[e + 2] + b.z, v[e + 3] + b.w);
+      }
+    }
+  }
+  ptx::tmem_fence_before();
+  __syncthreads();
+  if (t < 32) ptx::tmem_dealloc(tmem_base, 512);
+}
+
 }  // namespace
 
-int64_t parallel_tc_packed_floats(int L, int s) { return (int64_t)L * tc_layer_floats(s); }
+__host__ __device__ constexpr int64_t tc_head_floats(int s) { return (int64_t)(s / 64 + 4) * 2 * kHW; }
+
+int64_t parallel_tc_packed_floats(int L, int s) { return (int64_t)L * tc_layer_floats(s) + tc_head_floats(s); }
 
 // [K/4][rows][4] operand images of every layer (host, once per dvw_load_weights): GEMM-1
 // chunks kc = 0 (W_prev) and 1 (W_cur), each 128 rows of the weight and 128 rows of its
@@ -279,7 +414,7 @@ cudaError_t pack_parallel_tc(const float* w, const Offsets& o, int L, int r, int
     return x - h;
   };
   const int64_t per = tc_layer_floats(s);
-  std::vector<float> h((size_t)(L * per), 0.0f);
+  std::vector<float> h((size_t)(L * per + tc_head_floats(s)), 0.0f);
   for (int j = 0; j < L; ++j) {
     const float* lw = w + (int64_t)j * o.layer_stride;
     float* out = h.data() + (int64_t)j * per;
@@ -307,7 +442,37 @@ cudaError_t pack_parallel_tc(const float* w, const Offsets& o, int L, int r, int
       r0 += n;
     }
   }
+  // the head: W_relu [256][s] (K = s) then W_out [256][256], 64-K chunks of hi | lo images
+  float* hd = h.data() + (int64_t)L * per;
+  auto put = [&](const float* W, int K) {
+    for (int kc = 0; kc < K / 64; ++kc, hd += 2 * kHW)
+      for (int k = 0; k < 64; ++k)
+        for (int n = 0; n < kLevels; ++n) {
+          const float v = W[(int64_t)n * K + 64 * kc + k];
+          hd[((k / 4) * 256 + n) * 4 + k % 4] = v;
+          hd[kHW + ((k / 4) * 256 + n) * 4 + k % 4] = lo_of(v);
+        }
+  };
+  put(w + o.w_relu, s);
+  put(w + o.w_out, kLevels);
   return cudaMemcpy(dst, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice);
+}
+
+cudaError_t launch_parallel_head_tc(const RunArgs& a, const float* q, const float* pk, cudaStream_t st) {
+  const dim3 grid((unsigned)((a.N + kTM - 1) / kTM), (unsigned)a.n_streams);
+  const int smem = (int)sizeof(float) * (2 * kActF + 2 * kHW);
+  const float* ph = pk + (int64_t)a.L * tc_layer_floats(a.s);
+  cudaError_t e;
+  if (a.s == 256) {
+    e = cudaFuncSetAttribute(k_head_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) k_head_tc<256><<<grid, kThr, smem, st>>>(a, q, ph);
+  } else if (a.s == 128) {
+    e = cudaFuncSetAttribute(k_head_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) k_head_tc<128><<<grid, kThr, smem, st>>>(a, q, ph);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
 cudaError_t launch_parallel_layer_tc(const RunArgs& a, int j, const float* xin, float* xout, float* q,
