@@ -60,6 +60,14 @@ def tf32_peak_tflops():
         return 1590.0 * TF32_RATIO, "B200_PROFILING.md fallback bf16 1.59 PFLOP/s x 0.5"
 
 
+def hbm_peak_gbs():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json), else the guide's fallback."""
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"], "of measured"
+    except Exception:
+        return 6650.0, "of fallback (B200_PROFILING.md)"
+
+
 def macs_per_sample(cfg) -> int:
     """l (5 r^2 + r s) + a s + a^2 (SURVEY.md §8(a) per-sample totals)."""
     L, r, s, a = cfg.n_layers, cfg.residual, cfg.skip, cfg.levels
@@ -395,10 +403,17 @@ def main():
         achieved_tflops = flop_launch / (kernel_ms / 1e3) / 1e12
         kname = info["last_kernel_name"]
         fast = kname == "tc" and args.precision != "fp32"
+        line_hbm = None
         if kname == "tc":
             peak, peak_src = tf32_peak_tflops()
+            traffic = load_ncu_traffic(args.workload, n * S)
+            if traffic is not None:  # the north_star's second batched-mode figure: HBM GB/s
+                hpk, hsrc = hbm_peak_gbs()
+                hgbs = traffic / (kernel_ms / 1e3) / 1e9
+                line_hbm = {"achieved_gbs": hgbs, "peak_gbs": hpk, "frac": hgbs / hpk,
+                            "note": f"ncu DRAM bytes per stream-sample x stream-samples / launch time, {hsrc}"}
             roof = {"bound": "tensor", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved_tflops / peak, "traffic": load_ncu_traffic(args.workload, n * S),
+                    "frac": achieved_tflops / peak, "traffic": traffic,
                     "note": "algorithmic FLOP (2 x MAC/sample x samples x streams) / launch time vs dense tf32 "
                             f"peak ({peak_src}); " + ("one tf32 pass (DVW_PRECISION_TF32); " if fast else
                             "the 3-pass split issues ~3.2x these FLOPs on the tensor pipe; ") +
@@ -436,6 +451,8 @@ def main():
             "gpu_launches": (int(info["last_launches"]) + (5 if cond_net is not None else 0)) * args.steps,
             "roofline": roof,
         }
+        if line_hbm is not None:
+            line["hbm"] = line_hbm
         if gather is not None:
             line["gather_results"] = gather
         if latency is not None:
