@@ -49,14 +49,17 @@ __device__ __forceinline__ void wait_bar(uint32_t bar, uint32_t parity) {
 }
 
 // Rows t0 - shift + i (zero outside [0, T)) of X [T][64] into the operand pair (hi, lo).
-// Thread i loads its own row (16 float4, all in flight at once), then writes the 16 groups.
-__device__ __forceinline__ void stage_rows(float* hi, float* lo, const float* X, int T, int t0, int shift) {
-  const int i = threadIdx.x, tg = t0 - shift + i;
-  float4 v[16];
+// Thread i loads its own row (16 float4, all in flight at once: load_row), then writes the 16
+// groups of the operand pair (store_row).
+__device__ __forceinline__ void load_row(float4 (&v)[16], const float* X, int T, int t0, int shift) {
+  const int tg = t0 - shift + (int)threadIdx.x;
   const bool in = tg >= 0 && tg < T;
   const float4* src = reinterpret_cast<const float4*>(X + (int64_t)(in ? tg : 0) * R);
 #pragma unroll
   for (int g = 0; g < 16; ++g) v[g] = in ? __ldg(src + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void store_row(float* hi, float* lo, const float4 (&v)[16]) {
+  const int i = threadIdx.x;
 #pragma unroll
   for (int g = 0; g < 16; ++g) {
     const int o = (g * kTM + i) * 4;
@@ -72,8 +75,8 @@ struct Sync {
 };
 
 // D[:, 0:2n) = / += A (K = 64, operand pair at a_hi/a_lo) times the staged weight chunk
-// (n real rows + their n lo rows), then wait for it.  Thread 0 issues; everybody waits.
-__device__ __forceinline__ void mma_chunk(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t wsm, int n, bool acc,
+// (n real rows + their n lo rows).  Thread 0 issues (mma_issue); everybody waits (mma_wait).
+__device__ __forceinline__ void mma_issue(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t wsm, int n, bool acc,
                                           Sync& sy) {
   if (threadIdx.x == 0) {
     wait_bar(sy.bar_w, sy.ph_w);
@@ -90,9 +93,16 @@ __device__ __forceinline__ void mma_chunk(uint32_t d, uint32_t a_hi, uint32_t a_
     mma_commit(sy.bar_m);
   }
   sy.ph_w ^= 1;
+}
+__device__ __forceinline__ void mma_wait(Sync& sy) {
   wait_bar(sy.bar_m, sy.ph_m);
   sy.ph_m ^= 1;
   ptx::tmem_fence_after();
+}
+__device__ __forceinline__ void mma_chunk(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t wsm, int n, bool acc,
+                                          Sync& sy) {
+  mma_issue(d, a_hi, a_lo, wsm, n, acc, sy);
+  mma_wait(sy);
 }
 
 __device__ __forceinline__ void fetch_w(uint32_t wsm, const float* src, int floats, const Sync& sy) {
@@ -140,10 +150,21 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
   const uint32_t s_hi = ptx::smem_u32(a_hi), s_lo = ptx::smem_u32(a_lo), s_w = ptx::smem_u32(wsm);
   const uint32_t lane_addr = d + ((uint32_t)(32 * (t >> 5)) << 16);
   const float* bj = A.w + lo + A.off.b;
-  {  // the gate's addend row, loaded while GEMM 1 runs (each thread reads back only its own row)
+  // ---- GEMM 1: chunk 0 = W_prev with x_j(t - d), chunk 1 = W_cur with x_j(t).  While chunk 0's
+  //      MMAs run: the x_j(t) rows load into registers and the gate's (L + B) table fills.
+  const float* w2 = pl + 2 * kW1F;
+  {
+    float4 v[16];
+    fetch_w(s_w, pl, kW1F, sy);
+    load_row(v, xin, T, t0, A.dil[j]);
+    store_row(a_hi, a_lo, v);
+    fence_proxy_async_smem();
+    __syncthreads();
+    mma_issue(d, s_hi, s_lo, s_w, 128, false, sy);
+    load_row(v, xin, T, t0, 0);
     const float* Lr = A.cond + (((int64_t)st * A.n_frames + (tg < T ? tg : 0) / A.hop) * A.L + j) * 2 * R;
 #pragma unroll 8
-    for (int c = 0; c < 2 * R; c += 4) {
+    for (int c = 0; c < 2 * R; c += 4) {  // each thread reads back only its own row
       const float4 lv = tg < T ? __ldg(reinterpret_cast<const float4*>(Lr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
       const float4 bv = __ldg(reinterpret_cast<const float4*>(bj + c));
       float* o = lb + t * kLBP + c;
@@ -152,17 +173,12 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
       o[2] = bv.z + lv.z;
       o[3] = bv.w + lv.w;
     }
-  }
-
-  // ---- GEMM 1: chunk 0 = W_prev with x_j(t - d), chunk 1 = W_cur with x_j(t); each weight
-  //      bulk copy overlaps the staging of the activations
-  const float* w2 = pl + 2 * kW1F;
-  for (int kc = 0; kc < 2; ++kc) {
-    fetch_w(s_w, pl + kc * kW1F, kW1F, sy);
-    stage_rows(a_hi, a_lo, xin, T, t0, kc == 0 ? A.dil[j] : 0);
+    mma_wait(sy);
+    fetch_w(s_w, pl + kW1F, kW1F, sy);
+    store_row(a_hi, a_lo, v);
     fence_proxy_async_smem();
     __syncthreads();
-    mma_chunk(d, s_hi, s_lo, s_w, 128, kc > 0, sy);
+    mma_chunk(d, s_hi, s_lo, s_w, 128, true, sy);
   }
   fetch_w(s_w, w2, 16 * 2 * 128 * 4, sy);  // GEMM 2's first chunk, during the gate
   // ---- gate: + B + L(t / hop); h -> operand pair for GEMM 2
@@ -183,7 +199,9 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
       const int c = 16 * cc + e;
       const float xh = (ah[e] + ah2[e]) + lb[t * kLBP + c];
       const float xg = (ag[e] + ag2[e]) + lb[t * kLBP + R + c];
-      h[e] = A.approx == 0 ? gate(xh, xg) : A.approx == 1 ? gate_approx(xh, xg) : gate_appc(xh, xg);
+      // exact tier: the branch-free MUFU form of tanh / sigma (reading R13, abs. error ~1e-7, as
+      // the cluster kernel); libdevice tanhf/expf cost ~200 cycles per channel here
+      h[e] = A.approx == 0 ? gate_fast(xh, xg) : A.approx == 1 ? gate_approx(xh, xg) : gate_appc(xh, xg);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
