@@ -26,7 +26,8 @@ namespace {
 
 constexpr int R = 64;            // residual channels this kernel is built for
 constexpr int kTM = 128;         // timesteps per tile (= MMA M = TMEM lanes)
-constexpr int kThr = 128;        // one thread per timestep
+constexpr int kThr = 128;        // head: one thread per timestep
+constexpr int kLThr = 256;       // layers: two threads per timestep (warps w and w + 4 share TMEM lanes)
 constexpr int kActF = 16 * kTM * 4;  // one 64-channel activation operand [16][128][4] (floats)
 constexpr int kW1F = 16 * 256 * 4;   // one GEMM-1 weight chunk: 64 K x (128 hi + 128 lo rows)
 constexpr int kLBP = 2 * R + 1;      // padded row of the per-timestep (L + B) table
@@ -49,20 +50,19 @@ __device__ __forceinline__ void wait_bar(uint32_t bar, uint32_t parity) {
 }
 
 // Rows t0 - shift + i (zero outside [0, T)) of X [T][64] into the operand pair (hi, lo).
-// Thread i loads its own row (16 float4, all in flight at once: load_row), then writes the 16
-// groups of the operand pair (store_row).
-__device__ __forceinline__ void load_row(float4 (&v)[16], const float* X, int T, int t0, int shift) {
-  const int tg = t0 - shift + (int)threadIdx.x;
+// Thread (row i, half hf) loads 8 of the row's 16 channel groups (all in flight at once:
+// load_row), then writes them into the operand pair (store_row).
+__device__ __forceinline__ void load_row(float4 (&v)[8], const float* X, int T, int t0, int shift, int i, int hf) {
+  const int tg = t0 - shift + i;
   const bool in = tg >= 0 && tg < T;
-  const float4* src = reinterpret_cast<const float4*>(X + (int64_t)(in ? tg : 0) * R);
+  const float4* src = reinterpret_cast<const float4*>(X + (int64_t)(in ? tg : 0) * R) + 8 * hf;
 #pragma unroll
-  for (int g = 0; g < 16; ++g) v[g] = in ? __ldg(src + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int g = 0; g < 8; ++g) v[g] = in ? __ldg(src + g) : make_float4(0.f, 0.f, 0.f, 0.f);
 }
-__device__ __forceinline__ void store_row(float* hi, float* lo, const float4 (&v)[16]) {
-  const int i = threadIdx.x;
+__device__ __forceinline__ void store_row(float* hi, float* lo, const float4 (&v)[8], int i, int hf) {
 #pragma unroll
-  for (int g = 0; g < 16; ++g) {
-    const int o = (g * kTM + i) * 4;
+  for (int g = 0; g < 8; ++g) {
+    const int o = ((8 * hf + g) * kTM + i) * 4;
     *reinterpret_cast<float4*>(hi + o) = v[g];
     *reinterpret_cast<float4*>(lo + o) =
         make_float4(tf32_lo(v[g].x), tf32_lo(v[g].y), tf32_lo(v[g].z), tf32_lo(v[g].w));
@@ -119,8 +119,8 @@ __device__ __forceinline__ void release_tmem() {
 }
 
 template <int S>
-__global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const float* Xin, float* Xout, float* Q,
-                                                      const float* pk) {
+__global__ void __launch_bounds__(kLThr, 1) k_layer_tc(RunArgs A, int j, const float* Xin, float* Xout, float* Q,
+                                                       const float* pk) {
   extern __shared__ __align__(1024) float sm[];
   float* a_hi = sm;            // [16][128][4]
   float* a_lo = sm + kActF;    // [16][128][4]
@@ -128,17 +128,18 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
   float* lb = wsm + kW1F;      // [128][2R + 1]: L^(j)(t / hop) + B for this thread's timestep
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ uint32_t tmem_base;
-  const int t = threadIdx.x, st = blockIdx.y, t0 = blockIdx.x * kTM;
+  const int t = threadIdx.x & (kTM - 1), hf = threadIdx.x >> 7;  // timestep row, half of the work
+  const int st = blockIdx.y, t0 = blockIdx.x * kTM;
   const int T = (int)A.N;
   const int tg = t0 + t;
   const int64_t lo = (int64_t)j * A.off.layer_stride;
   const float* xin = Xin + (int64_t)st * T * R;
   const float* pl = pk + (int64_t)j * tc_layer_floats(S);
-  if (t < 32) ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 256);
+  if (threadIdx.x < 32) ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 256);
   Sync sy;
   sy.bar_w = ptx::smem_u32(&bars[0]);
   sy.bar_m = ptx::smem_u32(&bars[1]);
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     ptx::mbar_init(sy.bar_w, 1);
     ptx::mbar_init(sy.bar_m, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -148,23 +149,23 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
   ptx::tmem_fence_after();
   const uint32_t d = tmem_base;
   const uint32_t s_hi = ptx::smem_u32(a_hi), s_lo = ptx::smem_u32(a_lo), s_w = ptx::smem_u32(wsm);
-  const uint32_t lane_addr = d + ((uint32_t)(32 * (t >> 5)) << 16);
+  const uint32_t lane_addr = d + ((uint32_t)(32 * (t >> 5)) << 16);  // warp w: lanes 32 (w % 4) ..
   const float* bj = A.w + lo + A.off.b;
   // ---- GEMM 1: chunk 0 = W_prev with x_j(t - d), chunk 1 = W_cur with x_j(t).  While chunk 0's
   //      MMAs run: the x_j(t) rows load into registers and the gate's (L + B) table fills.
   const float* w2 = pl + 2 * kW1F;
   {
-    float4 v[16];
+    float4 v[8];
     fetch_w(s_w, pl, kW1F, sy);
-    load_row(v, xin, T, t0, A.dil[j]);
-    store_row(a_hi, a_lo, v);
+    load_row(v, xin, T, t0, A.dil[j], t, hf);
+    store_row(a_hi, a_lo, v, t, hf);
     fence_proxy_async_smem();
     __syncthreads();
     mma_issue(d, s_hi, s_lo, s_w, 128, false, sy);
-    load_row(v, xin, T, t0, 0);
+    load_row(v, xin, T, t0, 0, t, hf);
     const float* Lr = A.cond + (((int64_t)st * A.n_frames + (tg < T ? tg : 0) / A.hop) * A.L + j) * 2 * R;
 #pragma unroll 8
-    for (int c = 0; c < 2 * R; c += 4) {  // each thread reads back only its own row
+    for (int c = R * hf; c < R * hf + R; c += 4) {  // the row's half hf; read back after the barriers
       const float4 lv = tg < T ? __ldg(reinterpret_cast<const float4*>(Lr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
       const float4 bv = __ldg(reinterpret_cast<const float4*>(bj + c));
       float* o = lb + t * kLBP + c;
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
     }
     mma_wait(sy);
     fetch_w(s_w, pl + kW1F, kW1F, sy);
-    store_row(a_hi, a_lo, v);
+    store_row(a_hi, a_lo, v, t, hf);
     fence_proxy_async_smem();
     __syncthreads();
     mma_chunk(d, s_hi, s_lo, s_w, 128, true, sy);
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
   fetch_w(s_w, w2, 16 * 2 * 128 * 4, sy);  // GEMM 2's first chunk, during the gate
   // ---- gate: + B + L(t / hop); h -> operand pair for GEMM 2
 #pragma unroll 1
-  for (int cc = 0; cc < 4; ++cc) {  // channels 16 cc .. 16 cc + 15
+  for (int cc = 2 * hf; cc < 2 * hf + 2; ++cc) {  // channels 16 cc .. 16 cc + 15 (this thread's half)
     float ah[16], ah2[16], ag[16], ag2[16];
     ptx::tmem_ld16(lane_addr + 16 * cc, ah);
     ptx::tmem_ld16(lane_addr + 128 + 16 * cc, ah2);
@@ -227,21 +228,23 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
     const int tr = live ? tg : 0;
     // the addends of this chunk's rows (x_j for rows < R, the running q above), in flight
     // while the MMAs run
-    float4 base[8][4];
+    float4 base[4][4];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
+    for (int k = 0; k < 4; ++k) {
+      const int g = hf + 2 * k;  // this thread's 16-row groups
       if (16 * g < n) {
         const int row = r0 + 16 * g;  // 16 rows, all on one side of R
         const float4* src = row < R ? reinterpret_cast<const float4*>(xin + (int64_t)tr * R + row)
                                     : reinterpret_cast<const float4*>(q + (int64_t)tr * S + (row - R));
 #pragma unroll
-        for (int e = 0; e < 4; ++e) base[g][e] = row < R ? __ldg(src + e) : src[e];
+        for (int e = 0; e < 4; ++e) base[k][e] = row < R ? __ldg(src + e) : src[e];
       }
     }
     mma_chunk(d, s_hi, s_lo, s_w, n, false, sy);
     if (r0 + n < R + S) fetch_w(s_w, w2 + 16 * 2 * n * 4, 16 * 2 * std::min(128, R + S - r0 - n) * 4, sy);
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
+    for (int k = 0; k < 4; ++k) {
+      const int g = hf + 2 * k;
       if (16 * g < n) {
         const int row = r0 + 16 * g;
         float v[16], v2[16];
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
                                 : reinterpret_cast<float4*>(q + (int64_t)tg * S + (row - R));
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            float4 o = base[g][e];
+            float4 o = base[k][e];
             if (row < R) {  // x_{j+1} = x_j + W_res h + B_res
               const float4 br = __ldg(reinterpret_cast<const float4*>(bres + row) + e);
               o.x += (v[4 * e] + v2[4 * e]) + br.x;
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(kThr, 1) k_layer_tc(RunArgs A, int j, const fl
     w2 += 16 * 2 * n * 4;
     r0 += n;
   }
-  if (t < 32) ptx::tmem_dealloc(d, 256);
+  if (threadIdx.x < 32) ptx::tmem_dealloc(d, 256);
 }
 
 // ---------------------------------------------------------------------------- the head
@@ -500,10 +503,10 @@ cudaError_t launch_parallel_layer_tc(const RunArgs& a, int j, const float* xin, 
   cudaError_t e;
   if (a.s == 256) {
     e = cudaFuncSetAttribute(k_layer_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) k_layer_tc<256><<<grid, kThr, smem, st>>>(a, j, xin, xout, q, pk);
+    if (e == cudaSuccess) k_layer_tc<256><<<grid, kLThr, smem, st>>>(a, j, xin, xout, q, pk);
   } else if (a.s == 128) {
     e = cudaFuncSetAttribute(k_layer_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) k_layer_tc<128><<<grid, kThr, smem, st>>>(a, j, xin, xout, q, pk);
+    if (e == cudaSuccess) k_layer_tc<128><<<grid, kLThr, smem, st>>>(a, j, xin, xout, q, pk);
   } else {
     return cudaErrorInvalidValue;
   }
