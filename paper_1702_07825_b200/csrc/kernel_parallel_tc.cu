@@ -26,8 +26,7 @@ namespace {
 
 constexpr int R = 64;            // residual channels this kernel is built for
 constexpr int kTM = 128;         // timesteps per tile (= MMA M = TMEM lanes)
-constexpr int kThr = 128;        // head: one thread per timestep
-constexpr int kLThr = 256;       // layers: two threads per timestep (warps w and w + 4 share TMEM lanes)
+constexpr int kLThr = 256;       // two threads per timestep (warps w and w + 4 share TMEM lanes)
 constexpr int kActF = 16 * kTM * 4;  // one 64-channel activation operand [16][128][4] (floats)
 constexpr int kW1F = 16 * 256 * 4;   // one GEMM-1 weight chunk: 64 K x (128 hi + 128 lo rows)
 constexpr int kLBP = 2 * R + 1;      // padded row of the per-timestep (L + B) table
@@ -313,12 +312,11 @@ __device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, u
   ptx::tmem_fence_after();
 }
 
-// 64 values of this thread's row into the operand pair (hi, lo), column group base g0 = 0.
-__device__ __forceinline__ void put_row64(float* hi, float* lo, const float (&v)[64]) {
-  const int i = threadIdx.x;
+// 32 values (channel groups 8 hf .. 8 hf + 7) of row i into the operand pair (hi, lo).
+__device__ __forceinline__ void put_row32(float* hi, float* lo, const float (&v)[32], int i, int hf) {
 #pragma unroll
-  for (int g = 0; g < 16; ++g) {
-    const int o = (g * kTM + i) * 4;
+  for (int g = 0; g < 8; ++g) {
+    const int o = ((8 * hf + g) * kTM + i) * 4;
     *reinterpret_cast<float4*>(hi + o) = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
     *reinterpret_cast<float4*>(lo + o) = make_float4(tf32_lo(v[4 * g]), tf32_lo(v[4 * g + 1]),
                                                      tf32_lo(v[4 * g + 2]), tf32_lo(v[4 * g + 3]));
@@ -326,22 +324,23 @@ __device__ __forceinline__ void put_row64(float* hi, float* lo, const float (&v)
 }
 
 template <int S>
-__global__ void __launch_bounds__(kThr, 1) k_head_tc(RunArgs A, const float* Q, const float* ph) {
+__global__ void __launch_bounds__(kLThr, 1) k_head_tc(RunArgs A, const float* Q, const float* ph) {
   extern __shared__ __align__(1024) float sm[];
   float* a_hi = sm;
   float* a_lo = sm + kActF;
   float* w = sm + 2 * kActF;  // [hi image | lo image]
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ uint32_t tmem_base;
-  const int t = threadIdx.x, st = blockIdx.y, t0 = blockIdx.x * kTM;
+  const int t = threadIdx.x & (kTM - 1), hf = threadIdx.x >> 7;  // timestep row, half of the work
+  const int st = blockIdx.y, t0 = blockIdx.x * kTM;
   const int T = (int)A.N;
   const int tg = t0 + t;
   const bool live = tg < T;
-  if (t < 32) ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 512);
+  if (threadIdx.x < 32) ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 512);
   Sync sy;
   sy.bar_w = ptx::smem_u32(&bars[0]);
   sy.bar_m = ptx::smem_u32(&bars[1]);
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     ptx::mbar_init(sy.bar_w, 1);
     ptx::mbar_init(sy.bar_m, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -357,16 +356,17 @@ __global__ void __launch_bounds__(kThr, 1) k_head_tc(RunArgs A, const float* Q, 
 #pragma unroll 1
   for (int kc = 0; kc < S / 64; ++kc) {
     fetch_w(s_w, ph + (int64_t)kc * 2 * kHW, 2 * kHW, sy);
-    float v[64];
+    float v[32];
 #pragma unroll
-    for (int g = 0; g < 16; ++g) {
-      const float4 x = live ? *reinterpret_cast<const float4*>(qrow + 64 * kc + 4 * g) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int g = 0; g < 8; ++g) {
+      const float4 x = live ? *reinterpret_cast<const float4*>(qrow + 64 * kc + 32 * hf + 4 * g)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
       v[4 * g] = fmaxf(x.x, 0.0f);
       v[4 * g + 1] = fmaxf(x.y, 0.0f);
       v[4 * g + 2] = fmaxf(x.z, 0.0f);
       v[4 * g + 3] = fmaxf(x.w, 0.0f);
     }
-    put_row64(a_hi, a_lo, v);
+    put_row32(a_hi, a_lo, v, t, hf);
     fence_proxy_async_smem();
     __syncthreads();
     mma3(d_za, s_hi, s_lo, s_w, s_w + kHW * 4, kc > 0, sy);
@@ -377,19 +377,19 @@ __global__ void __launch_bounds__(kThr, 1) k_head_tc(RunArgs A, const float* Q, 
 #pragma unroll 1
   for (int kc = 0; kc < 4; ++kc) {
     fetch_w(s_w, wout + (int64_t)kc * 2 * kHW, 2 * kHW, sy);
-    float v[64];
+    float v[32];
 #pragma unroll
-    for (int c = 0; c < 64; c += 16) ptx::tmem_ld16(d_za + lane + 64 * kc + c, v + c);
-    ptx::tmem_wait_ld<64>(v);
+    for (int c = 0; c < 32; c += 16) ptx::tmem_ld16(d_za + lane + 64 * kc + 32 * hf + c, v + c);
+    ptx::tmem_wait_ld<32>(v);
 #pragma unroll
-    for (int c = 0; c < 64; c += 4) {
-      const float4 b = __ldg(reinterpret_cast<const float4*>(brelu + 64 * kc + c));
+    for (int c = 0; c < 32; c += 4) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(brelu + 64 * kc + 32 * hf + c));
       v[c] = fmaxf(v[c] + b.x, 0.0f);
       v[c + 1] = fmaxf(v[c + 1] + b.y, 0.0f);
       v[c + 2] = fmaxf(v[c + 2] + b.z, 0.0f);
       v[c + 3] = fmaxf(v[c + 3] + b.w, 0.0f);
     }
-    put_row64(a_hi, a_lo, v);
+    put_row32(a_hi, a_lo, v, t, hf);
     ptx::tmem_fence_before();
     fence_proxy_async_smem();
     __syncthreads();
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(kThr, 1) k_head_tc(RunArgs A, const float* Q, 
   const float* bout = A.w + A.off.b_out;
   float* out = A.out_logits + ((int64_t)st * T + (live ? tg : 0)) * kLevels;
 #pragma unroll 1
-  for (int c = 0; c < kLevels; c += 16) {
+  for (int c = 128 * hf; c < 128 * hf + 128; c += 16) {
     float v[16];
     ptx::tmem_ld16(d_lg + lane + c, v);
     ptx::tmem_wait_ld<16>(v);
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kThr, 1) k_head_tc(RunArgs A, const float* Q, 
   }
   ptx::tmem_fence_before();
   __syncthreads();
-  if (t < 32) ptx::tmem_dealloc(tmem_base, 512);
+  if (threadIdx.x < 32) ptx::tmem_dealloc(tmem_base, 512);
 }
 
 }  // namespace
@@ -486,10 +486,10 @@ cudaError_t launch_parallel_head_tc(const RunArgs& a, const float* q, const floa
   cudaError_t e;
   if (a.s == 256) {
     e = cudaFuncSetAttribute(k_head_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) k_head_tc<256><<<grid, kThr, smem, st>>>(a, q, ph);
+    if (e == cudaSuccess) k_head_tc<256><<<grid, kLThr, smem, st>>>(a, q, ph);
   } else if (a.s == 128) {
     e = cudaFuncSetAttribute(k_head_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) k_head_tc<128><<<grid, kThr, smem, st>>>(a, q, ph);
+    if (e == cudaSuccess) k_head_tc<128><<<grid, kLThr, smem, st>>>(a, q, ph);
   } else {
     return cudaErrorInvalidValue;
   }

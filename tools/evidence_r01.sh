@@ -18,3 +18,4 @@ ncu --set full --import-source on --clock-control none -k regex:k_cluster -c 1 -
 ncu --set full --import-source on --clock-control none -k regex:k_cluster -c 1 -o gpurun_out/ev/cluster_c3 python tools/ncu_c2.py --n 2000 --layers 40 > gpurun_out/ev/ncu_c3.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:k_batch -c 1 -o gpurun_out/ev/batch_c4 python bench.py --workload C4 --samples 200 --steps 1 --warmup 0 --no-cpu --no-e2e > gpurun_out/ev/ncu_c4.log 2>&1
 ncu --set full --clock-control none -k regex:k_layer -c 1 -o gpurun_out/ev/parallel_c2 python tools/bench_logits.py > gpurun_out/ev/ncu_par.log 2>&1
+ncu --set full --clock-control none -k regex:k_batch -c 1 -o gpurun_out/ev/batch_c5 python bench.py --workload C5 --samples 100 --steps 1 --warmup 0 --no-cpu --no-e2e > gpurun_out/ev/ncu_c5.log 2>&1
