@@ -28,6 +28,11 @@
  *     z_s = relu(q); z_a = relu(W_relu z_s + B_relu); l = W_out z_a + B_out   (step 3)
  *     p   = softmax(l); y_n = inverse-CDF draw with u_n         (R11)
  *
+ * Pins (tests/test_oracle_pins.py, test_appc_oracle.py): mu-law against torchaudio, the
+ * receptive field, causality, softmax sums, closed-form draws (zero weights, one-hot and
+ * bias-only logits), the independent brute-force oracle (bruteforce.py), the App. A.4
+ * strategies' limits (t = 1, k = a), and App. C's printed maximum errors.
+ *
  * Weight blob (include/dvw.h, restated here independently):
  *   per layer j: W_prev[2r][r] W_cur[2r][r] B[2r] W_res[r][r] B_res[r] W_skip[s][r]
  *   then W_emb_prev[r][a] W_emb_cur[r][a] B_emb[r] B_skip[s] W_relu[a][s]

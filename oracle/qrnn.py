@@ -15,6 +15,13 @@ i, out[2i+1] = backward channel i of the second layer; each WaveNet layer j then
 linear projection L^(j)_t = P^(j) out_t + B^(j) to 2r channels (SPEC build_conditioning),
 at frame rate -- the generator repeats frame f for samples [f hop, (f+1) hop).
 
+Pins (tests/test_qrnn_oracle.py): the fo-pooling recurrence against its unrolled closed form,
+the forget-gate limits (f -> 0: h = h~; f -> 1: h carries), zero weights giving exactly the
+projection bias, causality of each direction (a frame perturbation moves only frames on its
+side), reversal of the input swapping the two directions, shapes / interleave / blob size.
+The output VALUES for random weights are "parity unpinned by the paper" (it prints none):
+beyond those properties they are pinned only by the GPU conditioner agreeing with them.
+
 Weight blob (fp32, this order), per QRNN layer q = 1, 2 (C_in = features for q = 1, 2H for
 q = 2), per direction (forward, then backward):
     W [3 gates: h, o, f][2 taps: t-1, t][H][C_in],  B [3][H]
