@@ -51,7 +51,7 @@ constexpr int kTmemCols = 128;
 // its first block of columns and hi*lo in a second block (the stacked-B pass below):
 //   layer: [0,48) = tanh 16 | sigmoid 16 | residual 16, [48,96) the hi*lo partner
 //   skip / head (64 rows): [0,64) and [64,128)
-constexpr uint32_t kColA = 0, kColA2 = 48, kColQ = 0, kColQ2 = 64, kColH = 0, kColH2 = 64;
+constexpr uint32_t kColA = 0, kColA2 = 48, kColQ = 0, kColQ2 = 64, kColH = 0;
 constexpr int kTileRows = 64;  // rows of a skip or head tile
 
 constexpr uint64_t kTimeoutNs = 4000000000ull;
@@ -302,10 +302,6 @@ __device__ __forceinline__ void st_act(float* base_hi, int64_t half, int c, int 
     float4 lo = make_float4(tf32_lo(v[0]), tf32_lo(v[1]), tf32_lo(v[2]), tf32_lo(v[3]));
     __stcg(reinterpret_cast<float4*>(base_hi + half + o), lo);
   }
-}
-
-__device__ __forceinline__ float4 ld_act(const float* base_hi, int c, int i) {
-  return __ldcg(reinterpret_cast<const float4*>(base_hi + canon(c, i)));
 }
 
 // Loads that must be issued where they are written (before a wait), not sunk to
