@@ -444,8 +444,8 @@ DVW_API dvw_status dvw_load_weights(dvw_model* m, const float* blob, int64_t num
     DVW_CUDA(pack_cluster_weights(m->cplan, hp, m->off, m->d_packed), "packing weights");
     wb += (int64_t)need;
   }
-  if (m->r == 64) {  // tensor-core images for the parallel teacher-forced layers
-    const size_t need = sizeof(float) * (size_t)parallel_tc_packed_floats(m->L, m->s);
+  if (m->r == 64 || m->r == 128) {  // tensor-core images for the parallel teacher-forced pass
+    const size_t need = sizeof(float) * (size_t)parallel_tc_packed_floats(m->L, m->r, m->s);
     if (m->d_ptc && m->ptc_bytes < need) {
       cudaFree(m->d_ptc);
       m->d_ptc = nullptr;

@@ -236,11 +236,11 @@ cudaError_t launch_stream_kernel(const RunArgs& a, cudaStream_t st, LaunchInfo* 
 // Teacher-forced logits in parallel over time (kernel_parallel.cu): workspace for a group of
 // streams, then one call per group.
 size_t parallel_workspace_bytes(int r, int s, int64_t n_samples, int n_streams);
-// pk_tc: the tensor-core layer images (pack_parallel_tc), r = 64 only; nullptr -> SIMT layers.
+// pk_tc: the tensor-core images (pack_parallel_tc), r = 64 or 128; nullptr -> SIMT layers and head.
 cudaError_t launch_parallel_logits(const RunArgs& a, void* ws, cudaStream_t st, LaunchInfo* info,
                                    const float* pk_tc = nullptr);
-// Tensor-core layer pass (kernel_parallel_tc.cu, r = 64): packed image size, host packing, one layer.
-int64_t parallel_tc_packed_floats(int L, int s);
+// Tensor-core layer pass (kernel_parallel_tc.cu, r = 64 or 128): packed image size, host packing, one layer.
+int64_t parallel_tc_packed_floats(int L, int r, int s);
 cudaError_t pack_parallel_tc(const float* w, const Offsets& o, int L, int r, int s, void* dst);
 cudaError_t launch_parallel_layer_tc(const RunArgs& a, int j, const float* xin, float* xout, float* q,
                                      const float* pk, cudaStream_t st);

@@ -296,13 +296,13 @@ cudaError_t run_rs(const RunArgs& a, float* ws, cudaStream_t st, LaunchInfo* inf
   const int lsm = (int)sizeof(float) * (3 * R * kTile + kKC * std::max(2 * R, S));
   cudaError_t e = cudaFuncSetAttribute(k_layer<R, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, lsm);
   for (int j = 0; e == cudaSuccess && j < a.L; ++j) {
-    if (R == 64 && pk_tc) e = launch_parallel_layer_tc(a, j, X[j & 1], X[(j + 1) & 1], Q, pk_tc, st);
+    if ((R == 64 || R == 128) && pk_tc) e = launch_parallel_layer_tc(a, j, X[j & 1], X[(j + 1) & 1], Q, pk_tc, st);
     else k_layer<R, S><<<grid, kPT, lsm, st>>>(a, j, X[j & 1], X[(j + 1) & 1], Q);
   }
   const int hsm = (int)sizeof(float) * ((S + kLevels) * kTile + kKC * kLevels);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_head<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
   if (e == cudaSuccess) {
-    if (R == 64 && pk_tc) e = launch_parallel_head_tc(a, Q, pk_tc, st);
+    if ((R == 64 || R == 128) && pk_tc) e = launch_parallel_head_tc(a, Q, pk_tc, st);
     else k_head<S><<<grid, kPT, hsm, st>>>(a, Q);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -326,8 +326,8 @@ cudaError_t launch_parallel_logits(const RunArgs& a, void* ws, cudaStream_t st, 
   if (a.r == 32 && a.s == 256) return run_rs<32, 256>(a, w, st, info, nullptr);
   if (a.r == 64 && a.s == 128) return run_rs<64, 128>(a, w, st, info, pk_tc);
   if (a.r == 64 && a.s == 256) return run_rs<64, 256>(a, w, st, info, pk_tc);
-  if (a.r == 128 && a.s == 128) return run_rs<128, 128>(a, w, st, info, nullptr);
-  if (a.r == 128 && a.s == 256) return run_rs<128, 256>(a, w, st, info, nullptr);
+  if (a.r == 128 && a.s == 128) return run_rs<128, 128>(a, w, st, info, pk_tc);
+  if (a.r == 128 && a.s == 256) return run_rs<128, 256>(a, w, st, info, pk_tc);
   return cudaErrorNotSupported;
 }
 

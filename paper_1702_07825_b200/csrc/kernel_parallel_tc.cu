@@ -290,16 +290,16 @@ __global__ void __launch_bounds__(kLThr, 1) k_layer_tc(RunArgs A, int j, const f
 constexpr int kHW = 16 * 256 * 4;  // floats of one 64-K x 256-row image
 
 __device__ __forceinline__ void mma3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t w_hi, uint32_t w_lo,
-                                     bool acc, Sync& sy) {
+                                     bool acc, Sync& sy, int n = 256) {
   if (threadIdx.x == 0) {
     wait_bar(sy.bar_w, sy.ph_w);
     ptx::tmem_fence_after();
-    const uint32_t id = idesc_tf32(256);
+    const uint32_t id = idesc_tf32(n);
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
-      const uint32_t ao = ks * 2 * kTM * 16, bo = ks * 2 * 256 * 16;
+      const uint32_t ao = ks * 2 * kTM * 16, bo = ks * 2 * n * 16;
       const uint64_t dah = sdesc(a_hi + ao, kTM * 16, 128), dal = sdesc(a_lo + ao, kTM * 16, 128);
-      const uint64_t dbh = sdesc(w_hi + bo, 256 * 16, 128), dbl = sdesc(w_lo + bo, 256 * 16, 128);
+      const uint64_t dbh = sdesc(w_hi + bo, n * 16, 128), dbl = sdesc(w_lo + bo, n * 16, 128);
       mma_tf32(d, dah, dbh, id, (acc || ks > 0) ? 1u : 0u);
       mma_tf32(d, dah, dbl, id, 1u);
       mma_tf32(d, dal, dbh, id, 1u);
@@ -415,17 +415,158 @@ __global__ void __launch_bounds__(kLThr, 1) k_head_tc(RunArgs A, const float* Q,
   if (threadIdx.x < 32) ptx::tmem_dealloc(tmem_base, 512);
 }
 
+// ------------------------------------------------------------------ r = 128 (C4) layers
+// The same layer pass for r = 128, 256 threads, three tf32 passes into the same TMEM columns
+// (as the head): GEMM 1 K = 256 in four 64-chunks, N = 256 (D columns [0, 256)); the gate's
+// h stays in registers -- thread half hf holds channels 64 hf .. 64 hf + 63, exactly GEMM 2's
+// K-chunk hf -- so GEMM 2 (K = 128, rows [W_res; W_skip] in chunks of <= 256) can reuse GEMM
+// 1's columns.  Packed per layer: GEMM-1 chunks (hi | lo [16][256][4]), then for each GEMM-2
+// K-chunk its row chunks (hi | lo [16][n][4]).
+constexpr int R2 = 128;
+__host__ __device__ constexpr int64_t tc128_layer_floats(int s) { return 8 * (int64_t)kHW + 256 * (int64_t)(R2 + s); }
+
+template <int S>
+__global__ void __launch_bounds__(kLThr, 1) k_layer_tc128(RunArgs A, int j, const float* Xin, float* Xout, float* Q,
+                                                          const float* pk) {
+  extern __shared__ __align__(1024) float sm[];
+  float* a_hi = sm;
+  float* a_lo = sm + kActF;
+  float* w = sm + 2 * kActF;  // [hi image | lo image], <= 2 x [16][256][4]
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ uint32_t tmem_base;
+  const int t = threadIdx.x & (kTM - 1), hf = threadIdx.x >> 7;
+  const int st = blockIdx.y, t0 = blockIdx.x * kTM;
+  const int T = (int)A.N;
+  const int tg = t0 + t;
+  const bool live = tg < T;
+  const int64_t lo = (int64_t)j * A.off.layer_stride;
+  const float* xin = Xin + (int64_t)st * T * R2;
+  const float* pl = pk + (int64_t)j * tc128_layer_floats(S);
+  if (threadIdx.x < 32) ptx::tmem_alloc(ptx::smem_u32(&tmem_base), 512);
+  Sync sy;
+  sy.bar_w = ptx::smem_u32(&bars[0]);
+  sy.bar_m = ptx::smem_u32(&bars[1]);
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(sy.bar_w, 1);
+    ptx::mbar_init(sy.bar_m, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  ptx::tmem_fence_before();
+  __syncthreads();
+  ptx::tmem_fence_after();
+  const uint32_t d = tmem_base, lane = (uint32_t)(32 * (t >> 5)) << 16;
+  const uint32_t s_hi = ptx::smem_u32(a_hi), s_lo = ptx::smem_u32(a_lo), s_w = ptx::smem_u32(w);
+  // ---- GEMM 1: K-chunks 0, 1 = W_prev with x_j(t - d); 2, 3 = W_cur with x_j(t)
+#pragma unroll 1
+  for (int kc = 0; kc < 4; ++kc) {
+    fetch_w(s_w, pl + (int64_t)kc * 2 * kHW, 2 * kHW, sy);
+    const int tr = t0 - (kc < 2 ? A.dil[j] : 0) + t;
+    const bool in = tr >= 0 && tr < T;
+    const float4* src = reinterpret_cast<const float4*>(xin + (int64_t)(in ? tr : 0) * R2 + 64 * (kc & 1)) + 8 * hf;
+    float4 v[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) v[g] = in ? __ldg(src + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+    store_row(a_hi, a_lo, v, t, hf);
+    fence_proxy_async_smem();
+    __syncthreads();
+    mma3(d, s_hi, s_lo, s_w, s_w + kHW * 4, kc > 0, sy);
+  }
+  // ---- gate: this thread's 64 channels, h kept in registers
+  const float* bj = A.w + lo + A.off.b;
+  const float* L = A.cond + (((int64_t)st * A.n_frames + (live ? tg : 0) / A.hop) * A.L + j) * 2 * R2;
+  float h[64];
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    const int c0 = 64 * hf + 16 * cc;
+    float ah[16], ag[16];
+    ptx::tmem_ld16(d + lane + c0, ah);
+    ptx::tmem_ld16(d + lane + R2 + c0, ag);
+    ptx::tmem_wait_ld<16>(ah);
+    ptx::tmem_wait_ld<16>(ag);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int c = c0 + e;
+      const float xh = ah[e] + __ldg(bj + c) + (live ? __ldg(L + c) : 0.0f);
+      const float xg = ag[e] + __ldg(bj + R2 + c) + (live ? __ldg(L + R2 + c) : 0.0f);
+      h[16 * cc + e] = A.approx == 0 ? gate_fast(xh, xg) : A.approx == 1 ? gate_approx(xh, xg) : gate_appc(xh, xg);
+    }
+  }
+  ptx::tmem_fence_before();  // every lane has read GEMM 1's columns before GEMM 2 overwrites them
+  __syncthreads();
+  // ---- GEMM 2: K-chunk kc2 = h channels 64 kc2 .. (held by the threads with hf = kc2)
+  const float* w2 = pl + 8 * (int64_t)kHW;
+#pragma unroll 1
+  for (int kc2 = 0; kc2 < 2; ++kc2) {
+    if (hf == kc2) {
+#pragma unroll
+      for (int g = 0; g < 16; ++g) {
+        const int o = (g * kTM + t) * 4;
+        *reinterpret_cast<float4*>(a_hi + o) = make_float4(h[4 * g], h[4 * g + 1], h[4 * g + 2], h[4 * g + 3]);
+        *reinterpret_cast<float4*>(a_lo + o) =
+            make_float4(tf32_lo(h[4 * g]), tf32_lo(h[4 * g + 1]), tf32_lo(h[4 * g + 2]), tf32_lo(h[4 * g + 3]));
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+#pragma unroll 1
+    for (int r0 = 0; r0 < R2 + S; r0 += 256) {
+      const int n = std::min(256, R2 + S - r0);
+      fetch_w(s_w, w2, 2 * 16 * n * 4, sy);
+      mma3(d + r0, s_hi, s_lo, s_w, s_w + 16 * n * 4 * 4, kc2 > 0, sy, n);
+      w2 += 2 * 16 * n * 4;
+    }
+  }
+  // ---- epilogue: rows r of D = [W_res; W_skip] h (column r)
+  const float* bres = A.w + lo + A.off.b_res;
+  float* xout = Xout + (int64_t)st * T * R2;
+  float* q = Q + (int64_t)st * T * S;
+#pragma unroll 1
+  for (int g = hf; g < (R2 + S) / 16; g += 2) {
+    const int row = 16 * g;
+    float v[16];
+    ptx::tmem_ld16(d + lane + row, v);
+    ptx::tmem_wait_ld<16>(v);
+    if (!live) continue;
+    if (row < R2) {  // x_{j+1} = x_j + W_res h + B_res
+      const float4* xr = reinterpret_cast<const float4*>(xin + (int64_t)tg * R2 + row);
+      float4* xo = reinterpret_cast<float4*>(xout + (int64_t)tg * R2 + row);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float4 x = __ldg(xr + e), b = __ldg(reinterpret_cast<const float4*>(bres + row) + e);
+        xo[e] = make_float4(x.x + (v[4 * e] + b.x), x.y + (v[4 * e + 1] + b.y), x.z + (v[4 * e + 2] + b.z),
+                            x.w + (v[4 * e + 3] + b.w));
+      }
+    } else {  // q += W_skip h
+      float4* qq = reinterpret_cast<float4*>(q + (int64_t)tg * S + (row - R2));
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float4 a = qq[e];
+        a.x += v[4 * e];
+        a.y += v[4 * e + 1];
+        a.z += v[4 * e + 2];
+        a.w += v[4 * e + 3];
+        qq[e] = a;
+      }
+    }
+  }
+  ptx::tmem_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) ptx::tmem_dealloc(d, 512);
+}
+
 }  // namespace
 
 __host__ __device__ constexpr int64_t tc_head_floats(int s) { return (int64_t)(s / 64 + 4) * 2 * kHW; }
 
-int64_t parallel_tc_packed_floats(int L, int s) { return (int64_t)L * tc_layer_floats(s) + tc_head_floats(s); }
+static int64_t layer_floats(int r, int s) { return r == R2 ? tc128_layer_floats(s) : tc_layer_floats(s); }
+
+int64_t parallel_tc_packed_floats(int L, int r, int s) { return (int64_t)L * layer_floats(r, s) + tc_head_floats(s); }
 
 // [K/4][rows][4] operand images of every layer (host, once per dvw_load_weights): GEMM-1
 // chunks kc = 0 (W_prev) and 1 (W_cur), each 128 rows of the weight and 128 rows of its
 // tf32 residual; then GEMM-2 chunks of <= 128 rows of [W_res; W_skip] and their residuals.
 cudaError_t pack_parallel_tc(const float* w, const Offsets& o, int L, int r, int s, void* dst) {
-  if (r != R) return cudaErrorInvalidValue;
+  if (r != R && r != R2) return cudaErrorInvalidValue;
   auto lo_of = [](float x) {
     uint32_t u;
     std::memcpy(&u, &x, 4);
@@ -434,9 +575,36 @@ cudaError_t pack_parallel_tc(const float* w, const Offsets& o, int L, int r, int
     std::memcpy(&h, &u, 4);
     return x - h;
   };
-  const int64_t per = tc_layer_floats(s);
+  const int64_t per = layer_floats(r, s);
   std::vector<float> h((size_t)(L * per + tc_head_floats(s)), 0.0f);
-  for (int j = 0; j < L; ++j) {
+  if (r == R2) {  // r = 128: GEMM-1 64-K chunks (hi | lo [16][256][4]), GEMM-2 (K-chunk, row chunk)
+    for (int j = 0; j < L; ++j) {
+      const float* lw = w + (int64_t)j * o.layer_stride;
+      float* c = h.data() + (int64_t)j * per;
+      for (int kc = 0; kc < 4; ++kc, c += 2 * kHW) {
+        const float* W = lw + (kc < 2 ? o.w_prev : o.w_cur);  // [2r][r]
+        for (int k = 0; k < 64; ++k)
+          for (int n = 0; n < 2 * R2; ++n) {
+            const float v = W[(int64_t)n * R2 + 64 * (kc & 1) + k];
+            c[((k / 4) * 256 + n) * 4 + k % 4] = v;
+            c[kHW + ((k / 4) * 256 + n) * 4 + k % 4] = lo_of(v);
+          }
+      }
+      for (int kc2 = 0; kc2 < 2; ++kc2)
+        for (int r0 = 0; r0 < R2 + s; r0 += 256) {
+          const int n = std::min(256, R2 + s - r0);
+          for (int k = 0; k < 64; ++k)
+            for (int i = 0; i < n; ++i) {
+              const int row = r0 + i, kk = 64 * kc2 + k;
+              const float v = row < R2 ? lw[o.w_res + (int64_t)row * R2 + kk] : lw[o.w_skip + (int64_t)(row - R2) * R2 + kk];
+              c[((k / 4) * n + i) * 4 + k % 4] = v;
+              c[16 * n * 4 + ((k / 4) * n + i) * 4 + k % 4] = lo_of(v);
+            }
+          c += 2 * 16 * n * 4;
+        }
+    }
+  }
+  for (int j = 0; r == R && j < L; ++j) {
     const float* lw = w + (int64_t)j * o.layer_stride;
     float* out = h.data() + (int64_t)j * per;
     for (int kc = 0; kc < 2; ++kc) {
@@ -482,7 +650,7 @@ cudaError_t pack_parallel_tc(const float* w, const Offsets& o, int L, int r, int
 cudaError_t launch_parallel_head_tc(const RunArgs& a, const float* q, const float* pk, cudaStream_t st) {
   const dim3 grid((unsigned)((a.N + kTM - 1) / kTM), (unsigned)a.n_streams);
   const int smem = (int)sizeof(float) * (2 * kActF + 2 * kHW);
-  const float* ph = pk + (int64_t)a.L * tc_layer_floats(a.s);
+  const float* ph = pk + (int64_t)a.L * layer_floats(a.r, a.s);
   cudaError_t e;
   if (a.s == 256) {
     e = cudaFuncSetAttribute(k_head_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -499,8 +667,21 @@ cudaError_t launch_parallel_head_tc(const RunArgs& a, const float* q, const floa
 cudaError_t launch_parallel_layer_tc(const RunArgs& a, int j, const float* xin, float* xout, float* q,
                                      const float* pk, cudaStream_t st) {
   const dim3 grid((unsigned)((a.N + kTM - 1) / kTM), (unsigned)a.n_streams);
-  const int smem = (int)sizeof(float) * kSmemF;
   cudaError_t e;
+  if (a.r == R2) {
+    const int smem128 = (int)sizeof(float) * (2 * kActF + 2 * kHW);
+    if (a.s == 256) {
+      e = cudaFuncSetAttribute(k_layer_tc128<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem128);
+      if (e == cudaSuccess) k_layer_tc128<256><<<grid, kLThr, smem128, st>>>(a, j, xin, xout, q, pk);
+    } else if (a.s == 128) {
+      e = cudaFuncSetAttribute(k_layer_tc128<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem128);
+      if (e == cudaSuccess) k_layer_tc128<128><<<grid, kLThr, smem128, st>>>(a, j, xin, xout, q, pk);
+    } else {
+      return cudaErrorInvalidValue;
+    }
+    return e == cudaSuccess ? cudaGetLastError() : e;
+  }
+  const int smem = (int)sizeof(float) * kSmemF;
   if (a.s == 256) {
     e = cudaFuncSetAttribute(k_layer_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) k_layer_tc<256><<<grid, kLThr, smem, st>>>(a, j, xin, xout, q, pk);
