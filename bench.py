@@ -371,6 +371,32 @@ def main():
                            "codes equal to the one-call run"}
         sess.close()
 
+    # batch 1: teacher-forced logits of the same utterance on its own codes (dvw_logits, AUTO ->
+    # the parallel-over-time kernel, tcgen05 at r = 64 / 128), outside the timed region
+    tf_logits = None
+    if S == 1 and cond_net is None:
+        model.set_kernel("auto")
+        codes_dev = torch.from_numpy(gpu_codes0)[None].to(dev)
+        lg_buf = torch.empty((1, n, 256), dtype=torch.float32, device=dev)
+        model.logits(d_cond, codes_dev, HOP, out=lg_buf)
+        lev = []
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            model.logits(d_cond, codes_dev, HOP, out=lg_buf)
+            b.record(stream)
+            lev.append((a, b))
+        torch.cuda.synchronize(dev)
+        lms = float(np.median([a.elapsed_time(b) for a, b in lev]))
+        linfo = model.info()
+        tf_logits = {"ms_per_utterance": lms, "samples_per_s": n / (lms / 1e3), "kernel": linfo["last_kernel_name"],
+                     "launches": int(linfo["last_launches"]),
+                     "note": "dvw_logits on the generated codes (pre-softmax, all timesteps of a layer at once); "
+                             "not part of the metric; its parity with the oracle is tested "
+                             "(tests/test_gpu_parity.py, full C2 utterance)"}
+        model.set_kernel(args.kernel)
+        del lg_buf
+
     # max over ranks
     t_max, e_max = kernel_ms, (e2e_step if e2e_step is not None else -1.0)
     total_streams = S
@@ -457,6 +483,8 @@ def main():
             line["gather_results"] = gather
         if latency is not None:
             line["latency"] = latency
+        if tf_logits is not None:
+            line["teacher_forced_logits"] = tf_logits
         if not args.no_cpu:
             cond0 = d_cond[0].cpu().numpy()
             u0 = d_u[0].cpu().numpy()
