@@ -650,7 +650,9 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
           m.rr[jl][R + hrow] = v[1] + cf[jl * 2 * R + R + hrow];
         }
         if (ct == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 21 + jl);
-        bar_arrive(bar_ra(jl), kMain);
+        // sync, not arrive: C's next matvec (R_{j+1}) then starts only once A is past this
+        // layer's matvec, so it overlaps A's gate instead of competing with A's FMAs
+        ptx::bar_sync(bar_ra(jl), kMain);
       }
     }
   }
