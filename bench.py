@@ -350,7 +350,9 @@ def main():
     # batch 1: per-sample latency at 1,000-sample granularity -- the same
     # utterance through a streaming session in 1,000-sample chunks, CUDA events per chunk
     latency = None
-    if S == 1 and cond_net is None and info["last_kernel_name"] in ("cluster", "stream") and n >= 2000:
+    # (exact tiers only: approximate-tier sessions run on the stream kernel, not the one timed)
+    if (S == 1 and cond_net is None and info["last_kernel_name"] in ("cluster", "stream") and n >= 2000
+            and args.precision in ("fp32", "tf32")):
         sess = model.session(1)
         chunk = 1000
         cev = []
