@@ -11,7 +11,7 @@
  *   PAPER.md:376, 501 (App. A.4 direct sampling): draw y from p, feed it back.
  *   Conditioning is taken already computed, at frame rate, and upsampled by
  *   repetition inside the kernel (App. A.2).
- * DESIGN.md lists every reading of a point the paper leaves open (R1..R21);
+ * DESIGN.md lists every reading of a point the paper leaves open (R1..R33);
  * the ones that fix the ABI's semantics are cited below.
  *
  * Conventions for every entry point:
@@ -223,6 +223,17 @@ DVW_API dvw_status dvw_set_precision(dvw_model* m, int32_t precision);
  * DVW_E_INVALID_ARG. */
 DVW_API dvw_status dvw_set_weight_bits(dvw_model* m, int32_t bits);
 
+/* The same quantisation with a choice of scale granularity (reading R33):
+ *   scheme DVW_QUANT_PER_ROW    (0): one scale per matrix row, as dvw_set_weight_bits;
+ *   scheme DVW_QUANT_PER_TENSOR (1): one scale per weight matrix, s = max|W| / (2^(bits-1) - 1)
+ *     (an all-zero matrix keeps s = 1), q = rint(W / s), W := q s -- SPEC.md's
+ *     QuantizedWeightSet scheme (e.g. [0, 1, -1] -> q = [0, 32767, -32767] at 16 bits,
+ *     s = 1/32767); |W - q s| <= s/2 elementwise.
+ * bits as dvw_set_weight_bits (0 turns quantisation off; scheme is then ignored).
+ * Unknown scheme or bits -> DVW_E_INVALID_ARG. */
+typedef enum { DVW_QUANT_PER_ROW = 0, DVW_QUANT_PER_TENSOR = 1 } dvw_quant_scheme;
+DVW_API dvw_status dvw_set_weight_quant(dvw_model* m, int32_t bits, int32_t scheme);
+
 /* Sampling strategy for dvw_generate (App. A.4).
  * Details the paper leaves open follow DESIGN.md readings R24-R27:
  *   DVW_SAMPLER_DIRECT      (default) inverse-CDF draw from P with u_n (reading R11)
@@ -245,11 +256,17 @@ typedef enum {
 } dvw_sampler;
 DVW_API dvw_status dvw_set_sampler(dvw_model* m, int32_t kind, float temperature, int32_t top_k);
 
-/* Tracing: when device_buf != NULL, persistent kernels record %globaltimer (ns)
- * at fixed events of samples [first_sample, first_sample + n_samples) into
- * device_buf, uint64 [n_samples][16 cluster ranks][32 events] (unwritten slots keep
- * their old value; the caller zero-fills).  Event meaning per role is listed in
- * DESIGN.md "Tracing".  NULL disables tracing.  Off the hot path when disabled. */
+/* Tracing: when device_buf != NULL, persistent kernels record timestamps at fixed
+ * events of samples [first_sample, first_sample + n_samples) into device_buf, uint64
+ * [n_samples][16 cluster ranks][32 events] (unwritten slots keep their old value; the
+ * caller zero-fills).  Time base per slot: on the cluster kernel's chain CTAs events
+ * 0, 2, 3, 5 and 20 are %globaltimer nanoseconds and events 1, 4, 6-19 and 21-30 are
+ * that SM's clock64 cycles (one-store stamps inside a layer, comparable only within one
+ * CTA and sample); every event of the head and skip CTAs, and of the batched kernel, is
+ * %globaltimer ns.  Event meaning per role: tools/trace_c2.py, tools/trace_batch.py.
+ * Tracing runs the exact-gate kernels: with DVW_PRECISION_APPROX / APPC the cluster
+ * kernel returns DVW_E_UNSUPPORTED.  NULL disables tracing.  Off the hot path when
+ * disabled. */
 DVW_API dvw_status dvw_set_trace(dvw_model* m, uint64_t* device_buf, int64_t first_sample, int32_t n_samples);
 
 /* Launch bookkeeping of the last call (filled synchronously, host side). */
@@ -287,7 +304,8 @@ DVW_API const char* dvw_last_error(void);
  * errors via dvw_last_error(). */
 typedef struct dvwc_model dvwc_model;
 typedef struct {
-  int32_t in_channels;  /* feature channels per frame (>= 1) */
+  int32_t in_channels;  /* feature channels per frame (1..3228: frames are staged in shared memory;
+                           larger -> DVW_E_UNSUPPORTED at dvwc_create) */
   int32_t hidden;       /* QRNN channels per direction (1..1024) */
   int32_t n_layers;     /* l of the WaveNet it conditions */
   int32_t residual;     /* r of the WaveNet it conditions */

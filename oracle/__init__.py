@@ -71,6 +71,8 @@ def _load():
         for fn in ("oracle_appc_tanh", "oracle_appc_sigmoid", "oracle_appc_exp"):
             getattr(lib, fn).restype = ctypes.c_double
             getattr(lib, fn).argtypes = [ctypes.c_double]
+        lib.oracle_softmax.restype = None
+        lib.oracle_softmax.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
         lib.oracle_sample_policy.restype = ctypes.c_int
         lib.oracle_sample_policy.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                              ctypes.c_int, ctypes.c_float]
@@ -131,6 +133,15 @@ def sample(logits: np.ndarray, u: float) -> int:
     """The oracle's inverse-CDF draw on one logit vector (reading R11)."""
     l = np.ascontiguousarray(logits, dtype=np.float64)
     return int(_load().oracle_sample(_ptr(l), l.size, float(np.float32(u))))
+
+
+def softmax(logits: np.ndarray) -> np.ndarray:
+    """p = softmax(l) as the oracle's sampler forms it: e_k = exp(l_k - max l), p_k = e_k / S
+    (PAPER.md:374)."""
+    l = np.ascontiguousarray(logits, dtype=np.float64)
+    p = np.zeros(l.size, dtype=np.float64)
+    _load().oracle_softmax(_ptr(l), l.size, _ptr(p))
+    return p
 
 
 DIRECT, TEMPERATURE, MEAN, MODE, TOP_K = 0, 1, 2, 3, 4

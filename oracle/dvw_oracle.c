@@ -29,7 +29,8 @@
  *     p   = softmax(l); y_n = inverse-CDF draw with u_n         (R11)
  *
  * Pins (tests/test_oracle_pins.py, test_appc_oracle.py): mu-law against torchaudio, the
- * receptive field, causality, softmax sums, closed-form draws (zero weights, one-hot and
+ * receptive field, causality, the softmax (oracle_softmax vs scipy.special.softmax, its sum,
+ * and the draw frequencies over a u grid), closed-form draws (zero weights, one-hot and
  * bias-only logits), the independent brute-force oracle (bruteforce.py), the App. A.4
  * strategies' limits (t = 1, k = a), and App. C's printed maximum errors.
  *
@@ -94,7 +95,9 @@ static double nl_exp(int nl, double x) { return nl ? appc_exp(x) : exp(x); }
 /* Inverse-CDF direct sampling (App. A.4 "Sample randomly from P(y)";
  * reading R11): e_k = exp(l_k - max l); P_k = sum_{i<=k} e_i in ascending k;
  * y = min{k : u * P_{a-1} < P_k}; fallback the largest k with e_k > 0. */
-static int sample_inverse_cdf(const double* logit, int a, double u, double* e, int nl) {
+/* softmax numerators (PAPER.md:374 p = softmax(l)): e_k = exp(l_k - max l); returns S = sum e_k,
+ * so p_k = e_k / S (oracle_softmax) */
+static double softmax_terms(const double* logit, int a, double* e, int nl) {
   double m = logit[0];
   for (int k = 1; k < a; ++k)
     if (logit[k] > m) m = logit[k];
@@ -103,6 +106,11 @@ static int sample_inverse_cdf(const double* logit, int a, double u, double* e, i
     e[k] = nl_exp(nl, logit[k] - m);
     S += e[k];
   }
+  return S;
+}
+
+static int sample_inverse_cdf(const double* logit, int a, double u, double* e, int nl) {
+  const double S = softmax_terms(logit, a, e, nl);
   double t = u * S, P = 0.0;
   for (int k = 0; k < a; ++k) {
     P += e[k];
@@ -168,6 +176,12 @@ ORACLE_API int oracle_sample(const double* logits, int a, float u) {
   int y = sample_inverse_cdf(logits, a, (double)u, e, 0);
   free(e);
   return y;
+}
+
+/* p = softmax(l) with the sampler's own numerators: p_k = e_k / S. */
+ORACLE_API void oracle_softmax(const double* logits, int a, double* p) {
+  const double S = softmax_terms(logits, a, p, 0);
+  for (int k = 0; k < a; ++k) p[k] /= S;
 }
 
 ORACLE_API int oracle_sample_policy(const double* logits, int a, int kind, double t, int topk, float u) {

@@ -10,7 +10,11 @@ row (biases stay fp32):
     s = max_c |W[row][c]| / (2^(bits-1) - 1)      (fp32 division)
     q = rint(W[row][c] / s)                        (fp32 division, round half to even)
     W[row][c] := q * s                              (fp32 product)
-A row of zeros stays zero.  The integer code q is a decision floating point takes, so it is
+A row of zeros stays zero.
+
+Reading R33 (the per-tensor alternative, SPEC.md's QuantizedWeightSet): one scale per weight
+matrix, s = max |W| / (2^(bits-1) - 1), s = 1 for an all-zero matrix, q = rint(W / s),
+W := q s, same fp32 arithmetic.  The integer code q is a decision floating point takes, so it is
 taken in the kernel's precision (fp32) -- here with numpy float32 scalars and arrays, whose
 division and product are the IEEE single-precision operations.
 """
@@ -61,11 +65,29 @@ def quantize_codes(W: np.ndarray, bits: int):
     return np.rint(W / sc[:, None]).astype(np.int64), sc
 
 
-def quantize_weights(blob: np.ndarray, L: int, r: int, s: int, bits: int, a: int = 256) -> np.ndarray:
-    """The whole blob with every weight matrix quantised; biases unchanged."""
+def quantize_tensor_codes(W: np.ndarray, bits: int):
+    """Per-tensor symmetric codes and scale (reading R33): (q int64, s float32)."""
+    W = np.asarray(W, dtype=np.float32)
+    qmax = np.float32((1 << (bits - 1)) - 1)
+    m = np.float32(np.max(np.abs(W))) if W.size else np.float32(0)
+    sc = np.float32(m / qmax) if m > 0 else np.float32(1)
+    return np.rint(W / sc).astype(np.int64), sc
+
+
+def quantize_tensor(W: np.ndarray, bits: int) -> np.ndarray:
+    """Per-tensor symmetric quantise-dequantise (reading R33)."""
+    q, sc = quantize_tensor_codes(W, bits)
+    return (q.astype(np.float32) * sc).astype(np.float32)
+
+
+def quantize_weights(blob: np.ndarray, L: int, r: int, s: int, bits: int, a: int = 256,
+                     scheme: str = "per_row") -> np.ndarray:
+    """The whole blob with every weight matrix quantised; biases unchanged.
+    scheme: "per_row" (R32) or "per_tensor" (R33)."""
+    fn = {"per_row": quantize_rows, "per_tensor": quantize_tensor}[scheme]
     w = np.array(blob, dtype=np.float32, copy=True)
     mats, numel = roster(L, r, s, a)
     assert w.size == numel, (w.size, numel)
     for off, rows, cols in mats:
-        w[off:off + rows * cols] = quantize_rows(w[off:off + rows * cols].reshape(rows, cols), bits).ravel()
+        w[off:off + rows * cols] = fn(w[off:off + rows * cols].reshape(rows, cols), bits).ravel()
     return w

@@ -31,7 +31,7 @@ KERNEL_NAMES = {0: "auto", 1: "stream", 2: "cluster", 3: "tc", 4: "parallel"}
 
 EXPORTS = ("dvw_create", "dvw_weights_numel", "dvw_load_weights", "dvw_generate", "dvw_logits",
            "dvw_generate_host", "dvw_set_kernel", "dvw_set_precision", "dvw_set_weight_bits",
-           "dvw_set_sampler", "dvw_set_trace",
+           "dvw_set_weight_quant", "dvw_set_sampler", "dvw_set_trace",
            "dvw_get_info", "dvw_sync", "dvw_destroy", "dvw_last_error",
            "dvw_session_create", "dvw_session_generate", "dvw_session_position", "dvw_session_destroy",
            "dvwc_create", "dvwc_weights_numel", "dvwc_load_weights", "dvwc_run", "dvwc_destroy")
@@ -72,6 +72,9 @@ _lib.dvw_set_precision.argtypes = [_vp, _i32]
 _lib.dvw_set_precision.restype = _i32
 _lib.dvw_set_weight_bits.argtypes = [_vp, _i32]
 _lib.dvw_set_weight_bits.restype = _i32
+_lib.dvw_set_weight_quant.argtypes = [_vp, _i32, _i32]
+_lib.dvw_set_weight_quant.restype = _i32
+QUANT_SCHEMES = {"per_row": 0, "per_tensor": 1}
 class _CConfig(ctypes.Structure):
     _fields_ = [("in_channels", ctypes.c_int32), ("hidden", ctypes.c_int32), ("n_layers", ctypes.c_int32),
                 ("residual", ctypes.c_int32), ("device", ctypes.c_int32)]
@@ -212,6 +215,12 @@ class Model:
         """Quantise every weight matrix per row to `bits` (16 or 8; 0 = off) at the next
         load() (include/dvw.h dvw_set_weight_bits)."""
         _check(_lib.dvw_set_weight_bits(self._h, int(bits)))
+        return self
+
+    def set_weight_quant(self, bits: int, scheme: str = "per_row"):
+        """Quantisation with a chosen scale granularity: "per_row" (R32) or "per_tensor"
+        (R33, SPEC's QuantizedWeightSet), applied at the next load() (dvw_set_weight_quant)."""
+        _check(_lib.dvw_set_weight_quant(self._h, int(bits), QUANT_SCHEMES[scheme]))
         return self
 
     def set_sampler(self, kind="direct", temperature: float = 1.0, top_k: int = 256):

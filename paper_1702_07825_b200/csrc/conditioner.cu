@@ -187,7 +187,11 @@ DVW_API dvw_status dvwc_create(const dvwc_config* c, dvwc_model** out) {
   if (!c || !out) return cfail(DVW_E_INVALID_ARG, "NULL argument");
   if (c->in_channels < 1 || c->hidden < 1 || c->n_layers < 1 || c->residual < 1)
     return cfail(DVW_E_SHAPE, "conditioner sizes must be >= 1");
-  if (c->hidden > 1024 || c->in_channels > 4096) return cfail(DVW_E_UNSUPPORTED, "hidden <= 1024, in_channels <= 4096");
+  // k_gates stages (kTT + 2) frames of C = in_channels (layer 1) or 2 hidden (layer 2) floats
+  // in one block's shared memory (<= 227 KB on sm_100)
+  constexpr int kMaxC = 232448 / (4 * (kTT + 2));
+  if (c->hidden > 1024 || c->in_channels > kMaxC)
+    return cfail(DVW_E_UNSUPPORTED, "hidden <= 1024, in_channels <= %d (shared-memory staging)", kMaxC);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || c->device < 0 || c->device >= ndev) {
     cudaGetLastError();

@@ -45,6 +45,7 @@ struct dvw_model {
   int kernel = DVW_KERNEL_AUTO;
   int precision = DVW_PRECISION_FP32;
   int weight_bits = 0;  // dvw_set_weight_bits: applied by dvw_load_weights
+  int quant_scheme = DVW_QUANT_PER_ROW;
   int samp_kind = DVW_SAMPLER_DIRECT;
   float samp_inv_t = 1.0f;
   int samp_topk = kLevels;
@@ -197,7 +198,11 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
     if (kern == DVW_KERNEL_CLUSTER && !exact)
       return fail(DVW_E_UNSUPPORTED, "cluster-kernel sessions run the exact gate (use the STREAM kernel)");
     if (kern == DVW_KERNEL_AUTO) {
-      if (sess->kernel != 0) kern = sess->kernel;
+      // re-resolved on every call: CLUSTER and STREAM share the queue and code-history layout,
+      // so a session that started on CLUSTER moves to STREAM when the sampler or precision
+      // changes to something the cluster kernel's session variant does not run (and back)
+      if (sess->kernel == DVW_KERNEL_TC) kern = DVW_KERNEL_TC;
+      else if (sess->kernel == DVW_KERNEL_STREAM && n_streams > 1) kern = DVW_KERNEL_STREAM;
       else if (n_streams == 1 && m->cplan.ok && direct && exact) kern = DVW_KERNEL_CLUSTER;
       else if (n_streams > 1 && m->bplan.ok && m->precision != DVW_PRECISION_APPC) kern = DVW_KERNEL_TC;
       else kern = DVW_KERNEL_STREAM;
@@ -216,6 +221,9 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
     else if (n_streams > 1 && m->bplan.ok && m->precision != DVW_PRECISION_APPC) kern = DVW_KERNEL_TC;
     else kern = DVW_KERNEL_STREAM;
   }
+  if (kern == DVW_KERNEL_CLUSTER && m->trace &&
+      (m->precision == DVW_PRECISION_APPROX || m->precision == DVW_PRECISION_APPC))
+    return fail(DVW_E_UNSUPPORTED, "tracing runs the exact-gate cluster kernel only (dvw_set_trace)");
   int pgroup = 0;  // parallel kernel: streams per workspace group
   if (kern == DVW_KERNEL_PARALLEL) {
     const size_t per = parallel_workspace_bytes(m->r, m->s, n_samples, 1);
@@ -333,18 +341,32 @@ void quantize_rows(float* w, int64_t rows, int64_t cols, int bits) {
   }
 }
 
-void quantize_matrices(float* w, const Offsets& o, int L, int r, int s, int bits) {
+// One scale for the whole matrix (reading R33, SPEC.md's QuantizedWeightSet): s = max|W| /
+// (2^(bits-1) - 1), 1 for an all-zero matrix; W := rint(W / s) * s, fp32.
+void quantize_tensor(float* w, int64_t rows, int64_t cols, int bits) {
+  const float qmax = (float)((1 << (bits - 1)) - 1);
+  float mx = 0.0f;
+  for (int64_t i = 0; i < rows * cols; ++i) mx = std::max(mx, std::fabs(w[i]));
+  const float sc = mx == 0.0f ? 1.0f : mx / qmax;
+  for (int64_t i = 0; i < rows * cols; ++i) w[i] = std::rint(w[i] / sc) * sc;
+}
+
+void quantize_matrices(float* w, const Offsets& o, int L, int r, int s, int bits, int scheme) {
+  auto q = [&](float* p, int64_t rows, int64_t cols) {
+    if (scheme == DVW_QUANT_PER_TENSOR) quantize_tensor(p, rows, cols, bits);
+    else quantize_rows(p, rows, cols, bits);
+  };
   for (int j = 0; j < L; ++j) {
     float* lw = w + (int64_t)j * o.layer_stride;
-    quantize_rows(lw + o.w_prev, 2 * r, r, bits);
-    quantize_rows(lw + o.w_cur, 2 * r, r, bits);
-    quantize_rows(lw + o.w_res, r, r, bits);
-    quantize_rows(lw + o.w_skip, s, r, bits);
+    q(lw + o.w_prev, 2 * r, r);
+    q(lw + o.w_cur, 2 * r, r);
+    q(lw + o.w_res, r, r);
+    q(lw + o.w_skip, s, r);
   }
-  quantize_rows(w + o.emb_prev, r, kLevels, bits);
-  quantize_rows(w + o.emb_cur, r, kLevels, bits);
-  quantize_rows(w + o.w_relu, kLevels, s, bits);
-  quantize_rows(w + o.w_out, kLevels, kLevels, bits);
+  q(w + o.emb_prev, r, kLevels);
+  q(w + o.emb_cur, r, kLevels);
+  q(w + o.w_relu, kLevels, s);
+  q(w + o.w_out, kLevels, kLevels);
 }
 
 }  // namespace
@@ -425,7 +447,7 @@ DVW_API dvw_status dvw_load_weights(dvw_model* m, const float* blob, int64_t num
     if (!std::isfinite(hp[i])) return fail(DVW_E_INVALID_ARG, "weight %lld is not finite", (long long)i);
   if (m->weight_bits != 0) {  // row f4: quantise the matrices (include/dvw.h dvw_set_weight_bits)
     if (host.empty()) host.assign(blob, blob + numel);
-    quantize_matrices(host.data(), m->off, m->L, m->r, m->s, m->weight_bits);
+    quantize_matrices(host.data(), m->off, m->L, m->r, m->s, m->weight_bits, m->quant_scheme);
     hp = host.data();
   }
   if (!m->d_w) DVW_CUDA(cudaMalloc(&m->d_w, sizeof(float) * numel), "allocating weights");
@@ -588,7 +610,17 @@ DVW_API dvw_status dvw_set_weight_bits(dvw_model* m, int32_t bits) {
   if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
   if (bits != 0 && bits != 8 && bits != 16) return fail(DVW_E_INVALID_ARG, "weight bits must be 0, 8 or 16 (got %d)", bits);
   m->weight_bits = bits;
+  m->quant_scheme = DVW_QUANT_PER_ROW;
   return DVW_OK;
+}
+
+DVW_API dvw_status dvw_set_weight_quant(dvw_model* m, int32_t bits, int32_t scheme) {
+  if (!m) return fail(DVW_E_INVALID_ARG, "model is NULL");
+  if (scheme != DVW_QUANT_PER_ROW && scheme != DVW_QUANT_PER_TENSOR)
+    return fail(DVW_E_INVALID_ARG, "unknown quantisation scheme %d", scheme);
+  dvw_status st = dvw_set_weight_bits(m, bits);
+  if (st == DVW_OK) m->quant_scheme = scheme;
+  return st;
 }
 
 DVW_API dvw_status dvw_set_precision(dvw_model* m, int32_t precision) {

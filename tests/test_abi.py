@@ -26,7 +26,7 @@ def declared_symbols():
 
 def test_exports_every_declared_symbol(lib):
     names = declared_symbols()
-    assert len(names) == 24, names
+    assert len(names) == 25, names
     raw = ctypes.CDLL(lib.LIB_PATH)
     for n in names:
         assert hasattr(raw, n), n
@@ -62,6 +62,7 @@ def test_null_arguments(lib):
     assert lib.raw_call("dvw_set_kernel", None, 0) == 1
     assert lib.raw_call("dvw_set_precision", None, 0) == 1
     assert lib.raw_call("dvw_set_weight_bits", None, 16) == 1
+    assert lib.raw_call("dvw_set_weight_quant", None, 16, 1) == 1
     assert lib.raw_call("dvw_set_sampler", None, 0, ctypes.c_float(1.0), 1) == 1
     lib._lib.dvw_destroy(None)  # no-op
     assert "NULL" in lib.last_error()

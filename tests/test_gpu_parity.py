@@ -19,6 +19,13 @@ GATE = 1e-3        # north_star teacher-forced tolerance
 FP32_FAITHFUL = 2e-5
 
 
+def mismatch_budget(n_steps, per_16k=2):
+    """Allowed per-step mismatches against the fp64 oracle for an fp32-faithful tier
+    (SURVEY.md §8(c) calibration: ~3e-7 per step predicted, 0 of 32,000 measured in the
+    emulation; a rate far above ~1e-5 is a numerics bug): 2 per 16,000 steps, at least 1."""
+    return max(1, int(np.ceil(n_steps * per_16k / 16000)))
+
+
 @pytest.fixture(scope="module")
 def L():
     if not torch.cuda.is_available():
@@ -283,7 +290,7 @@ def test_tc_fast_tf32_mode_within_gate(L, cfg):
     print(f"tf32 {cfg}: max|dlogit| = {worst:.2e}, per-step mismatches {mism}/{N * len(utts)}")
     assert worst <= GATE
     assert worst > FP32_FAITHFUL / 10  # it really is the reduced-precision path
-    assert mism <= 0.05 * N * len(utts)
+    assert mism <= 0.01 * N * len(utts)  # predicted ~2.6e-3 per step (10.7 x 2.4e-4)
     m.set_precision("fp32")
     lg32 = m.logits(dev(cond), dev(codes), hop).cpu().numpy()
     _, ref_lg, _ = oracle_tf(cfg, w, cond[0], hop, codes[0])
@@ -385,7 +392,7 @@ def test_approx_gate_tier_within_gate(L, kernel):
     mism = int(np.sum(sampled != codes))
     print(f"approx {kernel}: max|dlogit| = {err:.2e}, per-step mismatches {mism}/{N}")
     assert err <= GATE
-    assert mism <= 0.01 * N
+    assert mism <= mismatch_budget(N, per_16k=20)  # predicted ~5e-6 per step (10.7 x 5e-7)
     m.set_precision("fp32")
     lg32 = m.logits(dev(cond)[None], dev(codes)[None], hop).cpu().numpy()[0]
     assert float(np.max(np.abs(lg32.astype(np.float64) - ref_lg))) <= FP32_FAITHFUL
@@ -419,7 +426,7 @@ def test_appc_tier_matches_oracle_appc(L, kernel, cfg):
     if kernel != "parallel":
         mism = int(np.sum(sampled != codes))
         print(f"  free-running per-step mismatches {mism}/{N}")
-        assert mism <= 0.005 * N
+        assert mism <= mismatch_budget(N)
 
 
 def test_appc_tier_routing(L):
@@ -438,6 +445,60 @@ def test_appc_tier_routing(L):
     m.set_kernel("tc")
     with pytest.raises(L.DvwError):
         m.generate(dev(cond), dev(u), hop)
+
+
+@pytest.mark.parametrize("kernel", ["cluster", "stream"])
+def test_per_tensor_quantisation_matches_oracle(L, kernel):
+    """Reading R33 (SPEC's per-tensor QuantizedWeightSet): dvw_set_weight_quant(16, per_tensor)
+    equals the fp64 oracle on the oracle's own per-tensor quantised blob."""
+    from oracle import quant
+    cfg = synth.C1
+    N, hop = 800, 64
+    w = synth.make_weights(cfg, 0)
+    wq = quant.quantize_weights(w, cfg.n_layers, cfg.residual, cfg.skip, 16, scheme="per_tensor")
+    cond = synth.make_cond(cfg, synth.n_frames_for(N, hop), 0)
+    u = synth.make_uniforms(N, 0)
+    m = L.Model.from_config(cfg).set_weight_quant(16, "per_tensor").load(w).set_kernel(kernel)
+    codes = m.generate(dev(cond)[None], dev(u)[None], hop).cpu().numpy()[0]
+    lg = m.logits(dev(cond)[None], dev(codes)[None], hop).cpu().numpy()[0]
+    _, ref, sampled = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, wq, cond, hop, N, uniforms=u,
+                                 forced=codes, want_sampled=True)
+    assert float(np.max(np.abs(lg.astype(np.float64) - ref))) <= FP32_FAITHFUL
+    assert int(np.sum(sampled != codes)) <= mismatch_budget(N)
+
+
+def test_session_follows_sampler_and_precision_changes(L):
+    """a session that started on the cluster kernel moves to the stream kernel
+    when the sampler changes (the cluster kernel draws directly only) and back when it is
+    direct again; every chunk follows the strategy in force (oracle teacher-forced on the
+    session's codes: direct draws with u, then argmax for "mode")."""
+    cfg = synth.C1
+    N, hop = 600, 64
+    w = synth.make_weights(cfg, 0, "peaky")
+    cond = synth.make_cond(cfg, synth.n_frames_for(N, hop), 0)
+    u = synth.make_uniforms(N, 0)
+    m = L.Model.from_config(cfg).load(w)
+    dc, du = dev(cond)[None], dev(u)[None]
+    sess = m.session(1)
+    parts, kern = [], []
+    for lo, hi, samp in [(0, 200, "direct"), (200, 400, "mode"), (400, 600, "direct")]:
+        m.set_sampler(samp)
+        parts.append(sess.generate(dc, du[:, lo:hi].contiguous(), hop).cpu().numpy()[0])
+        kern.append(m.info()["last_kernel_name"])
+    sess.close()
+    assert kern == ["cluster", "stream", "cluster"], kern
+    codes = np.concatenate(parts)
+    _, lg, sampled = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, N, uniforms=u,
+                                forced=codes, want_sampled=True)
+    assert np.array_equal(sampled[:200], codes[:200])
+    assert np.array_equal(np.argmax(lg[200:400], axis=1), codes[200:400])
+    assert np.array_equal(sampled[400:], codes[400:])
+    # an approximate tier mid-session also leaves the cluster kernel
+    m.set_precision("approx")
+    sess = m.session(1)
+    sess.generate(dc, du[:, :100].contiguous(), hop)
+    assert m.info()["last_kernel_name"] == "stream"
+    sess.close()
 
 
 @pytest.mark.parametrize("kernel", ["cluster", "stream", "tc", "parallel"])
@@ -472,7 +533,7 @@ def test_quantized_weights_match_oracle_on_quantized_blob(L, kernel, bits):
         print(f"int{bits} {kernel} stream {st}: max|dlogit| vs oracle(quantised) {err:.2e}")
         assert err <= FP32_FAITHFUL
         if kernel != "parallel":
-            assert int(np.sum(sampled != codes[st])) <= 0.005 * N
+            assert int(np.sum(sampled != codes[st])) <= mismatch_budget(N)
     # quantisation applies at load: switching it off and reloading restores the fp32 model
     m.set_weight_bits(0).load(w).set_kernel("stream")
     lg0 = m.logits(dev(cond[:1]), dev(codes[:1]), hop).cpu().numpy()[0]
@@ -620,7 +681,7 @@ def test_c2_full_utterance_cluster_bench_config(L):
                                     forced=codes, want_sampled=True)
     mism = int(np.sum(sampled != codes))
     print(f"C2 16,000 samples: per-step mismatches {mism}")
-    assert np.array_equal(sampled[:1600], codes[:1600]) and mism <= 16
+    assert np.array_equal(sampled[:1600], codes[:1600]) and mism <= mismatch_budget(N)
     lg = m.set_kernel("parallel").logits(dev(cond)[None], dev(codes)[None], hop).cpu().numpy()[0]
     win = slice(N - 64, N)
     assert float(np.max(np.abs(lg[win].astype(np.float64) - ref_lg[win]))) <= FP32_FAITHFUL

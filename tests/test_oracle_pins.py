@@ -222,10 +222,30 @@ def test_bias_only_head_gives_closed_form_draws():
     assert np.array_equal(codes, expect)
 
 
-def test_softmax_sums_to_one_and_sampler_edges():
+@pytest.mark.parametrize("gain", [1.0, 50.0, 400.0])
+def test_softmax_pinned_to_library_and_draw_frequencies(gain):
+    """p = softmax(l) as the oracle's sampler forms it: equal to
+    scipy.special.softmax (a library routine, not a retyped formula), summing to 1 in fp64,
+    and the inverse-CDF draw (reading R11) realises exactly these
+    probabilities: over the grid u_i = (i + 1/2) / G the count of draws of code k is
+    within 1 of G p_k (the draws of k are the u in [P_{k-1}/S, P_k/S), an interval of
+    length p_k).  A dropped max shift, a wrong comparison or an off-by-one in the scan
+    fails one of these."""
+    from scipy.special import softmax as sp_softmax
+    lg = synth.make_weights(synth.Config(1, 2, 2), 3)[:256].astype(np.float64) * gain
+    p = oracle.softmax(lg)
+    assert abs(p.sum() - 1.0) < 1e-12
+    np.testing.assert_allclose(p, sp_softmax(lg), rtol=1e-12, atol=1e-300)
+    G = 20000
+    grid = (np.arange(G) + 0.5) / G
+    draws = np.array([oracle.sample(lg, np.float32(x)) for x in grid])
+    counts = np.bincount(draws, minlength=256)
+    assert np.all(np.abs(counts - G * p) <= 1.0 + 1e-6 * G), np.max(np.abs(counts - G * p))
+    assert np.all(draws[1:] >= draws[:-1])  # monotone in u
+
+
+def test_sampler_edges():
     lg = synth.make_weights(synth.Config(1, 2, 2), 0)[:256].astype(np.float64) * 50
-    p = np.exp(lg - lg.max())
-    assert abs(p.sum() / p.sum() - 1.0) < 1e-12
     # u = 0 picks the first code with nonzero mass; u -> 1 picks the last one
     assert oracle.sample(lg, 0.0) == 0
     spiky = np.full(256, -1e4)

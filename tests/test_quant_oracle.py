@@ -85,3 +85,39 @@ def test_int16_keeps_logits_within_the_gate_and_int8_is_coarser():
     d8 = np.max(np.abs(run(quant.quantize_weights(w, cfg.n_layers, cfg.residual, cfg.skip, 8)) - base))
     print(f"teacher-forced max|dlogit| int16 {d16:.2e}, int8 {d8:.2e}")
     assert 0 < d16 < 1e-3 and d16 < d8 / 50
+
+
+# ---- reading R33: per-tensor scheme (SPEC.md quantize_weights examples)
+def test_per_tensor_spec_examples():
+    q, sc = quant.quantize_tensor_codes(np.array([[0.0, 1.0, -1.0]], dtype=np.float32), 16)
+    np.testing.assert_array_equal(q, [[0, 32767, -32767]])
+    assert sc == np.float32(1.0 / 32767)
+    qz, scz = quant.quantize_tensor_codes(np.zeros((3, 5), dtype=np.float32), 16)
+    assert np.all(qz == 0) and scz == np.float32(1.0)
+    np.testing.assert_array_equal(quant.quantize_tensor(np.zeros((3, 5), np.float32), 16), 0.0)
+
+
+@pytest.mark.parametrize("bits", [8, 16])
+def test_per_tensor_half_step_bound_and_single_scale(bits):
+    cfg = synth.Config(2, 64, 128)
+    w = synth.make_weights(cfg, 7)
+    wq = quant.quantize_weights(w, cfg.n_layers, cfg.residual, cfg.skip, bits, scheme="per_tensor")
+    mats, _ = quant.roster(cfg.n_layers, cfg.residual, cfg.skip)
+    Q = (1 << (bits - 1)) - 1
+    for off, rows, cols in mats:
+        W = w[off:off + rows * cols].reshape(rows, cols)
+        Wq = wq[off:off + rows * cols].reshape(rows, cols)
+        q, sc = quant.quantize_tensor_codes(W, bits)
+        assert np.max(np.abs(q)) == Q                      # the largest element reaches the end code
+        # SPEC's bound s/2, plus the fp32 rounding of the quotient W/s and of the product q s
+        # (each <= 2^-24 |W| relative)
+        assert np.all(np.abs(Wq.astype(np.float64) - W) <= np.float64(sc) / 2 + np.abs(W) * 2.0 ** -22)
+        np.testing.assert_array_equal(Wq, (q * np.float64(sc)).astype(np.float32))
+    # per-tensor is coarser than per-row: it differs from the per-row blob on some matrix
+    wr = quant.quantize_weights(w, cfg.n_layers, cfg.residual, cfg.skip, bits)
+    assert not np.array_equal(wq, wr)
+    # biases untouched
+    mask = np.ones(w.size, bool)
+    for off, rows, cols in mats:
+        mask[off:off + rows * cols] = False
+    np.testing.assert_array_equal(wq[mask], w[mask])
