@@ -218,16 +218,12 @@ def cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, budget_samples, gpu_t
     return cpu, parity
 
 
-def device_inputs(cfg, n, utts, dev, seed_base=1000):
-    """Batched workloads: conditioning and uniforms drawn on the device, U(-0.5, 0.5) and
-    U[0, 1) like synth.make_cond / make_uniforms, from a torch generator seeded by the
-    first utterance id (host arrays of 2,048 x 5 s would not fit)."""
-    import torch
-    g = torch.Generator(device=dev).manual_seed(seed_base + int(utts[0]))
-    nf = synth.n_frames_for(n, HOP)
-    cond = torch.rand((len(utts), nf, cfg.n_layers, 2 * cfg.residual), generator=g, device=dev) - 0.5
-    u = torch.rand((len(utts), n), generator=g, device=dev)
-    return cond, u
+def device_inputs(cfg, n, utts, dev):
+    """Batched workloads: conditioning U(-0.5, 0.5) and uniforms U[0, 1) drawn on the device,
+    each element a counter-based hash of (role, utterance id, index) (synth.make_batch_hashed_torch;
+    DESIGN.md "Input recipe"): an utterance's inputs do not depend on its batch, rank or the GPU
+    count, so its codes are comparable across every G (host arrays of 2,048 x 5 s would not fit)."""
+    return synth.make_batch_hashed_torch(cfg, n, utts, HOP, dev)
 
 
 def main():
@@ -267,7 +263,7 @@ def main():
     dev = torch.device("cuda", local if ws > 1 else 0)
     torch.cuda.set_device(dev)
     from paper_1702_07825_b200._lib import Conditioner, Model
-    from paper_1702_07825_b200.shard import gather_codes, shard_range
+    from paper_1702_07825_b200.shard import gather_codes, generate_sharded, shard_range
 
     cfg, n = wl["cfg"], wl["n"]
     if wl["split"]:
@@ -311,8 +307,18 @@ def main():
             cond_net.run(d_feat, out=d_cond)
         model.generate(d_cond, d_u, HOP, out=out)
 
-    for _ in range(args.warmup):
-        step()
+    n_utts = wl["streams"] if wl["split"] else S * ws
+    for i in range(args.warmup):
+        if i == 0 and cond_net is None:
+            # the first warm-up step through the sharder: this rank's contiguous block of the
+            # n_utts utterances (PAPER.md:416 independent utterances; no collective)
+            def resident(ids):
+                assert list(ids) == utts, (ids[:3], utts[:3])
+                return d_cond, d_u
+            local, _, _ = generate_sharded(model, resident, n_utts, n, HOP, gather=False)
+            out.copy_(local)
+        else:
+            step()
     barrier()
     info = model.info()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -405,7 +411,6 @@ def main():
     gather = None
     if ws > 1:
         # results to rank 0 after the timed work: the only collective (NCCL all_gather of uint8 codes)
-        n_utts = wl["streams"] if wl["split"] else S * ws
         g0 = torch.cuda.Event(enable_timing=True)
         g1 = torch.cuda.Event(enable_timing=True)
         torch.distributed.barrier()

@@ -59,15 +59,20 @@ def gather_codes(local: torch.Tensor, n_utts: int, group=None) -> Optional[torch
 
 
 def generate_sharded(model, make_inputs: Callable[[Sequence[int]], Tuple[torch.Tensor, torch.Tensor]],
-                     n_utts: int, n_samples: int, hop: int, gather: bool = True, group=None):
+                     n_utts: int, n_samples: int, hop: int, gather: bool = True, group=None,
+                     world: Optional[int] = None, rank: Optional[int] = None):
     """Generate this rank's shard with one batched dvw_generate call; optionally
-    gather all codes to rank 0.  Returns (local_codes, gathered_or_None, (start, count))."""
-    _, world, rank = _dist()
+    gather all codes to rank 0.  Returns (local_codes, gathered_or_None, (start, count)).
+    world / rank override the process group's (a single process simulating one shard of a
+    G-GPU run, as the sharding-invariance test does); gathering needs the real group."""
+    _, w0, r0 = _dist()
+    world = w0 if world is None else world
+    rank = r0 if rank is None else rank
     start, count = shard_range(n_utts, world, rank)
     if count == 0:
         local = torch.empty((0, n_samples), dtype=torch.uint8, device="cuda")
     else:
         cond, u = make_inputs(list(range(start, start + count)))
         local = model.generate(cond, u, hop)
-    full = gather_codes(local, n_utts, group) if gather else None
+    full = gather_codes(local, n_utts, group) if (gather and world == w0) else None
     return local, full, (start, count)

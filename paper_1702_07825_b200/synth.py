@@ -137,6 +137,89 @@ def make_batch(cfg: Config, n_samples: int, utts: Sequence[int], hop: int = DEFA
     return cond, uni
 
 
+# ---------------------------------------------------------------- counter-based inputs (batched)
+# The batched workloads (C4: 256 x 5 s, C5: 2,048 x 5 s -- 52 GB of conditioning) are drawn on
+# the device.  Each element is a stateless hash of (role, utterance, element index), so an
+# utterance's inputs never depend on which other utterances share its batch, its rank or the
+# GPU count (sharding invariance), and numpy (host) and torch (device)
+# produce the same fp32 values.  Hash: Wellons' "lowbias32" 32-bit integer permutation,
+# chained over the key; value = top 24 bits / 2^24 (exact in fp32), in [0, 1).
+_M32 = 0xFFFFFFFF
+ROLE_COND, ROLE_UNIFORM = 1, 2
+
+
+def _mix32_np(x):
+    x = np.asarray(x, dtype=np.uint64) & _M32
+    x ^= x >> np.uint64(16)
+    x = (x * np.uint64(0x7FEB352D)) & _M32
+    x ^= x >> np.uint64(15)
+    x = (x * np.uint64(0x846CA68B)) & _M32
+    x ^= x >> np.uint64(16)
+    return x
+
+
+def _keys(role: int, utt: int):
+    k0 = int(_mix32_np((role * 0x9E3779B9 + 0x632BE5AB) & _M32))
+    k1 = int(_mix32_np(k0 ^ (utt & _M32)))
+    return k0, k1
+
+
+def hashed_uniform_np(role: int, utt: int, idx) -> np.ndarray:
+    """fp32 U[0, 1) of element(s) idx of (role, utterance) -- host reference of the device draw."""
+    k0, k1 = _keys(role, utt)
+    v = _mix32_np(_mix32_np(np.asarray(idx, dtype=np.uint64) ^ np.uint64(k1)) ^ np.uint64(k0))
+    return ((v >> np.uint64(8)).astype(np.float64) * 2.0 ** -24).astype(np.float32)
+
+
+def make_cond_hashed(cfg: Config, n_frames: int, utt: int) -> np.ndarray:
+    """Host copy of utterance utt's hashed conditioning: U(-0.5, 0.5) fp32 [F][l][2r]."""
+    n = n_frames * cfg.n_layers * 2 * cfg.residual
+    v = hashed_uniform_np(ROLE_COND, utt, np.arange(n, dtype=np.uint64)) - np.float32(0.5)
+    return v.reshape(n_frames, cfg.n_layers, 2 * cfg.residual)
+
+
+def make_uniforms_hashed(n_samples: int, utt: int) -> np.ndarray:
+    return hashed_uniform_np(ROLE_UNIFORM, utt, np.arange(n_samples, dtype=np.uint64))
+
+
+def _mix32_torch(x):
+    # int64 holding a uint32; products wrap mod 2^64 and the mask keeps the exact low 32 bits
+    x = x ^ (x >> 16)
+    x = (x * 0x7FEB352D) & _M32
+    x = x ^ (x >> 15)
+    x = (x * 0x846CA68B) & _M32
+    return x ^ (x >> 16)
+
+
+def _hashed_fill_torch(out, role: int, utts, chunk_elems: int = 1 << 27):
+    """out [U][...] float32 (any device) <- hashed U[0, 1) per (role, utts[i], flat index)."""
+    import torch
+    per = out[0].numel() if out.shape[0] else 0
+    flat = out.view(out.shape[0], -1)
+    step = max(1, chunk_elems // max(per, 1))
+    idx = torch.arange(per, dtype=torch.int64, device=out.device)
+    for i0 in range(0, out.shape[0], step):
+        us = utts[i0:i0 + step]
+        ks = [_keys(role, int(u)) for u in us]
+        k0 = torch.tensor([k[0] for k in ks], dtype=torch.int64, device=out.device)[:, None]
+        k1 = torch.tensor([k[1] for k in ks], dtype=torch.int64, device=out.device)[:, None]
+        v = _mix32_torch(_mix32_torch(idx[None, :] ^ k1) ^ k0)
+        flat[i0:i0 + len(us)] = ((v >> 8).to(torch.float64) * 2.0 ** -24).to(torch.float32)
+
+
+def make_batch_hashed_torch(cfg: Config, n_samples: int, utts: Sequence[int], hop: int, device):
+    """(cond [U][F][l][2r], uniforms [U][N]) for utterance ids `utts`, drawn on `device` with
+    the counter-based hash: equal to make_cond_hashed / make_uniforms_hashed element for element."""
+    import torch
+    nf = n_frames_for(n_samples, hop)
+    cond = torch.empty((len(utts), nf, cfg.n_layers, 2 * cfg.residual), dtype=torch.float32, device=device)
+    uni = torch.empty((len(utts), n_samples), dtype=torch.float32, device=device)
+    _hashed_fill_torch(cond, ROLE_COND, list(utts))
+    cond -= 0.5
+    _hashed_fill_torch(uni, ROLE_UNIFORM, list(utts))
+    return cond, uni
+
+
 def make_codes(n_samples: int, utt: int = 0, levels: int = LEVELS) -> np.ndarray:
     """Random uint8 code history for teacher-forced runs (role key 3)."""
     rng = np.random.default_rng([3, utt])

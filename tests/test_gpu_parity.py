@@ -707,3 +707,34 @@ def test_tc_full_stream_counts_bench_launch_config(L, cfg, S, N, check):
     for i in check:
         ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[i], hop, N, uniforms=u[i])
         assert np.array_equal(codes[i], ref), i
+
+
+# ------------------------------------------------------------------ sharding invariance
+def test_sharding_invariance_hashed_inputs_bitwise(L):
+    """C5's model (l=40, r=64, s=256) over 40 utterances whose inputs are the bench's
+    counter-based per-(role, utterance) draws on the device: every simulated shard of a
+    G = 2, 4, 8 GPU run (shard.generate_sharded with an explicit rank, its own inputs drawn
+    for its own utterance ids) reproduces the unsharded run's codes bitwise,
+    and sampled utterances equal the fp64 oracle on the host copy of the same inputs."""
+    import torch
+    from paper_1702_07825_b200.shard import generate_sharded
+    cfg = synth.C5
+    U, N, hop = 40, 300, 64
+    w = synth.make_weights(cfg, 0)
+    m = L.Model.from_config(cfg).load(w).set_kernel("tc")
+
+    def make_inputs(ids):
+        return synth.make_batch_hashed_torch(cfg, N, list(ids), hop, "cuda")
+
+    full, _, (s0, c0) = generate_sharded(m, make_inputs, U, N, hop, gather=False, world=1, rank=0)
+    assert (s0, c0) == (0, U)
+    full = full.cpu().numpy()
+    for G in (2, 4, 8):
+        for k in range(G):
+            local, _, (start, count) = generate_sharded(m, make_inputs, U, N, hop, gather=False, world=G, rank=k)
+            assert np.array_equal(local.cpu().numpy(), full[start:start + count]), (G, k)
+    for u in (0, 17, 39):
+        cond = synth.make_cond_hashed(cfg, synth.n_frames_for(N, hop), u)
+        uu = synth.make_uniforms_hashed(N, u)
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, N, uniforms=uu)
+        assert np.array_equal(full[u], ref), u

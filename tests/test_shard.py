@@ -83,3 +83,57 @@ def test_gather_codes_gloo_world2(n_utts):
 def test_gather_codes_single_process_is_identity():
     local = torch.arange(12, dtype=torch.uint8).reshape(3, 4)
     assert gather_codes(local, 3) is local
+
+
+# ---- counter-based batched inputs (synth.make_batch_hashed_torch): keyed per (role, utterance)
+def test_hashed_inputs_host_equals_device_recipe_and_independent_of_batch():
+    from paper_1702_07825_b200 import synth
+    cfg = synth.Config(3, 8, 16)
+    N, hop = 200, 16
+    full_c, full_u = synth.make_batch_hashed_torch(cfg, N, list(range(10)), hop, "cpu")
+    # the same utterances in another batch composition / order / shard: identical values
+    sub_c, sub_u = synth.make_batch_hashed_torch(cfg, N, [7, 2, 9], hop, "cpu")
+    for i, u in enumerate([7, 2, 9]):
+        assert torch.equal(sub_c[i], full_c[u]) and torch.equal(sub_u[i], full_u[u])
+        # host recipe equals the torch (device) recipe element for element
+        np.testing.assert_array_equal(synth.make_cond_hashed(cfg, synth.n_frames_for(N, hop), u), sub_c[i].numpy())
+        np.testing.assert_array_equal(synth.make_uniforms_hashed(N, u), sub_u[i].numpy())
+    # ranges: cond in [-0.5, 0.5), uniforms in [0, 1) on the 2^-24 grid; utterances differ
+    assert float(full_c.min()) >= -0.5 and float(full_c.max()) < 0.5
+    assert float(full_u.min()) >= 0.0 and float(full_u.max()) < 1.0
+    assert torch.all(full_u * 2 ** 24 == torch.floor(full_u * 2 ** 24))
+    assert not torch.equal(full_u[0], full_u[1]) and not torch.equal(full_c[0], full_c[1])
+
+
+def test_hashed_uniforms_look_uniform():
+    from paper_1702_07825_b200 import synth
+    x = synth.make_uniforms_hashed(1 << 18, 11).astype(np.float64)
+    assert abs(x.mean() - 0.5) < 0.003 and abs(x.var() - 1 / 12) < 0.002
+    hist = np.bincount((x * 64).astype(int), minlength=64)
+    assert np.all(np.abs(hist - x.size / 64) < 6 * np.sqrt(x.size / 64))
+    assert abs(np.corrcoef(x[:-1], x[1:])[0, 1]) < 0.01
+    # the role and utterance keys decorrelate streams
+    y = synth.make_uniforms_hashed(1 << 18, 12).astype(np.float64)
+    assert abs(np.corrcoef(x, y)[0, 1]) < 0.01
+
+
+def test_generate_sharded_simulated_ranks_cover_the_utterances():
+    """generate_sharded with an explicit (world, rank) runs exactly that shard's utterances."""
+    from paper_1702_07825_b200.shard import generate_sharded
+
+    class Fake:
+        def generate(self, cond, u, hop):
+            return (cond[:, 0, 0, :u.shape[1]] * 0 + torch.tensor([float(x) for x in seen[-1]])[:, None]).to(torch.uint8)
+
+    seen = []
+
+    def make_inputs(ids):
+        seen.append(list(ids))
+        return torch.zeros((len(ids), 1, 1, 4)), torch.zeros((len(ids), 4))
+
+    rows = []
+    for k in range(3):
+        local, full, (start, count) = generate_sharded(Fake(), make_inputs, 10, 4, 1, world=3, rank=k)
+        assert full is None and local.shape == (count, 4)
+        rows += local[:, 0].tolist()
+    assert rows == list(range(10))
