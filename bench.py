@@ -153,6 +153,20 @@ def load_ncu_traffic(workload: str, stream_samples: int):
         return None
 
 
+def load_active_sm_pipes(workload: str):
+    """FMA-pipe and shared-memory utilisation of the ACTIVE SMs of the batch-1 kernel, from the
+    committed ncu capture (profiles/ncu_summary.json; the metrics are averaged over all 148 SMs
+    there, so avg x 148 / active SMs is the active-SM mean)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        d = json.load(open(p))[workload]
+        a = d["active_sm_pipes"]
+        return {"active_sms": a["active_sms"], "fma_pipe_pct_active_sms": a["fma_pct"],
+                "smem_pct_active_sms": a["smem_pct"], "pipes_source": a["source"]}
+    except Exception:
+        return {}
+
+
 def run_reference(args, wl):
     """The oracle (CPU, fp64, one core) on bounded samples of the workload."""
     ws, rank, _ = dist_env()
@@ -239,6 +253,8 @@ def main():
                          "batch-1 gates (f4); appc: the paper's App. C approximations (f4; parity against "
                          "the oracle's App. C mode)")
     ap.add_argument("--samples", type=int, default=0, help="override samples per utterance (0 = workload's)")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="override streams per GPU (0 = workload's; e.g. C2 with 8 streams = one cluster each)")
     ap.add_argument("--ref-samples", type=int, default=1600, help="samples per reference step")
     ap.add_argument("--cpu-samples", type=int, default=16000, help="oracle samples for cpu_baseline")
     ap.add_argument("--with-conditioner", action="store_true",
@@ -251,6 +267,9 @@ def main():
     if args.samples:
         wl["n"] = args.samples
         wl["desc"] += f" [overridden: {args.samples} samples per utterance]"
+    if args.streams:
+        wl["streams"] = args.streams
+        wl["desc"] += f" [overridden: {args.streams} streams]"
     if args.impl == "reference":
         return run_reference(args, wl)
 
@@ -321,6 +340,10 @@ def main():
             step()
     barrier()
     info = model.info()
+    floor = None
+    if info["last_kernel_name"] == "cluster":
+        from paper_1702_07825_b200._lib import measure_floor
+        floor = measure_floor(dev.index)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(dev.index) as clk:
         barrier()
@@ -451,6 +474,31 @@ def main():
                             f"peak ({peak_src}); " + ("one tf32 pass (DVW_PRECISION_TF32); " if fast else
                             "the 3-pass split issues ~3.2x these FLOPs on the tensor pipe; ") +
                             "the step is phase-latency bound (DESIGN.md Batched kernel)"}
+        elif kname == "cluster" and floor is not None:
+            # batch 1 is latency-bound: the roofline is the measured latency floor
+            # of the critical path, l x layer + (chain CTAs + 2) x hop + 3 x head stage + sampler,
+            # each piece microbenchmarked on this GPU now (dvw_measure_floor)
+            nc = int(info["chain_ctas"])
+            fc = (cfg.n_layers * floor["layer_cycles"] + (nc + 2) * floor["hop_cycles"]
+                  + 3 * floor["head_stage_cycles"] + floor["sampler_cycles"])
+            ghz = (clk.summary().get("sm_mhz") or floor["sm_ghz"] * 1e3) / 1e3
+            floor_us = fc / ghz / 1e3
+            us = kernel_ms * 1e3 / n
+            peak = 1e6 / floor_us  # samples/s per stream at the floor
+            roof = {"bound": "latency", "achieved": 1e6 / us, "peak": peak, "unit": "samples/s per stream",
+                    "frac": floor_us / us, "floor_us": floor_us, "us_per_sample": us,
+                    "traffic": load_ncu_traffic(args.workload, n * S),
+                    "floor_parts_cycles": {"layer": floor["layer_cycles"], "hop": floor["hop_cycles"],
+                                           "head_stage": floor["head_stage_cycles"],
+                                           "sampler": floor["sampler_cycles"], "n_layers": cfg.n_layers,
+                                           "hops": nc + 2, "head_stages": 3, "total": fc,
+                                           "sm_ghz_probe": floor["sm_ghz"], "sm_ghz_used": ghz},
+                    "alu": {"achieved_tflops": achieved_tflops, "chip_fp32_peak_tflops": FP32_FMA_PEAK_TFLOPS,
+                            "frac": achieved_tflops / FP32_FMA_PEAK_TFLOPS},
+                    "note": "frac = measured latency floor / measured us per sample (dvw_measure_floor: one "
+                            "chain layer alone on an SM, one DSMEM hop, one head stage, one sampler draw; "
+                            "DESIGN.md Roofline); alu = whole-chip FP32 context"}
+            roof.update(load_active_sm_pipes(args.workload))
         else:
             roof = {"bound": "alu", "achieved": achieved_tflops, "peak": FP32_FMA_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": achieved_tflops / FP32_FMA_PEAK_TFLOPS,

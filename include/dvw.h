@@ -75,9 +75,11 @@ typedef struct {
   int32_t device;
 } dvw_config;
 
-/* Kernel selection.  AUTO: dvw_generate picks CLUSTER for
- * n_streams == 1 when the model fits its residency plan (and the sampler is direct), TC for
- * n_streams > 1, else STREAM; dvw_logits picks PARALLEL. */
+/* Kernel selection.  AUTO: dvw_generate picks CLUSTER when the model
+ * fits its residency plan, the sampler is direct and n_streams is at most the number of
+ * clusters the device runs at once times 16 (one cluster per stream, the rest in waves),
+ * TC for larger batches, else STREAM; dvw_logits picks PARALLEL.  A pinned CLUSTER kernel
+ * takes any n_streams (clusters beyond the co-resident count run in waves). */
 typedef enum {
   DVW_KERNEL_AUTO = 0,
   DVW_KERNEL_STREAM = 1,   /* one CTA per stream, weights read from L2 every sample */
@@ -94,6 +96,8 @@ typedef struct {
   int64_t last_launches;     /* kernel launches issued by the last call */
   int64_t weight_bytes;      /* bytes of packed device weights the handle owns */
   int64_t workspace_bytes;   /* bytes of per-stream state (dilation rings) */
+  int32_t chain_ctas;        /* cluster kernel's plan: chain CTAs (layers per CTA = ceil(l / chain_ctas)); 0 if none */
+  int32_t max_clusters;      /* cluster kernel's plan: clusters co-resident on the device */
 } dvw_info;
 
 /* Create a handle on cfg->device.  Validates sizes (DVW_E_SHAPE / DVW_E_UNSUPPORTED).
@@ -159,12 +163,15 @@ DVW_API dvw_status dvw_generate_host(dvw_model* m, const float* cond_host, int64
  *                          utterance, fp32 [n_streams][n_frames][l][2r] with
  *                          n_frames >= ceil((position + n_samples) / hop); uniforms and
  *                          out_codes are the chunk's, [n_streams][n_samples].  hop must not
- *                          change within a session.  AUTO runs one stream on the CLUSTER
- *                          kernel (direct sampler, exact gate), several on the batched TC
- *                          kernel (the session then keeps its workspace: queues, x^(0) and
- *                          codes of every launch group), else the STREAM kernel.  The kernel of
- *                          the first call is kept; a later call pinned to a kernel with another
- *                          state layout -> DVW_E_STATE.  Calls on one session must be ordered
+ *                          change within a session.  AUTO runs up to the co-resident
+ *                          cluster count of streams on the CLUSTER kernel (direct sampler,
+ *                          exact gate), larger batches on the batched TC kernel (the session
+ *                          then keeps its workspace: queues, x^(0) and codes of every launch
+ *                          group), else the STREAM kernel -- re-resolved on every call, since
+ *                          CLUSTER and STREAM share one state layout (a session moves between
+ *                          them when the sampler or precision changes).  A TC session stays
+ *                          on TC; a call pinned to a kernel with another state layout ->
+ *                          DVW_E_STATE.  Calls on one session must be ordered
  *                          (same CUDA stream).
  *   dvw_session_position : samples generated so far (-1 for NULL)
  * The session is bound to the model's device and dilation schedule. */
@@ -201,7 +208,8 @@ DVW_API dvw_status dvw_set_kernel(dvw_model* m, int32_t kernel);
  *     reading R31): tanh and sigma from e~(x) = 1 + |x| + 0.5658 x^2 + 0.143 x^4 in every
  *     gate, and the softmax's e^x by the 2^x bit-pattern construction with the rational
  *     g(z) in the sampler (all strategies).  CLUSTER, STREAM (generation, sessions) and
- *     PARALLEL (logits) kernels; TC -> DVW_E_UNSUPPORTED (AUTO picks STREAM for batches).
+ *     PARALLEL (logits) kernels; TC -> DVW_E_UNSUPPORTED (AUTO picks CLUSTER, else STREAM,
+ *     for batches).
  *     Parity is with the oracle's App. C mode (oracle.run(..., nonlin="appc")). */
 typedef enum {
   DVW_PRECISION_FP32 = 0,
@@ -271,6 +279,26 @@ DVW_API dvw_status dvw_set_trace(dvw_model* m, uint64_t* device_buf, int64_t fir
 
 /* Launch bookkeeping of the last call (filled synchronously, host side). */
 DVW_API dvw_status dvw_get_info(const dvw_model* m, dvw_info* out);
+
+/* Latency floor of the batch-1 critical path (SURVEY.md §8(d) "measured latency floor";
+ * PAPER.md:225-229 per-layer budget, PAPER.md:600-606 synchronisation as the GPU bottleneck).
+ * Runs four microbenchmarks on `device` (a few ms, synchronous) built from the cluster
+ * kernel's own device functions, each timed with clock64 on one SM:
+ *   layer_cycles      one chain layer alone: LDS of h, the 2r x r matvec, pair shuffle, gate,
+ *                     STS of h and the named barrier that publishes it (r = 64)
+ *   hop_cycles        one DSMEM hand-off between two CTAs of a cluster (st.async completing
+ *                     transaction bytes on the peer's mbarrier; ping-pong / 2)
+ *   head_stage_cycles one head stage: a 64-row slice of a 256 x 256 matvec, the transposing
+ *                     shuffle reduction, STS and a 256-thread barrier
+ *   sampler_cycles    one inverse-CDF draw by one warp
+ *   sm_ghz            SM clock during the probe (clock64 / %globaltimer over ~10 ms)
+ * The floor of a model on the cluster kernel is l x layer + (chain CTAs + 2) x hop +
+ * 3 x head_stage + sampler (bench.py "roofline").  Errors: DVW_E_INVALID_ARG (NULL out,
+ * bad device), DVW_E_CUDA. */
+typedef struct {
+  double layer_cycles, hop_cycles, head_stage_cycles, sampler_cycles, sm_ghz;
+} dvw_floor;
+DVW_API dvw_status dvw_measure_floor(int32_t device, dvw_floor* out);
 
 /* Wait for the handle's outstanding work; returns DVW_E_DEVICE_TIMEOUT if a
  * device watchdog fired, DVW_E_CUDA on an asynchronous CUDA error. */

@@ -32,7 +32,7 @@ KERNEL_NAMES = {0: "auto", 1: "stream", 2: "cluster", 3: "tc", 4: "parallel"}
 EXPORTS = ("dvw_create", "dvw_weights_numel", "dvw_load_weights", "dvw_generate", "dvw_logits",
            "dvw_generate_host", "dvw_set_kernel", "dvw_set_precision", "dvw_set_weight_bits",
            "dvw_set_weight_quant", "dvw_set_sampler", "dvw_set_trace",
-           "dvw_get_info", "dvw_sync", "dvw_destroy", "dvw_last_error",
+           "dvw_get_info", "dvw_measure_floor", "dvw_sync", "dvw_destroy", "dvw_last_error",
            "dvw_session_create", "dvw_session_generate", "dvw_session_position", "dvw_session_destroy",
            "dvwc_create", "dvwc_weights_numel", "dvwc_load_weights", "dvwc_run", "dvwc_destroy")
 SAMPLERS = {"direct": 0, "temperature": 1, "mean": 2, "mode": 3, "top_k": 4}
@@ -50,7 +50,8 @@ class _Info(ctypes.Structure):
     _fields_ = [("last_kernel", ctypes.c_int32), ("last_grid", ctypes.c_int32),
                 ("last_cluster", ctypes.c_int32), ("last_threads", ctypes.c_int32),
                 ("last_launches", ctypes.c_int64), ("weight_bytes", ctypes.c_int64),
-                ("workspace_bytes", ctypes.c_int64)]
+                ("workspace_bytes", ctypes.c_int64), ("chain_ctas", ctypes.c_int32),
+                ("max_clusters", ctypes.c_int32)]
 
 
 _vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
@@ -105,6 +106,14 @@ _lib.dvw_set_trace.argtypes = [_vp, _vp, _i64, _i32]
 _lib.dvw_set_trace.restype = _i32
 _lib.dvw_get_info.argtypes = [_vp, ctypes.POINTER(_Info)]
 _lib.dvw_get_info.restype = _i32
+class _Floor(ctypes.Structure):
+    _fields_ = [("layer_cycles", ctypes.c_double), ("hop_cycles", ctypes.c_double),
+                ("head_stage_cycles", ctypes.c_double), ("sampler_cycles", ctypes.c_double),
+                ("sm_ghz", ctypes.c_double)]
+
+
+_lib.dvw_measure_floor.argtypes = [_i32, ctypes.POINTER(_Floor)]
+_lib.dvw_measure_floor.restype = _i32
 _lib.dvw_sync.argtypes = [_vp]
 _lib.dvw_sync.restype = _i32
 _lib.dvw_destroy.argtypes = [_vp]
@@ -289,6 +298,13 @@ class Model:
         _check(_lib.dvw_generate_host(self._h, hptr(cond), F, hop, hptr(uniforms), N, S, hptr(out),
                                       _stream_handle(stream)))
         return out
+
+
+def measure_floor(device: int = 0) -> dict:
+    """dvw_measure_floor: cycles of the batch-1 critical path's pieces on `device`."""
+    f = _Floor()
+    _check(_lib.dvw_measure_floor(int(device), ctypes.byref(f)))
+    return {k: getattr(f, k) for k, _ in _Floor._fields_}
 
 
 def raw_call(name: str, *args) -> int:

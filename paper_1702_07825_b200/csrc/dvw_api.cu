@@ -162,6 +162,17 @@ dvw_status check_device_error(dvw_model* m) {
   return DVW_OK;
 }
 
+// AUTO: batches up to this many streams run on the cluster kernel, one cluster per stream
+// (max_clusters co-resident, the rest in waves); larger batches on the batched tensor-core
+// kernel (or the stream kernel).  Crossover measured at C2 (profiles/r2_cluster_streams.json):
+// 4 co-resident 14-CTA clusters give 4 x 133k samples/s for any batch, the batched kernel
+// ~7k samples/s per stream up to 128 streams -- it wins above ~75 streams.
+constexpr int kClusterWaves = 16;
+int cluster_streams(const dvw_model* m) {
+  if (!m->cplan.ok) return 0;
+  return m->trace ? 1 : kClusterWaves * m->cplan.max_clusters;
+}
+
 dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, const float* uniforms,
                const uint8_t* forced, int64_t n_samples, int32_t n_streams, uint8_t* out_codes,
                float* out_logits, void* stream, dvw_session* sess = nullptr) {
@@ -203,7 +214,7 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
       // changes to something the cluster kernel's session variant does not run (and back)
       if (sess->kernel == DVW_KERNEL_TC) kern = DVW_KERNEL_TC;
       else if (sess->kernel == DVW_KERNEL_STREAM && n_streams > 1) kern = DVW_KERNEL_STREAM;
-      else if (n_streams == 1 && m->cplan.ok && direct && exact) kern = DVW_KERNEL_CLUSTER;
+      else if (n_streams <= cluster_streams(m) && direct && exact) kern = DVW_KERNEL_CLUSTER;
       else if (n_streams > 1 && m->bplan.ok && m->precision != DVW_PRECISION_APPC) kern = DVW_KERNEL_TC;
       else kern = DVW_KERNEL_STREAM;
     }
@@ -217,13 +228,15 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   if (kern == DVW_KERNEL_TC && m->precision == DVW_PRECISION_APPC)
     return fail(DVW_E_UNSUPPORTED, "the App. C tier runs on the CLUSTER, STREAM and PARALLEL kernels");
   if (kern == DVW_KERNEL_AUTO) {
-    if (n_streams == 1 && m->cplan.ok && direct) kern = DVW_KERNEL_CLUSTER;
+    if (n_streams <= cluster_streams(m) && direct) kern = DVW_KERNEL_CLUSTER;
     else if (n_streams > 1 && m->bplan.ok && m->precision != DVW_PRECISION_APPC) kern = DVW_KERNEL_TC;
     else kern = DVW_KERNEL_STREAM;
   }
   if (kern == DVW_KERNEL_CLUSTER && m->trace &&
       (m->precision == DVW_PRECISION_APPROX || m->precision == DVW_PRECISION_APPC))
     return fail(DVW_E_UNSUPPORTED, "tracing runs the exact-gate cluster kernel only (dvw_set_trace)");
+  if (kern == DVW_KERNEL_CLUSTER && m->trace && n_streams > 1)
+    return fail(DVW_E_UNSUPPORTED, "tracing records one stream (dvw_set_trace)");
   int pgroup = 0;  // parallel kernel: streams per workspace group
   if (kern == DVW_KERNEL_PARALLEL) {
     const size_t per = parallel_workspace_bytes(m->r, m->s, n_samples, 1);
@@ -424,6 +437,8 @@ DVW_API dvw_status dvw_create(const dvw_config* cfg, dvw_model** out) {
     return cuda_fail(e, "dvw_create device setup");
   }
   m->cplan = plan_cluster(m->L, m->r, m->s, m->device);
+  m->info.chain_ctas = m->cplan.ok ? m->cplan.nc : 0;
+  m->info.max_clusters = m->cplan.ok ? m->cplan.max_clusters : 0;
   m->bplan = plan_batch(m->L, m->r, m->s, m->device);
   *out = m;
   return DVW_OK;
@@ -651,6 +666,23 @@ DVW_API dvw_status dvw_set_trace(dvw_model* m, uint64_t* device_buf, int64_t fir
   m->trace = device_buf;
   m->trace_n0 = first_sample;
   m->trace_count = device_buf ? n_samples : 0;
+  return DVW_OK;
+}
+
+DVW_API dvw_status dvw_measure_floor(int32_t device, dvw_floor* out) {
+  if (!out) return fail(DVW_E_INVALID_ARG, "out is NULL");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return fail(DVW_E_INVALID_ARG, "device %d not available", device);
+  }
+  FloorProbe f{};
+  DVW_CUDA(measure_floor(device, &f), "latency-floor probes");
+  out->layer_cycles = f.layer_cycles;
+  out->hop_cycles = f.hop_cycles;
+  out->head_stage_cycles = f.head_stage_cycles;
+  out->sampler_cycles = f.sampler_cycles;
+  out->sm_ghz = f.sm_ghz;
   return DVW_OK;
 }
 

@@ -113,7 +113,21 @@ struct Ctx {
   Mail* mail;
   int* err;
   int size;
+  int64_t sidx;  // the stream this cluster generates (one cluster per stream: cluster index)
 };
+
+// This cluster's stream inside the [S][...] caller buffers.
+__device__ __forceinline__ const float* s_uniforms(const RunArgs& A, const Ctx& cx) {
+  return A.uniforms ? A.uniforms + cx.sidx * A.N : nullptr;
+}
+__device__ __forceinline__ const uint8_t* s_forced(const RunArgs& A, const Ctx& cx) {
+  return A.forced ? A.forced + cx.sidx * A.N : nullptr;
+}
+__device__ __forceinline__ float* s_logits(const RunArgs& A, const Ctx& cx) {
+  return A.out_logits + cx.sidx * A.N * kLevels;
+}
+__device__ __forceinline__ uint8_t* s_codes(const RunArgs& A, const Ctx& cx) { return A.out_codes + cx.sidx * A.N; }
+__device__ __forceinline__ int* s_ystate(const RunArgs& A, const Ctx& cx) { return A.ystate + 2 * cx.sidx; }
 
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -351,8 +365,10 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
     const float* embp_g = P.pk + P.p.embp_off;  // W_emb_prev^T [256][R] in global memory
     float ep0, ep1;
     if (n > 0) {
-      const float u = A.uniforms ? __ldg(A.uniforms + n - 1) : 0.0f;
-      const int yf = A.forced ? (int)__ldg(A.forced + n - 1) : 0;
+      const float* ub = s_uniforms(A, cx);
+      const uint8_t* fb = s_forced(A, cx);
+      const float u = ub ? __ldg(ub + n - 1) : 0.0f;
+      const int yf = fb ? (int)__ldg(fb + n - 1) : 0;
       ep0 = __ldg(embp_g + y1 * R + k);  // W_emb_prev[:, y_{n-2}] (= y1 before the update)
       ep1 = __ldg(embp_g + y1 * R + k + 32);
       uint64_t* tp = (k == 0) ? trace_slot<TRACE>(A, n) : nullptr;
@@ -361,8 +377,8 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
       stamp<TRACE>(tp, 1);
       if (k == 0) trace<TRACE>(A, n - 1, 3);
       int y;
-      if (A.forced) {
-        float4* o = reinterpret_cast<float4*>(A.out_logits + (n - 1) * kLevels) + 2 * k;
+      if (fb) {
+        float4* o = reinterpret_cast<float4*>(s_logits(A, cx) + (n - 1) * kLevels) + 2 * k;
         o[0] = lds4(m.logits_in + 8 * k);
         o[1] = lds4(m.logits_in + 8 * k + 4);
         y = yf;
@@ -370,7 +386,7 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
         stamp<TRACE>(tp, 4);
         y = sample_warp<NL>(m.logits_in, u, k);
         stamp<TRACE>(tp, 6);
-        if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
+        if (k == 0) s_codes(A, cx)[n - 1] = (uint8_t)y;
       }
       if (k == 0) trace<TRACE>(A, n, 20);
       y2 = y1;
@@ -396,16 +412,17 @@ __device__ __forceinline__ int final_draw(const Params& P, const Ctx& cx, int k)
   Mail& m = *cx.mail;
   if (k >= 32) return 0;
   const int64_t n = A.N;
-  const float u = A.uniforms ? __ldg(A.uniforms + n - 1) : 0.0f;
+  const float* ub = s_uniforms(A, cx);
+  const float u = ub ? __ldg(ub + n - 1) : 0.0f;
   wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11);
   int y = 0;
   if (A.forced) {
-    float4* o = reinterpret_cast<float4*>(A.out_logits + (n - 1) * kLevels) + 2 * k;
+    float4* o = reinterpret_cast<float4*>(s_logits(A, cx) + (n - 1) * kLevels) + 2 * k;
     o[0] = lds4(m.logits_in + 8 * k);
     o[1] = lds4(m.logits_in + 8 * k + 4);
   } else {
     y = sample_warp<NL>(m.logits_in, u, k);
-    if (k == 0) A.out_codes[n - 1] = (uint8_t)y;
+    if (k == 0) s_codes(A, cx)[n - 1] = (uint8_t)y;
   }
   return y;
 }
@@ -459,7 +476,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
   const uint32_t tm = tmem_lane_addr(m) + kColA;
   const float* wembc = sw + sm_emb(LP);  // CTA 0: [256][R]
   const float* bemb = wembc + kLevels * R;
-  int y1 = SESS ? A.ystate[0] : kLevels / 2, y2 = SESS ? A.ystate[1] : kLevels / 2;
+  int y1 = SESS ? s_ystate(A, cx)[0] : kLevels / 2, y2 = SESS ? s_ystate(A, cx)[1] : kLevels / 2;
   float w[64];
 
   for (int64_t n = 0; n < A.N; ++n) {
@@ -520,8 +537,8 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
   if (c == 0 && A.N > 0) {
     const int y = final_draw<NL>(P, cx, a);
     if (SESS && a == 0 && !A.forced) {  // streaming session: the code history for the next call
-      A.ystate[0] = y;
-      A.ystate[1] = y1;
+      s_ystate(A, cx)[0] = y;
+      s_ystate(A, cx)[1] = y1;
     }
   }
 }
@@ -548,7 +565,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
   const float* bres = sw + sm_bres(LP);  // [LPC][R]: B_res_{j0+jl-1}
   const float* wembc = sw + sm_emb(LP);
   const float* bemb = wembc + kLevels * R;
-  int y1 = SESS ? A.ystate[0] : kLevels / 2, y2 = SESS ? A.ystate[1] : kLevels / 2;
+  int y1 = SESS ? s_ystate(A, cx)[0] : kLevels / 2, y2 = SESS ? s_ystate(A, cx)[1] : kLevels / 2;
   float wr[32];
 
   for (int64_t n = 0; n < A.N; ++n) {
@@ -621,7 +638,7 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
   const float* cf = sw + sm_fold(LP);  // [LPC][2R]
   const float* wembc = sw + sm_emb(LP);
   const float* bemb = wembc + kLevels * R;
-  int y1 = SESS ? A.ystate[0] : kLevels / 2, y2 = SESS ? A.ystate[1] : kLevels / 2;
+  int y1 = SESS ? s_ystate(A, cx)[0] : kLevels / 2, y2 = SESS ? s_ystate(A, cx)[1] : kLevels / 2;
   float w[64];
 
   for (int64_t n = 0; n < A.N; ++n) {
@@ -741,6 +758,8 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
   const float* bj = sw + sm_b(LP);  // [LPC][2R]
   const int L = A.L;
   const bool xskip = LP == 4 && first < pl.nxs;  // LP = 3 plans never have chain-skip layers
+  const float* condb = A.cond + cx.sidx * A.n_frames * L * 2 * R;  // this cluster's stream
+  float* ringb = A.ring + cx.sidx * A.ring_floats;
 
   for (int64_t n = 0; n < A.N; ++n) {
     const int pp = (int)((n - 1) & 1);  // parity of sample n-1
@@ -765,9 +784,9 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
 #pragma unroll
         for (int q = 0; q < 16; ++q) wv[q] = ldg4(wp + (q * 128 + at) * 4);
       }
-      const float lv = __ldg(A.cond + (f * L + j) * 2 * R + at);
+      const float lv = __ldg(condb + (f * L + j) * 2 * R + at);
       if (at < R) {
-        float* ring = A.ring + A.ring_off[j];
+        float* ring = ringb + A.ring_off[j];
         const float xc = m.xs[pp][jl][pad16(at)];  // x_j(n-1) of this call (unused when n = 0)
         float xpv = 0.0f;
         // x_j(ng - d): slot (ng - d) mod d = ng mod d; at n = 0 of a continued session x_j(ng - 1)
@@ -803,7 +822,7 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       const int64_t ng = A.n0 + A.N - 1;
       for (int jl = 0; jl < nl; ++jl) {
         const int d = A.dil[first + jl];
-        A.ring[A.ring_off[first + jl] + (int64_t)(ng % d) * R + at] = m.xs[pp][jl][pad16(at)];
+        ringb[A.ring_off[first + jl] + (int64_t)(ng % d) * R + at] = m.xs[pp][jl][pad16(at)];
       }
     }
   }
@@ -987,7 +1006,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   const ClusterPlan& pl = P.p;
   const int rank = (int)ptx::cluster_rank();
   const int t = threadIdx.x;
-  Ctx cx{mail, P.a.err, pl.size};
+  Ctx cx{mail, P.a.err, pl.size, (int64_t)(blockIdx.x / pl.size)};
 
   int role = kIdle, idx = 0;
   if (rank < pl.nc) { role = kChain; idx = rank; }
@@ -1208,6 +1227,7 @@ ClusterPlan plan_lp(int L, int r, int s, int device, int lp) {
   else nclus = lp == 3 ? max_active_clusters<128, 3>(p.size, p.smem_bytes) : max_active_clusters<128, 4>(p.size, p.smem_bytes);
   if (prev >= 0) cudaSetDevice(prev);
   if (nclus < 1) { p.why = "cluster cannot be scheduled on this device"; return p; }
+  p.max_clusters = nclus;
   p.ok = true;
   p.why = "ok";
   return p;
@@ -1365,14 +1385,16 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
 cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const void* packed, cudaStream_t st,
                                   LaunchInfo* info) {
   if (!p.ok) return cudaErrorNotSupported;
-  if (a.n_streams != 1) return cudaErrorInvalidValue;
+  if (a.n_streams < 1 || (a.trace && a.n_streams != 1)) return cudaErrorInvalidValue;
   Params P;
   P.a = a;
   P.p = p;
   P.pk = static_cast<const float*>(packed);
   const bool tr = a.trace != nullptr;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.size);
+  // one cluster per stream: cluster c generates stream c (Ctx::sidx); clusters never wait for
+  // each other, so more clusters than fit at once simply run in waves
+  cfg.gridDim = dim3(p.size * a.n_streams);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = p.smem_bytes;
   cfg.stream = st;
@@ -1406,10 +1428,194 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
     DVW_LAUNCH(128, 4);
   }
 #undef DVW_LAUNCH
-  info->grid = p.size;
+  info->grid = p.size * a.n_streams;
   info->cluster = p.size;
   info->threads = kThreads;
   info->launches = 1;
+  return e;
+}
+
+// ------------------------------------------------------------------ latency-floor microbenchmarks
+// (dvw_measure_floor; SURVEY.md §8(d) "measured latency floor").  Each kernel times, with clock64
+// on one SM, the minimal dependent form of one piece of the batch-1 critical path, built from the
+// same device functions the cluster kernel runs:
+//   layer   : one chain layer with nothing else on the SM -- LDS of h, the 128 x 64 matvec
+//             (tile_dot_half<2>, 32 FFMA2 per thread), the pair shuffle, gate_fast, STS of h and
+//             the named barrier that publishes it (warpgroup A alone)
+//   hop     : one DSMEM hand-off -- st.async of 4 bytes completing transaction bytes on the peer
+//             CTA's mbarrier, observed by the peer's try_wait (ping-pong / 2)
+//   head    : one head stage -- 64-row x 256-column slice (tile_dot<4,16>), 4 transposing shuffle
+//             levels, STS and a 256-thread named barrier
+//   sampler : one inverse-CDF draw by one warp (sample_warp), each draw dependent on the last
+namespace {
+__global__ void __launch_bounds__(128, 1) k_probe_layer(int iters, unsigned long long* out) {
+  __shared__ __align__(16) float hs[2][kHLen];
+  const int a = threadIdx.x, hrow = a >> 1, half = a & 1, voff = 40 * half;
+  float w[64];
+#pragma unroll
+  for (int q = 0; q < 64; ++q) w[q] = 0.01f * (float)((q * 7 + a * 13) % 17 - 8);
+  const float pre0 = 0.01f * (a % 5), pre1 = -0.02f * (a % 3);
+  for (int i = a; i < 2 * kHLen; i += 128) (&hs[0][0])[i] = 0.1f;
+  __syncthreads();
+  long long t0 = 0;
+  float acc = 0.0f;
+#pragma unroll 1
+  for (int n = -64; n < iters; ++n) {
+    if (n == 0) t0 = clock64();
+    const int p = n & 1;
+    float v[2];
+    tile_dot_half<2>(w, hs[p] + voff, v);
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
+    const float hv = gate_fast(v[0] + pre0, v[1] + pre1);
+    if (half == 0) hs[p ^ 1][pad16(hrow)] = hv;
+    acc += hv;
+    ptx::bar_sync(1, 128);
+  }
+  const long long t1 = clock64();
+  if (a == 0) {
+    out[0] = (unsigned long long)(t1 - t0);
+    out[1] = __float_as_uint(acc);
+  }
+}
+
+__global__ void __launch_bounds__(32, 1) k_probe_hop(int iters, unsigned long long* out) {
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(16) float box[4];
+  const uint32_t rank = ptx::cluster_rank();
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(ptx::smem_u32(&bar), 1);
+    ptx::fence_mbar_init();
+    ptx::mbar_arm(ptx::smem_u32(&bar), 4);
+  }
+  __syncwarp();
+  ptx::cluster_sync();
+  const uint32_t peer = rank ^ 1u;
+  const uint32_t rbox = ptx::mapa(ptx::smem_u32(&box[0]), peer), rbar = ptx::mapa(ptx::smem_u32(&bar), peer);
+  long long t0 = 0;
+  if (threadIdx.x == 0) {
+    t0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < iters; ++i) {
+      if (rank == 0) {
+        ptx::st_async(rbox, (float)i, rbar);
+        while (!ptx::mbar_try_wait_cta(ptx::smem_u32(&bar), (uint32_t)(i & 1))) {
+        }
+        ptx::mbar_arm(ptx::smem_u32(&bar), 4);
+      } else {
+        while (!ptx::mbar_try_wait_cta(ptx::smem_u32(&bar), (uint32_t)(i & 1))) {
+        }
+        ptx::mbar_arm(ptx::smem_u32(&bar), 4);
+        ptx::st_async(rbox, box[0] + 1.0f, rbar);
+      }
+    }
+    if (rank == 0) out[2] = (unsigned long long)(clock64() - t0);
+  }
+  __syncwarp();
+  ptx::cluster_sync();
+}
+
+__global__ void __launch_bounds__(256, 1) k_probe_head(int iters, unsigned long long* out) {
+  __shared__ __align__(16) float zb[2][kVLen];
+  const int k = threadIdx.x, c16 = k & 15, orow = 4 * (k >> 4) + ((k >> 2) & 3);
+  float w[64];
+#pragma unroll
+  for (int q = 0; q < 64; ++q) w[q] = 0.003f * (float)((q * 5 + k * 11) % 13 - 6);
+  for (int i = k; i < 2 * kVLen; i += 256) (&zb[0][0])[i] = 0.05f;
+  __syncthreads();
+  long long t0 = 0;
+  float acc = 0.0f;
+#pragma unroll 1
+  for (int n = -32; n < iters; ++n) {
+    if (n == 0) t0 = clock64();
+    const int p = n & 1;
+    float lg[4];
+    tile_dot<4, 16>(w, &zb[p][20 * c16], lg);
+    xpose_level<4>(lg, k, 8);
+    xpose_level<2>(*reinterpret_cast<float(*)[2]>(lg), k, 4);
+    lg[0] += __shfl_xor_sync(0xffffffffu, lg[0], 2);
+    lg[0] += __shfl_xor_sync(0xffffffffu, lg[0], 1);
+    const float z = fmaxf(lg[0], 0.0f) * 0.5f;
+    if ((k & 3) == 0) zb[p ^ 1][pad16(64 * (n & 3) + orow)] = z;
+    acc += z;
+    ptx::bar_sync(1, 256);
+  }
+  const long long t1 = clock64();
+  if (k == 0) {
+    out[3] = (unsigned long long)(t1 - t0);
+    out[4] = __float_as_uint(acc);
+  }
+}
+
+__global__ void __launch_bounds__(32, 1) k_probe_sampler(int iters, unsigned long long* out) {
+  __shared__ __align__(16) float lg[kLevels];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < kLevels; i += 32) lg[i] = 0.05f * (float)((i * 37) % 23) - 0.5f;
+  __syncwarp();
+  long long t0 = 0;
+  int y = 0;
+#pragma unroll 1
+  for (int n = -16; n < iters; ++n) {
+    if (n == 0) t0 = clock64();
+    const float u = (float)((n * 2654435761u + (unsigned)y * 97u) >> 8) * 5.9604645e-08f;
+    y = sample_warp<0>(lg, u, lane);
+    if (lane == 0) lg[y] += 1e-3f;  // the next draw depends on this one
+    __syncwarp();
+  }
+  const long long t1 = clock64();
+  if (lane == 0) {
+    out[5] = (unsigned long long)(t1 - t0);
+    out[6] = (unsigned long long)y;
+  }
+}
+
+__global__ void k_probe_clock(int spin, unsigned long long* out) {
+  const uint64_t g0 = ptx::globaltimer();
+  const long long c0 = clock64();
+  while (clock64() - c0 < spin) {
+  }
+  out[7] = (unsigned long long)(clock64() - c0);
+  out[8] = (unsigned long long)(ptx::globaltimer() - g0);
+}
+}  // namespace
+
+cudaError_t measure_floor(int device, FloorProbe* f) {
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  unsigned long long* d = nullptr;
+  unsigned long long h[16] = {};
+  constexpr int kIters = 20000;
+  cudaError_t e = cudaMalloc(&d, sizeof(h));
+  if (e == cudaSuccess) e = cudaMemset(d, 0, sizeof(h));
+  if (e == cudaSuccess) {
+    k_probe_clock<<<1, 1>>>(20000000, d);  // ~10 ms: the SM clock under this (latency-bound) load
+    k_probe_layer<<<1, 128>>>(kIters, d);
+    k_probe_head<<<1, 256>>>(kIters, d);
+    k_probe_sampler<<<1, 32>>>(kIters / 4, d);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(32);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_probe_hop, kIters, d);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  if (d) cudaFree(d);
+  if (e == cudaSuccess) {
+    f->layer_cycles = (double)h[0] / kIters;
+    f->hop_cycles = (double)h[2] / (2.0 * kIters);
+    f->head_stage_cycles = (double)h[3] / kIters;
+    f->sampler_cycles = (double)h[5] / (kIters / 4);
+    f->sm_ghz = h[8] ? (double)h[7] / (double)h[8] : 0.0;
+  }
+  if (prev >= 0) cudaSetDevice(prev);
   return e;
 }
 

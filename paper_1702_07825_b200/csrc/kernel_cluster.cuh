@@ -1,7 +1,8 @@
 // kernel_cluster.cuh -- batch-1 persistent cluster kernel: residency plan + launch.
 //
 // One thread-block cluster (<= 16 CTAs, one per SM) holds the whole model on
-// chip and generates every sample of one utterance in a single launch.  CTA
+// chip and generates every sample of one utterance in a single launch; a batch of
+// streams launches one cluster per stream (up to max_clusters run at once).  CTA
 // roles:
 //   chain CTAs  c = 0..nc-1 : layers [lp c, lp c + lp), lp = 3 or 4: W_cur and the folded
 //                             W_cur W_res in tensor memory, W_res in tensor memory (lp 3)
@@ -50,12 +51,19 @@ struct ClusterPlan {
   int64_t embp_off = 0;           // W_emb_prev transposed [256][r]
   int64_t pk_total = 0;           // floats
   int smem_bytes = 0;
+  int max_clusters = 0;           // co-resident clusters on the device (one stream each)
 };
 
 ClusterPlan plan_cluster(int L, int r, int s, int device);
 size_t packed_bytes(const ClusterPlan& p);
 // Build the residency layout on the host from the raw roster-order blob and upload it.
 cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* host_blob, const Offsets& o, void* packed);
+// Latency-floor microbenchmarks of the batch-1 critical path's pieces (dvw_measure_floor).
+struct FloorProbe {
+  double layer_cycles, hop_cycles, head_stage_cycles, sampler_cycles, sm_ghz;
+};
+cudaError_t measure_floor(int device, FloorProbe* out);
+
 cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const void* packed, cudaStream_t st,
                                   LaunchInfo* info);
 

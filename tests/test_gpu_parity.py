@@ -150,7 +150,7 @@ def test_determinism_and_edge_sizes(L, kernel):
     m.generate(dev(synth.make_cond(cfg, 1, 0))[None], torch.zeros((1, 0), device="cuda"), 64, out=out)
 
 
-@pytest.mark.parametrize("kernel", ["stream", "tc"])
+@pytest.mark.parametrize("kernel", ["stream", "cluster", "tc"])
 def test_multi_stream_is_position_independent(L, kernel):
     """Utterance u's codes do not depend on batch size or position (bitwise)."""
     cfg = synth.C1
@@ -431,7 +431,7 @@ def test_appc_tier_matches_oracle_appc(L, kernel, cfg):
 
 def test_appc_tier_routing(L):
     """App. C runs on CLUSTER / STREAM / PARALLEL; the batched TC kernel refuses it, and AUTO
-    sends a multi-stream batch to the stream kernel."""
+    sends a small multi-stream batch to the cluster kernel (one cluster per stream)."""
     cfg = synth.C1
     N, hop = 64, 8
     w = synth.make_weights(cfg, 0)
@@ -439,7 +439,7 @@ def test_appc_tier_routing(L):
     u = np.stack([synth.make_uniforms(N, s) for s in range(2)])
     m = L.Model.from_config(cfg).load(w).set_precision("appc")
     codes = m.generate(dev(cond), dev(u), hop)
-    assert m.info()["last_kernel_name"] == "stream"
+    assert m.info()["last_kernel_name"] == "cluster"
     ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[1], hop, N, uniforms=u[1], nonlin="appc")
     assert np.array_equal(codes.cpu().numpy()[1], ref)
     m.set_kernel("tc")
@@ -738,3 +738,49 @@ def test_sharding_invariance_hashed_inputs_bitwise(L):
         uu = synth.make_uniforms_hashed(N, u)
         ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, N, uniforms=uu)
         assert np.array_equal(full[u], ref), u
+
+
+# ------------------------------------------------------------------ one cluster per stream (small batches)
+@pytest.mark.parametrize("cfg,S,N", [(synth.C2, 6, 1600), (synth.C2, 14, 300), (synth.C3, 3, 400)],
+                         ids=["C2-6", "C2-14-waves", "C3-3"])
+def test_cluster_kernel_one_cluster_per_stream(L, cfg, S, N):
+    """A batch on the cluster kernel launches one cluster per stream (14 CTAs each at C2, 16 at
+    C3): every stream equals the fp64 oracle code for code, also when the batch has more
+    clusters than fit at once (C2 x 14 = 196 CTAs > 148 SMs: later clusters run in waves)."""
+    hop = 64
+    w = synth.make_weights(cfg, 0)
+    utts = list(range(3, 3 + S))
+    cond, u = synth.make_batch(cfg, N, utts, hop)
+    m = L.Model.from_config(cfg).load(w).set_kernel("cluster")
+    codes = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    info = m.info()
+    assert info["last_kernel_name"] == "cluster" and info["last_grid"] == S * info["last_cluster"]
+    for i in range(S):
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[i], hop, N, uniforms=u[i])
+        assert np.array_equal(codes[i], ref), i
+    # teacher forced through the cluster kernel, several streams
+    lg = m.logits(dev(cond[:2]), dev(codes[:2]), hop).cpu().numpy()
+    for i in range(2):
+        _, ref_lg, _ = oracle_tf(cfg, w, cond[i], hop, codes[i])
+        assert float(np.max(np.abs(lg[i].astype(np.float64) - ref_lg))) <= FP32_FAITHFUL
+
+
+def test_auto_routes_small_batches_to_clusters(L):
+    """AUTO: up to the co-resident cluster count of streams run one cluster each; larger
+    batches go to the batched tensor-core kernel; a multi-stream session on clusters continues
+    bitwise like one call."""
+    cfg = synth.C2
+    N, hop = 256, 64
+    w = synth.make_weights(cfg, 0)
+    m = L.Model.from_config(cfg).load(w)
+    cond, u = synth.make_batch(cfg, N, list(range(4)), hop)
+    one = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    assert m.info()["last_kernel_name"] == "cluster"
+    big_c, big_u = synth.make_batch(cfg, 64, list(range(200)), hop)
+    m.generate(dev(big_c), dev(big_u), hop)
+    assert m.info()["last_kernel_name"] == "tc"
+    sess = m.session(4)
+    parts = [sess.generate(dev(cond), dev(u[:, a:b]).contiguous(), hop).cpu().numpy() for a, b in ((0, 100), (100, 256))]
+    assert m.info()["last_kernel_name"] == "cluster"
+    sess.close()
+    assert np.array_equal(np.concatenate(parts, axis=1), one)
