@@ -232,6 +232,47 @@ def cpu_baseline_and_parity(cfg, n, w, cond, u, gpu_codes, budget_samples, gpu_t
     return cpu, parity
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_c1_aggregate(n_samples=1600):
+    """the oracle on C1 (l=20, r=64, s=128, 1,600 samples, utterance 0)
+    on one thread, then K = len(os.sched_getaffinity(0)) independent C1 utterances (0..K-1) on K
+    threads at once (the C oracle releases the GIL inside its ctypes call); aggregate samples/s."""
+    import concurrent.futures as cf
+    import oracle
+    c1 = synth.Config(20, 64, 128)
+    w = synth.make_weights(c1, 0)
+    nf = (n_samples + HOP - 1) // HOP
+    K = len(os.sched_getaffinity(0))
+    inputs = [(synth.make_cond(c1, nf, u), synth.make_uniforms(n_samples, u)) for u in range(K)]
+
+    def one(k):
+        cond, u = inputs[k]
+        t0 = time.perf_counter()
+        oracle.run(c1.n_layers, c1.residual, c1.skip, w, cond, HOP, n_samples, uniforms=u,
+                   dilations=c1.dilation_list(), want_logits=False)
+        return time.perf_counter() - t0
+
+    single = one(0)
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=K) as ex:
+        list(ex.map(one, range(K)))
+    wall = time.perf_counter() - t0
+    return {"config": "C1 l=20 r=64 s=128, 1,600 samples per utterance (0.1 s at 16 kHz)",
+            "single_thread_s": single, "single_thread_samples_per_s": n_samples / single,
+            "threads": K, "aggregate_wall_s": wall, "aggregate_samples_per_s": K * n_samples / wall}
+
+
 def device_inputs(cfg, n, utts, dev):
     """Batched workloads: conditioning U(-0.5, 0.5) and uniforms U[0, 1) drawn on the device,
     each element a counter-based hash of (role, utterance id, index) (synth.make_batch_hashed_torch;
@@ -548,6 +589,10 @@ def main():
             tf = model.logits(d_cond[0:1].contiguous(), out[0:1, :k].contiguous(), HOP)[0].cpu().numpy()
             cpu, parity = cpu_baseline_and_parity(cfg, n, w, cond0, u0, gpu_codes0, args.cpu_samples, tf,
                                                   nonlin="appc" if args.precision == "appc" else "exact")
+            cpu["cpu_model"] = cpu_model()
+            cpu["host_threads"] = len(os.sched_getaffinity(0))
+            if rank == 0 and args.workload in ("C1", "C2"):
+                cpu["c1"] = cpu_c1_aggregate()
             line["cpu_baseline"] = cpu
             line["parity"] = parity
         print(json.dumps(line), flush=True)

@@ -22,7 +22,7 @@ FLAGS = [
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
     "-I", os.path.join(ROOT, "include"),
-]
+] + os.environ.get("DVW_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -6,6 +6,7 @@
 // reporting.  Every step of the generation itself runs in the kernels.
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <algorithm>
 #include <cstring>
@@ -301,6 +302,8 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   A.trace = m->trace;
   A.trace_n0 = m->trace_n0;
   A.trace_count = m->trace_count;
+  // watchdog test hook: honoured only by the TRACE instantiation of the cluster kernel
+  A.fault = (m->trace && getenv("DVW_FAULT_INJECT")) ? atoi(getenv("DVW_FAULT_INJECT")) : 0;
 
   LaunchInfo li{};
   cudaError_t e;

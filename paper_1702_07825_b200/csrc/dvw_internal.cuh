@@ -77,6 +77,8 @@ struct RunArgs {
   uint64_t* trace;       // optional %globaltimer trace [trace_count][16 CTAs][32 events] (dvw_set_trace)
   int64_t trace_n0;
   int trace_count;
+  int fault;             // test hook (TRACE instantiation only): 1 = the heads drop sample trace_n0's
+                         // logits hand-off, so CTA 0's spin-wait must end in the watchdog
 };
 
 // ---------------------------------------------------------------- device helpers

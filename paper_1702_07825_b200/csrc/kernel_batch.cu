@@ -1,5 +1,6 @@
 // kernel_batch.cu -- batched multi-stream kernel: tcgen05 (kind::tf32, 3 passes)
-// projections, one cooperative persistent launch, grid barrier between phases.
+// projections; one persistent launch per launch group, one thread-block cluster per
+// stream block of 128 streams, the hardware cluster barrier between phases.
 //
 // Step n of every stream, as phases (0-based layer j; §5.1):
 //   phase j (0 <= j < l): layer tile t of stream block sb computes, for channels
@@ -8,9 +9,9 @@
 //         h^(j) = tanh(a_tanh) * sigma(a_sigma)
 //       where, for j >= 1, W_cur^(j) x^(j) is evaluated as
 //         W_cur^(j) x^(j-1) + M^(j) h^(j-1) + W_cur^(j) B_res^(j-1),  M^(j) = W_cur^(j) W_res^(j-1)
-//       (the residual update of PAPER.md:437 folded in, M formed in fp64 on the host),
-//       so a layer needs only the PREVIOUS phase's outputs and one barrier per layer
-//       suffices.  The same CTA also finishes the residual update of layer j-1,
+//       (the residual update of PAPER.md:437 folded in, M formed in fp64 on the host;
+//       reading R22), so a layer needs only the PREVIOUS phase's outputs and one barrier
+//       per layer suffices.  The same CTA also finishes the residual update of layer j-1,
 //         x^(j) = x^(j-1) + W_res^(j-1) h^(j-1) + B_res^(j-1)
 //       and stores it into layer j's dilation queue ("never recompute").
 //       Skip tile u accumulates q += W_skip^(j-1) h^(j-1) in TMEM.
@@ -21,13 +22,13 @@
 //                embedding x^(0)_{n+1} = W_emb_prev[:, y_{n-1}] + W_emb_cur[:, y_n] + B_emb
 //                 into x^(0) and layer 0's queue.
 // One thread-block cluster per stream block of 128 streams holds all of its tiles
-// (r/16 layer tiles + s/64 skip tiles + 4 head tiles <= 16 CTAs); the phases are
-// separated by a hardware cluster barrier, and stream blocks never wait for each other.
-// Operands: A = activations of 128 streams (M = 128, TMEM lane = stream), B = a weight
-// tile (N = 48 or 64 rows), K staged 32 channels at a time through a 5-deep ring of
-// shared-memory stages filled by cp.async.bulk; every fp32 operand is split into
-// hi = x (the MMA reads its tf32 truncation) and lo = x - tf32(x), and each K-step
-// issues hi*hi + hi*lo + lo*hi (reading R22).
+// (r/16 layer tiles + s/64 skip tiles + 4 head tiles <= 16 CTAs); stream blocks never
+// wait for each other.  Operands: A = activations of 128 streams (M = 128, TMEM lane =
+// stream), B = a weight tile (N = 32 or 48 or 64 rows, stacked with its tf32 residual
+// rows), K staged 32 channels at a time through a kStages-deep ring of shared-memory
+// stages filled by cp.async.bulk; every fp32 operand is split into hi = x (the MMA reads
+// its tf32 truncation) and lo = x - tf32(x), and each K-step issues hi*[hi; lo] (one MMA
+// over the stacked rows) and lo*hi (reading R23).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -273,7 +274,7 @@ __device__ __forceinline__ bool issue(const BParams& P, Ctl& cl, float* stages, 
     const uint32_t d = cl.tmem + k.dcol;
 #pragma unroll
     for (int ks = 0; ks < kChunk / 8; ++ks) {
-      // D[:, 0:NS) += A_hi . [W_hi; (0); W_lo]^T ; D[:, 0:N) += A_lo . W_hi^T (reading R22)
+      // D[:, 0:NS) += A_hi . [W_hi; (0); W_lo]^T ; D[:, 0:N) += A_lo . W_hi^T (reading R23)
       const uint32_t ao = ks * 2 * 128 * 16, bo = ks * 2 * k.NS * 16;
       const uint64_t dah = sdesc(a_hi + ao, 128 * 16, 128), dal = sdesc(a_lo + ao, 128 * 16, 128);
       const uint64_t db = sdesc(wb + bo, k.NS * 16, 128);
@@ -718,7 +719,7 @@ cudaError_t pack_batch_weights(const BatchPlan& p, const float* w, const Offsets
   std::vector<float> pk((size_t)p.total, 0.0f);
   // One K-chunk block of a B operand in the K-major core-matrix order [8][NS][4]:
   // rows [0, N) = the weight rows (hi: fp32 value), rows [lo0, lo0 + N) = their tf32
-  // residuals, other rows zero (the kernel's stacked-B pass, reading R22).
+  // residuals, other rows zero (the kernel's stacked-B pass, reading R23).
   auto put_block = [&](float* dst, int N, int NS, const std::vector<float>& rows /* N x 32 */) {
     const int lo0 = NS - N;
     for (int rr = 0; rr < N; ++rr)

@@ -38,6 +38,13 @@
 #include "kernel_cluster.cuh"
 #include "ptx.cuh"
 
+// Timing diagnostics only (codes become wrong): build with -DDVW_DIAG=<mask> into a scratch
+// copy (tools/diag_c2.sh).  1: X skips the W_prev matvec; 2: C skips its matvec; 4: B skips
+// its matvec; 8: X skips the queue / conditioning / W_prev work; 16: the draw is floor(256 u).
+#ifndef DVW_DIAG
+#define DVW_DIAG 0
+#endif
+
 namespace dvw {
 namespace {
 
@@ -384,7 +391,8 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
         y = yf;
       } else {
         stamp<TRACE>(tp, 4);
-        y = sample_warp<NL>(m.logits_in, u, k);
+        if constexpr ((DVW_DIAG & 16) != 0) y = min((int)(u * 256.0f) + (m.logits_in[0] > 1e30f), 255);
+        else y = sample_warp<NL>(m.logits_in, u, k);
         stamp<TRACE>(tp, 6);
         if (k == 0) s_codes(A, cx)[n - 1] = (uint8_t)y;
       }
@@ -599,7 +607,8 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
         const float xi = xv[pad16(row)];
         if constexpr (LP == 3) ptx::tmem_wait_ld<32>(wr);
         float v[1];
-        tile_dot_half<1>(wr, hv + voff, v);
+        if constexpr ((DVW_DIAG & 4) != 0) v[0] = hv[voff] * wr[0];
+        else tile_dot_half<1>(wr, hv + voff, v);
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
         const float xn = xi + (v[0] + bres[jl * R + row]);
         if (writer) {
@@ -658,7 +667,8 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
         }
         ptx::tmem_wait_ld<64>(w);
         float v[2];
-        tile_dot_half<2>(w, xv + voff, v);
+        if constexpr ((DVW_DIAG & 2) != 0) { v[0] = xv[voff] * w[0]; v[1] = xv[voff + 1] * w[1]; }
+        else tile_dot_half<2>(w, xv + voff, v);
         if (jl + 1 < nl) ptx::tmem_load_async<64>(tm + 64 * (jl + 1), w);
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
         v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
@@ -772,10 +782,14 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
     const int64_t ng = SESS ? A.n0 + n : n;  // global sample index (streaming sessions continue at n0)
     const int64_t f = ng / A.hop;
     for (int jl = 0; jl < nl; ++jl) {
+      if constexpr ((DVW_DIAG & 8) != 0) { m.pre[jl][at] = 0.0f; continue; }
       const int j = first + jl;
       const int d = A.dil[j];
       float4 wv[16];
-      if constexpr (LP == 3) {
+      if constexpr ((DVW_DIAG & 1) != 0) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) wv[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else if constexpr (LP == 3) {
         const float* wp = sw + jl * 16 * 128 * 4;  // shared memory
 #pragma unroll
         for (int q = 0; q < 16; ++q) wv[q] = lds4(wp + (q * 128 + at) * 4);
@@ -798,7 +812,7 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       ptx::bar_sync(kBarAux, kAux);
       float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
+      for (int q = 0; q < ((DVW_DIAG & 1) ? 0 : 16); ++q) {
         const float4 x = lds4(&m.xp[4 * q]);
         a01 = ffma2(wv[q].x, wv[q].y, x.x, x.y, a01);
         a23 = ffma2(wv[q].z, wv[q].w, x.z, x.w, a23);
@@ -931,7 +945,9 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     xpose_level<2>(*reinterpret_cast<float(*)[2]>(lg), k, 4);
     lg[0] += __shfl_xor_sync(0xffffffffu, lg[0], 2);
     lg[0] += __shfl_xor_sync(0xffffffffu, lg[0], 1);
-    if (owriter)
+    bool drop = false;  // watchdog test hook (TRACE instantiation only; DVW_FAULT_INJECT=1)
+    if constexpr (TRACE) drop = A.fault == 1 && n == A.trace_n0;
+    if (owriter && !drop)
       ptx::st_async(remote(&m.logits_in[64 * hidx + orow], 0), lg[0] + bout[orow], remote(&m.bar_logits, 0));
     if (k == 0) trace<TRACE>(A, n, 3);
   }
