@@ -11,7 +11,7 @@
  *   PAPER.md:376, 501 (App. A.4 direct sampling): draw y from p, feed it back.
  *   Conditioning is taken already computed, at frame rate, and upsampled by
  *   repetition inside the kernel (App. A.2).
- * DESIGN.md lists every reading of a point the paper leaves open (R1..R33);
+ * DESIGN.md lists every reading of a point the paper leaves open (R1..R34);
  * the ones that fix the ABI's semantics are cited below.
  *
  * Conventions for every entry point:

@@ -806,7 +806,7 @@ def test_watchdog_fires_on_dropped_handoff_and_handle_recovers(L, monkeypatch):
     m.generate(dev(cond)[None], dev(u)[None], hop)
     with pytest.raises(L.DvwError) as ei:
         m.sync()
-    assert ei.value.name == "DVW_E_DEVICE_TIMEOUT"
+    assert ei.value.name == "DVW_E_DEVICE_TIMEOUT", str(ei.value)
     assert time.perf_counter() - t0 < 30.0
     monkeypatch.delenv("DVW_FAULT_INJECT")
     m.set_trace(None)
