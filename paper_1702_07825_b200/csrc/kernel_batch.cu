@@ -47,15 +47,12 @@ constexpr int kChunk = 32;                   // K channels per staged chunk
 constexpr int kActChunk = 128 * kChunk;      // floats of one activation chunk (hi or lo)
 constexpr int kMaxN = 64;
 constexpr int kStageFloats = 2 * kActChunk + kMaxN * kChunk * 2;
-constexpr int kTmemCols = 256;
+constexpr int kTmemCols = 128;
 // TMEM accumulator columns (a CTA has one role).  Each tile accumulates hi*hi + lo*hi in
 // its first block of columns and hi*lo in a second block (the stacked-B pass below):
 //   layer: [0,48) = tanh 16 | sigmoid 16 | residual 16, [48,96) the hi*lo partner
 //   skip / head (64 rows): [0,64) and [64,128)
 constexpr uint32_t kColA = 0, kColA2 = 48, kColQ = 0, kColQ2 = 64, kColH = 0;
-// the lo*hi pass accumulates into its own columns (layer: [96, 144), skip / head: [128, 192)), so the
-// two MMAs of a K-step are independent and the tensor pipe overlaps them instead of chaining them
-constexpr uint32_t kColLoA = 96, kColLoQ = 128;
 constexpr int kTileRows = 64;  // rows of a skip or head tile
 
 constexpr uint64_t kTimeoutNs = 4000000000ull;
@@ -275,7 +272,6 @@ __device__ __forceinline__ bool issue(const BParams& P, Ctl& cl, float* stages, 
     const uint32_t wb = a_hi + 2 * kActChunk * 4;
     const uint32_t id2 = idesc_tf32(k.NS), id1 = idesc_tf32(k.N);
     const uint32_t d = cl.tmem + k.dcol;
-    const uint32_t dlo = cl.tmem + (role == kLayer ? kColLoA : kColLoQ);
 #pragma unroll
     for (int ks = 0; ks < kChunk / 8; ++ks) {
       // D[:, 0:NS) += A_hi . [W_hi; (0); W_lo]^T ; D[:, 0:N) += A_lo . W_hi^T (reading R23)
@@ -286,7 +282,7 @@ __device__ __forceinline__ bool issue(const BParams& P, Ctl& cl, float* stages, 
         mma_tf32(d, dah, db, id1, (k.acc || ks > 0) ? 1u : 0u);
       } else {
         mma_tf32(d, dah, db, id2, (k.acc || ks > 0) ? 1u : 0u);
-        mma_tf32(dlo, dal, db, id1, (k.acc || ks > 0) ? 1u : 0u);
+        mma_tf32(d, dal, db, id1, 1u);
       }
     }
     mma_commit(ptx::smem_u32(&cl.freeb[st]));
@@ -429,37 +425,22 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
   if (t == 0 && ph == 3) btrace(P, n, 15);
   if (role == kLayer) {
     const int j = ph, c0 = 16 * idx + 8 * half;
-    float Dt[8], Ds[8], Dx[8] = {}, Et[8], Es[8], Ex[8] = {}, Ft[8], Fs[8], Fx[8] = {};
+    float Dt[8], Ds[8], Dx[8] = {}, Et[8], Es[8], Ex[8] = {};
     tmem_cols<8>(lane_base + kColA + 8 * half, Dt);
     tmem_cols<8>(lane_base + kColA + 16 + 8 * half, Ds);
-    if constexpr (!FAST) {
-      tmem_cols<8>(lane_base + kColA2 + 8 * half, Et);
-      tmem_cols<8>(lane_base + kColA2 + 16 + 8 * half, Es);
-      tmem_cols<8>(lane_base + kColLoA + 8 * half, Ft);
-      tmem_cols<8>(lane_base + kColLoA + 16 + 8 * half, Fs);
-    }
+    tmem_cols<8>(lane_base + kColA2 + 8 * half, Et);
+    tmem_cols<8>(lane_base + kColA2 + 16 + 8 * half, Es);
     if (j >= 1) {
       tmem_cols<8>(lane_base + kColA + 32 + 8 * half, Dx);
-      if constexpr (!FAST) {
-        tmem_cols<8>(lane_base + kColA2 + 32 + 8 * half, Ex);
-        tmem_cols<8>(lane_base + kColLoA + 32 + 8 * half, Fx);
-      }
+      tmem_cols<8>(lane_base + kColA2 + 32 + 8 * half, Ex);
     }
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int q = 0; q < 8; ++q)
-      asm volatile("" : "+f"(Dt[q]), "+f"(Ds[q]), "+f"(Dx[q]), "+f"(Et[q]), "+f"(Es[q]), "+f"(Ex[q]), "+f"(Ft[q]),
-                   "+f"(Fs[q]), "+f"(Fx[q]));
-    if constexpr (FAST) {  // the hi*lo and lo*hi columns were not written this phase
+      asm volatile("" : "+f"(Dt[q]), "+f"(Ds[q]), "+f"(Dx[q]), "+f"(Et[q]), "+f"(Es[q]), "+f"(Ex[q]));
+    if constexpr (FAST) {  // the hi*lo partner columns were not written this phase
 #pragma unroll
-      for (int q = 0; q < 8; ++q) Et[q] = Es[q] = Ex[q] = Ft[q] = Fs[q] = Fx[q] = 0.0f;
-    } else {  // hi*hi + lo*hi, in a fixed order
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        Dt[q] += Ft[q];
-        Ds[q] += Fs[q];
-        Dx[q] += Fx[q];
-      }
+      for (int q = 0; q < 8; ++q) Et[q] = Es[q] = Ex[q] = 0.0f;
     }
     if (t == 0 && ph == 3) btrace(P, n, 16);
     const int64_t half_f = (int64_t)P.nsb * r * 128;
@@ -489,22 +470,18 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
   } else {
     if (role == kSkipT && ph != P.L) return;  // accumulation continues in TMEM
     // 64-row tile: thread (stream i, half) finishes rows [64 idx + 32 half, +32)
-    float D[32], E[32], F[32];
-    const uint32_t c0t = kColQ + 32 * half, c1t = kColQ2 + 32 * half, c2t = kColLoQ + 32 * half;  // kColQ == kColH
+    float D[32], E[32];
+    const uint32_t c0t = kColQ + 32 * half, c1t = kColQ2 + 32 * half;  // kColQ == kColH
     tmem_cols<16>(lane_base + c0t, *reinterpret_cast<float(*)[16]>(D));
     tmem_cols<16>(lane_base + c0t + 16, *reinterpret_cast<float(*)[16]>(D + 16));
-    if constexpr (!FAST) {
-      tmem_cols<16>(lane_base + c1t, *reinterpret_cast<float(*)[16]>(E));
-      tmem_cols<16>(lane_base + c1t + 16, *reinterpret_cast<float(*)[16]>(E + 16));
-      tmem_cols<16>(lane_base + c2t, *reinterpret_cast<float(*)[16]>(F));
-      tmem_cols<16>(lane_base + c2t + 16, *reinterpret_cast<float(*)[16]>(F + 16));
-    }
+    tmem_cols<16>(lane_base + c1t, *reinterpret_cast<float(*)[16]>(E));
+    tmem_cols<16>(lane_base + c1t + 16, *reinterpret_cast<float(*)[16]>(E + 16));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int q = 0; q < 32; ++q) asm volatile("" : "+f"(D[q]), "+f"(E[q]), "+f"(F[q]));
+    for (int q = 0; q < 32; ++q) asm volatile("" : "+f"(D[q]), "+f"(E[q]));
     if constexpr (!FAST) {
 #pragma unroll
-      for (int q = 0; q < 32; ++q) D[q] = (D[q] + F[q]) + E[q];
+      for (int q = 0; q < 32; ++q) D[q] += E[q];
     }
     const int c0 = kTileRows * idx + 32 * half;
     if (role == kSkipT) {  // z_s = relu(q + B_skip)

@@ -44,22 +44,10 @@
 #ifndef DVW_DIAG
 #define DVW_DIAG 0
 #endif
-// Experiments under A/B measurement (tools/diag_c2.sh with DVW_EXP): 1: A's matvec with four
-// accumulator chains per row; 2: B's and C's with one; 4: W_emb_prev column loaded before the
-// logits wait (volatile, so it is not sunk past it).
+// Accumulator-chain variants under A/B measurement (profiles/r2_experiments.md): bit 1: A's matvec
+// with four float2 chains per row (always at LP = 4); bit 2: B's and C's with one (default).
 #ifndef DVW_EXP
 #define DVW_EXP 2
-#endif
-// A/B switches for the round-2 changes (tools/diag_c2.sh): chain CTA 0 with the per-code layer-0
-// table (chain0_*), the per-thread dead flag in wait(), the skip CTAs' parity-staged partials
-#ifndef DVW_CHAIN0
-#define DVW_CHAIN0 1
-#endif
-#ifndef DVW_DEADFLAG
-#define DVW_DEADFLAG 1
-#endif
-#ifndef DVW_SKIPSTAGE
-#define DVW_SKIPSTAGE 1
 #endif
 
 namespace dvw {
@@ -87,14 +75,6 @@ __device__ __forceinline__ constexpr int bar_ra(int jl) { return 7 + jl; }  // c
 constexpr int kBarHX = 11;   // chain: A arrives (h of local layer jl in hs), X syncs and forwards it,
                              // 256; one id per local layer (11..14)
 constexpr int kBarHS = 4;    // head / skip CTAs only (aliases a chain-only id): A + B, 256
-constexpr int kBarY = 15;    // chain CTA 0 at LP = 3: A arrives (code y_{n-1} in ybuf), B and C sync, 384
-constexpr int kBarC0 = 4;    // chain CTA 0 at LP = 3: warpgroup C alone (aliases bar_xr(0), unused there), 128
-// chain CTA 0 at LP = 3 (layers 0 and 1): TMEM columns
-constexpr int kC0M = 0;      // A: M_1 = W_cur_1 W_res_0 (64)
-constexpr int kC0C0 = 64;    // C: W_cur_0 (64), for U
-constexpr int kC0C1 = 128;   // C: W_cur_1 (64), for R_1
-constexpr int kC0B = 192;    // B: W_res_0 (32)
-constexpr int kC0T = 256;    // A: T0 = W_cur_0 W_emb_cur, lane (tanh g | sigmoid g interleaved) x code (256)
 
 // chain TMEM columns (per lane), local layer jl of layers j0..j0+LP-1:
 //   A [0, 64 LP)       : W_cur_0 (CTA 0, jl = 0) or M_j = W_cur_j W_res_{j-1}   (64 each)
@@ -103,9 +83,6 @@ constexpr int kC0T = 256;    // A: T0 = W_cur_0 W_emb_cur, lane (tanh g | sigmoi
 constexpr int kColA = 0;
 
 enum Role { kChain = 0, kHead = 1, kSkip = 2, kIdle = 3 };
-// chain_A/B/C run CTA 0 (sampler + embedding) only where chain0_* does not (LP = 4)
-template <int LP>
-constexpr bool kOldC0 = LP == 4 || !DVW_CHAIN0;
 
 // Vectors are read in column chunks of C floats; chunk c starts at c (C + 4), so the
 // (up to 8) chunks one warp instruction touches occupy distinct bank groups.
@@ -136,12 +113,6 @@ struct __align__(16) Mail {
   double dscr[8];
   float fscr[8];
   int iscr[16];
-  // chain CTA 0 at LP = 3 (chain0_*): the drawn code, U_n = W_cur_0 (W_emb_prev[:, y_{n-2}] + B_emb)
-  // by sample parity, and warpgroup C's scratch vectors
-  int ybuf[2];
-  float U[2][2 * R];
-  alignas(16) float xc[kHLen];
-  alignas(16) float ue[kHLen];
 };
 
 struct Params {
@@ -155,9 +126,11 @@ struct Ctx {
   int* err;
   int size;
   int64_t sidx;  // the stream this cluster generates (one cluster per stream: cluster index)
-  // per thread (each thread builds its own Ctx): set by this thread's first failed wait; from then on
-  // every wait fails at once and no barrier is re-armed -- after an abort a barrier can be stuck in a
-  // phase, and a parity probe of the other phase would succeed spuriously and arm it a second time
+  // per thread (every thread builds its own Ctx): set by the thread's first failed wait.  From then on
+  // the thread never re-arms a barrier: after an abort a barrier can stay in one phase, and a later
+  // parity probe of the other phase succeeds spuriously -- arming it again would arrive twice in
+  // that phase (an mbarrier fault).  The roles still run every sample, so named barriers between
+  // warpgroups stay matched.
   mutable bool dead;
 };
 
@@ -174,19 +147,8 @@ __device__ __forceinline__ float* s_logits(const RunArgs& A, const Ctx& cx) {
 __device__ __forceinline__ uint8_t* s_codes(const RunArgs& A, const Ctx& cx) { return A.out_codes + cx.sidx * A.N; }
 __device__ __forceinline__ int* s_ystate(const RunArgs& A, const Ctx& cx) { return A.ystate + 2 * cx.sidx; }
 
-// Named barriers: producer warps arrive and consumer warps sync at different code locations (warp
-// specialisation).  DVW_BAR_ALIGNED=0 uses the non-.aligned forms, which PTX defines for that use
-// (compute-sanitizer synccheck flags the .aligned ones), at the price of a WARPSYNC per barrier.
-#ifndef DVW_BAR_ALIGNED
-#define DVW_BAR_ALIGNED 1
-#endif
 __device__ __forceinline__ void bar_arrive(int id, int n) {
-  if constexpr (DVW_BAR_ALIGNED) asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-  else asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bsync(int id, int n) {
-  if constexpr (DVW_BAR_ALIGNED) asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-  else asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 __device__ __forceinline__ void raise_abort(const Ctx& cx, int code) {
@@ -207,34 +169,23 @@ __device__ __forceinline__ void raise_abort(const Ctx& cx, int code) {
 // CTA-scope acquire: every hand-off into this CTA is a st.async into its own shared memory,
 // tracked by the mbarrier's transaction count, so observing the phase makes the data visible;
 // a cluster-scope acquire would also invalidate L1 (CCTL.IVALL) on every wake-up.
-// The watchdog's bookkeeping, out of line (it runs only after 16 unsuccessful probes, so the hot
-// wake-up path never calls it, and the ~25 wait sites do not each carry a copy: instruction-cache
-// footprint).  Returns the start time, or 0 = give up (abort seen, or timeout: raises the abort).
-__device__ __noinline__ uint64_t wait_check(const Ctx& cx, uint64_t t0, int code) {
-  if (*reinterpret_cast<volatile int*>(&cx.mail->abort_flag)) {
-    cx.dead = true;
-    return 0;
-  }
-  const uint64_t now = ptx::globaltimer();
-  if (t0 == 0) return now;
-  if (now - t0 > kTimeoutNs) {
-    raise_abort(cx, code);
-    cx.dead = true;
-    return 0;
-  }
-  return t0;
-}
-
 __device__ __forceinline__ bool wait(const Ctx& cx, uint64_t* bar, uint32_t parity, int code) {
-  if (DVW_DEADFLAG && cx.dead) return false;
   const uint32_t b = ptx::smem_u32(bar);
-  uint64_t t0 = 0;
+  if (ptx::mbar_try_wait_cta(b, parity)) return true;
+  const uint64_t t0 = ptx::globaltimer();
 #pragma unroll 1
   for (uint32_t i = 1;; ++i) {
     if (ptx::mbar_try_wait_cta(b, parity)) return true;
-    if ((i & 15) == 0) {
-      t0 = wait_check(cx, t0, code);
-      if (t0 == 0) return false;
+    if ((i & 7) == 0) {
+      if (*reinterpret_cast<volatile int*>(&cx.mail->abort_flag)) {
+        cx.dead = true;
+        return false;
+      }
+      if (ptx::globaltimer() - t0 > kTimeoutNs) {
+        raise_abort(cx, code);
+        cx.dead = true;
+        return false;
+      }
     }
   }
 }
@@ -331,7 +282,8 @@ __device__ __forceinline__ void tile_dot_half(const float* w, const float* v, fl
 }
 
 // tile_dot_half with four (NCH = 4) or one (NCH = 1) float2 accumulator chains per row instead
-// of two; fixed combine order (bitwise deterministic).
+// of two; fixed combine order (bitwise deterministic).  One chain makes B's and C's matvecs
+// yield issue slots to A's (C2 7.45 vs 7.51 us); four make A's faster at LP = 4 (C3).
 template <int RQ, int NCH>
 __device__ __forceinline__ void tile_dot_half_n(const float* w, const float* v, float (&acc)[RQ]) {
   float2 s[RQ][NCH];
@@ -358,12 +310,6 @@ __device__ __forceinline__ void tile_dot_half_n(const float* w, const float* v, 
     else
       acc[m] = s[m][0].x + s[m][0].y;
   }
-}
-
-__device__ __forceinline__ float ldg_early(const float* p) {
-  float v;
-  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
-  return v;
 }
 
 // One transposing level of a butterfly reduction: lanes whose `bit` is set keep
@@ -476,16 +422,10 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
       const uint8_t* fb = s_forced(A, cx);
       const float u = ub ? __ldg(ub + n - 1) : 0.0f;
       const int yf = fb ? (int)__ldg(fb + n - 1) : 0;
-      if constexpr ((DVW_EXP & 4) != 0) {
-        ep0 = ldg_early(embp_g + y1 * R + k);  // W_emb_prev[:, y_{n-2}] (= y1 before the update)
-        ep1 = ldg_early(embp_g + y1 * R + k + 32);
-      } else {
-        ep0 = __ldg(embp_g + y1 * R + k);  // W_emb_prev[:, y_{n-2}] (= y1 before the update)
-        ep1 = __ldg(embp_g + y1 * R + k + 32);
-      }
+      ep0 = __ldg(embp_g + y1 * R + k);  // W_emb_prev[:, y_{n-2}] (= y1 before the update)
+      ep1 = __ldg(embp_g + y1 * R + k + 32);
       uint64_t* tp = (k == 0) ? trace_slot<TRACE>(A, n) : nullptr;
-      if (wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11) && k == 0)
-        ptx::mbar_arm(ptx::smem_u32(&m.bar_logits), kLevels * 4);
+      if (wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11) && k == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_logits), kLevels * 4);
       stamp<TRACE>(tp, 1);
       if (k == 0) trace<TRACE>(A, n - 1, 3);
       int y;
@@ -514,13 +454,13 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
     x0[pad16(k + 32)] = (ep1 + wembc[y1 * R + k + 32]) + bemb[k + 32];
     if (k == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 7);
   }
-  bsync(kBarMath, kMath);
+  ptx::bar_sync(kBarMath, kMath);
   if (k == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 30);
 }
 
 // The final draw (sample N-1) after the last layer pass (first warp of A); returns it.
 template <int NL = 0>
-__device__ __noinline__ int final_draw(const Params& P, const Ctx& cx, int k) {
+__device__ __forceinline__ int final_draw(const Params& P, const Ctx& cx, int k) {
   const RunArgs& A = P.a;
   Mail& m = *cx.mail;
   if (k >= 32) return 0;
@@ -595,10 +535,10 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
   for (int64_t n = 0; n < A.N; ++n) {
     const int p = (int)(n & 1);
     ptx::tmem_load_async<64>(tm, w);  // layer j0's tile, hidden behind the waits
-    if (kOldC0<LP> && c == 0) {
+    if (c == 0) {
       sample_and_embed<TRACE, NL>(P, cx, n, a, y1, y2, wembc, bemb);
     } else {
-      if (wait(cx, &m.bar_hin, (uint32_t)p, 12) && a == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_hin), R * 4);
+      if (wait(cx, &m.bar_hin, (uint32_t)p, 12) && a == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_hin), R * 4);
     }
     if (a == 0) trace<TRACE>(A, n, 0);
     uint64_t* tp = (a == 0) ? trace_slot<TRACE>(A, n) : nullptr;
@@ -607,12 +547,10 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
 #pragma unroll
     for (int jl = 0; jl < LP; ++jl) {
       if (jl < nl) {
-        const bool direct = (kOldC0<LP> && c == 0 && jl == 0);  // a_0 = W_cur_0 x_0
+        const bool direct = (c == 0 && jl == 0);  // a_0 = W_cur_0 x_0
         stamp<TRACE>(tp, 8 + 2 * jl);
         const float pre0 = m.pre[jl][hrow], pre1 = m.pre[jl][R + hrow];
         float v[2];
-        // four accumulator chains per row at LP = 4 (C3 14.51 vs 14.98 us), two at LP = 3 (C2 7.45 vs
-        // 7.63 us): measured A/B (tools/diag_c2.sh), code-layout sensitive
         if constexpr ((DVW_EXP & 1) != 0 || LP == 4)
           tile_dot_half_n<2, 4>(w, (direct ? m.xs[p][0] : (jl == 0 ? m.hin : m.hs[p][jl - 1])) + voff, v);
         else
@@ -622,7 +560,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
         v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
         if (!direct) {
           stamp<TRACE>(tp, 14 + jl);
-          bsync(bar_ra(jl), kMain);  // R_j from C
+          ptx::bar_sync(bar_ra(jl), kMain);  // R_j from C
           stamp<TRACE>(tp, 17 + jl);
           v[0] += m.rr[jl][hrow];
           v[1] += m.rr[jl][R + hrow];
@@ -644,7 +582,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
           stamp<TRACE>(tp, 9 + 2 * jl);
         } else {
           if (writer) m.hs[p][jl][pad16(hrow)] = hv;
-          bsync(kBarH, kMain);     // h_j complete for A (next layer) and B
+          ptx::bar_sync(kBarH, kMain);     // h_j complete for A (next layer) and B
           bar_arrive(kBarHX + jl, kMain);  // ... and for X, which forwards it to the skip / head CTAs
           stamp<TRACE>(tp, 9 + 2 * jl);
           ptx::tmem_wait_ld<64>(w);
@@ -652,7 +590,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
       }
     }
   }
-  if (kOldC0<LP> && c == 0 && A.N > 0) {
+  if (c == 0 && A.N > 0) {
     const int y = final_draw<NL>(P, cx, a);
     if (SESS && a == 0 && !A.forced) {  // streaming session: the code history for the next call
       s_ystate(A, cx)[0] = y;
@@ -676,7 +614,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
   const bool writer = half == 0;
   const int voff = 40 * half;
   const int nl = pl.chain_nl[c];
-  const int xb = (kOldC0<LP> && c == 0) ? 1 : 0;
+  const int xb = (c == 0) ? 1 : 0;
   const bool last_cta = (c == pl.nc - 1);
   const float* wres = sw + kSmWres;  // LP = 4: [LPC][8][128][4] in shared memory
   const uint32_t tmb = tmem_lane_addr(m) + kColB3;  // LP = 3: tensor memory
@@ -688,7 +626,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
 
   for (int64_t n = 0; n < A.N; ++n) {
     const int p = (int)(n & 1);
-    if (kOldC0<LP> && c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
+    if (c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
 #pragma unroll
     for (int jl = 0; jl < LP; ++jl) {
       if (jl < nl && jl >= xb) {
@@ -710,7 +648,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
           xv = m.xin;
         } else {
           if (b == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 24 + jl - 1);  // B arrives for h_{j0+jl-1}
-          bsync(kBarH, kMain);  // h_{j0+jl-1} from A
+          ptx::bar_sync(kBarH, kMain);  // h_{j0+jl-1} from A
           hv = m.hs[p][jl - 1];
           xv = m.xs[p][jl - 1];
         }
@@ -736,7 +674,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_done));
     }
   }
-  if (kOldC0<LP> && c == 0 && A.N > 0) final_draw(P, cx, k);
+  if (c == 0 && A.N > 0) final_draw(P, cx, k);
 }
 
 // ------------------------------------------------------------------ chain CTA, warpgroup C (R terms)
@@ -753,7 +691,7 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
   const bool writer = half == 0;
   const int voff = 40 * half;
   const int nl = pl.chain_nl[c];
-  const int xb = (kOldC0<LP> && c == 0) ? 1 : 0;
+  const int xb = (c == 0) ? 1 : 0;
   const uint32_t tm = tmem_lane_addr(m) + col_c(LP);
   const float* cf = sw + sm_fold(LP);  // [LPC][2R]
   const float* wembc = sw + sm_emb(LP);
@@ -764,16 +702,16 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
   for (int64_t n = 0; n < A.N; ++n) {
     const int p = (int)(n & 1);
     if (nl > xb) ptx::tmem_load_async<64>(tm + 64 * xb, w);
-    if (kOldC0<LP> && c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
+    if (c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
 #pragma unroll
     for (int jl = 0; jl < LP; ++jl) {
       if (jl < nl && jl >= xb) {
         const float* xv;
         if (jl == 0) {
-          if (wait(cx, &m.bar_xin, (uint32_t)p, 15) && ct == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_xin), R * 4);
+          if (wait(cx, &m.bar_xin, (uint32_t)p, 15) && ct == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_xin), R * 4);
           xv = m.xin;
         } else {
-          if (jl - 1 >= xb) bsync(bar_xr(jl - 1), kMain);  // x_{j0+jl-1} from B
+          if (jl - 1 >= xb) ptx::bar_sync(bar_xr(jl - 1), kMain);  // x_{j0+jl-1} from B
           xv = m.xs[p][jl - 1];
         }
         ptx::tmem_wait_ld<64>(w);
@@ -791,246 +729,11 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
         if (ct == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 21 + jl);
         // sync, not arrive: C's next matvec (R_{j+1}) then starts only once A is past this
         // layer's matvec, so it overlaps A's gate instead of competing with A's FMAs
-        bsync(bar_ra(jl), kMain);
+        ptx::bar_sync(bar_ra(jl), kMain);
       }
     }
   }
-  if (kOldC0<LP> && c == 0 && A.N > 0) final_draw(P, cx, k);
-}
-
-
-// ------------------------------------------------------------------ chain CTA 0 at LP = 3 (layers 0, 1)
-// Layer 0 of sample n without a matvec after the draw (reading R34): with x_0 = W_emb_prev[:, y_{n-2}] +
-// W_emb_cur[:, y_{n-1}] + B_emb,
-//   a_0 = W_cur_0 x_0 + pre_0 = T0[:, y_{n-1}] + U_n + pre_0,  T0 = W_cur_0 W_emb_cur (fp64 on the host,
-//   rounded once; one TMEM column per code), U_n = W_cur_0 (W_emb_prev[:, y_{n-2}] + B_emb)
-// where U_n is computed by warpgroup C one sample ahead (y_{n-2} is drawn a sample earlier).  Every
-// warp of A draws y_{n-1} itself (the same deterministic draw, App. A.4), reads its lane's T0 entry
-// at column y and applies the gate: no block barrier between the draw and layer 0.  B and C learn
-// y from A through kBarY and build x_0 off the chain (queues, R_1 = W_cur_1 x_0 + c_1, x_1).
-__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
-  uint32_t r;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-  return __uint_as_float(r);
-}
-
-template <bool TRACE, int NL, bool SESS>
-__device__ void chain0_A(const Params& P, const Ctx& cx, const float* sw) {
-  const RunArgs& A = P.a;
-  const ClusterPlan& pl = P.p;
-  Mail& m = *cx.mail;
-  const int a = threadIdx.x - kAux;  // 0..127
-  const int lane = a & 31, hrow = a >> 1, half = a & 1;
-  const bool writer = half == 0;
-  const int voff = 40 * half;
-  const int nl = pl.chain_nl[0];
-  const bool last_cta = pl.nc == 1;
-  const uint32_t tl = tmem_lane_addr(m);
-  int y1 = SESS ? s_ystate(A, cx)[0] : kLevels / 2, y2 = SESS ? s_ystate(A, cx)[1] : kLevels / 2;
-  (void)y2;
-  float w[64];
-  const float* ub = s_uniforms(A, cx);
-  const uint8_t* fb = s_forced(A, cx);
-
-  for (int64_t n = 0; n < A.N; ++n) {
-    const int p = (int)(n & 1);
-    if (nl > 1) ptx::tmem_load_async<64>(tl + kC0M, w);  // M_1, hidden behind the waits
-    uint64_t* tp = (a == 0) ? trace_slot<TRACE>(A, n) : nullptr;
-    int y = y1;  // y_{n-1}
-    if (n > 0) {
-      const float u = ub ? __ldg(ub + n - 1) : 0.0f;
-      const int yf = fb ? (int)__ldg(fb + n - 1) : 0;
-      if (wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11) && a == 0)
-        ptx::mbar_arm(ptx::smem_u32(&m.bar_logits), kLevels * 4);
-      stamp<TRACE>(tp, 1);
-      if (a == 0) trace<TRACE>(A, n - 1, 3);
-      if (fb) {
-        if (a < 32) {
-          float4* o = reinterpret_cast<float4*>(s_logits(A, cx) + (n - 1) * kLevels) + 2 * lane;
-          o[0] = lds4(m.logits_in + 8 * lane);
-          o[1] = lds4(m.logits_in + 8 * lane + 4);
-        }
-        y = yf;
-      } else {
-        stamp<TRACE>(tp, 4);
-        if constexpr ((DVW_DIAG & 16) != 0) y = min((int)(u * 256.0f) + (m.logits_in[0] > 1e30f), 255);
-        else y = sample_warp<NL>(m.logits_in, u, lane);  // every warp of A: the same draw
-        stamp<TRACE>(tp, 6);
-        if (a == 0) s_codes(A, cx)[n - 1] = (uint8_t)y;
-      }
-      if (a == 0) trace<TRACE>(A, n, 20);
-    }
-    y2 = y1;
-    y1 = y;
-    bsync(bar_ra(0), kMain);  // U_n from C (computed during the previous sample)
-    if (a == 0) m.ybuf[p] = y;
-    bar_arrive(kBarY, kMath);         // B and C take y_{n-1} from here
-    const float tv = tmem_ld1(tl + kC0T + (uint32_t)y);  // T0[row(a)][y_{n-1}]
-    stamp<TRACE>(tp, 7);
-    if (a == 0) trace<TRACE>(A, n, 0);
-    wait(cx, &m.bar_pre, (uint32_t)p, 13);
-    stamp<TRACE>(tp, 8);
-    const float ot = __shfl_xor_sync(0xffffffffu, tv, 1);
-    const float vt = half ? ot : tv, vs = half ? tv : ot;  // lane 2g: tanh row g, lane 2g+1: sigmoid row g
-    const float a0 = (vt + m.U[p][hrow]) + m.pre[0][hrow];
-    const float a1 = (vs + m.U[p][R + hrow]) + m.pre[0][R + hrow];
-    const float h0 = NL == 1 ? gate_approx(a0, a1) : NL == 2 ? gate_appc(a0, a1) : gate_fast(a0, a1);
-    stamp<TRACE>(tp, 27);
-    if (nl == 1) {  // l = 1: h_0 goes to the heads (X forwards it)
-      if (writer) m.hs[p][0][pad16(hrow)] = h0;
-      bar_arrive(kBarHX, kMain);
-      continue;
-    }
-    if (writer) m.hs[p][0][pad16(hrow)] = h0;
-    bsync(kBarH, kMain);  // h_0 complete for A and B
-    bar_arrive(kBarHX, kMain);    // ... and for X
-    stamp<TRACE>(tp, 9);
-    ptx::tmem_wait_ld<64>(w);
-    // layer 1: a_1 = M_1 h_0 + R_1 + pre_1 (R22), the CTA's last layer
-    stamp<TRACE>(tp, 10);
-    float v[2];
-    tile_dot_half<2>(w, m.hs[p][0] + voff, v);
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-    v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
-    stamp<TRACE>(tp, 15);
-    bsync(bar_ra(1), kMain);  // R_1 from C
-    stamp<TRACE>(tp, 18);
-    v[0] += m.rr[1][hrow];
-    v[1] += m.rr[1][R + hrow];
-    const float pre0 = m.pre[1][hrow], pre1 = m.pre[1][R + hrow];
-    const float hv = NL == 1   ? gate_approx(v[0] + pre0, v[1] + pre1)
-                     : NL == 2 ? gate_appc(v[0] + pre0, v[1] + pre1)
-                               : gate_fast(v[0] + pre0, v[1] + pre1);
-    stamp<TRACE>(tp, 28);
-    if (writer) {
-      if (!last_cta) ptx::st_async(remote(&m.hin[pad16(hrow)], 1), hv, remote(&m.bar_hin, 1));
-      m.hs[p][1][pad16(hrow)] = hv;
-    }
-    bar_arrive(kBarHX + 1, kMain);
-    stamp<TRACE>(tp, 11);
-  }
-  if (A.N > 0) {
-    const int y = final_draw<NL>(P, cx, a);
-    if (SESS && a == 0 && !A.forced) {
-      s_ystate(A, cx)[0] = y;
-      s_ystate(A, cx)[1] = y1;
-    }
-  }
-}
-
-// x_0 (for the queue and x_1) and x_1 = x_0 + W_res_0 h_0 + B_res_0.
-template <bool TRACE, bool SESS>
-__device__ void chain0_B(const Params& P, const Ctx& cx, const float* sw) {
-  const RunArgs& A = P.a;
-  const ClusterPlan& pl = P.p;
-  Mail& m = *cx.mail;
-  const int b = threadIdx.x - kAux - 128;  // 0..127
-  const int row = b >> 1, half = b & 1;
-  const bool writer = half == 0;
-  const int voff = 40 * half;
-  const int nl = pl.chain_nl[0];
-  const bool last_cta = pl.nc == 1;
-  const uint32_t tl = tmem_lane_addr(m);
-  const float* bres = sw + sm_bres(3);  // [LPC][R]: B_res_0 at jl = 1
-  const float* wembc = sw + sm_emb(3);  // W_emb_cur^T [256][R]
-  const float* bemb = wembc + kLevels * R;
-  const float* embp_g = P.pk + P.p.embp_off;  // W_emb_prev^T [256][R]
-  int yk = SESS ? s_ystate(A, cx)[1] : kLevels / 2;  // y_{n-2} at the start of sample n
-  float wr[32];
-
-  for (int64_t n = 0; n < A.N; ++n) {
-    const int p = (int)(n & 1);
-    if (nl > 1) ptx::tmem_load_async<32>(tl + kC0B, wr);
-    const float ep = ldg_early(embp_g + yk * R + row);  // W_emb_prev[row, y_{n-2}]
-    bsync(kBarY, kMath);
-    const int y = m.ybuf[p];                                 // y_{n-1}
-    const float x0 = (ep + wembc[y * R + row]) + bemb[row];  // same order as the direct embedding
-    yk = y;
-    if (writer) m.xs[p][0][pad16(row)] = x0;
-    if (nl > 1) {
-      bsync(kBarH, kMain);  // h_0 from A
-      ptx::tmem_wait_ld<32>(wr);
-      float v[1];
-      if constexpr ((DVW_EXP & 2) != 0) tile_dot_half_n<1, 1>(wr, m.hs[p][0] + voff, v);
-      else tile_dot_half<1>(wr, m.hs[p][0] + voff, v);
-      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-      const float x1 = x0 + (v[0] + bres[R + row]);
-      if (writer) {
-        m.xs[p][1][pad16(row)] = x1;
-        if (!last_cta) ptx::st_async(remote(&m.xin[pad16(row)], 1), x1, remote(&m.bar_xin, 1));
-      }
-    }
-    if (b == 0) {
-      trace<TRACE>(A, n, 2);
-      ptx::mbar_arrive(ptx::smem_u32(&m.bar_done));
-    }
-  }
-}
-
-// R_1 = W_cur_1 x_0 + c_1 for A's layer 1, and U_{n+1} = W_cur_0 (W_emb_prev[:, y_{n-1}] + B_emb) for
-// A's layer 0 of the next sample.
-template <bool TRACE, bool SESS>
-__device__ void chain0_C(const Params& P, const Ctx& cx, const float* sw) {
-  const RunArgs& A = P.a;
-  const ClusterPlan& pl = P.p;
-  Mail& m = *cx.mail;
-  const int ct = threadIdx.x - kAux - 256;  // 0..127
-  const int hrow = ct >> 1, half = ct & 1;
-  const bool writer = half == 0;
-  const int voff = 40 * half;
-  const int nl = pl.chain_nl[0];
-  const uint32_t tl = tmem_lane_addr(m);
-  const float* cf = sw + sm_fold(3);    // [LPC][2R]: c_1 at jl = 1
-  const float* wembc = sw + sm_emb(3);
-  const float* bemb = wembc + kLevels * R;
-  const float* embp_g = P.pk + P.p.embp_off;
-  int yk = SESS ? s_ystate(A, cx)[1] : kLevels / 2;  // y_{n-2} at the start of sample n
-  float w[64];
-
-  // U = W_cur_0 (W_emb_prev[:, yp] + B_emb) into U[slot]; then A may read it (bar_ra(0))
-  auto make_u = [&](int yp, int slot) {
-    ptx::tmem_load_async<64>(tl + kC0C0, w);
-    if (ct < R) m.ue[pad16(ct)] = __ldg(embp_g + yp * R + ct) + bemb[ct];
-    bsync(kBarC0, 128);
-    ptx::tmem_wait_ld<64>(w);
-    float v[2];
-    if constexpr ((DVW_EXP & 2) != 0) tile_dot_half_n<2, 1>(w, m.ue + voff, v);
-    else tile_dot_half<2>(w, m.ue + voff, v);
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-    v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
-    if (writer) {
-      m.U[slot][hrow] = v[0];
-      m.U[slot][R + hrow] = v[1];
-    }
-    bar_arrive(bar_ra(0), kMain);
-  };
-  make_u(yk, 0);  // U_0 from y_{-2}
-  for (int64_t n = 0; n < A.N; ++n) {
-    const int p = (int)(n & 1);
-    if (nl > 1) ptx::tmem_load_async<64>(tl + kC0C1, w);
-    const float ep = (ct < R) ? ldg_early(embp_g + yk * R + ct) : 0.0f;  // W_emb_prev[ct, y_{n-2}]
-    bsync(kBarY, kMath);
-    const int y = m.ybuf[p];  // y_{n-1}
-    yk = y;
-    if (nl > 1) {
-      if (ct < R) m.xc[pad16(ct)] = (ep + wembc[y * R + ct]) + bemb[ct];  // x_0
-      bsync(kBarC0, 128);
-      ptx::tmem_wait_ld<64>(w);
-      float v[2];
-      if constexpr ((DVW_EXP & 2) != 0) tile_dot_half_n<2, 1>(w, m.xc + voff, v);
-      else tile_dot_half<2>(w, m.xc + voff, v);
-      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-      v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
-      if (writer) {
-        m.rr[1][hrow] = v[0] + cf[2 * R + hrow];
-        m.rr[1][R + hrow] = v[1] + cf[2 * R + R + hrow];
-      }
-      if (ct == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 22);
-      bsync(bar_ra(1), kMain);
-    }
-    if (n + 1 < A.N) make_u(y, p ^ 1);  // U_{n+1} from y_{n-1}
-  }
+  if (c == 0 && A.N > 0) final_draw(P, cx, k);
 }
 
 // ------------------------------------------------------------------ chain CTA, warpgroup X (aux)
@@ -1040,7 +743,7 @@ __device__ void chain0_C(const Params& P, const Ctx& cx, const float* sw) {
 __device__ __forceinline__ void aux_forward(const ClusterPlan& pl, Mail& m, int first, int nl, int at, int p) {
   for (int jl = 0; jl < nl; ++jl) {
     const int j = first + jl;
-    bsync(kBarHX + jl, kMain);
+    ptx::bar_sync(kBarHX + jl, kMain);
     if (j >= pl.L - 2) {
       const int sl = pl.L - 1 - j;
       if (at < 16 * NH) {
@@ -1093,7 +796,7 @@ __device__ __forceinline__ void aux_chain_skip(const Params& P, const Ctx& cx, i
   }
 #pragma unroll
   for (int rr = 0; rr < RR; ++rr) m.zs[at + 128 * rr] = part[rr];
-  bsync(kBarAux, kAux);
+  ptx::bar_sync(kBarAux, kAux);
   const int slot = pl.xpart_slot[c];
 #pragma unroll
   for (int i = at; i < (S / 4) * NH; i += kAux) {  // S / 4 float4 per head
@@ -1156,7 +859,7 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
         if (n > 0 && d >= 2) ring[(int64_t)((ng - 1) % d) * R + at] = xc;
         m.xp[at] = xpv;
       }
-      bsync(kBarAux, kAux);
+      ptx::bar_sync(kBarAux, kAux);
       float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < ((DVW_DIAG & 1) ? 0 : 16); ++q) {
@@ -1165,7 +868,7 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
         a23 = ffma2(wv[q].z, wv[q].w, x.z, x.w, a23);
       }
       m.pre[jl][at] = (bj[jl * 2 * R + at] + lv) + ((a01.x + a01.y) + (a23.x + a23.y));
-      bsync(kBarAux, kAux);
+      ptx::bar_sync(kBarAux, kAux);
     }
     if (at == 0) {
       trace<TRACE>(A, n, 5);
@@ -1237,7 +940,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     float d2 = 0.0f;
     if (has2) {
       ptx::tmem_load_async<RQ * 16>(tm + cSk2, w);  // W_skip^(l-1) tile
-      if (wait(cx, &m.bar_h[1], par, 24) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[1]), R * 4);
+      if (wait(cx, &m.bar_h[1], par, 24) && k == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[1]), R * 4);
       if (k == 0) trace<TRACE>(A, n, 4);
       ptx::tmem_wait_ld<RQ * 16>(w);
       float v2[RQ];
@@ -1246,7 +949,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
       if (k == 0) trace<TRACE>(A, n, 6);
     }
     ptx::tmem_load_async<RQ * 16>(tm, w);  // W_skip^(l) tile, hidden behind the wait
-    if (wait(cx, &m.bar_h[0], par, 21) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[0]), R * 4);
+    if (wait(cx, &m.bar_h[0], par, 21) && k == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[0]), R * 4);
     if (k == 0) trace<TRACE>(A, n, 0);
     ptx::tmem_wait_ld<RQ * 16>(w);
     float v[RQ];
@@ -1254,7 +957,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     ptx::tmem_load_async<4 * CZ>(tm + cRelu, w);
     v[0] = finish(v);
     if (np > 0) {
-      if (wait(cx, &m.bar_part, par, 22) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_part), np * S * 4);
+      if (wait(cx, &m.bar_part, par, 22) && k == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_part), np * S * 4);
     }
     if (k == 0) trace<TRACE>(A, n, 1);
     if (qwriter) {
@@ -1264,7 +967,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
       qv += v[0];
       m.zs[cpad<CZ>(qrow)] = fmaxf(qv, 0.0f);
     }
-    bsync(kBarHS, kMain);
+    ptx::bar_sync(kBarHS, kMain);
     if (k == 0) trace<TRACE>(A, n, 7);
     // z_a = relu(W_relu z_s + B_relu)
     ptx::tmem_wait_ld<4 * CZ>(w);
@@ -1282,7 +985,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
       ptx::st_async(remote(&m.za_in[dst], pl.nc + (k & 3)), zav, remote(&m.bar_za, pl.nc + (k & 3)));
     }
     if (k == 0) trace<TRACE>(A, n, 9);
-    if (wait(cx, &m.bar_za, par, 23) && k == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_za), kLevels * 4);
+    if (wait(cx, &m.bar_za, par, 23) && k == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_za), kLevels * 4);
     if (k == 0) trace<TRACE>(A, n, 2);
     // logits = W_out z_a + B_out
     ptx::tmem_wait_ld<64>(w);
@@ -1336,7 +1039,7 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
     for (int sl = 0; sl < nown; ++sl) {
       const bool in_tmem = sl >= nsm;
       if (in_tmem) ptx::tmem_load_async<QS>(tm + (sl - nsm) * QS, wl);
-      if (wait(cx, &m.bar_h[sl], par, 31) && t == 0) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
+      if (wait(cx, &m.bar_h[sl], par, 31) && t == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
       if (in_tmem) {
         ptx::tmem_wait_ld<QS>(wl);
       } else {
@@ -1352,11 +1055,11 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
       part += finish(v);
     }
     // staged by sample parity (a skip CTA's own part[] is otherwise unused): the next sample's
-    // writes can never meet this sample's reads, with no second barrier
-    float* stage = DVW_SKIPSTAGE ? m.part[par] : m.zs;
+    // writes can never meet this sample's reads (compute-sanitizer racecheck), with no second barrier
+    float* stage = m.part[par];
     if (writer) stage[row] = part;
     if (t == 0) trace<TRACE>(A, n, 1);
-    bsync(kBarHS, kMain);
+    ptx::bar_sync(kBarHS, kMain);
     if (t < (S / 4) * NH) {
       const int hh = t / (S / 4), e = t % (S / 4);
       ptx::st_async4(remote(&m.part[k][4 * e], pl.nc + hh), lds4(&stage[4 * e]), remote(&m.bar_part, pl.nc + hh));
@@ -1370,7 +1073,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   Mail* mail = reinterpret_cast<Mail*>(smem_raw);
   float* sw = reinterpret_cast<float*>(smem_raw + ((sizeof(Mail) + 127) & ~size_t(127)));
   const ClusterPlan& pl = P.p;
-  if ((int)(blockIdx.x / pl.size) >= P.a.n_streams) return;  // grid padding (DVW_PAD_CLUSTERS): idle cluster
   const int rank = (int)ptx::cluster_rank();
   const int t = threadIdx.x;
   Ctx cx{mail, P.a.err, pl.size, (int64_t)(blockIdx.x / pl.size), false};
@@ -1415,11 +1117,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   if (t >= kAux && role != kIdle) {
     const int wg = (t - kAux) >> 7;  // 0 = A, 1 = B, 2 = C
     int c0 = 0, c1 = 0;
-    if (role == kChain && LP == 3 && DVW_CHAIN0 && idx == 0) {  // chain0_*: A [0,64) + [256,512), C [64,192), B [192,224)
-      if (wg == 0) { c0 = kC0M; c1 = kC0T + kLevels; }
-      else if (wg == 2) { c0 = kC0C0; c1 = kC0B; }
-      else { c0 = kC0B; c1 = kC0B + 32; }
-    } else if (role == kChain) {
+    if (role == kChain) {
       if (wg == 0) { c0 = kColA; c1 = col_c(LP); }
       else if (wg == 2) { c0 = col_c(LP); c1 = 2 * col_c(LP); }
       else if (LP == 3) { c0 = kColB3; c1 = kColB3 + 3 * 32; }
@@ -1432,7 +1130,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     const float* img = P.pk + pl.pk_off[rank];
     const uint32_t ta = tmem_lane_addr(*mail);
     for (int col = c0; col < c1; col += 16) {
-      if (role == kChain && LP == 3 && DVW_CHAIN0 && idx == 0 && wg == 0 && col == kC0M + 64) col = kC0T;  // skip C's and B's
       float v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = __ldg(img + (int64_t)(col + i) * 128 + lane);
@@ -1446,11 +1143,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   ptx::cluster_sync();
 
   if (t >= kAux) {
-    if (role == kChain && LP == 3 && DVW_CHAIN0 && idx == 0) {
-      if (t < kAux + 128) chain0_A<TRACE, NL, SESS>(P, cx, sw);
-      else if (t < kAux + 256) chain0_B<TRACE, SESS>(P, cx, sw);
-      else chain0_C<TRACE, SESS>(P, cx, sw);
-    } else if (role == kChain) {
+    if (role == kChain) {
       if (t < kAux + 128) chain_A<LP, TRACE, NL, SESS>(P, cx, idx, sw);
       else if (t < kAux + 256) chain_B<LP, TRACE, SESS>(P, cx, idx, sw);
       else chain_C<LP, TRACE, SESS>(P, cx, idx, sw);
@@ -1460,7 +1153,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
       if (t < kAux + kMain) skip_main<S, TRACE>(P, cx, idx, sw);
     }
     ptx::tmem_fence_before();
-    bsync(kBarMath, kMath);
+    ptx::bar_sync(kBarMath, kMath);
     if (t == kAux) ptx::mbar_arrive(ptx::smem_u32(&mail->bar_exit));
     __syncwarp();
     ptx::cluster_sync();
@@ -1528,12 +1221,10 @@ ClusterPlan plan_lp(int L, int r, int s, int device, int lp) {
   if (r != R) { p.why = "cluster kernel is built for r = 64"; return p; }
   if (s != 128 && s != 256) { p.why = "cluster kernel needs s in {128, 256}"; return p; }
   if (L > kCMaxLayers) { p.why = "too many layers"; return p; }
-  // LP = 3: chain CTA 0 holds layers 0 and 1 only (its TMEM keeps the per-code table T0, chain0_*)
-  const int first0 = (lp == 3 && DVW_CHAIN0) ? std::min(2, L) : std::min(lp, L);
-  p.nc = 1 + (L - first0 + lp - 1) / lp;
+  p.nc = (L + lp - 1) / lp;
   for (int c = 0; c < p.nc; ++c) {
-    p.chain_first[c] = c == 0 ? 0 : first0 + (c - 1) * lp;
-    p.chain_nl[c] = c == 0 ? first0 : std::min(lp, L - p.chain_first[c]);
+    p.chain_first[c] = c * lp;
+    p.chain_nl[c] = std::min(lp, L - c * lp);
     p.xpart_slot[c] = -1;
   }
   p.nh = NH;
@@ -1662,30 +1353,7 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
       // local layer jl (layer j = first + jl) with jl >= xb: M_j = W_cur_j W_res_{j-1}, c_j = W_cur_j B_res_{j-1}
       std::vector<std::vector<float>> M(LPC), cf(LPC);
       for (int jl = xb; jl < nl; ++jl) fold(first + jl - 1, M[jl], cf[jl]);
-      const bool c0t = rank == 0 && lp == 3 && DVW_CHAIN0;  // chain0_* layout (kC0*)
-      if (c0t) {
-        // T0[row][y] = sum_k W_cur_0[row][k] W_emb_cur[k][y] in fp64, rounded once (reading R34);
-        // lane 2g holds tanh row g, lane 2g+1 sigmoid row g
-        for (int lane = 0; lane < 128; ++lane) {
-          const int g = lane >> 1, half = lane & 1, row = half ? R + g : g;
-          for (int y = 0; y < kLevels; ++y) {
-            double acc = 0.0;
-            for (int k = 0; k < R; ++k) acc += (double)W(0, o.w_cur, row, k, R) * (double)w[o.emb_cur + (int64_t)k * kLevels + y];
-            put(kC0T + y, lane, (float)acc);
-          }
-          for (int q = 0; q < 64; ++q) {
-            const int trow = (q < 32) ? g : R + g, col = 32 * half + (q & 31);
-            put(kC0C0 + q, lane, W(0, o.w_cur, trow, col, R));
-            if (nl > 1) {
-              put(kC0M + q, lane, M[1][trow * R + col]);
-              put(kC0C1 + q, lane, W(1, o.w_cur, trow, col, R));
-            }
-          }
-          if (nl > 1)
-            for (int q = 0; q < 32; ++q) put(kC0B + q, lane, W(0, o.w_res, g, 32 * half + q, R));
-        }
-      }
-      for (int lane = 0; lane < 128 && !c0t; ++lane) {
+      for (int lane = 0; lane < 128; ++lane) {
         const int g = lane >> 1, half = lane & 1;  // rows g (tanh), R + g (sigmoid); columns [32 half, +32)
         for (int jl = 0; jl < nl; ++jl)
           for (int q = 0; q < 64; ++q) {
@@ -1795,11 +1463,7 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   cudaLaunchConfig_t cfg{};
   // one cluster per stream: cluster c generates stream c (Ctx::sidx); clusters never wait for
   // each other, so more clusters than fit at once simply run in waves
-  // experiment switch: DVW_PAD_CLUSTERS=k appends k idle clusters that exit at once (does a grid of
-  // >= 148 CTAs change the clocks / issue throttling a 14-CTA launch sees?)
-  const char* pe = std::getenv("DVW_PAD_CLUSTERS");
-  const int pad = pe ? std::max(0, std::atoi(pe)) : 0;
-  cfg.gridDim = dim3(p.size * (a.n_streams + pad));
+  cfg.gridDim = dim3(p.size * a.n_streams);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = p.smem_bytes;
   cfg.stream = st;
@@ -1875,7 +1539,7 @@ __global__ void __launch_bounds__(128, 1) k_probe_layer(int iters, unsigned long
     const float hv = gate_fast(v[0] + pre0, v[1] + pre1);
     if (half == 0) hs[p ^ 1][pad16(hrow)] = hv;
     acc += hv;
-    bsync(1, 128);
+    ptx::bar_sync(1, 128);
   }
   const long long t1 = clock64();
   if (a == 0) {
@@ -1943,7 +1607,7 @@ __global__ void __launch_bounds__(256, 1) k_probe_head(int iters, unsigned long 
     const float z = fmaxf(lg[0], 0.0f) * 0.5f;
     if ((k & 3) == 0) zb[p ^ 1][pad16(64 * (n & 3) + orow)] = z;
     acc += z;
-    bsync(1, 256);
+    ptx::bar_sync(1, 256);
   }
   const long long t1 = clock64();
   if (k == 0) {
