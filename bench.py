@@ -301,6 +301,8 @@ def main():
     ap.add_argument("--with-conditioner", action="store_true",
                     help="start each step from frame-rate features: the GPU QRNN conditioner (row f2) "
                          "runs inside the timed step before generation")
+    ap.add_argument("--as-shard-of", type=int, default=1,
+                    help="split workloads (C5): run rank 0's shard of a G-GPU job on this one GPU")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -326,7 +328,11 @@ def main():
     from paper_1702_07825_b200.shard import gather_codes, generate_sharded, shard_range
 
     cfg, n = wl["cfg"], wl["n"]
-    if wl["split"]:
+    if wl["split"] and args.as_shard_of > 1 and ws == 1:
+        # one GPU runs exactly the block rank 0 of a G-GPU job would run (per-GPU rate at that G;
+        # no collective on the path, so the G-GPU aggregate is G x this when ranks are alike)
+        start, S = shard_range(wl["streams"], args.as_shard_of, 0)
+    elif wl["split"]:
         start, S = shard_range(wl["streams"], ws, rank)
     else:
         S = wl["streams"]
@@ -367,7 +373,7 @@ def main():
             cond_net.run(d_feat, out=d_cond)
         model.generate(d_cond, d_u, HOP, out=out)
 
-    n_utts = wl["streams"] if wl["split"] else S * ws
+    n_utts = (S if args.as_shard_of > 1 else wl["streams"]) if wl["split"] else S * ws
     for i in range(args.warmup):
         if i == 0 and cond_net is None:
             # the first warm-up step through the sharder: this rank's contiguous block of the
@@ -557,7 +563,10 @@ def main():
             "data": "synthetic",
             "config": {"workload": wl["desc"], "samples_per_step": n, "streams_per_gpu": S,
                        "streams_total": total_streams,
-                       "parallelism": f"{ws} GPU(s), independent utterances, no collective on the path",
+                       "parallelism": (f"{ws} GPU(s), independent utterances, no collective on the path"
+                                       if args.as_shard_of <= 1 else
+                                       f"1 GPU running rank 0's shard of a {args.as_shard_of}-GPU job "
+                                       f"(the per-GPU rate at G = {args.as_shard_of}; not a multi-GPU run)"),
                        "kernel": kname, "grid": info["last_grid"], "cluster_ctas": info["last_cluster"],
                        "launches_per_step": info["last_launches"] + (5 if cond_net is not None else 0),
                        "conditioner": ("GPU QRNN (2 bidirectional fo-pooling layers, 227 features, 64 hidden) "

@@ -258,8 +258,7 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
       sess->bws_bytes = need;
     }
   } else if (kern == DVW_KERNEL_TC) {
-    const int nsb = std::min(m->bplan.max_sb, (n_streams + 127) / 128);
-    const size_t need = batch_workspace_bytes(m->bplan, m->dil.data(), nsb);
+    const size_t need = batch_workspace_bytes(m->bplan, m->dil.data(), n_streams);
     if (m->bws_bytes < need) {
       if (m->d_bws) cudaFree(m->d_bws);
       m->d_bws = nullptr;

@@ -232,6 +232,7 @@ __device__ __forceinline__ int sample_256(float logit, float u, double* dscratch
 struct LaunchInfo {
   int grid = 0, cluster = 1, threads = 0;
   int64_t launches = 0;
+  int rows_per_block = 0;  // batched kernel: streams per stream block (cluster)
 };
 
 cudaError_t launch_stream_kernel(const RunArgs& a, cudaStream_t st, LaunchInfo* info);

@@ -30,6 +30,7 @@
 // its tf32 truncation) and lo = x - tf32(x), and each K-step issues hi*[hi; lo] (one MMA
 // over the stacked rows) and lo*hi (reading R23).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -42,11 +43,14 @@ namespace dvw {
 namespace {
 
 constexpr int kBT = 256;  // 8 warps; warp w reads TMEM lanes [32(w%4), +32) = its streams, half w/4 of the columns
-constexpr int kStages = 4;
+constexpr int kMaxStages = 8;  // ring depth: as many stages as fit (4 at 128 rows per block, up to 8)
 constexpr int kChunk = 32;                   // K channels per staged chunk
-constexpr int kActChunk = 128 * kChunk;      // floats of one activation chunk (hi or lo)
+constexpr int kActChunk = 128 * kChunk;      // floats of one activation chunk slot (hi or lo), up to 128 rows
 constexpr int kMaxN = 64;
-constexpr int kStageFloats = 2 * kActChunk + kMaxN * kChunk * 2;
+// one stage = [A_hi: r8 x 32][A_lo: r8 x 32][W: up to 2 kMaxN rows x 32] floats
+__host__ __device__ constexpr int stage_floats(int r8) { return 2 * r8 * kChunk + kMaxN * kChunk * 2; }
+constexpr int kCtlBytes = 256;  // Ctl (mbarriers) ahead of the stages
+constexpr int kSmemBytes = kCtlBytes + 4 * stage_floats(128) * 4;  // 4 stages at 128 rows: 192 KB + control
 constexpr int kTmemCols = 128;
 // TMEM accumulator columns (a CTA has one role).  Each tile accumulates hi*hi + lo*hi in
 // its first block of columns and hi*lo in a second block (the stacked-B pass below):
@@ -61,27 +65,32 @@ struct BParams {
   RunArgs a;
   const float* pk;
   int L, r, s, TA, TQ, TH, per_sb, nsb;
+  int rpb, r8;    // streams per stream block (<= 128) and the image's row count (rpb rounded up to 8)
+  int nst;        // ring depth (stages of stage_floats(r8) that fit the shared memory)
   int64_t la_off, la_floats, q_off, q_floats, hr_off, hr_floats, ho_off, ho_floats, bias_off;
 
   float* hb[2];   // h^(k) in hb[k & 1]
-  float* zs;      // [hi | lo] nsb x [s/32][8][128][4]
-  float* za;      // [hi | lo] nsb x [8][8][128][4]
-  float* logits;  // [nsb*128][256]
-  float* ring;    // per layer j: (d_j + 1) slots of [hi | lo] nsb x [r/32][8][128][4]
-  int* yh;        // [nsb*128][2]: y_{n-1}, y_{n-2}
+  float* zs;      // [hi | lo] nsb x [s/32][8][r8][4]
+  float* za;      // [hi | lo] nsb x [8][8][r8][4]
+  float* logits;  // [nsb*rpb][256]
+  float* ring;    // per layer j: (d_j + 1) slots of [hi | lo] nsb x [r/32][8][r8][4]
+  int* yh;        // [nsb*rpb][2]: y_{n-1}, y_{n-2}
   int* abort_flag;  // [nsb]: per stream block (cluster)
   int32_t dil[kBMaxLayers];
   int64_t ring_off[kBMaxLayers];  // floats
 };
 
 struct __align__(8) Ctl {
-  uint64_t full[kStages], freeb[kStages], done;
+  uint64_t full[kMaxStages], freeb[kMaxStages], done;
   uint32_t tmem;
   int abort;
 };
 
-// (channel c, stream row i) inside one stream block's [C/32][8][128][4] image
-__device__ __forceinline__ int canon(int c, int i) { return ((c >> 5) * 8 + ((c & 31) >> 2)) * 512 + i * 4 + (c & 3); }
+// (channel c, stream row i) inside one stream block's [C/32][8][r8][4] image: only the block's rows
+// are stored and staged; the MMA's M = 128 rows past r8 read other data and are never used
+__device__ __forceinline__ int canon(int c, int i, int r8) {
+  return ((c >> 5) * 8 + ((c & 31) >> 2)) * (r8 * 4) + i * 4 + (c & 3);
+}
 
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
@@ -159,7 +168,7 @@ struct Chunk {
 // it back from the same place.  [hi | lo] halves, stream block sb.
 __device__ __forceinline__ const float* x_now(const BParams& P, int j, int64_t n) {
   const int d = P.dil[j];
-  return P.ring + P.ring_off[j] + (int64_t)(n % (d + 1)) * 2 * ((int64_t)P.nsb * P.r * 128);
+  return P.ring + P.ring_off[j] + (int64_t)(n % (d + 1)) * 2 * ((int64_t)P.nsb * P.r * P.r8);
 }
 
 __device__ __forceinline__ int job_chunks(const BParams& P, int role, int ph) {
@@ -173,7 +182,7 @@ __device__ __forceinline__ int job_chunks(const BParams& P, int role, int ph) {
 
 __device__ __forceinline__ Chunk job_chunk(const BParams& P, int role, int idx, int sb, int ph, int64_t n, int c) {
   const int r = P.r, nR = r / kChunk;
-  const int64_t actR = (int64_t)P.nsb * r * 128;  // floats of one [hi | lo] half
+  const int64_t actR = (int64_t)P.nsb * r * P.r8;  // floats of one [hi | lo] half
   Chunk k{};
   if (role == kLayer) {
     const int j = ph;
@@ -207,14 +216,14 @@ __device__ __forceinline__ Chunk job_chunk(const BParams& P, int role, int idx, 
       k.N = 48;
       k.NS = 96;
     }
-    k.ah = src + ((int64_t)sb * r + kc * kChunk) * 128;
+    k.ah = src + ((int64_t)sb * r + kc * kChunk) * P.r8;
     k.al = k.ah + actR;
     k.dcol = kColA;
     k.acc = c > 0;
   } else if (role == kSkipT) {
     const int j = ph - 1;
     const float* src = P.hb[j & 1];
-    k.ah = src + ((int64_t)sb * r + c * kChunk) * 128;
+    k.ah = src + ((int64_t)sb * r + c * kChunk) * P.r8;
     k.al = k.ah + actR;
     k.w = P.pk + P.q_off + ((int64_t)j * P.TQ + idx) * P.q_floats + (int64_t)c * 2 * kTileRows * 32;
     k.N = kTileRows;
@@ -225,8 +234,8 @@ __device__ __forceinline__ Chunk job_chunk(const BParams& P, int role, int idx, 
     const bool relu = ph == P.L + 1;
     const int C = relu ? P.s : kLevels;
     const float* src = relu ? P.zs : P.za;
-    k.ah = src + ((int64_t)sb * C + c * kChunk) * 128;
-    k.al = k.ah + (int64_t)P.nsb * C * 128;
+    k.ah = src + ((int64_t)sb * C + c * kChunk) * P.r8;
+    k.al = k.ah + (int64_t)P.nsb * C * P.r8;
     k.w = P.pk + (relu ? P.hr_off + idx * P.hr_floats : P.ho_off + idx * P.ho_floats) +
           (int64_t)c * 2 * kTileRows * 32;
     k.N = kTileRows;
@@ -242,16 +251,17 @@ template <bool FAST>
 __device__ __forceinline__ bool produce(const BParams& P, Ctl& cl, float* stages, int role, int idx, int sb, int ph,
                                         int64_t n, int nch, uint32_t cseq) {
   for (int c = 0; c < nch; ++c) {
-    const uint32_t g = cseq + c, st = g % kStages, use = g / kStages;
+    const uint32_t g = cseq + c, st = g % P.nst, use = g / P.nst;
     if (use > 0 && !mwait(P, cl, &cl.freeb[st], (use - 1) & 1, 42)) return false;
     const Chunk k = job_chunk(P, role, idx, sb, ph, n, c);
-    float* sbase = stages + (int64_t)st * kStageFloats;
+    float* sbase = stages + (int64_t)st * stage_floats(P.r8);
     const uint32_t bar = ptx::smem_u32(&cl.full[st]);
     const uint32_t wbytes = (uint32_t)k.NS * kChunk * 4;
-    ptx::mbar_arm(bar, (FAST ? 1 : 2) * kActChunk * 4 + wbytes);
-    bulk_g2s(ptx::smem_u32(sbase), k.ah, kActChunk * 4, bar);
-    if (!FAST) bulk_g2s(ptx::smem_u32(sbase + kActChunk), k.al, kActChunk * 4, bar);
-    bulk_g2s(ptx::smem_u32(sbase + 2 * kActChunk), k.w, wbytes, bar);
+    const uint32_t abytes = (uint32_t)P.r8 * kChunk * 4;  // the block's rows only
+    ptx::mbar_arm(bar, (FAST ? 1 : 2) * abytes + wbytes);
+    bulk_g2s(ptx::smem_u32(sbase), k.ah, abytes, bar);
+    if (!FAST) bulk_g2s(ptx::smem_u32(sbase + P.r8 * kChunk), k.al, abytes, bar);
+    bulk_g2s(ptx::smem_u32(sbase + 2 * P.r8 * kChunk), k.w, wbytes, bar);
   }
   if (ph == 3) btrace(P, n, 12);
   return true;
@@ -262,21 +272,21 @@ template <bool FAST>
 __device__ __forceinline__ bool issue(const BParams& P, Ctl& cl, float* stages, int role, int idx, int sb, int ph,
                                       int64_t n, int nch, uint32_t cseq) {
   for (int c = 0; c < nch; ++c) {
-    const uint32_t g = cseq + c, st = g % kStages, use = g / kStages;
+    const uint32_t g = cseq + c, st = g % P.nst, use = g / P.nst;
     if (!mwait(P, cl, &cl.full[st], use & 1, 43)) return false;
     if (c == 0 && ph == 3) btrace(P, n, 13);
     ptx::tmem_fence_after();
     const Chunk k = job_chunk(P, role, idx, sb, ph, n, c);
-    const uint32_t a_hi = ptx::smem_u32(stages + (int64_t)st * kStageFloats);
-    const uint32_t a_lo = a_hi + kActChunk * 4;
-    const uint32_t wb = a_hi + 2 * kActChunk * 4;
+    const uint32_t a_hi = ptx::smem_u32(stages + (int64_t)st * stage_floats(P.r8));
+    const uint32_t a_lo = a_hi + P.r8 * kChunk * 4;
+    const uint32_t wb = a_hi + 2 * P.r8 * kChunk * 4;
     const uint32_t id2 = idesc_tf32(k.NS), id1 = idesc_tf32(k.N);
     const uint32_t d = cl.tmem + k.dcol;
 #pragma unroll
     for (int ks = 0; ks < kChunk / 8; ++ks) {
       // D[:, 0:NS) += A_hi . [W_hi; (0); W_lo]^T ; D[:, 0:N) += A_lo . W_hi^T (reading R23)
-      const uint32_t ao = ks * 2 * 128 * 16, bo = ks * 2 * k.NS * 16;
-      const uint64_t dah = sdesc(a_hi + ao, 128 * 16, 128), dal = sdesc(a_lo + ao, 128 * 16, 128);
+      const uint32_t ao = ks * 2 * P.r8 * 16, bo = ks * 2 * k.NS * 16;
+      const uint64_t dah = sdesc(a_hi + ao, P.r8 * 16, 128), dal = sdesc(a_lo + ao, P.r8 * 16, 128);
       const uint64_t db = sdesc(wb + bo, k.NS * 16, 128);
       if constexpr (FAST) {  // DVW_PRECISION_TF32: D[:, 0:N) += A_hi . W_hi^T only
         mma_tf32(d, dah, db, id1, (k.acc || ks > 0) ? 1u : 0u);
@@ -293,10 +303,10 @@ __device__ __forceinline__ bool issue(const BParams& P, Ctl& cl, float* stages, 
 }
 
 __device__ __forceinline__ void st_act(float* base_hi, int64_t half, int c, int i, const float (&v)[4],
-                                       bool with_lo = true) {
-  // 4 consecutive channels c..c+3 (c % 4 == 0) of stream row i; the lo half is not read
+                                       bool with_lo, int r8) {
+  // 4 consecutive channels c..c+3 (c % 4 == 0) of stream row i < r8; the lo half is not read
   // in the one-pass tf32 mode
-  const int o = canon(c, i);
+  const int o = canon(c, i, r8);
   float4 hi = make_float4(v[0], v[1], v[2], v[3]);
   __stcg(reinterpret_cast<float4*>(base_hi + o), hi);
   if (with_lo) {
@@ -332,16 +342,16 @@ __device__ __forceinline__ int sample_warp_g(const RunArgs& A, const float* logi
 // into layer 0's queue slot (n+1) mod (d_0+1) (where phase 0 reads it); one warp, stream g.
 __device__ __forceinline__ void embed(const BParams& P, int g, int64_t n1, int yprev, int ycur, int lane) {
   const RunArgs& A = P.a;
-  const int r = P.r, sb = g >> 7, i = g & 127;
-  const int64_t half = (int64_t)P.nsb * r * 128;
+  const int r = P.r, sb = g / P.rpb, i = g % P.rpb;
+  const int64_t half = (int64_t)P.nsb * r * P.r8;
   const float* ep = A.w + A.off.emb_prev;
   const float* ec = A.w + A.off.emb_cur;
   const float* be = A.w + A.off.b_emb;
   const int d = P.dil[0];
-  float* q = P.ring + P.ring_off[0] + (int64_t)(n1 % (d + 1)) * 2 * half + (int64_t)sb * r * 128;
+  float* q = P.ring + P.ring_off[0] + (int64_t)(n1 % (d + 1)) * 2 * half + (int64_t)sb * r * P.r8;
   for (int c = lane; c < r; c += 32) {
     const float v = (__ldg(ep + (int64_t)c * kLevels + yprev) + __ldg(ec + (int64_t)c * kLevels + ycur)) + __ldg(be + c);
-    const int o = canon(c, i);
+    const int o = canon(c, i, P.r8);
     __stcg(q + o, v);
     __stcg(q + half + o, tf32_lo(v));
   }
@@ -375,7 +385,7 @@ __device__ __forceinline__ void prefetch(const BParams& P, int role, int idx, in
   const RunArgs& A = P.a;
   if (role != kLayer || ph >= P.L) return;
   const int t = threadIdx.x, i = t & 127, half = t >> 7;
-  const int g = sb * 128 + i, r = P.r, j = ph;
+  const int g = sb * P.rpb + i, r = P.r, j = ph;
   const int c0 = 16 * idx + 8 * half;
   const float* bias = P.pk + P.bias_off + (int64_t)j * 2 * r;
   float* bv = pre.b;
@@ -385,7 +395,7 @@ __device__ __forceinline__ void prefetch(const BParams& P, int role, int idx, in
     bv[4 * q] = a.x; bv[4 * q + 1] = a.y; bv[4 * q + 2] = a.z; bv[4 * q + 3] = a.w;
     bv[8 + 4 * q] = b.x; bv[8 + 4 * q + 1] = b.y; bv[8 + 4 * q + 2] = b.z; bv[8 + 4 * q + 3] = b.w;
   }
-  if (g < A.n_streams) {
+  if (i < P.rpb && g < A.n_streams) {
     const float* cp = A.cond + (((int64_t)g * A.n_frames + n / A.hop) * P.L + j) * 2 * r;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -399,11 +409,11 @@ __device__ __forceinline__ void prefetch(const BParams& P, int role, int idx, in
     for (int q = 0; q < 16; ++q) pre.L[q] = 0.0f;
   }
   if (j >= 1) {
-    const float* xin = x_now(P, j - 1, n) + (int64_t)sb * r * 128;
+    const float* xin = x_now(P, j - 1, n) + (int64_t)sb * r * P.r8;
     const float* bres = A.w + A.off.b_res + (int64_t)(j - 1) * A.off.layer_stride + c0;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const float4 v = ld4_early_cg(xin + canon(c0 + 4 * q, i));
+      const float4 v = ld4_early_cg(xin + canon(c0 + 4 * q, i < P.r8 ? i : 0, P.r8));
       const float4 bb = ld4_early_nc(bres + 4 * q);
       pre.x[4 * q] = v.x; pre.x[4 * q + 1] = v.y; pre.x[4 * q + 2] = v.z; pre.x[4 * q + 3] = v.w;
       pre.br[4 * q] = bb.x; pre.br[4 * q + 1] = bb.y; pre.br[4 * q + 2] = bb.z; pre.br[4 * q + 3] = bb.w;
@@ -416,8 +426,9 @@ template <bool FAST>
 __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, int ph, int64_t n, const Pre& pre) {
   const RunArgs& A = P.a;
   const int t = threadIdx.x, w = t >> 5, i = t & 127, half = t >> 7;
-  const int g = sb * 128 + i;
-  const bool live = g < A.n_streams;
+  const int g = sb * P.rpb + i;
+  const bool live = i < P.rpb && g < A.n_streams;
+  const bool row = i < P.r8;  // a row of the block's image (padding rows past rpb are stored too)
   const uint32_t lane_base = cl.tmem + ((uint32_t)(32 * (w & 3)) << 16);
   const int r = P.r;
   if (t == 0 && ph == 3) btrace(P, n, 19);
@@ -443,8 +454,8 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
       for (int q = 0; q < 8; ++q) Et[q] = Es[q] = Ex[q] = 0.0f;
     }
     if (t == 0 && ph == 3) btrace(P, n, 16);
-    const int64_t half_f = (int64_t)P.nsb * r * 128;
-    float* hdst = P.hb[j & 1] + (int64_t)sb * r * 128;
+    const int64_t half_f = (int64_t)P.nsb * r * P.r8;
+    float* hdst = P.hb[j & 1] + (int64_t)sb * r * P.r8;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       float hv[4];
@@ -453,18 +464,18 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
         const int c = 4 * q + e;
         hv[e] = gate_fast(((Dt[c] + Et[c]) + pre.b[c]) + pre.L[c], ((Ds[c] + Es[c]) + pre.b[8 + c]) + pre.L[8 + c]);
       }
-      st_act(hdst, half_f, c0 + 4 * q, i, hv, !FAST);
+      if (row) st_act(hdst, half_f, c0 + 4 * q, i, hv, !FAST, P.r8);
     }
     if (t == 0 && ph == 3) btrace(P, n, 17);
     if (j >= 1) {
       const int d = P.dil[j];
-      float* qd = P.ring + P.ring_off[j] + (int64_t)(n % (d + 1)) * 2 * half_f + (int64_t)sb * r * 128;
+      float* qd = P.ring + P.ring_off[j] + (int64_t)(n % (d + 1)) * 2 * half_f + (int64_t)sb * r * P.r8;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         float xv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) xv[e] = pre.x[4 * q + e] + ((Dx[4 * q + e] + Ex[4 * q + e]) + pre.br[4 * q + e]);
-        st_act(qd, half_f, c0 + 4 * q, i, xv, !FAST);
+        if (row) st_act(qd, half_f, c0 + 4 * q, i, xv, !FAST, P.r8);
       }
     }
   } else {
@@ -486,25 +497,25 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
     const int c0 = kTileRows * idx + 32 * half;
     if (role == kSkipT) {  // z_s = relu(q + B_skip)
       const float* bsk = A.w + A.off.b_skip + c0;
-      const int64_t half_f = (int64_t)P.nsb * P.s * 128;
-      float* dst = P.zs + (int64_t)sb * P.s * 128;
+      const int64_t half_f = (int64_t)P.nsb * P.s * P.r8;
+      float* dst = P.zs + (int64_t)sb * P.s * P.r8;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = fmaxf(D[4 * q + e] + __ldg(bsk + 4 * q + e), 0.0f);
-        st_act(dst, half_f, c0 + 4 * q, i, v, !FAST);
+        if (row) st_act(dst, half_f, c0 + 4 * q, i, v, !FAST, P.r8);
       }
     } else if (ph == P.L + 1) {  // z_a = relu(W_relu z_s + B_relu)
       const float* bb = A.w + A.off.b_relu + c0;
-      const int64_t half_f = (int64_t)P.nsb * kLevels * 128;
-      float* dst = P.za + (int64_t)sb * kLevels * 128;
+      const int64_t half_f = (int64_t)P.nsb * kLevels * P.r8;
+      float* dst = P.za + (int64_t)sb * kLevels * P.r8;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) v[e] = fmaxf(D[4 * q + e] + __ldg(bb + 4 * q + e), 0.0f);
-        st_act(dst, half_f, c0 + 4 * q, i, v, !FAST);
+        if (row) st_act(dst, half_f, c0 + 4 * q, i, v, !FAST, P.r8);
       }
     } else {  // logits = W_out z_a + B_out
       const float* bb = A.w + A.off.b_out + c0;
@@ -514,7 +525,7 @@ __device__ void epilogue(const BParams& P, Ctl& cl, int role, int idx, int sb, i
       for (int q = 0; q < 8; ++q) {
         float4 v = make_float4(D[4 * q] + __ldg(bb + 4 * q), D[4 * q + 1] + __ldg(bb + 4 * q + 1),
                                D[4 * q + 2] + __ldg(bb + 4 * q + 2), D[4 * q + 3] + __ldg(bb + 4 * q + 3));
-        __stcg(reinterpret_cast<float4*>(lg) + q, v);
+        if (i < P.rpb) __stcg(reinterpret_cast<float4*>(lg) + q, v);
         if (ol) reinterpret_cast<float4*>(ol)[q] = v;
       }
     }
@@ -525,7 +536,8 @@ template <bool FAST>
 __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Ctl& cl = *reinterpret_cast<Ctl*>(smem_raw);
-  float* stages = reinterpret_cast<float*>(smem_raw + 128);
+  static_assert(sizeof(Ctl) <= kCtlBytes, "Ctl");
+  float* stages = reinterpret_cast<float*>(smem_raw + kCtlBytes);
   const RunArgs& A = P.a;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int b = blockIdx.x;
@@ -538,7 +550,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
   if (w == 0) ptx::tmem_alloc(ptx::smem_u32(&cl.tmem), kTmemCols);
   if (t == 0) {
     cl.abort = 0;
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       ptx::mbar_init(ptx::smem_u32(&cl.full[s]), 1);
       ptx::mbar_init(ptx::smem_u32(&cl.freeb[s]), 1);
     }
@@ -553,12 +565,12 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
   // the warps of this cluster serve the streams of its stream block (sampler, embedding)
   const int nwarps = P.per_sb * (kBT / 32);
   const int gw = k * (kBT / 32) + w;
-  const int g_end = min(A.n_streams, (sb + 1) * 128);
+  const int g_end = min(A.n_streams, (sb + 1) * P.rpb);
 
   // x^(0)_0 from y_{-1} = y_{-2} = 128 (R4).  A streaming session (n0 > 0) continues from
   // the queues, x^(0)_{n0} and the code history its previous call left in the workspace.
   if (A.n0 == 0) {
-    for (int g = sb * 128 + gw; g < g_end; g += nwarps) {
+    for (int g = sb * P.rpb + gw; g < g_end; g += nwarps) {
       embed(P, g, 0, kLevels / 2, kLevels / 2, lane);
       if (lane == 0) {
         P.yh[2 * g] = kLevels / 2;
@@ -605,7 +617,7 @@ __global__ void __launch_bounds__(kBT, 1) k_batch(const __grid_constant__ BParam
         }
       } else if (ok) {
         // sample y_n and embed x^(0)_{n+1}; one warp per stream
-        for (int g = sb * 128 + gw; g < g_end; g += nwarps) {
+        for (int g = sb * P.rpb + gw; g < g_end; g += nwarps) {
           const int y1 = __ldcg(P.yh + 2 * g);
           int y;
           if (A.forced) {
@@ -677,7 +689,7 @@ BatchPlan plan_batch(int L, int r, int s, int device) {
   p.bias_off = off;
   off += (int64_t)L * 2 * r;
   p.total = off;
-  p.smem_bytes = 128 + kStages * kStageFloats * 4;
+  p.smem_bytes = kSmemBytes;
   // stream blocks per launch = clusters that are co-resident (one wave)
   int prev = -1;
   cudaGetDevice(&prev);
@@ -809,7 +821,7 @@ struct WsLayout {
   int64_t hb[2], zs, za, logits, ring, yh, abort, total;  // byte offsets
   int64_t ring_off[kBMaxLayers];                                 // floats from ring
 };
-WsLayout ws_layout(const BatchPlan& p, const int32_t* dil, int nsb) {
+WsLayout ws_layout(const BatchPlan& p, const int32_t* dil, int nsb, int rpb) {
   WsLayout l{};
   int64_t off = 0;
   auto take = [&](int64_t bytes) {
@@ -817,18 +829,19 @@ WsLayout ws_layout(const BatchPlan& p, const int32_t* dil, int nsb) {
     off += (bytes + 255) & ~int64_t(255);
     return o;
   };
-  const int64_t act = (int64_t)2 * nsb * p.r * 128 * 4;
+  const int r8 = (rpb + 7) & ~7;
+  const int64_t act = (int64_t)2 * nsb * p.r * r8 * 4;
   l.hb[0] = take(act);
   l.hb[1] = take(act);
-  l.zs = take((int64_t)2 * nsb * p.s * 128 * 4);
-  l.za = take((int64_t)2 * nsb * kLevels * 128 * 4);
-  l.logits = take((int64_t)nsb * 128 * kLevels * 4);
-  l.yh = take((int64_t)nsb * 128 * 2 * 4);
+  l.zs = take((int64_t)2 * nsb * p.s * r8 * 4);
+  l.za = take((int64_t)2 * nsb * kLevels * r8 * 4);
+  l.logits = take((int64_t)nsb * rpb * kLevels * 4);
+  l.yh = take((int64_t)nsb * rpb * 2 * 4);
   l.abort = take((int64_t)nsb * 4);
   int64_t rf = 0;
   for (int j = 0; j < p.L; ++j) {
     l.ring_off[j] = rf;
-    rf += (int64_t)(dil[j] + 1) * 2 * nsb * p.r * 128;
+    rf += (int64_t)(dil[j] + 1) * 2 * nsb * p.r * r8;
   }
   l.ring = take(rf * 4);
   l.total = off;
@@ -836,17 +849,34 @@ WsLayout ws_layout(const BatchPlan& p, const int32_t* dil, int nsb) {
 }
 }  // namespace
 
-size_t batch_workspace_bytes(const BatchPlan& p, const int32_t* dil, int nsb) {
-  return (size_t)ws_layout(p, dil, nsb).total;
+// Launch groups of a batch (the same for every call with this n_streams, so a session's per-group
+// workspace stays valid): as few groups as co-resident clusters allow, the streams spread evenly
+// over up to max_sb stream blocks per group (fewer rows per block, more clusters busy).
+BatchGrouping batch_grouping(const BatchPlan& p, int n_streams) {
+  BatchGrouping g;
+  const int cap = p.max_sb * 128;
+  g.groups = (n_streams + cap - 1) / cap;
+  g.per_group = (n_streams + g.groups - 1) / g.groups;
+  g.nsb = std::min(p.max_sb, g.per_group);
+  g.rpb = (g.per_group + g.nsb - 1) / g.nsb;
+  // A/B switch: DVW_BATCH_BALANCE=0 packs full 128-stream blocks (round 1)
+  if (const char* e = std::getenv("DVW_BATCH_BALANCE"))
+    if (std::atoi(e) == 0) {
+      g.per_group = std::min(cap, n_streams);
+      g.rpb = 128;
+    }
+  g.nsb = (g.per_group + g.rpb - 1) / g.rpb;
+  return g;
+}
+
+size_t batch_workspace_bytes(const BatchPlan& p, const int32_t* dil, int n_streams) {
+  const BatchGrouping g = batch_grouping(p, n_streams);
+  return (size_t)ws_layout(p, dil, g.nsb, g.rpb).total;
 }
 
 size_t batch_session_bytes(const BatchPlan& p, const int32_t* dil, int n_streams) {
-  size_t total = 0;
-  for (int g0 = 0; g0 < n_streams; g0 += p.max_sb * 128) {
-    const int ns = std::min(p.max_sb * 128, n_streams - g0);
-    total += (size_t)ws_layout(p, dil, (ns + 127) / 128).total;
-  }
-  return total;
+  const BatchGrouping g = batch_grouping(p, n_streams);
+  return (size_t)g.groups * (size_t)ws_layout(p, dil, g.nsb, g.rpb).total;
 }
 
 cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void* packed, void* ws, size_t ws_bytes,
@@ -854,14 +884,14 @@ cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void
                                 bool session) {
   if (!p.ok) return cudaErrorNotSupported;
   // (plan_batch set the kernel's shared-memory and cluster-size attributes)
-  const int per_launch = p.max_sb * 128;
+  const BatchGrouping gr = batch_grouping(p, a.n_streams);
+  const WsLayout l = ws_layout(p, dil_host, gr.nsb, gr.rpb);
   int64_t launches = 0;
   int grid = 0;
   size_t wsoff = 0;  // a session keeps every launch group's workspace (queues, x^(0), codes)
-  for (int g0 = 0; g0 < a.n_streams; g0 += per_launch) {
-    const int ns = std::min(per_launch, a.n_streams - g0);
-    const int nsb = (ns + 127) / 128;
-    const WsLayout l = ws_layout(p, dil_host, nsb);
+  for (int g0 = 0; g0 < a.n_streams; g0 += gr.per_group) {
+    const int ns = std::min(gr.per_group, a.n_streams - g0);
+    const int nsb = (ns + gr.rpb - 1) / gr.rpb;
     if (wsoff + (size_t)l.total > ws_bytes) return cudaErrorInvalidValue;
     char* gws = static_cast<char*>(ws) + wsoff;
     if (session) wsoff += (size_t)l.total;
@@ -879,7 +909,16 @@ cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void
     P.pk = static_cast<const float*>(packed);
     P.L = p.L; P.r = p.r; P.s = p.s;
     P.TA = p.TA; P.TQ = p.TQ; P.TH = p.TH; P.per_sb = p.per_sb;
-    P.nsb = nsb;
+    P.nsb = gr.nsb;  // image layout (the workspace holds gr.nsb blocks; this group runs nsb of them)
+    P.rpb = gr.rpb;
+    P.r8 = (gr.rpb + 7) & ~7;
+    P.nst = std::min(kMaxStages, (p.smem_bytes - kCtlBytes) / (stage_floats(P.r8) * 4));
+    // a deeper ring measured slower (C4 at 37 streams per block, 7 stages: 1.14 M vs 1.26 M samples/s):
+    // 4 stages unless DVW_BATCH_STAGES says otherwise (A/B)
+    {
+      const char* e = std::getenv("DVW_BATCH_STAGES");
+      P.nst = std::min(P.nst, e ? std::max(2, std::atoi(e)) : 4);
+    }
 
     P.la_off = p.la_off; P.la_floats = p.la_floats;
     P.q_off = p.q_off; P.q_floats = p.q_floats;
@@ -921,6 +960,7 @@ cudaError_t launch_batch_kernel(const RunArgs& a, const BatchPlan& p, const void
   info->cluster = p.per_sb;
   info->threads = kBT;
   info->launches = launches;
+  info->rows_per_block = gr.rpb;
   return cudaSuccess;
 }
 

@@ -39,13 +39,20 @@ struct BatchPlan {
   int smem_bytes = 0;
 };
 
+// How a batch of n_streams is laid out: `groups` launches of up to per_group streams, each over
+// nsb stream blocks (clusters) of rpb <= 128 streams.
+struct BatchGrouping {
+  int groups = 0, per_group = 0, nsb = 0, rpb = 0;
+};
+
 BatchPlan plan_batch(int L, int r, int s, int device);
+BatchGrouping batch_grouping(const BatchPlan& p, int n_streams);
 cudaError_t pack_batch_weights(const BatchPlan& p, const float* host_blob, const Offsets& o, void* packed);
-// Workspace for `nsb` stream blocks with dilations `dil` (host array, length L).
-size_t batch_workspace_bytes(const BatchPlan& p, const int32_t* dil, int nsb);
+// Workspace of one launch group of an n_streams call with dilations `dil` (host array, length L).
+size_t batch_workspace_bytes(const BatchPlan& p, const int32_t* dil, int n_streams);
 // Workspace a streaming session keeps for n_streams: one region per launch group.
 size_t batch_session_bytes(const BatchPlan& p, const int32_t* dil, int n_streams);
-// Runs n_streams (any count; groups of max_sb * 128 run back to back on `st`).
+// Runs n_streams (any count; the launch groups of batch_grouping run back to back on `st`).
 // fast: one tf32 pass (DVW_PRECISION_TF32) instead of the fp32-faithful split.
 // session: `ws` holds every group's region (batch_session_bytes), zeroed only when a.n0 == 0,
 // and the kernel continues from the queues and code history left there (global index a.n0 + n);
