@@ -378,7 +378,17 @@ __device__ __forceinline__ int sample_warp(const float* logits, float u, int lan
   const float mx = __uint_as_float((kmx & 0x80000000u) ? (kmx & 0x7fffffffu) : ~kmx);
   float e[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) e[i] = NL == 2 ? appc_exp(l[i] - mx) : expf(l[i] - mx);  // App. C.2 (R31)
+  for (int i = 0; i < 8; ++i) {
+    if constexpr (NL == 2) {
+      e[i] = appc_exp(l[i] - mx);  // App. C.2 (R31)
+    } else if constexpr ((DVW_EXP & 8) != 0) {  // A/B: exp as one MUFU ex2 of (l - m) log2(e)
+      float r;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((l[i] - mx) * 1.4426950408889634f));
+      e[i] = r;
+    } else {
+      e[i] = expf(l[i] - mx);
+    }
+  }
   // fp32 pass
   float q[8];
   q[0] = e[0];

@@ -815,3 +815,23 @@ def test_watchdog_fires_on_dropped_handoff_and_handle_recovers(L, monkeypatch):
     ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond, hop, N, uniforms=u,
                            dilations=cfg.dilation_list(), want_logits=False)
     assert np.array_equal(codes.cpu().numpy()[0], ref)
+
+
+@pytest.mark.parametrize("S", [129, 300])
+def test_tc_balanced_blocks_position_independent(L, S):
+    """The batched kernel spreads a launch group's streams evenly over the co-resident clusters
+    (rows per block = ceil(S / blocks), not 128): a stream's codes do not depend on how many
+    streams share its block or where it sits, and equal the oracle's."""
+    cfg = synth.Config(3, 64, 128)
+    N, hop = 96, 8
+    w = synth.make_weights(cfg, 0)
+    utts = list(range(S))
+    cond, u = synth.make_batch(cfg, N, utts, hop)
+    m = model(L, cfg, w, "tc")
+    many = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    for st in (0, S // 2, S - 1):
+        one = m.generate(dev(cond[st:st + 1]), dev(u[st:st + 1]), hop).cpu().numpy()[0]
+        assert np.array_equal(many[st], one), st
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[st], hop, N, uniforms=u[st],
+                               dilations=cfg.dilation_list(), want_logits=False)
+        assert np.array_equal(many[st], ref), st
