@@ -61,6 +61,9 @@ constexpr int kMain = 256;  // head / skip math threads: warpgroups A and B, [12
 constexpr int kMath = 384;  // warpgroups A, B, C: [128,512)
 constexpr int kThreads = kAux + kMath;
 constexpr int kTmemCols = 512;
+// Multi-stream variant (PIPE): up to kWP streams per cluster, their samples interleaved item by item
+// (item i = stream i % wc, sample i / wc), so up to wc samples are in flight along the chain at once.
+constexpr int kWP = 8;
 constexpr uint64_t kTimeoutNs = 2000000000ull;
 
 // named barriers (0 is __syncthreads).  A producer that only arrives gets one id per use
@@ -113,12 +116,21 @@ struct __align__(16) Mail {
   double dscr[8];
   float fscr[8];
   int iscr[16];
+  // multi-stream variant (PIPE): one mailbox barrier per stream of the cluster (the data live in the
+  // mailbox region after Mail, see mb_*), and CTA 0's code history per stream
+  uint64_t pb_hin[kWP], pb_xin[kWP], pb_logits[kWP], pb_part[kWP], pb_za[kWP];
+  uint64_t pb_h[kCMaxSlot][kWP];
+  int ys[kWP][2];
+  // PIPE: X's pre terms double-buffered by item parity, one barrier per parity (X runs an item ahead)
+  uint64_t bar_pre2[2];
+  float pre2[2][LPC][2 * R];
 };
 
 struct Params {
   RunArgs a;
   ClusterPlan p;
   const float* pk;
+  int wmax;  // streams per cluster (1, or up to kWP for the multi-stream variant)
 };
 
 struct Ctx {
@@ -132,19 +144,99 @@ struct Ctx {
   // that phase (an mbarrier fault).  The roles still run every sample, so named barriers between
   // warpgroups stay matched.
   mutable bool dead;
+  float* mb;  // PIPE: this CTA's mailbox region (per-stream inbound data; same offset in every CTA)
+  int wc;     // streams this cluster generates (1 unless PIPE)
 };
 
+// Coordinates of item `it` of a cluster's interleaved sequence: stream s (the mailbox slot), sample
+// n of that stream (mailbox barriers flip phase once per sample of their stream: parity n & 1),
+// and p = it & 1, the parity of the CTA-local double buffers (xs, hs, pre; one item after another).
+struct Item {
+  int64_t n;
+  int s, p;
+  uint32_t par;
+};
+template <bool PIPE>
+__device__ __forceinline__ Item item_of(int64_t it, int wc) {
+  Item x;
+  if constexpr (PIPE) {
+    x.s = (int)(it % wc);
+    x.n = it / wc;
+  } else {
+    x.s = 0;
+    x.n = it;
+  }
+  x.p = (int)(it & 1);
+  x.par = (uint32_t)(x.n & 1);
+  return x;
+}
+
+// Inbound mailboxes: single buffers in Mail (one stream), or per-stream slots in the mailbox region.
+// Region layout (floats): chain: hin [kWP][kHLen], xin [kWP][kHLen], logits [kWP][256];
+// head: hbuf slots 0-1 [2][kWP][kHLen], za [kWP][kVLen], part [npart][kWP][256]; skip: hbuf [slots][kWP][kHLen].
+template <bool PIPE>
+__device__ __forceinline__ float* mb_hin(const Ctx& cx, int s) {
+  if constexpr (PIPE) return cx.mb + s * kHLen; else return cx.mail->hin;
+}
+template <bool PIPE>
+__device__ __forceinline__ float* mb_xin(const Ctx& cx, int s) {
+  if constexpr (PIPE) return cx.mb + (kWP + s) * kHLen; else return cx.mail->xin;
+}
+template <bool PIPE>
+__device__ __forceinline__ float* mb_logits(const Ctx& cx, int s) {
+  if constexpr (PIPE) return cx.mb + 2 * kWP * kHLen + s * kLevels; else return cx.mail->logits_in;
+}
+template <bool PIPE>
+__device__ __forceinline__ float* mb_hbuf(const Ctx& cx, int sl, int s) {
+  if constexpr (PIPE) return cx.mb + (sl * kWP + s) * kHLen; else return cx.mail->hbuf[sl];
+}
+template <bool PIPE>
+__device__ __forceinline__ float* mb_za(const Ctx& cx, int s) {
+  if constexpr (PIPE) return cx.mb + 2 * kWP * kHLen + s * kVLen; else return cx.mail->za_in;
+}
+template <bool PIPE>
+__device__ __forceinline__ float* mb_part(const Ctx& cx, int kk, int s) {
+  if constexpr (PIPE) return cx.mb + 2 * kWP * kHLen + kWP * kVLen + (kk * kWP + s) * 256; else return cx.mail->part[kk];
+}
+template <bool PIPE>
+__device__ __forceinline__ uint64_t* b_hin(const Ctx& cx, int s) {
+  if constexpr (PIPE) return &cx.mail->pb_hin[s]; else return &cx.mail->bar_hin;
+}
+template <bool PIPE>
+__device__ __forceinline__ uint64_t* b_xin(const Ctx& cx, int s) {
+  if constexpr (PIPE) return &cx.mail->pb_xin[s]; else return &cx.mail->bar_xin;
+}
+template <bool PIPE>
+__device__ __forceinline__ uint64_t* b_logits(const Ctx& cx, int s) {
+  if constexpr (PIPE) return &cx.mail->pb_logits[s]; else return &cx.mail->bar_logits;
+}
+template <bool PIPE>
+__device__ __forceinline__ uint64_t* b_part(const Ctx& cx, int s) {
+  if constexpr (PIPE) return &cx.mail->pb_part[s]; else return &cx.mail->bar_part;
+}
+template <bool PIPE>
+__device__ __forceinline__ uint64_t* b_za(const Ctx& cx, int s) {
+  if constexpr (PIPE) return &cx.mail->pb_za[s]; else return &cx.mail->bar_za;
+}
+template <bool PIPE>
+__device__ __forceinline__ uint64_t* b_h(const Ctx& cx, int sl, int s) {
+  if constexpr (PIPE) return &cx.mail->pb_h[sl][s]; else return &cx.mail->bar_h[sl];
+}
+
 // This cluster's stream inside the [S][...] caller buffers.
-__device__ __forceinline__ const float* s_uniforms(const RunArgs& A, const Ctx& cx) {
-  return A.uniforms ? A.uniforms + cx.sidx * A.N : nullptr;
+// (s: the stream within a multi-stream cluster)
+__device__ __forceinline__ const float* s_uniforms(const RunArgs& A, const Ctx& cx, int s = 0) {
+  return A.uniforms ? A.uniforms + (cx.sidx + s) * A.N : nullptr;
 }
-__device__ __forceinline__ const uint8_t* s_forced(const RunArgs& A, const Ctx& cx) {
-  return A.forced ? A.forced + cx.sidx * A.N : nullptr;
+__device__ __forceinline__ const uint8_t* s_forced(const RunArgs& A, const Ctx& cx, int s = 0) {
+  return A.forced ? A.forced + (cx.sidx + s) * A.N : nullptr;
 }
-__device__ __forceinline__ float* s_logits(const RunArgs& A, const Ctx& cx) {
-  return A.out_logits + cx.sidx * A.N * kLevels;
+__device__ __forceinline__ float* s_logits(const RunArgs& A, const Ctx& cx, int s = 0) {
+  return A.out_logits + (cx.sidx + s) * A.N * kLevels;
 }
-__device__ __forceinline__ uint8_t* s_codes(const RunArgs& A, const Ctx& cx) { return A.out_codes + cx.sidx * A.N; }
+__device__ __forceinline__ uint8_t* s_codes(const RunArgs& A, const Ctx& cx, int s = 0) {
+  return A.out_codes + (cx.sidx + s) * A.N;
+}
 __device__ __forceinline__ int* s_ystate(const RunArgs& A, const Ctx& cx) { return A.ystate + 2 * cx.sidx; }
 
 __device__ __forceinline__ void bar_arrive(int id, int n) {
@@ -419,37 +511,44 @@ __device__ __forceinline__ int sample_warp(const float* logits, float u, int lan
 
 // Draw y_{n-1} from the inbound logits (App. A.4) and write x^(0)_n (step 1) into xs[n&1][0]
 // with the first warp of warpgroup A; warpgroups A, B, C wait at the closing barrier.
-template <bool TRACE, int NL = 0>
-__device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx, int64_t n, int k, int& y1,
+template <bool TRACE, int NL = 0, bool PIPE = false>
+__device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx, const Item& I, int k, int& y1,
                                                  int& y2, const float* wembc, const float* bemb) {
   const RunArgs& A = P.a;
   Mail& m = *cx.mail;
+  const int64_t n = I.n;
   if (k < 32) {
+    if constexpr (PIPE) {  // this stream's code history
+      y1 = m.ys[I.s][0];
+      y2 = m.ys[I.s][1];
+    }
     const float* embp_g = P.pk + P.p.embp_off;  // W_emb_prev^T [256][R] in global memory
     float ep0, ep1;
     if (n > 0) {
-      const float* ub = s_uniforms(A, cx);
-      const uint8_t* fb = s_forced(A, cx);
+      const float* ub = s_uniforms(A, cx, I.s);
+      const uint8_t* fb = s_forced(A, cx, I.s);
       const float u = ub ? __ldg(ub + n - 1) : 0.0f;
       const int yf = fb ? (int)__ldg(fb + n - 1) : 0;
       ep0 = __ldg(embp_g + y1 * R + k);  // W_emb_prev[:, y_{n-2}] (= y1 before the update)
       ep1 = __ldg(embp_g + y1 * R + k + 32);
       uint64_t* tp = (k == 0) ? trace_slot<TRACE>(A, n) : nullptr;
-      if (wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11) && k == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_logits), kLevels * 4);
+      const float* lin = mb_logits<PIPE>(cx, I.s);
+      if (wait(cx, b_logits<PIPE>(cx, I.s), (uint32_t)((n - 1) & 1), 11) && k == 0 && !cx.dead)
+        ptx::mbar_arm(ptx::smem_u32(b_logits<PIPE>(cx, I.s)), kLevels * 4);
       stamp<TRACE>(tp, 1);
       if (k == 0) trace<TRACE>(A, n - 1, 3);
       int y;
       if (fb) {
-        float4* o = reinterpret_cast<float4*>(s_logits(A, cx) + (n - 1) * kLevels) + 2 * k;
-        o[0] = lds4(m.logits_in + 8 * k);
-        o[1] = lds4(m.logits_in + 8 * k + 4);
+        float4* o = reinterpret_cast<float4*>(s_logits(A, cx, I.s) + (n - 1) * kLevels) + 2 * k;
+        o[0] = lds4(lin + 8 * k);
+        o[1] = lds4(lin + 8 * k + 4);
         y = yf;
       } else {
         stamp<TRACE>(tp, 4);
-        if constexpr ((DVW_DIAG & 16) != 0) y = min((int)(u * 256.0f) + (m.logits_in[0] > 1e30f), 255);
-        else y = sample_warp<NL>(m.logits_in, u, k);
+        if constexpr ((DVW_DIAG & 16) != 0) y = min((int)(u * 256.0f) + (lin[0] > 1e30f), 255);
+        else y = sample_warp<NL>(lin, u, k);
         stamp<TRACE>(tp, 6);
-        if (k == 0) s_codes(A, cx)[n - 1] = (uint8_t)y;
+        if (k == 0) s_codes(A, cx, I.s)[n - 1] = (uint8_t)y;
       }
       if (k == 0) trace<TRACE>(A, n, 20);
       y2 = y1;
@@ -458,8 +557,15 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
       ep0 = __ldg(embp_g + y2 * R + k);
       ep1 = __ldg(embp_g + y2 * R + k + 32);
     }
+    if constexpr (PIPE) {
+      __syncwarp();
+      if (k == 0) {
+        m.ys[I.s][0] = y1;
+        m.ys[I.s][1] = y2;
+      }
+    }
     // x^(0)_n = W_emb_prev[:, y_{n-2}] + W_emb_cur[:, y_{n-1}] + B_emb
-    float* x0 = m.xs[n & 1][0];
+    float* x0 = m.xs[I.p][0];
     x0[pad16(k)] = (ep0 + wembc[y1 * R + k]) + bemb[k];
     x0[pad16(k + 32)] = (ep1 + wembc[y1 * R + k + 32]) + bemb[k + 32];
     if (k == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 7);
@@ -469,23 +575,23 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
 }
 
 // The final draw (sample N-1) after the last layer pass (first warp of A); returns it.
-template <int NL = 0>
-__device__ __forceinline__ int final_draw(const Params& P, const Ctx& cx, int k) {
+template <int NL = 0, bool PIPE = false>
+__device__ __forceinline__ int final_draw(const Params& P, const Ctx& cx, int k, int s = 0) {
   const RunArgs& A = P.a;
-  Mail& m = *cx.mail;
   if (k >= 32) return 0;
   const int64_t n = A.N;
-  const float* ub = s_uniforms(A, cx);
+  const float* ub = s_uniforms(A, cx, s);
   const float u = ub ? __ldg(ub + n - 1) : 0.0f;
-  wait(cx, &m.bar_logits, (uint32_t)((n - 1) & 1), 11);
+  const float* lin = mb_logits<PIPE>(cx, s);
+  wait(cx, b_logits<PIPE>(cx, s), (uint32_t)((n - 1) & 1), 11);
   int y = 0;
   if (A.forced) {
-    float4* o = reinterpret_cast<float4*>(s_logits(A, cx) + (n - 1) * kLevels) + 2 * k;
-    o[0] = lds4(m.logits_in + 8 * k);
-    o[1] = lds4(m.logits_in + 8 * k + 4);
+    float4* o = reinterpret_cast<float4*>(s_logits(A, cx, s) + (n - 1) * kLevels) + 2 * k;
+    o[0] = lds4(lin + 8 * k);
+    o[1] = lds4(lin + 8 * k + 4);
   } else {
-    y = sample_warp<NL>(m.logits_in, u, k);
-    if (k == 0) s_codes(A, cx)[n - 1] = (uint8_t)y;
+    y = sample_warp<NL>(lin, u, k);
+    if (k == 0) s_codes(A, cx, s)[n - 1] = (uint8_t)y;
   }
   return y;
 }
@@ -525,7 +631,7 @@ constexpr int kColB3 = 384;
 // pair, where the gate runs.  B: row g of W_res, same columns.
 
 // ------------------------------------------------------------------ chain CTA, warpgroup A (the chain)
-template <int LP, bool TRACE, int NL, bool SESS>
+template <int LP, bool TRACE, int NL, bool SESS, bool PIPE>
 __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -542,29 +648,34 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
   int y1 = SESS ? s_ystate(A, cx)[0] : kLevels / 2, y2 = SESS ? s_ystate(A, cx)[1] : kLevels / 2;
   float w[64];
 
-  for (int64_t n = 0; n < A.N; ++n) {
-    const int p = (int)(n & 1);
+  for (int64_t it = 0; it < A.N * cx.wc; ++it) {
+    const Item I = item_of<PIPE>(it, cx.wc);
+    const int64_t n = I.n;
+    const int p = I.p;
+    const float* hinb = mb_hin<PIPE>(cx, I.s);
     ptx::tmem_load_async<64>(tm, w);  // layer j0's tile, hidden behind the waits
     if (c == 0) {
-      sample_and_embed<TRACE, NL>(P, cx, n, a, y1, y2, wembc, bemb);
+      sample_and_embed<TRACE, NL, PIPE>(P, cx, I, a, y1, y2, wembc, bemb);
     } else {
-      if (wait(cx, &m.bar_hin, (uint32_t)p, 12) && a == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_hin), R * 4);
+      if (wait(cx, b_hin<PIPE>(cx, I.s), I.par, 12) && a == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(b_hin<PIPE>(cx, I.s)), R * 4);
     }
     if (a == 0) trace<TRACE>(A, n, 0);
     uint64_t* tp = (a == 0) ? trace_slot<TRACE>(A, n) : nullptr;
-    wait(cx, &m.bar_pre, (uint32_t)p, 13);
+    if constexpr (PIPE) wait(cx, &m.bar_pre2[p], (uint32_t)((it >> 1) & 1), 13);
+    else wait(cx, &m.bar_pre, (uint32_t)p, 13);
+    const float* prev_pre = PIPE ? &m.pre2[p][0][0] : &m.pre[0][0];
     ptx::tmem_wait_ld<64>(w);
 #pragma unroll
     for (int jl = 0; jl < LP; ++jl) {
       if (jl < nl) {
         const bool direct = (c == 0 && jl == 0);  // a_0 = W_cur_0 x_0
         stamp<TRACE>(tp, 8 + 2 * jl);
-        const float pre0 = m.pre[jl][hrow], pre1 = m.pre[jl][R + hrow];
+        const float pre0 = prev_pre[jl * 2 * R + hrow], pre1 = prev_pre[jl * 2 * R + R + hrow];
         float v[2];
         if constexpr ((DVW_EXP & 1) != 0 || LP == 4)
-          tile_dot_half_n<2, 4>(w, (direct ? m.xs[p][0] : (jl == 0 ? m.hin : m.hs[p][jl - 1])) + voff, v);
+          tile_dot_half_n<2, 4>(w, (direct ? m.xs[p][0] : (jl == 0 ? hinb : m.hs[p][jl - 1])) + voff, v);
         else
-          tile_dot_half<2>(w, (direct ? m.xs[p][0] : (jl == 0 ? m.hin : m.hs[p][jl - 1])) + voff, v);
+          tile_dot_half<2>(w, (direct ? m.xs[p][0] : (jl == 0 ? hinb : m.hs[p][jl - 1])) + voff, v);
         if (jl + 1 < nl) ptx::tmem_load_async<64>(tm + 64 * (jl + 1), w);  // next layer's tile
         v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);  // both lanes of the pair: full (tanh, sigmoid) rows
         v[1] += __shfl_xor_sync(0xffffffffu, v[1], 1);
@@ -585,7 +696,8 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
           // four heads) -- the only hop on the critical chain between two CTAs
           // four heads: X sends one 16-byte st.async per thread (one instruction)
           if (writer) {
-            if (!last_cta) ptx::st_async(remote(&m.hin[pad16(hrow)], c + 1), hv, remote(&m.bar_hin, c + 1));
+            if (!last_cta)
+              ptx::st_async(remote(mb_hin<PIPE>(cx, I.s) + pad16(hrow), c + 1), hv, remote(b_hin<PIPE>(cx, I.s), c + 1));
             m.hs[p][jl][pad16(hrow)] = hv;
           }
           bar_arrive(kBarHX + jl, kMain);  // X forwards h_{L-1}, h_{L-2} / skip-layer h
@@ -601,10 +713,12 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
     }
   }
   if (c == 0 && A.N > 0) {
-    const int y = final_draw<NL>(P, cx, a);
-    if (SESS && a == 0 && !A.forced) {  // streaming session: the code history for the next call
-      s_ystate(A, cx)[0] = y;
-      s_ystate(A, cx)[1] = y1;
+    for (int s = 0; s < cx.wc; ++s) {
+      const int y = final_draw<NL, PIPE>(P, cx, a, s);
+      if (SESS && a == 0 && !A.forced) {  // streaming session: the code history for the next call
+        s_ystate(A, cx)[0] = y;
+        s_ystate(A, cx)[1] = y1;
+      }
     }
   }
 }
@@ -613,7 +727,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
 // x_{j0+jl} = x_{j0+jl-1} + W_res_{j0+jl-1} h_{j0+jl-1} + B_res_{j0+jl-1} for
 // jl >= xb (CTA 0 starts from the embedding): for the dilation queues, for C, and (jl = nl-1)
 // for the next chain CTA.
-template <int LP, bool TRACE, bool SESS>
+template <int LP, bool TRACE, bool SESS, bool PIPE>
 __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -634,9 +748,11 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
   int y1 = SESS ? s_ystate(A, cx)[0] : kLevels / 2, y2 = SESS ? s_ystate(A, cx)[1] : kLevels / 2;
   float wr[32];
 
-  for (int64_t n = 0; n < A.N; ++n) {
-    const int p = (int)(n & 1);
-    if (c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
+  for (int64_t it = 0; it < A.N * cx.wc; ++it) {
+    const Item I = item_of<PIPE>(it, cx.wc);
+    const int64_t n = I.n;
+    const int p = I.p;
+    if (c == 0) sample_and_embed<TRACE, 0, PIPE>(P, cx, I, k, y1, y2, wembc, bemb);
 #pragma unroll
     for (int jl = 0; jl < LP; ++jl) {
       if (jl < nl && jl >= xb) {
@@ -652,10 +768,10 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
         const float* hv;
         const float* xv;
         if (jl == 0) {  // inbound h_{j0-1}, x_{j0-1}
-          wait(cx, &m.bar_xin, (uint32_t)p, 16);
-          wait(cx, &m.bar_hin, (uint32_t)p, 17);
-          hv = m.hin;
-          xv = m.xin;
+          wait(cx, b_xin<PIPE>(cx, I.s), I.par, 16);
+          wait(cx, b_hin<PIPE>(cx, I.s), I.par, 17);
+          hv = mb_hin<PIPE>(cx, I.s);
+          xv = mb_xin<PIPE>(cx, I.s);
         } else {
           if (b == 0) stamp<TRACE>(trace_slot<TRACE>(A, n), 24 + jl - 1);  // B arrives for h_{j0+jl-1}
           ptx::bar_sync(kBarH, kMain);  // h_{j0+jl-1} from A
@@ -673,24 +789,26 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
         if (writer) {
           m.xs[p][jl][pad16(row)] = xn;
           if (jl + 1 == nl && !last_cta)
-            ptx::st_async(remote(&m.xin[pad16(row)], c + 1), xn, remote(&m.bar_xin, c + 1));
+            ptx::st_async(remote(mb_xin<PIPE>(cx, I.s) + pad16(row), c + 1), xn, remote(b_xin<PIPE>(cx, I.s), c + 1));
         }
         if (jl + 1 < nl) bar_arrive(bar_xr(jl), kMain);  // x_{j0+jl} ready: C computes R_{j0+jl+1}
       }
     }
     // the sample's x are all in xs[p]: the aux warpgroup may read them
-    if (b == 0) {
-      trace<TRACE>(A, n, 2);
+    // every warp of B arrives once its own rows of xs[p] are stored (4 arrivals complete the phase):
+    // X reads all 64 rows for the queues
+    __syncwarp();
+    if ((b & 31) == 0) {
+      if (b == 0) trace<TRACE>(A, n, 2);
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_done));
     }
   }
-  if (c == 0 && A.N > 0) final_draw(P, cx, k);
 }
 
 // ------------------------------------------------------------------ chain CTA, warpgroup C (R terms)
 // R_{j0+jl} = W_cur_{j0+jl} x_{j0+jl-1} + c_{j0+jl} for jl >= xb: jl = 0 from the inbound x_{j0-1},
 // jl >= 1 from x_{j0+jl-1} (B, or the embedding on CTA 0).
-template <int LP, bool TRACE, bool SESS>
+template <int LP, bool TRACE, bool SESS, bool PIPE>
 __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -709,17 +827,20 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
   int y1 = SESS ? s_ystate(A, cx)[0] : kLevels / 2, y2 = SESS ? s_ystate(A, cx)[1] : kLevels / 2;
   float w[64];
 
-  for (int64_t n = 0; n < A.N; ++n) {
-    const int p = (int)(n & 1);
+  for (int64_t it = 0; it < A.N * cx.wc; ++it) {
+    const Item I = item_of<PIPE>(it, cx.wc);
+    const int64_t n = I.n;
+    const int p = I.p;
     if (nl > xb) ptx::tmem_load_async<64>(tm + 64 * xb, w);
-    if (c == 0) sample_and_embed<TRACE>(P, cx, n, k, y1, y2, wembc, bemb);
+    if (c == 0) sample_and_embed<TRACE, 0, PIPE>(P, cx, I, k, y1, y2, wembc, bemb);
 #pragma unroll
     for (int jl = 0; jl < LP; ++jl) {
       if (jl < nl && jl >= xb) {
         const float* xv;
         if (jl == 0) {
-          if (wait(cx, &m.bar_xin, (uint32_t)p, 15) && ct == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_xin), R * 4);
-          xv = m.xin;
+          if (wait(cx, b_xin<PIPE>(cx, I.s), I.par, 15) && ct == 0 && !cx.dead)
+            ptx::mbar_arm(ptx::smem_u32(b_xin<PIPE>(cx, I.s)), R * 4);
+          xv = mb_xin<PIPE>(cx, I.s);
         } else {
           if (jl - 1 >= xb) ptx::bar_sync(bar_xr(jl - 1), kMain);  // x_{j0+jl-1} from B
           xv = m.xs[p][jl - 1];
@@ -743,14 +864,16 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
       }
     }
   }
-  if (c == 0 && A.N > 0) final_draw(P, cx, k);
 }
 
 // ------------------------------------------------------------------ chain CTA, warpgroup X (aux)
 // Forward h of sample n-1 as A publishes it: layers l-1 and l-2 to the heads' slots 0 and 1,
 // every other layer's to its skip CTA (16 x 16 B per
 // destination; a DSMEM store holds its warp for about one hop, hence not on A).
-__device__ __forceinline__ void aux_forward(const ClusterPlan& pl, Mail& m, int first, int nl, int at, int p) {
+template <bool PIPE>
+__device__ __forceinline__ void aux_forward(const ClusterPlan& pl, const Ctx& cx, int first, int nl, int at, int p,
+                                            int s) {
+  Mail& m = *cx.mail;
   for (int jl = 0; jl < nl; ++jl) {
     const int j = first + jl;
     ptx::bar_sync(kBarHX + jl, kMain);
@@ -758,13 +881,13 @@ __device__ __forceinline__ void aux_forward(const ClusterPlan& pl, Mail& m, int 
       const int sl = pl.L - 1 - j;
       if (at < 16 * NH) {
         const int hh = at >> 4, e = at & 15, off = 20 * (e >> 2) + 4 * (e & 3);
-        ptx::st_async4(remote(&m.hbuf[sl][off], pl.nc + hh), lds4(&m.hs[p][jl][off]),
-                       remote(&m.bar_h[sl], pl.nc + hh));
+        ptx::st_async4(remote(mb_hbuf<PIPE>(cx, sl, s) + off, pl.nc + hh), lds4(&m.hs[p][jl][off]),
+                       remote(b_h<PIPE>(cx, sl, s), pl.nc + hh));
       }
     } else if (at < 16 && pl.layer_skip_cta[j] >= 0) {
       const int off = 20 * (at >> 2) + 4 * (at & 3);
       const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
-      ptx::st_async4(remote(&m.hbuf[sl][off], kk), lds4(&m.hs[p][jl][off]), remote(&m.bar_h[sl], kk));
+      ptx::st_async4(remote(mb_hbuf<PIPE>(cx, sl, s) + off, kk), lds4(&m.hs[p][jl][off]), remote(b_h<PIPE>(cx, sl, s), kk));
     }
   }
 }
@@ -775,8 +898,8 @@ __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpre
 // sum_j W_skip_j h_j of sample n-1, W_skip streamed from L2 ([16][S][4], rows at and
 // at + 128), then sent to every head's partial slot.  Off the critical chain: these are the
 // earliest layers, at least two chain CTAs before the heads need the sum.
-template <int S>
-__device__ __forceinline__ void aux_chain_skip(const Params& P, const Ctx& cx, int c, int at, int pp) {
+template <int S, bool PIPE>
+__device__ __forceinline__ void aux_chain_skip(const Params& P, const Ctx& cx, int c, int at, int pp, int s) {
   const ClusterPlan& pl = P.p;
   Mail& m = *cx.mail;
   const int first = pl.chain_first[c], nl = pl.chain_nl[c];
@@ -811,14 +934,15 @@ __device__ __forceinline__ void aux_chain_skip(const Params& P, const Ctx& cx, i
 #pragma unroll
   for (int i = at; i < (S / 4) * NH; i += kAux) {  // S / 4 float4 per head
     const int hh = i / (S / 4), e = i % (S / 4);
-    ptx::st_async4(remote(&m.part[slot][4 * e], pl.nc + hh), lds4(&m.zs[4 * e]), remote(&m.bar_part, pl.nc + hh));
+    ptx::st_async4(remote(mb_part<PIPE>(cx, slot, s) + 4 * e, pl.nc + hh), lds4(&m.zs[4 * e]),
+                   remote(b_part<PIPE>(cx, s), pl.nc + hh));
   }
 }
 
 // For the coming sample n: queue write of x_j(n-1), queue read of x_j(n-d),
 // pre = B + L_j(n/hop) + W_prev x_j(n-d)  (Fig. 2 aux threads),
 // W_prev streamed from L2 ([16][128][4]; thread at = row of a).
-template <int S, int LP, bool TRACE, bool SESS>
+template <int S, int LP, bool TRACE, bool SESS, bool PIPE>
 __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -828,16 +952,23 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
   const float* bj = sw + sm_b(LP);  // [LPC][2R]
   const int L = A.L;
   const bool xskip = LP == 4 && first < pl.nxs;  // LP = 3 plans never have chain-skip layers
-  const float* condb = A.cond + cx.sidx * A.n_frames * L * 2 * R;  // this cluster's stream
-  float* ringb = A.ring + cx.sidx * A.ring_floats;
+  const int64_t nit = A.N * cx.wc;
 
-  for (int64_t n = 0; n < A.N; ++n) {
-    const int pp = (int)((n - 1) & 1);  // parity of sample n-1
-    if (n > 0) {
-      aux_forward(pl, m, first, nl, at, pp);
+  for (int64_t it = 0; it < nit; ++it) {
+    const Item I = item_of<PIPE>(it, cx.wc);
+    const int64_t n = I.n;
+    const int sp = PIPE ? (int)((it + cx.wc - 1) % cx.wc) : 0;  // stream of the previous item
+    const int64_t np = PIPE ? (it - 1) / cx.wc : n - 1;         // its sample
+    // this item's stream (one cluster per stream unless PIPE)
+    const float* condb = A.cond + (cx.sidx + I.s) * A.n_frames * L * 2 * R;
+    float* ringb = A.ring + (cx.sidx + I.s) * A.ring_floats;
+    float* ringp = A.ring + (cx.sidx + sp) * A.ring_floats;
+    const int pp = (int)((it - 1) & 1);  // local buffer parity of the previous item
+    if (it > 0) {
+      aux_forward<PIPE>(pl, cx, first, nl, at, pp, sp);
       wait(cx, &m.bar_done, (uint32_t)pp, 14);
       if constexpr (LP == 4)
-        if (xskip) aux_chain_skip<S>(P, cx, c, at, pp);
+        if (xskip) aux_chain_skip<S, PIPE>(P, cx, c, at, pp, sp);
     }
     const int64_t ng = SESS ? A.n0 + n : n;  // global sample index (streaming sessions continue at n0)
     const int64_t f = ng / A.hop;
@@ -861,12 +992,19 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       const float lv = __ldg(condb + (f * L + j) * 2 * R + at);
       if (at < R) {
         float* ring = ringb + A.ring_off[j];
-        const float xc = m.xs[pp][jl][pad16(at)];  // x_j(n-1) of this call (unused when n = 0)
+        const float xc = m.xs[pp][jl][pad16(at)];  // x_j of the previous item (unused at it = 0)
         float xpv = 0.0f;
-        // x_j(ng - d): slot (ng - d) mod d = ng mod d; at n = 0 of a continued session x_j(ng - 1)
-        // was flushed to the queue by the previous call
-        if (ng - d >= 0) xpv = (d == 1 && n > 0) ? xc : ring[(int64_t)(ng % d) * R + at];
-        if (n > 0 && d >= 2) ring[(int64_t)((ng - 1) % d) * R + at] = xc;
+        if constexpr (PIPE) {
+          // the previous item (another stream unless wc = 1) into its stream's queue, slot np mod d;
+          // then this stream's x_j(n - d) from slot n mod d (written wc items or more ago)
+          if (it > 0) ringp[A.ring_off[j] + (int64_t)(np % d) * R + at] = xc;
+          if (n - d >= 0) xpv = ring[(int64_t)(n % d) * R + at];
+        } else {
+          // x_j(ng - d): slot (ng - d) mod d = ng mod d; at n = 0 of a continued session x_j(ng - 1)
+          // was flushed to the queue by the previous call
+          if (ng - d >= 0) xpv = (d == 1 && n > 0) ? xc : ring[(int64_t)(ng % d) * R + at];
+          if (n > 0 && d >= 2) ring[(int64_t)((ng - 1) % d) * R + at] = xc;
+        }
         m.xp[at] = xpv;
       }
       ptx::bar_sync(kBarAux, kAux);
@@ -885,12 +1023,14 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_pre));
     }
   }
-  if (A.N > 0) {  // the last sample's h and chain-skip partial
-    const int pp = (int)((A.N - 1) & 1);
-    aux_forward(pl, m, first, nl, at, pp);
+  if (A.N > 0) {  // the last item's h and chain-skip partial
+    const int pp = (int)((nit - 1) & 1);
+    const int sl = PIPE ? cx.wc - 1 : 0;
+    float* ringb = A.ring + cx.sidx * A.ring_floats;
+    aux_forward<PIPE>(pl, cx, first, nl, at, pp, sl);
     if (xskip || SESS) wait(cx, &m.bar_done, (uint32_t)pp, 14);
     if constexpr (LP == 4) {
-      if (xskip) aux_chain_skip<S>(P, cx, c, at, pp);
+      if (xskip) aux_chain_skip<S, PIPE>(P, cx, c, at, pp, sl);
     }
     if (SESS && at < R) {  // streaming session: x_j of the last sample into its queue slot
       const int64_t ng = A.n0 + A.N - 1;
@@ -902,12 +1042,140 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
   }
 }
 
+// Multi-stream variant of the aux warpgroup.  Item i = (stream s, sample n).  X computes pre for
+// item i + 1 while A and B work on item i, retires item i (forwards its h, writes its x into its
+// stream's queues), then releases item i + 1 to A -- so A can never run two items ahead of X's
+// forwarding (the named barriers kBarHX + jl are shared by consecutive items).  Item i + 1's queue
+// entries x_j(n - d) belong to item i + 1 - wc d <= i - 1, already written (wc >= 2); a cluster
+// with one stream (a ragged last cluster) writes item i's queues before computing pre for i + 1.
+template <int S, int LP>
+__device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const float* sw) {
+  const RunArgs& A = P.a;
+  const ClusterPlan& pl = P.p;
+  Mail& m = *cx.mail;
+  const int at = threadIdx.x;  // 0..127 = row of a (2r rows)
+  const int first = pl.chain_first[c], nl = pl.chain_nl[c];
+  const float* bj = sw + sm_b(LP);  // [LPC][2R]
+  const int L = A.L;
+  const bool xskip = LP == 4 && first < pl.nxs;
+  const int64_t nit = A.N * cx.wc;
+  const bool early = cx.wc >= 2;
+
+  // pre of item `it` (stream s, sample n) into pre2[it & 1] (released separately)
+  auto make_pre = [&](int64_t it) {
+    const Item I = item_of<true>(it, cx.wc);
+    if constexpr ((DVW_DIAG & 8) != 0) {  // timing diagnostic: no queue / conditioning / W_prev work
+      for (int jl = 0; jl < nl; ++jl) m.pre2[I.p][jl][at] = 0.0f;
+      ptx::bar_sync(kBarAux, kAux);
+      return;
+    }
+    const float* condb = A.cond + (cx.sidx + I.s) * A.n_frames * L * 2 * R;
+    const float* ringb = A.ring + (cx.sidx + I.s) * A.ring_floats;
+    const int64_t f = I.n / A.hop;
+    // every layer's conditioning and queue entry in flight at once (one memory latency per item)
+    float lvs[LPC], xps[LPC];
+#pragma unroll
+    for (int jl = 0; jl < LPC; ++jl) {
+      if (jl < nl) {
+        const int j = first + jl;
+        const int d = A.dil[j];
+        lvs[jl] = __ldg(condb + (f * L + j) * 2 * R + at);
+        xps[jl] = (at < R && I.n - d >= 0) ? ringb[A.ring_off[j] + (int64_t)(I.n % d) * R + at] : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int jl = 0; jl < LPC; ++jl) {
+      if (jl >= nl) break;
+      const int j = first + jl;
+      float4 wv[16];
+      if constexpr (LP == 3) {
+        const float* wp = sw + jl * 16 * 128 * 4;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) wv[q] = lds4(wp + (q * 128 + at) * 4);
+      } else {
+        const float* wp = P.pk + pl.wprev_off + (int64_t)j * 16 * 128 * 4;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) wv[q] = ldg4(wp + (q * 128 + at) * 4);
+      }
+      const float lv = lvs[jl];
+      if (at < R) m.xp[at] = xps[jl];
+      ptx::bar_sync(kBarAux, kAux);
+      float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const float4 x = lds4(&m.xp[4 * q]);
+        a01 = ffma2(wv[q].x, wv[q].y, x.x, x.y, a01);
+        a23 = ffma2(wv[q].z, wv[q].w, x.z, x.w, a23);
+      }
+      m.pre2[I.p][jl][at] = (bj[jl * 2 * R + at] + lv) + ((a01.x + a01.y) + (a23.x + a23.y));
+      ptx::bar_sync(kBarAux, kAux);
+    }
+  };
+  auto release = [&](int64_t it) {
+    if (at == 0 && it < nit) ptx::mbar_arrive(ptx::smem_u32(&m.bar_pre2[it & 1]));
+  };
+  // item `it` published by A and finished by B: forward its h layer by layer (releasing item
+  // it + 1 right after A's last h when `early`), then its x into its stream's queues
+  auto retire = [&](int64_t it, bool rel) {
+    const Item I = item_of<true>(it, cx.wc);
+    for (int jl = 0; jl < nl; ++jl) {
+      const int j = first + jl;
+      ptx::bar_sync(kBarHX + jl, kMain);
+      // consecutive layers' hand-offs from different warps: an st.async holds its warp for about
+      // one hop, so the sends of layers jl and jl + 1 overlap instead of queueing on one warp
+      if (j >= pl.L - 2) {
+        const int sl = pl.L - 1 - j;
+        const int ht = at - 64 * (jl & 1);
+        if (ht >= 0 && ht < 16 * NH) {
+          const int hh = ht >> 4, e = ht & 15, off = 20 * (e >> 2) + 4 * (e & 3);
+          ptx::st_async4(remote(mb_hbuf<true>(cx, sl, I.s) + off, pl.nc + hh), lds4(&m.hs[I.p][jl][off]),
+                         remote(b_h<true>(cx, sl, I.s), pl.nc + hh));
+        }
+      } else if ((at >> 5) == (jl & 3) && (at & 31) < 16 && pl.layer_skip_cta[j] >= 0) {
+        const int st = at & 31, off = 20 * (st >> 2) + 4 * (st & 3);
+        const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
+        ptx::st_async4(remote(mb_hbuf<true>(cx, sl, I.s) + off, kk), lds4(&m.hs[I.p][jl][off]),
+                       remote(b_h<true>(cx, sl, I.s), kk));
+      }
+    }
+    wait(cx, &m.bar_done, (uint32_t)I.p, 14);
+    if constexpr (LP == 4)
+      if (xskip) aux_chain_skip<S, true>(P, cx, c, at, I.p, I.s);
+    if (at < R) {
+      float* ringb = A.ring + (cx.sidx + I.s) * A.ring_floats;
+      for (int jl = 0; jl < nl; ++jl) {
+        const int d = A.dil[first + jl];
+        ringb[A.ring_off[first + jl] + (int64_t)(I.n % d) * R + at] = m.xs[I.p][jl][pad16(at)];
+      }
+    }
+    ptx::bar_sync(kBarAux, kAux);
+    // item it + 1 goes to A only now: releasing it at A's last h of item it (so that A overlaps
+    // this retirement) measured no faster and broke the l = 40 (chain-skip) plans
+    if (rel) release(it + 1);
+  };
+  if (nit == 0) return;
+  make_pre(0);
+  release(0);
+  for (int64_t it = 0; it < nit; ++it) {
+    if (early) {
+      if (it + 1 < nit) make_pre(it + 1);
+      retire(it, true);
+    } else {
+      retire(it, false);
+      if (it + 1 < nit) {
+        make_pre(it + 1);
+        release(it + 1);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ head CTA (rows [64h, 64h+64))
 // Thread k (0..255):
 //   q   : rows {g + 64 m} (m < S/64), columns [16 cc, +16) of W_skip^(l); g = k/4, cc = k%4
 //   z_a : rows 64h + 4 (k/16) + m (m < 4), columns [(k%16) S/16, +S/16) of W_relu
 //   out : rows 64h + 4 (k/16) + m (m < 4), columns [16 (k%16), +16) of W_out
-template <int S, bool TRACE>
+template <int S, bool TRACE, bool PIPE>
 __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -941,8 +1209,13 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     return v[0];
   };
 
-  for (int64_t n = 0; n < A.N; ++n) {
-    const uint32_t par = (uint32_t)(n & 1);
+  for (int64_t it = 0; it < A.N * cx.wc; ++it) {
+    const Item I = item_of<PIPE>(it, cx.wc);
+    const int64_t n = I.n;
+    const uint32_t par = I.par;
+    const float* hb0 = mb_hbuf<PIPE>(cx, 0, I.s);
+    const float* hb1 = mb_hbuf<PIPE>(cx, 1, I.s);
+    const float* zin = mb_za<PIPE>(cx, I.s);
     // q = B_skip + sum_k partial_k + W_skip^(l-1) h^(l-1) + W_skip^(l) h^(l); z_s = relu(q)
     // (PAPER.md:365-372).  W_skip^(l-1) is applied here, from tensor memory, while the last
     // layer runs, so no skip CTA sits between the chain and the head (and the head's shared
@@ -950,29 +1223,32 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     float d2 = 0.0f;
     if (has2) {
       ptx::tmem_load_async<RQ * 16>(tm + cSk2, w);  // W_skip^(l-1) tile
-      if (wait(cx, &m.bar_h[1], par, 24) && k == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[1]), R * 4);
+      if (wait(cx, b_h<PIPE>(cx, 1, I.s), par, 24) && k == 0 && !cx.dead)
+        ptx::mbar_arm(ptx::smem_u32(b_h<PIPE>(cx, 1, I.s)), R * 4);
       if (k == 0) trace<TRACE>(A, n, 4);
       ptx::tmem_wait_ld<RQ * 16>(w);
       float v2[RQ];
-      tile_dot<RQ, 16>(w, &m.hbuf[1][20 * cc], v2);
+      tile_dot<RQ, 16>(w, hb1 + 20 * cc, v2);
       d2 = finish(v2);
       if (k == 0) trace<TRACE>(A, n, 6);
     }
     ptx::tmem_load_async<RQ * 16>(tm, w);  // W_skip^(l) tile, hidden behind the wait
-    if (wait(cx, &m.bar_h[0], par, 21) && k == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[0]), R * 4);
+    if (wait(cx, b_h<PIPE>(cx, 0, I.s), par, 21) && k == 0 && !cx.dead)
+      ptx::mbar_arm(ptx::smem_u32(b_h<PIPE>(cx, 0, I.s)), R * 4);
     if (k == 0) trace<TRACE>(A, n, 0);
     ptx::tmem_wait_ld<RQ * 16>(w);
     float v[RQ];
-    tile_dot<RQ, 16>(w, &m.hbuf[0][20 * cc], v);
+    tile_dot<RQ, 16>(w, hb0 + 20 * cc, v);
     ptx::tmem_load_async<4 * CZ>(tm + cRelu, w);
     v[0] = finish(v);
     if (np > 0) {
-      if (wait(cx, &m.bar_part, par, 22) && k == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_part), np * S * 4);
+      if (wait(cx, b_part<PIPE>(cx, I.s), par, 22) && k == 0 && !cx.dead)
+        ptx::mbar_arm(ptx::smem_u32(b_part<PIPE>(cx, I.s)), np * S * 4);
     }
     if (k == 0) trace<TRACE>(A, n, 1);
     if (qwriter) {
       float qv = bskip[qrow];
-      for (int kk = 0; kk < np; ++kk) qv += m.part[kk][qrow];
+      for (int kk = 0; kk < np; ++kk) qv += mb_part<PIPE>(cx, kk, I.s)[qrow];
       qv += d2;
       qv += v[0];
       m.zs[cpad<CZ>(qrow)] = fmaxf(qv, 0.0f);
@@ -992,15 +1268,16 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     {  // all four lanes of a quad hold z_a[orow]: lane k%4 sends it to head k%4 (one st.async
        // per lane -- a st.async holds its warp for about one hop, so never several in a row)
       const int dst = pad16(64 * hidx + orow);
-      ptx::st_async(remote(&m.za_in[dst], pl.nc + (k & 3)), zav, remote(&m.bar_za, pl.nc + (k & 3)));
+      ptx::st_async(remote(mb_za<PIPE>(cx, I.s) + dst, pl.nc + (k & 3)), zav, remote(b_za<PIPE>(cx, I.s), pl.nc + (k & 3)));
     }
     if (k == 0) trace<TRACE>(A, n, 9);
-    if (wait(cx, &m.bar_za, par, 23) && k == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_za), kLevels * 4);
+    if (wait(cx, b_za<PIPE>(cx, I.s), par, 23) && k == 0 && !cx.dead)
+      ptx::mbar_arm(ptx::smem_u32(b_za<PIPE>(cx, I.s)), kLevels * 4);
     if (k == 0) trace<TRACE>(A, n, 2);
     // logits = W_out z_a + B_out
     ptx::tmem_wait_ld<64>(w);
     float lg[4];
-    tile_dot<4, 16>(w, &m.za_in[20 * c16], lg);
+    tile_dot<4, 16>(w, zin + 20 * c16, lg);
     xpose_level<4>(lg, k, 8);
     xpose_level<2>(*reinterpret_cast<float(*)[2]>(lg), k, 4);
     lg[0] += __shfl_xor_sync(0xffffffffu, lg[0], 2);
@@ -1008,7 +1285,8 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     bool drop = false;  // watchdog test hook (TRACE instantiation only; DVW_FAULT_INJECT=1)
     if constexpr (TRACE) drop = A.fault == 1 && n == A.trace_n0;
     if (owriter && !drop)
-      ptx::st_async(remote(&m.logits_in[64 * hidx + orow], 0), lg[0] + bout[orow], remote(&m.bar_logits, 0));
+      ptx::st_async(remote(mb_logits<PIPE>(cx, I.s) + 64 * hidx + orow, 0), lg[0] + bout[orow],
+                    remote(b_logits<PIPE>(cx, I.s), 0));
     if (k == 0) trace<TRACE>(A, n, 3);
   }
 }
@@ -1016,7 +1294,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
 // ------------------------------------------------------------------ skip CTA
 // partial_k = sum over owned layers j (ascending) of W_skip^(j) h^(j).
 // Thread t: rows {g + 64 m} (m < S/64), columns [16 cc, +16); g = t/4, cc = t%4.
-template <int S, bool TRACE>
+template <int S, bool TRACE, bool PIPE>
 __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw) {
   const RunArgs& A = P.a;
   const ClusterPlan& pl = P.p;
@@ -1042,14 +1320,17 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
     return v[0];
   };
 
-  for (int64_t n = 0; n < A.N; ++n) {
-    const uint32_t par = (uint32_t)(n & 1);
+  for (int64_t it = 0; it < A.N * cx.wc; ++it) {
+    const Item I = item_of<PIPE>(it, cx.wc);
+    const int64_t n = I.n;
+    const uint32_t par = I.par;
     float part = 0.0f;
 #pragma unroll 1
     for (int sl = 0; sl < nown; ++sl) {
       const bool in_tmem = sl >= nsm;
       if (in_tmem) ptx::tmem_load_async<QS>(tm + (sl - nsm) * QS, wl);
-      if (wait(cx, &m.bar_h[sl], par, 31) && t == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(&m.bar_h[sl]), R * 4);
+      if (wait(cx, b_h<PIPE>(cx, sl, I.s), par, 31) && t == 0 && !cx.dead)
+        ptx::mbar_arm(ptx::smem_u32(b_h<PIPE>(cx, sl, I.s)), R * 4);
       if (in_tmem) {
         ptx::tmem_wait_ld<QS>(wl);
       } else {
@@ -1061,31 +1342,36 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
         }
       }
       float v[RQ];
-      tile_dot<RQ, 16>(wl, &m.hbuf[sl][20 * cc], v);
+      tile_dot<RQ, 16>(wl, mb_hbuf<PIPE>(cx, sl, I.s) + 20 * cc, v);
       part += finish(v);
     }
     // staged by sample parity (a skip CTA's own part[] is otherwise unused): the next sample's
     // writes can never meet this sample's reads (compute-sanitizer racecheck), with no second barrier
-    float* stage = m.part[par];
+    float* stage = m.part[I.p];
     if (writer) stage[row] = part;
     if (t == 0) trace<TRACE>(A, n, 1);
     ptx::bar_sync(kBarHS, kMain);
     if (t < (S / 4) * NH) {
       const int hh = t / (S / 4), e = t % (S / 4);
-      ptx::st_async4(remote(&m.part[k][4 * e], pl.nc + hh), lds4(&stage[4 * e]), remote(&m.bar_part, pl.nc + hh));
+      ptx::st_async4(remote(mb_part<PIPE>(cx, k, I.s) + 4 * e, pl.nc + hh), lds4(&stage[4 * e]),
+                     remote(b_part<PIPE>(cx, I.s), pl.nc + hh));
     }
   }
 }
 
-template <int S, int LP, bool TRACE, int NL = 0, bool SESS = false>
+template <int S, int LP, bool TRACE, int NL = 0, bool SESS = false, bool PIPE = false>
 __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Mail* mail = reinterpret_cast<Mail*>(smem_raw);
-  float* sw = reinterpret_cast<float*>(smem_raw + ((sizeof(Mail) + 127) & ~size_t(127)));
   const ClusterPlan& pl = P.p;
   const int rank = (int)ptx::cluster_rank();
   const int t = threadIdx.x;
-  Ctx cx{mail, P.a.err, pl.size, (int64_t)(blockIdx.x / pl.size), false};
+  constexpr size_t kMailBytes = (sizeof(Mail) + 127) & ~size_t(127);
+  // PIPE: [Mail][this role's mailbox region][weights image]; otherwise [Mail][weights image]
+  float* sw = reinterpret_cast<float*>(smem_raw + (PIPE ? (size_t)pl.sw_off_pipe[rank] : kMailBytes));
+  const int64_t sidx = (int64_t)(blockIdx.x / pl.size) * (PIPE ? P.wmax : 1);
+  const int wc = PIPE ? (int)min((int64_t)P.wmax, (int64_t)P.a.n_streams - sidx) : 1;
+  Ctx cx{mail, P.a.err, pl.size, sidx, false, reinterpret_cast<float*>(smem_raw + kMailBytes), wc};
 
   int role = kIdle, idx = 0;
   if (rank < pl.nc) { role = kChain; idx = rank; }
@@ -1099,7 +1385,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     ptx::mbar_init(ptx::smem_u32(&mail->bar_xin), 1);
     ptx::mbar_init(ptx::smem_u32(&mail->bar_logits), 1);
     ptx::mbar_init(ptx::smem_u32(&mail->bar_pre), 1);
-    ptx::mbar_init(ptx::smem_u32(&mail->bar_done), 1);
+    ptx::mbar_init(ptx::smem_u32(&mail->bar_done), 4);  // one arrival per warp of B
     ptx::mbar_init(ptx::smem_u32(&mail->bar_part), 1);
     ptx::mbar_init(ptx::smem_u32(&mail->bar_za), 1);
     ptx::mbar_init(ptx::smem_u32(&mail->bar_exit), 1);
@@ -1112,6 +1398,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_part), pl.npart * S * 4);
     ptx::mbar_arm(ptx::smem_u32(&mail->bar_za), kLevels * 4);
     for (int i = 0; i < kCMaxSlot; ++i) ptx::mbar_arm(ptx::smem_u32(&mail->bar_h[i]), R * 4);
+    if constexpr (PIPE) {  // one barrier per stream of the cluster for every inbound mailbox
+      for (int q = 0; q < kWP; ++q) {
+        ptx::mbar_init(ptx::smem_u32(&mail->pb_hin[q]), 1);
+        ptx::mbar_init(ptx::smem_u32(&mail->pb_xin[q]), 1);
+        ptx::mbar_init(ptx::smem_u32(&mail->pb_logits[q]), 1);
+        ptx::mbar_init(ptx::smem_u32(&mail->pb_part[q]), 1);
+        ptx::mbar_init(ptx::smem_u32(&mail->pb_za[q]), 1);
+        for (int i = 0; i < kCMaxSlot; ++i) ptx::mbar_init(ptx::smem_u32(&mail->pb_h[i][q]), 1);
+        mail->ys[q][0] = mail->ys[q][1] = kLevels / 2;  // R4
+      }
+      ptx::mbar_init(ptx::smem_u32(&mail->bar_pre2[0]), 1);
+      ptx::mbar_init(ptx::smem_u32(&mail->bar_pre2[1]), 1);
+      ptx::fence_mbar_init();
+      for (int q = 0; q < kWP; ++q) {
+        ptx::mbar_arm(ptx::smem_u32(&mail->pb_hin[q]), R * 4);
+        ptx::mbar_arm(ptx::smem_u32(&mail->pb_xin[q]), R * 4);
+        ptx::mbar_arm(ptx::smem_u32(&mail->pb_logits[q]), kLevels * 4);
+        ptx::mbar_arm(ptx::smem_u32(&mail->pb_part[q]), pl.npart * S * 4);
+        ptx::mbar_arm(ptx::smem_u32(&mail->pb_za[q]), kLevels * 4);
+        for (int i = 0; i < kCMaxSlot; ++i) ptx::mbar_arm(ptx::smem_u32(&mail->pb_h[i][q]), R * 4);
+      }
+    }
   }
   if (role != kIdle) {
     const float4* src = reinterpret_cast<const float4*>(P.pk + pl.pk_smem_off[rank]);
@@ -1154,13 +1462,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
 
   if (t >= kAux) {
     if (role == kChain) {
-      if (t < kAux + 128) chain_A<LP, TRACE, NL, SESS>(P, cx, idx, sw);
-      else if (t < kAux + 256) chain_B<LP, TRACE, SESS>(P, cx, idx, sw);
-      else chain_C<LP, TRACE, SESS>(P, cx, idx, sw);
+      if (t < kAux + 128) chain_A<LP, TRACE, NL, SESS, PIPE>(P, cx, idx, sw);
+      else if (t < kAux + 256) chain_B<LP, TRACE, SESS, PIPE>(P, cx, idx, sw);
+      else chain_C<LP, TRACE, SESS, PIPE>(P, cx, idx, sw);
     } else if (role == kHead) {
-      if (t < kAux + kMain) head_main<S, TRACE>(P, cx, idx, sw);
+      if (t < kAux + kMain) head_main<S, TRACE, PIPE>(P, cx, idx, sw);
     } else if (role == kSkip) {
-      if (t < kAux + kMain) skip_main<S, TRACE>(P, cx, idx, sw);
+      if (t < kAux + kMain) skip_main<S, TRACE, PIPE>(P, cx, idx, sw);
     }
     ptx::tmem_fence_before();
     ptx::bar_sync(kBarMath, kMath);
@@ -1169,7 +1477,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
     ptx::cluster_sync();
     return;
   }
-  if (role == kChain) chain_aux<S, LP, TRACE, SESS>(P, cx, idx, sw);
+  if constexpr (PIPE) {
+    if (role == kChain) chain_aux_pipe<S, LP>(P, cx, idx, sw);
+  } else {
+    if (role == kChain) chain_aux<S, LP, TRACE, SESS, PIPE>(P, cx, idx, sw);
+  }
   // Park until the math warps are done (try_wait suspends the warp), then free TMEM.
   while (!ptx::mbar_try_wait_cta(ptx::smem_u32(&mail->bar_exit), 0)) {
   }
@@ -1179,12 +1491,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
   ptx::cluster_sync();
 }
 
-template <int S, int LP, bool TRACE, int NL = 0, bool SESS = false>
+template <int S, int LP, bool TRACE, int NL = 0, bool SESS = false, bool PIPE = false>
 cudaError_t configure(int smem) {
-  cudaError_t e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, NL, SESS>,
+  cudaError_t e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, NL, SESS, PIPE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, NL, SESS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(k_cluster<S, LP, TRACE, NL, SESS, PIPE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
@@ -1209,6 +1521,32 @@ int max_active_clusters(int size, int smem) {
   cfg.numAttrs = 1;
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, k_cluster<S, LP, false>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// The multi-stream variant (production gate only): co-resident clusters at its shared-memory size.
+template <int S, int LP>
+int max_active_pipe(int size, int smem) {
+  if (configure<S, LP, false, 0, false, true>(smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(size);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = size;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_cluster<S, LP, false, 0, false, true>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return 0;
   }
@@ -1263,8 +1601,16 @@ ClusterPlan plan_lp(int L, int r, int s, int device, int lp) {
     p.layer_skip_cta[j] = -1;
     p.layer_skip_slot[j] = 0;
   }
-  for (int j = p.nxs; j < nskip; ++j) {  // round robin: consecutive layers go to different CTAs
-    const int k = (j - p.nxs) % p.nk;
+  // Skip CTA k takes a contiguous block of layers (DVW_SKIP_RR=1: round robin, A/B).  With several
+  // streams in flight (the multi-stream variant) a skip CTA holds an item from its first owned layer
+  // to its last, so a block spanning a third of the chain instead of all of it triples how many
+  // items it can serve per chain traversal; at batch 1 a block keeps up as well (one 64 x 256 matvec
+  // per arriving layer).
+  const char* rr = std::getenv("DVW_SKIP_RR");
+  const bool round_robin = rr && std::atoi(rr) == 1;
+  const int nsk = nskip - p.nxs, per = p.nk > 0 ? (nsk + p.nk - 1) / p.nk : 0;
+  for (int j = p.nxs; j < nskip; ++j) {
+    const int k = round_robin ? (j - p.nxs) % p.nk : (j - p.nxs) / per;
     p.layer_skip_cta[j] = p.nc + p.nh + k;
     p.layer_skip_slot[j] = p.skip_n[k]++;
   }
@@ -1307,6 +1653,31 @@ ClusterPlan plan_lp(int L, int r, int s, int device, int lp) {
   if (prev >= 0) cudaSetDevice(prev);
   if (nclus < 1) { p.why = "cluster cannot be scheduled on this device"; return p; }
   p.max_clusters = nclus;
+  // multi-stream variant: [Mail][per-stream inbound mailboxes of the CTA's role][weights image]
+  {
+    const size_t mailb = (sizeof(Mail) + 127) & ~size_t(127);
+    int smem_pipe = 0;
+    for (int rank = 0; rank < p.size; ++rank) {
+      int64_t mbf;
+      if (rank < p.nc) mbf = 2 * kWP * kHLen + kWP * kLevels;
+      else if (rank < p.nc + p.nh) mbf = 2 * kWP * kHLen + kWP * kVLen + (int64_t)p.npart * kWP * 256;
+      else mbf = (int64_t)p.skip_n[rank - p.nc - p.nh] * kWP * kHLen;
+      const int64_t off = (int64_t)mailb + ((mbf * 4 + 127) & ~int64_t(127));
+      p.sw_off_pipe[rank] = (int)off;
+      smem_pipe = std::max(smem_pipe, (int)(off + (int64_t)p.pk_smem_floats[rank] * 4));
+    }
+    p.smem_pipe = smem_pipe;
+    if (smem_pipe <= dev_smem) {
+      cudaGetDevice(&prev);
+      cudaSetDevice(device);
+      int np = 0;
+      if (s == 256) np = lp == 3 ? max_active_pipe<256, 3>(p.size, smem_pipe) : max_active_pipe<256, 4>(p.size, smem_pipe);
+      else np = lp == 3 ? max_active_pipe<128, 3>(p.size, smem_pipe) : max_active_pipe<128, 4>(p.size, smem_pipe);
+      if (prev >= 0) cudaSetDevice(prev);
+      p.max_clusters_pipe = np;
+      p.pipe_ok = np >= 1;
+    }
+  }
   p.ok = true;
   p.why = "ok";
   return p;
@@ -1469,13 +1840,27 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   P.a = a;
   P.p = p;
   P.pk = static_cast<const float*>(packed);
+  P.wmax = 1;
   const bool tr = a.trace != nullptr;
+  const bool ss = a.ystate != nullptr;
+  const bool ap = a.approx == 1 && !tr && !ss;
+  const bool pc = a.approx == 2 && !tr && !ss;
+  // Streams per cluster: one (cluster c generates stream c, Ctx::sidx), or -- for more streams than
+  // clusters fit at once, production gate, no session / trace -- up to kWP interleaved per cluster
+  // (the multi-stream variant), spread evenly.  DVW_CLUSTER_W=k forces k (A/B measurements).
+  int w = 1;
+  if (p.pipe_ok && !tr && !ss && a.approx == 0) {
+    const int cap = std::max(1, p.max_clusters_pipe);
+    if (a.n_streams > p.max_clusters) w = std::min(kWP, (a.n_streams + cap - 1) / cap);
+    if (const char* ev = std::getenv("DVW_CLUSTER_W")) w = std::max(1, std::min(kWP, std::atoi(ev)));
+  }
+  P.wmax = w;
+  const int nclu = (a.n_streams + w - 1) / w;
   cudaLaunchConfig_t cfg{};
-  // one cluster per stream: cluster c generates stream c (Ctx::sidx); clusters never wait for
-  // each other, so more clusters than fit at once simply run in waves
-  cfg.gridDim = dim3(p.size * a.n_streams);
+  // clusters never wait for each other, so more clusters than fit at once simply run in waves
+  cfg.gridDim = dim3(p.size * nclu);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = p.smem_bytes;
+  cfg.dynamicSmemBytes = w > 1 ? p.smem_pipe : p.smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1488,11 +1873,9 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   // variants: production (exact gate), TRACE (exact gate + timestamps), NL = 1 (hardware tanh),
   // NL = 2 (App. C gate and exp), SESS (streaming session: continues the queues and code
   // history; exact gate -- the API routes approximate-tier sessions to the stream kernel)
-  const bool ss = a.ystate != nullptr;
-  const bool ap = a.approx == 1 && !tr && !ss;
-  const bool pc = a.approx == 2 && !tr && !ss;
 #define DVW_LAUNCH(S_, LP_)                                                         \
-  e = ss   ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, 0, true>, P)       \
+  e = w > 1 ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, 0, false, true>, P) \
+      : ss ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, 0, true>, P)       \
       : tr ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, true>, P)                 \
       : ap ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, 1>, P)             \
       : pc ? cudaLaunchKernelEx(&cfg, k_cluster<S_, LP_, false, 2>, P)             \
@@ -1507,7 +1890,7 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
     DVW_LAUNCH(128, 4);
   }
 #undef DVW_LAUNCH
-  info->grid = p.size * a.n_streams;
+  info->grid = p.size * nclu;
   info->cluster = p.size;
   info->threads = kThreads;
   info->launches = 1;

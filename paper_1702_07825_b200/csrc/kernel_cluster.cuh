@@ -52,6 +52,11 @@ struct ClusterPlan {
   int64_t pk_total = 0;           // floats
   int smem_bytes = 0;
   int max_clusters = 0;           // co-resident clusters on the device (one stream each)
+  // multi-stream variant (several streams' samples interleaved per cluster; kernel_cluster.cu PIPE)
+  bool pipe_ok = false;
+  int smem_pipe = 0;              // its dynamic shared memory (Mail + per-stream mailboxes + image)
+  int max_clusters_pipe = 0;
+  int sw_off_pipe[kCMaxCta] = {}; // byte offset of each CTA's weights image in that layout
 };
 
 ClusterPlan plan_cluster(int L, int r, int s, int device);

@@ -743,7 +743,7 @@ def test_sharding_invariance_hashed_inputs_bitwise(L):
 # ------------------------------------------------------------------ one cluster per stream (small batches)
 @pytest.mark.parametrize("cfg,S,N", [(synth.C2, 6, 1600), (synth.C2, 14, 300), (synth.C3, 3, 400)],
                          ids=["C2-6", "C2-14-waves", "C3-3"])
-def test_cluster_kernel_one_cluster_per_stream(L, cfg, S, N):
+def test_cluster_kernel_one_cluster_per_stream(L, monkeypatch, cfg, S, N):
     """A batch on the cluster kernel launches one cluster per stream (14 CTAs each at C2, 16 at
     C3): every stream equals the fp64 oracle code for code, also when the batch has more
     clusters than fit at once (C2 x 14 = 196 CTAs > 148 SMs: later clusters run in waves)."""
@@ -752,7 +752,9 @@ def test_cluster_kernel_one_cluster_per_stream(L, cfg, S, N):
     utts = list(range(3, 3 + S))
     cond, u = synth.make_batch(cfg, N, utts, hop)
     m = L.Model.from_config(cfg).load(w).set_kernel("cluster")
+    monkeypatch.setenv("DVW_CLUSTER_W", "1")  # one stream per cluster (more streams interleave, below)
     codes = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    monkeypatch.delenv("DVW_CLUSTER_W")
     info = m.info()
     assert info["last_kernel_name"] == "cluster" and info["last_grid"] == S * info["last_cluster"]
     for i in range(S):
@@ -835,3 +837,29 @@ def test_tc_balanced_blocks_position_independent(L, S):
         ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[st], hop, N, uniforms=u[st],
                                dilations=cfg.dilation_list(), want_logits=False)
         assert np.array_equal(many[st], ref), st
+
+
+@pytest.mark.parametrize("cfg,S,W,N", [(synth.C2, 12, 8, 300), (synth.C2, 5, 4, 200), (synth.C3, 9, 8, 160),
+                                       (synth.Config(4, 64, 128), 20, 8, 96)],
+                         ids=["C2-12x8", "C2-5x4", "C3-9x8", "l4-20x8"])
+def test_cluster_multi_stream_interleaved_matches_oracle(L, monkeypatch, cfg, S, W, N):
+    """Multi-stream cluster kernel: up to W streams per cluster with their samples interleaved item
+    by item (item i = stream i % w, sample i / w; per-stream mailboxes and barriers):
+    every stream's codes equal the oracle's and the one-stream run's bitwise, for a ragged last
+    cluster (S not a multiple of W) and at LP = 3 and 4 (PAPER.md:416 independent utterances)."""
+    hop = 64
+    w = synth.make_weights(cfg, 0)
+    utts = list(range(S))
+    cond, u = synth.make_batch(cfg, N, utts, hop)
+    m = model(L, cfg, w, "cluster")
+    monkeypatch.setenv("DVW_CLUSTER_W", str(W))
+    many = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    m.sync()
+    assert m.info()["last_grid"] == m.info()["last_cluster"] * ((S + W - 1) // W)
+    monkeypatch.delenv("DVW_CLUSTER_W")
+    for st in sorted({0, 1, W - 1, W % S, S - 1}):
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[st], hop, N, uniforms=u[st],
+                               dilations=cfg.dilation_list(), want_logits=False)
+        assert np.array_equal(many[st], ref), st
+    one = m.generate(dev(cond[S - 1:S]), dev(u[S - 1:S]), hop).cpu().numpy()[0]
+    assert np.array_equal(many[S - 1], one)

@@ -21,6 +21,10 @@ for V in $VARS; do
       --expt-relaxed-constexpr -I $D/include $DEFS -c $C/kernel_cluster.cu -o $C/kernel_cluster.o
   $NV -gencode arch=compute_100a,code=sm_100a -shared -o $D/paper_1702_07825_b200/libdvw.so $C/*.o -lcuda
   echo "== $V" >> $OUT/diag.txt
-  DVW_PKG_ROOT=$D timeout 300 python tools/sweep_layers.py --layers ${LAYERS:-20,40} --n 8000 >> $OUT/diag.txt 2>&1
+  if [ -n "$DIAG_CMD" ]; then
+    (cd $D && cp -r /root/repo/bench.py /root/repo/oracle . 2>/dev/null; DVW_PKG_ROOT=$D timeout 600 bash -c "$DIAG_CMD") >> $OUT/diag.txt 2>&1
+  else
+    DVW_PKG_ROOT=$D timeout 300 python tools/sweep_layers.py --layers ${LAYERS:-20,40} --n 8000 >> $OUT/diag.txt 2>&1
+  fi
 done
 cat $OUT/diag.txt
