@@ -37,10 +37,13 @@
 
 #include "kernel_cluster.cuh"
 #include "ptx.cuh"
+#include "umma.cuh"
 
 // Timing diagnostics only (codes become wrong): build with -DDVW_DIAG=<mask> into a scratch
 // copy (tools/diag_c2.sh).  1: X skips the W_prev matvec; 2: C skips its matvec; 4: B skips
-// its matvec; 8: X skips the queue / conditioning / W_prev work; 16: the draw is floor(256 u).
+// its matvec; 8: X skips the queue / conditioning / W_prev work; 16: the draw is floor(256 u);
+// 32: skip CTAs skip their matvecs; 64: head CTAs skip theirs; 256: X skips the chain-skip matvec;
+// 512: X's weight stream (LP = 4 multi-stream) copies but does not compute; 1024: computes, no copies.
 #ifndef DVW_DIAG
 #define DVW_DIAG 0
 #endif
@@ -64,6 +67,24 @@ constexpr int kTmemCols = 512;
 // Multi-stream variant (PIPE): up to kWP streams per cluster, their samples interleaved item by item
 // (item i = stream i % wc, sample i / wc), so up to wc samples are in flight along the chain at once.
 constexpr int kWP = 8;
+// multi-stream variant: X's pre terms live in a ring of kPR slots (item i in slot i mod kPR), computed
+// kPB <= kPR - 1 items at a time (one W_prev pass and one memory latency per batch); chain-skip
+// partials of up to kXH items are computed together (one W_skip pass from L2 per batch)
+constexpr int kPR = 4;
+constexpr int kPB = kPR - 1;
+constexpr int kXH = 4;
+// LP = 4 multi-stream: X streams W_prev and the chain-skip W_skip from L2 through a ring of up to kWNB
+// shared-memory buffers of kWChunk floats (16 KB: 8 of a row block's 16 column quads), filled by 1-D
+// bulk copies (cp.async.bulk, mbarrier complete_tx) -- many KB in flight and no registers held
+constexpr int kWNB = 4;
+constexpr int kWChunk = 8 * 128 * 4;
+// A/B switch (profiles/r2_experiments.md): 1 = the bulk-copy weight stream above; 0 (default) = every X
+// thread loads its row's 16 float4 from L2 straight into registers (measured faster: C5 shape, 256
+// streams, 1.10 vs 0.96 M samples/s)
+#ifndef DVW_XSTREAM
+#define DVW_XSTREAM 0
+#endif
+constexpr bool kXStream = DVW_XSTREAM != 0;
 constexpr uint64_t kTimeoutNs = 2000000000ull;
 
 // named barriers (0 is __syncthreads).  A producer that only arrives gets one id per use
@@ -121,9 +142,9 @@ struct __align__(16) Mail {
   uint64_t pb_hin[kWP], pb_xin[kWP], pb_logits[kWP], pb_part[kWP], pb_za[kWP];
   uint64_t pb_h[kCMaxSlot][kWP];
   int ys[kWP][2];
-  // PIPE: X's pre terms double-buffered by item parity, one barrier per parity (X runs an item ahead)
-  uint64_t bar_pre2[2];
-  float pre2[2][LPC][2 * R];
+  // PIPE: one barrier per slot of X's pre ring (the ring itself is in the chain's mailbox region)
+  uint64_t bar_pre2[kPR];
+  uint64_t wfull[kWNB];  // PIPE, LP = 4: X's weight-stream buffers (bulk copy landed)
 };
 
 struct Params {
@@ -131,6 +152,8 @@ struct Params {
   ClusterPlan p;
   const float* pk;
   int wmax;  // streams per cluster (1, or up to kWP for the multi-stream variant)
+  int xpb;   // PIPE: X's pre batch (1..kPB; capped at streams - 1 per cluster)
+  int xsb;   // PIPE: chain-skip batch (1..kXH)
 };
 
 struct Ctx {
@@ -159,9 +182,10 @@ struct Item {
 template <bool PIPE>
 __device__ __forceinline__ Item item_of(int64_t it, int wc) {
   Item x;
-  if constexpr (PIPE) {
-    x.s = (int)(it % wc);
-    x.n = it / wc;
+  if constexpr (PIPE) {  // 32-bit division: the host keeps N x wc < 2^31 for this variant
+    const uint32_t iu = (uint32_t)it, w = (uint32_t)wc;
+    x.s = (int)(iu % w);
+    x.n = (int64_t)(iu / w);
   } else {
     x.s = 0;
     x.n = it;
@@ -186,6 +210,18 @@ template <bool PIPE>
 __device__ __forceinline__ float* mb_logits(const Ctx& cx, int s) {
   if constexpr (PIPE) return cx.mb + 2 * kWP * kHLen + s * kLevels; else return cx.mail->logits_in;
 }
+// chain mailbox region, after the logits: X's pre ring [kPR][LPC][2R], its queue-entry staging
+// [kPB][LPC][R], and (LP = 4) the chain-skip history [kXH][LPC][kHLen] + partial staging [kXH][256]
+constexpr int kMbPre = 2 * kWP * kHLen + kWP * kLevels;
+constexpr int kMbXst = kMbPre + kPR * LPC * 2 * R;
+constexpr int kMbHist = kMbXst + kPB * LPC * R;
+constexpr int kMbXstage = kMbHist + kXH * LPC * kHLen;
+constexpr int kMbChainEnd3 = kMbHist;                 // LP = 3: no chain-skip layers
+constexpr int kMbChainEnd4 = kMbXstage + kXH * 256;  // then (LP = 4) the weight-stream ring [xnb][kWChunk]
+__device__ __forceinline__ float* mb_pre(const Ctx& cx, int slot) { return cx.mb + kMbPre + slot * LPC * 2 * R; }
+__device__ __forceinline__ float* mb_xst(const Ctx& cx, int k) { return cx.mb + kMbXst + k * LPC * R; }
+__device__ __forceinline__ float* mb_hist(const Ctx& cx, int k) { return cx.mb + kMbHist + k * LPC * kHLen; }
+__device__ __forceinline__ float* mb_xstage(const Ctx& cx, int k) { return cx.mb + kMbXstage + k * 256; }
 template <bool PIPE>
 __device__ __forceinline__ float* mb_hbuf(const Ctx& cx, int sl, int s) {
   if constexpr (PIPE) return cx.mb + (sl * kWP + s) * kHLen; else return cx.mail->hbuf[sl];
@@ -661,9 +697,9 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
     }
     if (a == 0) trace<TRACE>(A, n, 0);
     uint64_t* tp = (a == 0) ? trace_slot<TRACE>(A, n) : nullptr;
-    if constexpr (PIPE) wait(cx, &m.bar_pre2[p], (uint32_t)((it >> 1) & 1), 13);
+    if constexpr (PIPE) wait(cx, &m.bar_pre2[it % kPR], (uint32_t)((it / kPR) & 1), 13);
     else wait(cx, &m.bar_pre, (uint32_t)p, 13);
-    const float* prev_pre = PIPE ? &m.pre2[p][0][0] : &m.pre[0][0];
+    const float* prev_pre = PIPE ? mb_pre(cx, (int)(it % kPR)) : &m.pre[0][0];
     ptx::tmem_wait_ld<64>(w);
 #pragma unroll
     for (int jl = 0; jl < LP; ++jl) {
@@ -910,13 +946,14 @@ __device__ __forceinline__ void aux_chain_skip(const Params& P, const Ctx& cx, i
   for (int jl = 0; jl < nl; ++jl) {
     const int j = first + jl;
     if (j >= pl.nxs) break;
+    if constexpr ((DVW_DIAG & 256) != 0) continue;
     const float* wsk = P.pk + pl.wskx_off + (int64_t)j * 16 * S * 4;
     const float* h = m.hs[pp][jl];
 #pragma unroll
     for (int rr = 0; rr < RR; ++rr) {
       float4 wv[16];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) wv[q] = ldg4(wsk + ((int64_t)q * S + at + 128 * rr) * 4);
+      for (int q = 0; q < 16; ++q) wv[q] = ldg4(wsk + ((int64_t)(rr * 16 + q) * 128 + at) * 4);
       float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
@@ -1042,12 +1079,15 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
   }
 }
 
-// Multi-stream variant of the aux warpgroup.  Item i = (stream s, sample n).  X computes pre for
-// item i + 1 while A and B work on item i, retires item i (forwards its h, writes its x into its
-// stream's queues), then releases item i + 1 to A -- so A can never run two items ahead of X's
-// forwarding (the named barriers kBarHX + jl are shared by consecutive items).  Item i + 1's queue
-// entries x_j(n - d) belong to item i + 1 - wc d <= i - 1, already written (wc >= 2); a cluster
-// with one stream (a ragged last cluster) writes item i's queues before computing pre for i + 1.
+// Multi-stream variant of the aux warpgroup.  Item i = (stream s, sample n).  X computes the pre terms
+// of the next kPB items at once (P.xpb, capped at wc - 1) while A and B work on item i: one W_prev
+// pass (L2 at LP = 4) and one memory latency (conditioning, queue entries) per batch instead of per
+// item.  X retires item i (forwards its h, writes its x into its stream's queues), then releases item
+// i + 1 to A -- so A can never run two items ahead of X's forwarding (the named barriers kBarHX + jl
+// are shared by consecutive items).  The queue entries x_j(n - d) of items i + 1 .. i + kPB belong to
+// items <= i + kPB - wc d <= i - 1 (kPB <= wc - 1), already retired; a cluster with one stream (a
+// ragged last cluster) writes item i's queues before computing pre for i + 1.  At LP = 4 the
+// chain-skip partials (layers < nxs, W_skip from L2) are computed for P.xsb items at a time.
 template <int S, int LP>
 __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const float* sw) {
   const RunArgs& A = P.a;
@@ -1060,62 +1100,251 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
   const bool xskip = LP == 4 && first < pl.nxs;
   const int64_t nit = A.N * cx.wc;
   const bool early = cx.wc >= 2;
-
-  // pre of item `it` (stream s, sample n) into pre2[it & 1] (released separately)
-  auto make_pre = [&](int64_t it) {
-    const Item I = item_of<true>(it, cx.wc);
-    if constexpr ((DVW_DIAG & 8) != 0) {  // timing diagnostic: no queue / conditioning / W_prev work
-      for (int jl = 0; jl < nl; ++jl) m.pre2[I.p][jl][at] = 0.0f;
+  const int pb = early ? max(1, min(P.xpb, cx.wc - 1)) : 1;
+  // a chain-skip batch holds items of distinct streams (xsb <= wc): the partial of item i waits
+  // for item i + xsb - 1, which must not be a later sample of i's own stream
+  const int xsb = max(1, min(min(P.xsb, kXH), cx.wc));
+  // LP = 4: weight stream.  A job is a list of nch 16-KB chunks (src(i)); chunk g of the CTA's
+  // running count uses buffer g mod nb (phase (g / nb) & 1).  Thread 0 keeps nb copies in flight;
+  // after body(i, buffer) every X thread passes kBarAux, so the buffer is free for chunk i + nb.
+  const int nb = pl.xnb[c];
+  uint32_t wg = 0;
+  auto stream_job = [&](int nch, auto&& src, auto&& body) {
+    auto issue = [&](int i) {
+      const int sl = (int)((wg + i) % nb);
+      const uint32_t bar = ptx::smem_u32(&m.wfull[sl]);
+      ptx::mbar_arm(bar, kWChunk * 4);
+      bulk_g2s(ptx::smem_u32(cx.mb + kMbChainEnd4 + sl * kWChunk), src(i), kWChunk * 4, bar);
+    };
+    constexpr bool kCopy = (DVW_DIAG & 1024) == 0, kBody = (DVW_DIAG & 512) == 0;  // timing diagnostics
+    if (at == 0 && kCopy)
+      for (int i = 0; i < min(nb, nch); ++i) issue(i);
+    for (int i = 0; i < nch; ++i) {
+      const int sl = (int)((wg + i) % nb);
+      if (kCopy) wait(cx, &m.wfull[sl], ((wg + i) / nb) & 1, 19);
+      if (kBody) body(i, (const float*)(cx.mb + kMbChainEnd4 + sl * kWChunk));
       ptx::bar_sync(kBarAux, kAux);
+      if (at == 0 && i + nb < nch && kCopy) issue(i + nb);
+    }
+    wg += nch;
+  };
+
+  // pre of items [i0, i0 + cnt) (cnt <= kPB) into their ring slots; ordered before the releases by
+  // the caller's next kBarAux barrier
+  auto make_pre = [&](int64_t i0, int cnt) {
+    if constexpr ((DVW_DIAG & 8) != 0) {  // timing diagnostic: no queue / conditioning / W_prev work
+      for (int k = 0; k < cnt; ++k)
+        for (int jl = 0; jl < nl; ++jl) mb_pre(cx, (int)((i0 + k) % kPR))[jl * 2 * R + at] = 0.0f;
       return;
     }
-    const float* condb = A.cond + (cx.sidx + I.s) * A.n_frames * L * 2 * R;
-    const float* ringb = A.ring + (cx.sidx + I.s) * A.ring_floats;
-    const int64_t f = I.n / A.hop;
-    // every layer's conditioning and queue entry in flight at once (one memory latency per item)
-    float lvs[LPC], xps[LPC];
+    // every item's conditioning and queue entries in flight at once (all loads issued before the
+    // first store): B + L into the item's slot, x_j(n - d) into the staging rows
+    float lv[kPB][LPC], xv[kPB][LPC];
 #pragma unroll
-    for (int jl = 0; jl < LPC; ++jl) {
-      if (jl < nl) {
-        const int j = first + jl;
-        const int d = A.dil[j];
-        lvs[jl] = __ldg(condb + (f * L + j) * 2 * R + at);
-        xps[jl] = (at < R && I.n - d >= 0) ? ringb[A.ring_off[j] + (int64_t)(I.n % d) * R + at] : 0.0f;
+    for (int k = 0; k < kPB; ++k) {
+      const Item I = item_of<true>(i0 + k, cx.wc);
+      const float* condb = A.cond + ((cx.sidx + I.s) * A.n_frames + (uint32_t)I.n / (uint32_t)A.hop) * L * 2 * R;
+      const float* ringb = A.ring + (cx.sidx + I.s) * A.ring_floats;
+#pragma unroll
+      for (int jl = 0; jl < LPC; ++jl) {
+        lv[k][jl] = xv[k][jl] = 0.0f;
+        if (k < cnt && jl < nl) {
+          const int j = first + jl;
+          const int d = A.dil[j];
+          lv[k][jl] = __ldg(condb + j * 2 * R + at);
+          if (at < R && I.n - d >= 0) xv[k][jl] = ringb[A.ring_off[j] + ((uint32_t)I.n % (uint32_t)d) * R + at];
+        }
       }
     }
 #pragma unroll
-    for (int jl = 0; jl < LPC; ++jl) {
-      if (jl >= nl) break;
-      const int j = first + jl;
-      float4 wv[16];
-      if constexpr (LP == 3) {
-        const float* wp = sw + jl * 16 * 128 * 4;
+    for (int k = 0; k < kPB; ++k) {
+      float* ps = mb_pre(cx, (int)((i0 + k) % kPR));
+      float* xs = mb_xst(cx, k);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) wv[q] = lds4(wp + (q * 128 + at) * 4);
-      } else {
-        const float* wp = P.pk + pl.wprev_off + (int64_t)j * 16 * 128 * 4;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) wv[q] = ldg4(wp + (q * 128 + at) * 4);
+      for (int jl = 0; jl < LPC; ++jl) {
+        if (k < cnt && jl < nl) {
+          ps[jl * 2 * R + at] = bj[jl * 2 * R + at] + lv[k][jl];
+          if (at < R) xs[jl * R + at] = xv[k][jl];
+        }
       }
-      const float lv = lvs[jl];
-      if (at < R) m.xp[at] = xps[jl];
-      ptx::bar_sync(kBarAux, kAux);
-      float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+    }
+    ptx::bar_sync(kBarAux, kAux);
+    // pre += W_prev x_j(n - d): each W_prev row loaded once per batch; k innermost:
+    // one weight float4 is live at a time, not every item's x rows
+    if constexpr (LP == 3 || !kXStream) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const float4 x = lds4(&m.xp[4 * q]);
-        a01 = ffma2(wv[q].x, wv[q].y, x.x, x.y, a01);
-        a23 = ffma2(wv[q].z, wv[q].w, x.z, x.w, a23);
+      for (int jl = 0; jl < LPC; ++jl) {
+        if (jl >= nl) break;
+        float4 wv[16];
+        if constexpr (LP == 3) {
+          const float* wp = sw + jl * 16 * 128 * 4;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) wv[q] = lds4(wp + (q * 128 + at) * 4);
+        } else {  // LP = 4: from L2, the row's 16 float4 in flight at once
+          const float* wp = P.pk + pl.wprev_off + (int64_t)(first + jl) * 16 * 128 * 4;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) wv[q] = ldg4(wp + (q * 128 + at) * 4);
+        }
+        float2 a01[kPB], a23[kPB];
+#pragma unroll
+        for (int k = 0; k < kPB; ++k) a01[k] = a23[k] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+#pragma unroll
+          for (int k = 0; k < kPB; ++k) {
+            if (k < cnt) {
+              const float4 x = lds4(mb_xst(cx, k) + jl * R + 4 * q);
+              a01[k] = ffma2(wv[q].x, wv[q].y, x.x, x.y, a01[k]);
+              a23[k] = ffma2(wv[q].z, wv[q].w, x.z, x.w, a23[k]);
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kPB; ++k) {
+          if (k < cnt) {
+            float* ps = mb_pre(cx, (int)((i0 + k) % kPR)) + jl * 2 * R + at;
+            *ps = *ps + ((a01[k].x + a01[k].y) + (a23[k].x + a23[k].y));
+          }
+        }
       }
-      m.pre2[I.p][jl][at] = (bj[jl * 2 * R + at] + lv) + ((a01.x + a01.y) + (a23.x + a23.y));
-      ptx::bar_sync(kBarAux, kAux);
+    } else {
+      // W_prev_j streamed through the weight ring: chunk 2 jl + hq = column quads [8 hq, 8 hq + 8)
+      float2 a01[kPB], a23[kPB];
+      stream_job(
+          2 * nl, [&](int i) { return P.pk + pl.wprev_off + (int64_t)(first + i / 2) * 16 * 128 * 4 + (i & 1) * kWChunk; },
+          [&](int i, const float* wb) {
+            const int jl = i >> 1;
+            if ((i & 1) == 0) {
+#pragma unroll
+              for (int k = 0; k < kPB; ++k) a01[k] = a23[k] = make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 wq = lds4(wb + (q * 128 + at) * 4);
+              const int qq = 8 * (i & 1) + q;
+#pragma unroll
+              for (int k = 0; k < kPB; ++k) {
+                if (k < cnt) {
+                  const float4 x = lds4(mb_xst(cx, k) + jl * R + 4 * qq);
+                  a01[k] = ffma2(wq.x, wq.y, x.x, x.y, a01[k]);
+                  a23[k] = ffma2(wq.z, wq.w, x.z, x.w, a23[k]);
+                }
+              }
+            }
+            if ((i & 1) == 1) {
+#pragma unroll
+              for (int k = 0; k < kPB; ++k) {
+                if (k < cnt) {
+                  float* ps = mb_pre(cx, (int)((i0 + k) % kPR)) + jl * 2 * R + at;
+                  *ps = *ps + ((a01[k].x + a01[k].y) + (a23[k].x + a23[k].y));
+                }
+              }
+            }
+          });
     }
   };
   auto release = [&](int64_t it) {
-    if (at == 0 && it < nit) ptx::mbar_arrive(ptx::smem_u32(&m.bar_pre2[it & 1]));
+    if (at == 0 && it < nit) ptx::mbar_arrive(ptx::smem_u32(&m.bar_pre2[it % kPR]));
   };
-  // item `it` published by A and finished by B: forward its h layer by layer (releasing item
-  // it + 1 right after A's last h when `early`), then its x into its stream's queues
+  // chain-skip partials sum_{j < nxs} W_skip_j h_j of the last `cnt` retired items
+  // (their h in the history slots), W_skip rows streamed from L2 once per batch, then sent to every
+  // head's partial slot of each item's stream
+  auto chain_skip = [&](int64_t ilast, int cnt) {
+    constexpr int RR = S / 128;  // rows per thread
+    float part[kXH][RR];
+#pragma unroll
+    for (int k = 0; k < kXH; ++k)
+#pragma unroll
+      for (int rr = 0; rr < RR; ++rr) part[k][rr] = 0.0f;
+    if constexpr (!kXStream) {
+      // W_skip_j row block rr ([nxs][RR][16][128][4]) from L2, the thread's 16 float4 in flight at
+      // once, applied to every item of the batch; partials accumulate layer by layer (oracle order)
+      for (int jl = 0; jl < nl; ++jl) {
+        const int j = first + jl;
+        if (j >= pl.nxs) break;
+        if constexpr ((DVW_DIAG & 256) != 0) continue;
+#pragma unroll
+        for (int rr = 0; rr < RR; ++rr) {
+          const float* wsk = P.pk + pl.wskx_off + ((int64_t)j * RR + rr) * 16 * 128 * 4;
+          float4 wv[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) wv[q] = ldg4(wsk + (q * 128 + at) * 4);
+          float2 s01[kXH], s23[kXH];
+#pragma unroll
+          for (int k = 0; k < kXH; ++k) s01[k] = s23[k] = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+#pragma unroll
+            for (int k = 0; k < kXH; ++k) {
+              if (k < cnt) {
+                const float4 x = lds4(mb_hist(cx, (int)((ilast - k) % kXH)) + jl * kHLen + pad16(4 * q));
+                s01[k] = ffma2(wv[q].x, wv[q].y, x.x, x.y, s01[k]);
+                s23[k] = ffma2(wv[q].z, wv[q].w, x.z, x.w, s23[k]);
+              }
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < kXH; ++k)
+            if (k < cnt) part[k][rr] += (s01[k].x + s01[k].y) + (s23[k].x + s23[k].y);
+        }
+      }
+    } else {
+    // W_skip_j row block rr ([nxs][RR][16][128][4]) in chunks of 8 column quads: chunk
+    // (jl RR + rr) 2 + hq; every item's partial accumulates layer by layer in the oracle's order
+    const int nsk = (DVW_DIAG & 256) ? 0 : max(0, min(nl, pl.nxs - first));
+    float2 s01[kXH], s23[kXH];
+    stream_job(
+        2 * RR * nsk, [&](int i) { return P.pk + pl.wskx_off + (int64_t)(first * RR + i / 2) * 16 * 128 * 4 + (i & 1) * kWChunk; },
+        [&](int i, const float* wb) {
+          const int jl = i / (2 * RR), rr = (i / 2) % RR;
+          if ((i & 1) == 0) {
+#pragma unroll
+            for (int k = 0; k < kXH; ++k) s01[k] = s23[k] = make_float2(0.f, 0.f);
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 wq = lds4(wb + (q * 128 + at) * 4);
+            const int qq = 8 * (i & 1) + q;
+#pragma unroll
+            for (int k = 0; k < kXH; ++k) {
+              if (k < cnt) {
+                const float4 x = lds4(mb_hist(cx, (int)((ilast - k) % kXH)) + jl * kHLen + pad16(4 * qq));
+                s01[k] = ffma2(wq.x, wq.y, x.x, x.y, s01[k]);
+                s23[k] = ffma2(wq.z, wq.w, x.z, x.w, s23[k]);
+              }
+            }
+          }
+          if ((i & 1) == 1) {
+#pragma unroll
+            for (int k = 0; k < kXH; ++k)
+              if (k < cnt) {
+#pragma unroll
+                for (int r2 = 0; r2 < RR; ++r2)
+                  if (r2 == rr) part[k][r2] += (s01[k].x + s01[k].y) + (s23[k].x + s23[k].y);
+              }
+          }
+        });
+    }
+#pragma unroll
+    for (int k = 0; k < kXH; ++k)
+      if (k < cnt)
+#pragma unroll
+        for (int rr = 0; rr < RR; ++rr) mb_xstage(cx, k)[at + 128 * rr] = part[k][rr];
+    ptx::bar_sync(kBarAux, kAux);
+    const int slot = pl.xpart_slot[c];
+    for (int k = cnt - 1; k >= 0; --k) {  // oldest item first
+      const int s = item_of<true>(ilast - k, cx.wc).s;
+      const float* st = mb_xstage(cx, k);
+#pragma unroll
+      for (int i = at; i < (S / 4) * NH; i += kAux) {  // S / 4 float4 per head
+        const int hh = i / (S / 4), e = i % (S / 4);
+        ptx::st_async4(remote(mb_part<true>(cx, slot, s) + 4 * e, pl.nc + hh), lds4(st + 4 * e),
+                       remote(b_part<true>(cx, s), pl.nc + hh));
+      }
+    }
+  };
+  // item `it` published by A and finished by B: forward its h layer by layer, then its x into its
+  // stream's queues; release item it + 1 to A when `rel`
   auto retire = [&](int64_t it, bool rel) {
     const Item I = item_of<true>(it, cx.wc);
     for (int jl = 0; jl < nl; ++jl) {
@@ -1139,31 +1368,63 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
       }
     }
     wait(cx, &m.bar_done, (uint32_t)I.p, 14);
-    if constexpr (LP == 4)
-      if (xskip) aux_chain_skip<S, true>(P, cx, c, at, I.p, I.s);
+    if constexpr (LP == 4) {
+      if (xskip) {  // h of the item for its chain-skip batch (hs[p] is reused two items later)
+        float* hh = mb_hist(cx, (int)(it % kXH));
+        for (int i = at; i < nl * kHLen; i += kAux) hh[i] = m.hs[I.p][i / kHLen][i % kHLen];
+      }
+    }
     if (at < R) {
       float* ringb = A.ring + (cx.sidx + I.s) * A.ring_floats;
       for (int jl = 0; jl < nl; ++jl) {
         const int d = A.dil[first + jl];
-        ringb[A.ring_off[first + jl] + (int64_t)(I.n % d) * R + at] = m.xs[I.p][jl][pad16(at)];
+        ringb[A.ring_off[first + jl] + ((uint32_t)I.n % (uint32_t)d) * R + at] = m.xs[I.p][jl][pad16(at)];
       }
     }
     ptx::bar_sync(kBarAux, kAux);
-    // item it + 1 goes to A only now: releasing it at A's last h of item it (so that A overlaps
-    // this retirement) measured no faster and broke the l = 40 (chain-skip) plans
     if (rel) release(it + 1);
   };
   if (nit == 0) return;
-  make_pre(0);
-  release(0);
-  for (int64_t it = 0; it < nit; ++it) {
-    if (early) {
-      if (it + 1 < nit) make_pre(it + 1);
+  // chain-skip batch ending at item `it` (after its retirement; the history slots are X-private)
+  auto skip_batch = [&](int64_t it) {
+    if constexpr (LP == 4) {
+      if (xskip) {
+        const int k = (int)(it % xsb);
+        if (k == xsb - 1 || it == nit - 1) chain_skip(it, k + 1);
+      }
+    }
+  };
+  if (early) {
+    // Item i + 1 is released as soon as item i is retired (its h forwarded, its x in the queues);
+    // X then computes the next pre batch and the chain-skip batch while A and B run item i + 1.
+    // Items 0 .. min(kPB, wc) - 1 are sample 0 of their streams (no queue entries yet); later
+    // batches [it + 2, it + 2 + pb) are computed after retiring item it, and item it + 1 + k needs
+    // items <= it + 1 + k - wc <= it retired (k <= pb <= wc - 1).  Pre slots in use: it + 1 (A) and
+    // the batch, pb + 1 <= kPR (item it's slot is free once it is retired).
+    int64_t nx = min((int64_t)min(kPB, cx.wc), nit);
+    make_pre(0, (int)nx);
+    ptx::bar_sync(kBarAux, kAux);
+    release(0);
+    for (int64_t it = 0; it < nit; ++it) {
       retire(it, true);
-    } else {
+      if (nx == it + 2 && nx < nit) {
+        const int cnt = (int)min((int64_t)pb, nit - nx);
+        make_pre(nx, cnt);
+        nx += cnt;
+      }
+      skip_batch(it);
+    }
+  } else {
+    // one stream: item it + 1 = sample n + 1 needs item it's x in the queues (d = 1)
+    make_pre(0, 1);
+    ptx::bar_sync(kBarAux, kAux);
+    release(0);
+    for (int64_t it = 0; it < nit; ++it) {
       retire(it, false);
+      skip_batch(it);
       if (it + 1 < nit) {
-        make_pre(it + 1);
+        make_pre(it + 1, 1);
+        ptx::bar_sync(kBarAux, kAux);
         release(it + 1);
       }
     }
@@ -1228,7 +1489,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
       if (k == 0) trace<TRACE>(A, n, 4);
       ptx::tmem_wait_ld<RQ * 16>(w);
       float v2[RQ];
-      tile_dot<RQ, 16>(w, hb1 + 20 * cc, v2);
+      if constexpr ((DVW_DIAG & 64) != 0) { for (int r = 0; r < RQ; ++r) v2[r] = w[r] * hb1[20 * cc]; } else tile_dot<RQ, 16>(w, hb1 + 20 * cc, v2);
       d2 = finish(v2);
       if (k == 0) trace<TRACE>(A, n, 6);
     }
@@ -1238,7 +1499,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     if (k == 0) trace<TRACE>(A, n, 0);
     ptx::tmem_wait_ld<RQ * 16>(w);
     float v[RQ];
-    tile_dot<RQ, 16>(w, hb0 + 20 * cc, v);
+    if constexpr ((DVW_DIAG & 64) != 0) { for (int r = 0; r < RQ; ++r) v[r] = w[r] * hb0[20 * cc]; } else tile_dot<RQ, 16>(w, hb0 + 20 * cc, v);
     ptx::tmem_load_async<4 * CZ>(tm + cRelu, w);
     v[0] = finish(v);
     if (np > 0) {
@@ -1258,7 +1519,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     // z_a = relu(W_relu z_s + B_relu)
     ptx::tmem_wait_ld<4 * CZ>(w);
     float za[4];
-    tile_dot<4, CZ>(w, &m.zs[(CZ + 4) * c16], za);
+    if constexpr ((DVW_DIAG & 64) != 0) { for (int r = 0; r < 4; ++r) za[r] = w[r] * m.zs[(CZ + 4) * c16]; } else tile_dot<4, CZ>(w, &m.zs[(CZ + 4) * c16], za);
     ptx::tmem_load_async<64>(tm + cOut, w);
     xpose_level<4>(za, k, 8);
     xpose_level<2>(*reinterpret_cast<float(*)[2]>(za), k, 4);
@@ -1277,7 +1538,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     // logits = W_out z_a + B_out
     ptx::tmem_wait_ld<64>(w);
     float lg[4];
-    tile_dot<4, 16>(w, zin + 20 * c16, lg);
+    if constexpr ((DVW_DIAG & 64) != 0) { for (int r = 0; r < 4; ++r) lg[r] = w[r] * zin[20 * c16]; } else tile_dot<4, 16>(w, zin + 20 * c16, lg);
     xpose_level<4>(lg, k, 8);
     xpose_level<2>(*reinterpret_cast<float(*)[2]>(lg), k, 4);
     lg[0] += __shfl_xor_sync(0xffffffffu, lg[0], 2);
@@ -1342,7 +1603,12 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
         }
       }
       float v[RQ];
-      tile_dot<RQ, 16>(wl, mb_hbuf<PIPE>(cx, sl, I.s) + 20 * cc, v);
+      if constexpr ((DVW_DIAG & 32) != 0) {
+#pragma unroll
+        for (int r = 0; r < RQ; ++r) v[r] = wl[r] * mb_hbuf<PIPE>(cx, sl, I.s)[20 * cc];
+      } else {
+        tile_dot<RQ, 16>(wl, mb_hbuf<PIPE>(cx, sl, I.s) + 20 * cc, v);
+      }
       part += finish(v);
     }
     // staged by sample parity (a skip CTA's own part[] is otherwise unused): the next sample's
@@ -1408,8 +1674,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_cluster(const __grid_constant__
         for (int i = 0; i < kCMaxSlot; ++i) ptx::mbar_init(ptx::smem_u32(&mail->pb_h[i][q]), 1);
         mail->ys[q][0] = mail->ys[q][1] = kLevels / 2;  // R4
       }
-      ptx::mbar_init(ptx::smem_u32(&mail->bar_pre2[0]), 1);
-      ptx::mbar_init(ptx::smem_u32(&mail->bar_pre2[1]), 1);
+      for (int q = 0; q < kPR; ++q) ptx::mbar_init(ptx::smem_u32(&mail->bar_pre2[q]), 1);
+      for (int q = 0; q < kWNB; ++q) ptx::mbar_init(ptx::smem_u32(&mail->wfull[q]), 1);
       ptx::fence_mbar_init();
       for (int q = 0; q < kWP; ++q) {
         ptx::mbar_arm(ptx::smem_u32(&mail->pb_hin[q]), R * 4);
@@ -1659,7 +1925,13 @@ ClusterPlan plan_lp(int L, int r, int s, int device, int lp) {
     int smem_pipe = 0;
     for (int rank = 0; rank < p.size; ++rank) {
       int64_t mbf;
-      if (rank < p.nc) mbf = 2 * kWP * kHLen + kWP * kLevels;
+      p.xnb[rank] = 0;
+      if (rank < p.nc && lp == 4 && kXStream) {  // weight-stream ring: as many 16-KB buffers as fit (<= kWNB)
+        const int64_t used = (int64_t)mailb + (int64_t)kMbChainEnd4 * 4 + (int64_t)p.pk_smem_floats[rank] * 4;
+        p.xnb[rank] = (int)std::min<int64_t>(kWNB, ((int64_t)dev_smem - used) / (kWChunk * 4));
+        if (p.xnb[rank] < 1) p.xnb[rank] = -1;  // does not fit: no multi-stream variant
+      }
+      if (rank < p.nc) mbf = lp == 4 ? kMbChainEnd4 + (int64_t)std::max(0, p.xnb[rank]) * kWChunk : kMbChainEnd3;
       else if (rank < p.nc + p.nh) mbf = 2 * kWP * kHLen + kWP * kVLen + (int64_t)p.npart * kWP * 256;
       else mbf = (int64_t)p.skip_n[rank - p.nc - p.nh] * kWP * kHLen;
       const int64_t off = (int64_t)mailb + ((mbf * 4 + 127) & ~int64_t(127));
@@ -1667,7 +1939,9 @@ ClusterPlan plan_lp(int L, int r, int s, int device, int lp) {
       smem_pipe = std::max(smem_pipe, (int)(off + (int64_t)p.pk_smem_floats[rank] * 4));
     }
     p.smem_pipe = smem_pipe;
-    if (smem_pipe <= dev_smem) {
+    bool fits = smem_pipe <= dev_smem;
+    for (int rank = 0; rank < p.nc; ++rank) fits = fits && p.xnb[rank] >= 0;
+    if (fits) {
       cudaGetDevice(&prev);
       cudaSetDevice(device);
       int np = 0;
@@ -1824,10 +2098,10 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
     for (int i = 0; i < 2 * R; ++i)
       for (int k = 0; k < R; ++k) wp[((k / 4) * 128 + i) * 4 + k % 4] = W(j, o.w_prev, i, k, R);
   }
-  for (int j = 0; j < p.nxs; ++j) {  // chain-skip W_skip_j [16][s][4]
+  for (int j = 0; j < p.nxs; ++j) {  // chain-skip W_skip_j [s/128 (row block)][16][128][4]
     float* ws = h.data() + p.wskx_off + (int64_t)j * 16 * s * 4;
     for (int i = 0; i < s; ++i)
-      for (int k = 0; k < R; ++k) ws[((k / 4) * s + i) * 4 + k % 4] = W(j, o.w_skip, i, k, R);
+      for (int k = 0; k < R; ++k) ws[(((i / 128) * 16 + k / 4) * 128 + i % 128) * 4 + k % 4] = W(j, o.w_skip, i, k, R);
   }
   return cudaMemcpy(packed, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice);
 }
@@ -1841,6 +2115,8 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   P.p = p;
   P.pk = static_cast<const float*>(packed);
   P.wmax = 1;
+  P.xpb = 1;
+  P.xsb = 1;
   const bool tr = a.trace != nullptr;
   const bool ss = a.ystate != nullptr;
   const bool ap = a.approx == 1 && !tr && !ss;
@@ -1849,12 +2125,16 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
   // clusters fit at once, production gate, no session / trace -- up to kWP interleaved per cluster
   // (the multi-stream variant), spread evenly.  DVW_CLUSTER_W=k forces k (A/B measurements).
   int w = 1;
-  if (p.pipe_ok && !tr && !ss && a.approx == 0) {
+  if (p.pipe_ok && !tr && !ss && a.approx == 0 && a.N * kWP < (int64_t(1) << 31)) {
     const int cap = std::max(1, p.max_clusters_pipe);
     if (a.n_streams > p.max_clusters) w = std::min(kWP, (a.n_streams + cap - 1) / cap);
     if (const char* ev = std::getenv("DVW_CLUSTER_W")) w = std::max(1, std::min(kWP, std::atoi(ev)));
   }
   P.wmax = w;
+  P.xpb = kPB;
+  P.xsb = kXH;
+  if (const char* ev = std::getenv("DVW_XPB")) P.xpb = std::max(1, std::min(kPB, std::atoi(ev)));
+  if (const char* ev = std::getenv("DVW_XSB")) P.xsb = std::max(1, std::min(kXH, std::atoi(ev)));
   const int nclu = (a.n_streams + w - 1) / w;
   cudaLaunchConfig_t cfg{};
   // clusters never wait for each other, so more clusters than fit at once simply run in waves

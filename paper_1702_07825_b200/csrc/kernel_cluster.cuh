@@ -57,6 +57,7 @@ struct ClusterPlan {
   int smem_pipe = 0;              // its dynamic shared memory (Mail + per-stream mailboxes + image)
   int max_clusters_pipe = 0;
   int sw_off_pipe[kCMaxCta] = {}; // byte offset of each CTA's weights image in that layout
+  int xnb[kCMaxCta] = {};         // LP = 4 chain CTAs: buffers of the aux warps' weight-stream ring
 };
 
 ClusterPlan plan_cluster(int L, int r, int s, int device);

@@ -863,3 +863,28 @@ def test_cluster_multi_stream_interleaved_matches_oracle(L, monkeypatch, cfg, S,
         assert np.array_equal(many[st], ref), st
     one = m.generate(dev(cond[S - 1:S]), dev(u[S - 1:S]), hop).cpu().numpy()[0]
     assert np.array_equal(many[S - 1], one)
+
+
+@pytest.mark.parametrize("xpb,xsb", [(1, 1), (2, 3), (3, 4)])
+def test_cluster_multi_stream_batch_sizes_bitwise(L, monkeypatch, xpb, xsb):
+    """Multi-stream cluster kernel, X's batching: the pre terms of up to 3 coming
+    items computed in one W_prev pass and the chain-skip partials (C3, layers < nxs) of up to 4
+    retired items in one W_skip pass give every stream the same codes bitwise for any batch sizes,
+    including ragged last batches (9 streams x 161 samples), and the oracle's codes."""
+    cfg, S, W, N, hop = synth.C3, 9, 8, 161, 64
+    w = synth.make_weights(cfg, 0)
+    cond, u = synth.make_batch(cfg, N, list(range(S)), hop)
+    m = model(L, cfg, w, "cluster")
+    monkeypatch.setenv("DVW_CLUSTER_W", str(W))
+    monkeypatch.setenv("DVW_XPB", str(xpb))
+    monkeypatch.setenv("DVW_XSB", str(xsb))
+    many = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    m.sync()
+    monkeypatch.delenv("DVW_XPB")
+    monkeypatch.delenv("DVW_XSB")
+    base = m.generate(dev(cond), dev(u), hop).cpu().numpy()
+    assert np.array_equal(many, base)
+    for st in (0, 7, 8):
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[st], hop, N, uniforms=u[st],
+                               dilations=cfg.dilation_list(), want_logits=False)
+        assert np.array_equal(many[st], ref), st
