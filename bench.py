@@ -44,7 +44,8 @@ WORKLOADS = {
                     "80,000 samples (5 s @16 kHz) each, hop 64"),
     "C5": dict(cfg=synth.C5, n=80000, streams=2048, split=True,
                desc="C5: l=40 r=64 s=256, 2,048 utterances of 80,000 samples (5 s) sharded across "
-                    "the GPUs (no collective on the path), batched (tcgen05), hop 64"),
+                    "the GPUs (no collective on the path), batched (AUTO: tcgen05 batched kernel, or "
+                    "streams interleaved on clusters below the measured crossover), hop 64"),
 }
 HOP = 64
 FP32_FMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 TFLOP/s
@@ -521,6 +522,23 @@ def main():
                             f"peak ({peak_src}); " + ("one tf32 pass (DVW_PRECISION_TF32); " if fast else
                             "the 3-pass split issues ~3.2x these FLOPs on the tensor pipe; ") +
                             "the step is phase-latency bound (DESIGN.md Batched kernel)"}
+        elif kname == "cluster" and S > 1:
+            # several streams interleaved per cluster (DESIGN.md §4.1 multi-stream variant): a throughput
+            # kernel, bounded per cluster by its chain CTAs' issue slots; report the algorithmic FP32 rate
+            # against the FFMA peak of the SMs the launch occupies at once (co-resident clusters x size)
+            ghz = (clk.summary().get("sm_mhz") or 1965.0) / 1e3
+            co = info["max_clusters_pipe"] if info["streams_per_cluster"] > 1 else info["max_clusters"]
+            act = min(int(info["last_grid"]), int(co) * int(info["last_cluster"]))
+            act_peak = act * 128 * 2 * ghz / 1e3
+            roof = {"bound": "alu", "achieved": achieved_tflops, "peak": act_peak, "unit": "TFLOP/s",
+                    "frac": achieved_tflops / act_peak, "active_sms": act,
+                    "streams_per_cluster": int(info["streams_per_cluster"]),
+                    "chip_fp32_peak_tflops": FP32_FMA_PEAK_TFLOPS,
+                    "traffic": None,
+                    "note": "multi-stream cluster kernel: algorithmic FLOP (2 x MAC/sample x samples x streams) "
+                            "/ launch time vs the FP32 FFMA peak of the SMs it occupies at once (128 lanes x 2 x "
+                            "SM clock each); per item the chain CTAs' serial layer work and their aux warps' "
+                            "L2 weight streaming bound it (DESIGN.md §4.1)"}
         elif kname == "cluster" and floor is not None:
             # batch 1 is latency-bound: the roofline is the measured latency floor
             # of the critical path, l x layer + (chain CTAs + 2) x hop + 3 x head stage + sampler,

@@ -98,6 +98,8 @@ typedef struct {
   int64_t workspace_bytes;   /* bytes of per-stream state (dilation rings) */
   int32_t chain_ctas;        /* cluster kernel's plan: chain CTAs (layers per CTA = ceil(l / chain_ctas)); 0 if none */
   int32_t max_clusters;      /* cluster kernel's plan: clusters co-resident on the device */
+  int32_t streams_per_cluster;  /* cluster kernel, last call: streams interleaved per cluster (1 = one each) */
+  int32_t max_clusters_pipe;    /* cluster kernel's plan: co-resident clusters of the multi-stream variant (0: none) */
 } dvw_info;
 
 /* Create a handle on cfg->device.  Validates sizes (DVW_E_SHAPE / DVW_E_UNSUPPORTED).

@@ -51,7 +51,8 @@ class _Info(ctypes.Structure):
                 ("last_cluster", ctypes.c_int32), ("last_threads", ctypes.c_int32),
                 ("last_launches", ctypes.c_int64), ("weight_bytes", ctypes.c_int64),
                 ("workspace_bytes", ctypes.c_int64), ("chain_ctas", ctypes.c_int32),
-                ("max_clusters", ctypes.c_int32)]
+                ("max_clusters", ctypes.c_int32), ("streams_per_cluster", ctypes.c_int32),
+                ("max_clusters_pipe", ctypes.c_int32)]
 
 
 _vp, _i32, _i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64

@@ -163,15 +163,20 @@ dvw_status check_device_error(dvw_model* m) {
   return DVW_OK;
 }
 
-// AUTO: batches up to this many streams run on the cluster kernel, one cluster per stream
-// (max_clusters co-resident, the rest in waves); larger batches on the batched tensor-core
-// kernel (or the stream kernel).  Crossover measured at C2 (profiles/r2_cluster_streams.json):
-// 4 co-resident 14-CTA clusters give 4 x 133k samples/s for any batch, the batched kernel
-// ~7k samples/s per stream up to 128 streams -- it wins above ~75 streams.
+// AUTO: batches up to this many streams run on the cluster kernel; larger batches on the batched
+// tensor-core kernel (or the stream kernel).  Up to max_clusters streams get one cluster each; more
+// streams run interleaved, up to 8 per cluster (the multi-stream variant, exact gate only), whose
+// aggregate is flat from ~56 streams on while the batched kernel's grows with the batch.  Crossover
+// measured on B200 (profiles/r2_auto_crossover.txt): C2 shape (LP = 3) cluster 2.48 M vs tc 1.64 M
+// samples/s at 256 streams, 2.70 M vs 2.85 M at 448; C5 shape (LP = 4) 1.09 M vs 0.87 M at 256,
+// 1.09 M vs 1.70 M at 512 -- hence 60 (LP = 3) / 48 (LP = 4) streams per co-resident cluster.
 constexpr int kClusterWaves = 16;
-int cluster_streams(const dvw_model* m) {
+int cluster_streams(const dvw_model* m, bool session = false) {
   if (!m->cplan.ok) return 0;
-  return m->trace ? 1 : kClusterWaves * m->cplan.max_clusters;
+  if (m->trace) return 1;
+  if (m->cplan.pipe_ok && m->precision == DVW_PRECISION_FP32 && !session)  // sessions: one stream per cluster
+    return (m->cplan.lpc == 3 ? 60 : 48) * m->cplan.max_clusters_pipe;
+  return kClusterWaves * m->cplan.max_clusters;
 }
 
 dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, const float* uniforms,
@@ -215,7 +220,7 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
       // changes to something the cluster kernel's session variant does not run (and back)
       if (sess->kernel == DVW_KERNEL_TC) kern = DVW_KERNEL_TC;
       else if (sess->kernel == DVW_KERNEL_STREAM && n_streams > 1) kern = DVW_KERNEL_STREAM;
-      else if (n_streams <= cluster_streams(m) && direct && exact) kern = DVW_KERNEL_CLUSTER;
+      else if (n_streams <= cluster_streams(m, true) && direct && exact) kern = DVW_KERNEL_CLUSTER;
       else if (n_streams > 1 && m->bplan.ok && m->precision != DVW_PRECISION_APPC) kern = DVW_KERNEL_TC;
       else kern = DVW_KERNEL_STREAM;
     }
@@ -339,6 +344,7 @@ dvw_status run(dvw_model* m, const float* cond, int64_t n_frames, int32_t hop, c
   m->info.last_cluster = li.cluster;
   m->info.last_threads = li.threads;
   m->info.last_launches = li.launches;
+  m->info.streams_per_cluster = kern == DVW_KERNEL_CLUSTER ? li.rows_per_block : 0;
   return DVW_OK;
 }
 
@@ -441,6 +447,7 @@ DVW_API dvw_status dvw_create(const dvw_config* cfg, dvw_model** out) {
   m->cplan = plan_cluster(m->L, m->r, m->s, m->device);
   m->info.chain_ctas = m->cplan.ok ? m->cplan.nc : 0;
   m->info.max_clusters = m->cplan.ok ? m->cplan.max_clusters : 0;
+  m->info.max_clusters_pipe = m->cplan.ok && m->cplan.pipe_ok ? m->cplan.max_clusters_pipe : 0;
   m->bplan = plan_batch(m->L, m->r, m->s, m->device);
   *out = m;
   return DVW_OK;

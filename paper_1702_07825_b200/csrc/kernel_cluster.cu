@@ -647,6 +647,8 @@ __host__ __device__ constexpr int sm_b(int lp) { return lp == 4 ? LPC * 32 * 128
 __host__ __device__ constexpr int sm_bres(int lp) { return sm_b(lp) + LPC * 2 * R; }
 __host__ __device__ constexpr int sm_fold(int lp) { return sm_bres(lp) + LPC * R; }
 __host__ __device__ constexpr int sm_emb(int lp) { return sm_fold(lp) + LPC * 2 * R; }
+// floats of a chain CTA's shared-memory image (see sm_*; LP = 4 appends nwp W_prev layers)
+__host__ __device__ constexpr int smem_chain(int c, int lp) { return sm_emb(lp) + (c == 0 ? kLevels * R + R : 0); }
 // TMEM: A [0, 64 LP), C [64 LP, 128 LP); at LP = 3 B's W_res tiles sit in [384, 480)
 __host__ __device__ constexpr int col_c(int lp) { return 64 * lp; }
 constexpr int kColB3 = 384;
@@ -1021,6 +1023,10 @@ __device__ void chain_aux(const Params& P, const Ctx& cx, int c, const float* sw
         const float* wp = sw + jl * 16 * 128 * 4;  // shared memory
 #pragma unroll
         for (int q = 0; q < 16; ++q) wv[q] = lds4(wp + (q * 128 + at) * 4);
+      } else if (jl < pl.nwp[c]) {  // LP = 4: the first nwp layers' W_prev in shared memory
+        const float* wp = sw + smem_chain(c, LP) + jl * 16 * 128 * 4;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) wv[q] = lds4(wp + (q * 128 + at) * 4);
       } else {
         const float* wp = P.pk + pl.wprev_off + (int64_t)j * 16 * 128 * 4;  // L2
 #pragma unroll
@@ -1178,6 +1184,10 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
         float4 wv[16];
         if constexpr (LP == 3) {
           const float* wp = sw + jl * 16 * 128 * 4;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) wv[q] = lds4(wp + (q * 128 + at) * 4);
+        } else if (jl < pl.nwp[c]) {  // LP = 4: resident in shared memory
+          const float* wp = sw + smem_chain(c, LP) + jl * 16 * 128 * 4;
 #pragma unroll
           for (int q = 0; q < 16; ++q) wv[q] = lds4(wp + (q * 128 + at) * 4);
         } else {  // LP = 4: from L2, the row's 16 float4 in flight at once
@@ -1819,8 +1829,6 @@ int max_active_pipe(int size, int smem) {
   return n;
 }
 
-// floats of a chain CTA's shared-memory image (see sm_*)
-int smem_chain(int c, int lp) { return sm_emb(lp) + (c == 0 ? kLevels * R + R : 0); }
 
 }  // namespace
 
@@ -1884,11 +1892,21 @@ ClusterPlan plan_lp(int L, int r, int s, int device, int lp) {
     if (p.skip_n[k] > cap) { p.why = "skip capacity"; return p; }
     p.skip_nsm[k] = std::max(0, p.skip_n[k] - maxtm);  // latest layers in tensor memory
   }
+  int dev_smem = 0;
+  cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   int64_t off = 0;
   int max_sw = 0;
   for (int rank = 0; rank < p.size; ++rank) {
     int swf = 0;
-    if (rank < p.nc) swf = smem_chain(rank, lp);
+    p.nwp[rank] = 0;
+    if (rank < p.nc && lp == 4 && !kXStream) {
+      swf = smem_chain(rank, lp);
+      // W_prev of the CTA's first layers into the shared memory left free in the (larger)
+      // multi-stream layout, so neither variant streams them from L2
+      const int64_t used = (int64_t)((sizeof(Mail) + 127) & ~size_t(127)) + (int64_t)kMbChainEnd4 * 4 + (int64_t)swf * 4;
+      p.nwp[rank] = (int)std::max<int64_t>(0, std::min<int64_t>(p.chain_nl[rank], ((int64_t)dev_smem - used) / (16 * 128 * 4 * 4)));
+      swf += p.nwp[rank] * 16 * 128 * 4;
+    } else if (rank < p.nc) swf = smem_chain(rank, lp);
     else if (rank < p.nc + p.nh) swf = s + 128;
     else swf = p.skip_nsm[rank - p.nc - p.nh] * lstride;
     p.pk_off[rank] = off;
@@ -1907,8 +1925,6 @@ ClusterPlan plan_lp(int L, int r, int s, int device, int lp) {
   off += (int64_t)p.nxs * 16 * s * 4;
   p.pk_total = off;
   p.smem_bytes = (int)(((sizeof(Mail) + 127) & ~size_t(127)) + (size_t)max_sw * 4);
-  int dev_smem = 0;
-  cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (p.smem_bytes > dev_smem) { p.why = "shared memory"; return p; }
   int prev = -1;
   cudaGetDevice(&prev);
@@ -2028,6 +2044,10 @@ cudaError_t pack_cluster_weights(const ClusterPlan& p, const float* w, const Off
         if (lp == 3)  // W_prev_j [16][128][4] in shared memory
           for (int i = 0; i < 2 * R; ++i)
             for (int k = 0; k < R; ++k) sm[(jl * 16 * 128 + (k / 4) * 128 + i) * 4 + k % 4] = W(j, o.w_prev, i, k, R);
+        if (lp == 4 && jl < p.nwp[rank])  // LP = 4: the first nwp layers' W_prev after the image
+          for (int i = 0; i < 2 * R; ++i)
+            for (int k = 0; k < R; ++k)
+              sm[smem_chain(rank, lp) + (jl * 16 * 128 + (k / 4) * 128 + i) * 4 + k % 4] = W(j, o.w_prev, i, k, R);
         for (int i = 0; i < 2 * R; ++i) sm[sm_b(lp) + jl * 2 * R + i] = w[(int64_t)j * o.layer_stride + o.b + i];
         if (jl >= xb) {
           for (int i = 0; i < R; ++i) sm[sm_bres(lp) + jl * R + i] = w[(int64_t)(j - 1) * o.layer_stride + o.b_res + i];
@@ -2172,6 +2192,7 @@ cudaError_t launch_cluster_kernel(const RunArgs& a, const ClusterPlan& p, const 
 #undef DVW_LAUNCH
   info->grid = p.size * nclu;
   info->cluster = p.size;
+  info->rows_per_block = w;
   info->threads = kThreads;
   info->launches = 1;
   return e;

@@ -57,6 +57,7 @@ struct ClusterPlan {
   int smem_pipe = 0;              // its dynamic shared memory (Mail + per-stream mailboxes + image)
   int max_clusters_pipe = 0;
   int sw_off_pipe[kCMaxCta] = {}; // byte offset of each CTA's weights image in that layout
+  int nwp[kCMaxCta] = {};         // LP = 4 chain CTAs: W_prev layers resident in shared memory (the rest stream from L2)
   int xnb[kCMaxCta] = {};         // LP = 4 chain CTAs: buffers of the aux warps' weight-stream ring
 };
 

@@ -768,9 +768,10 @@ def test_cluster_kernel_one_cluster_per_stream(L, monkeypatch, cfg, S, N):
 
 
 def test_auto_routes_small_batches_to_clusters(L):
-    """AUTO: up to the co-resident cluster count of streams run one cluster each; larger
-    batches go to the batched tensor-core kernel; a multi-stream session on clusters continues
-    bitwise like one call."""
+    """AUTO: up to the co-resident cluster count of streams run one cluster each, more up to the
+    measured crossover (60 per co-resident cluster at LP = 3, profiles/r2_auto_crossover.txt) run
+    interleaved on the clusters; larger batches go to the batched tensor-core kernel; a
+    multi-stream session on clusters continues bitwise like one call."""
     cfg = synth.C2
     N, hop = 256, 64
     w = synth.make_weights(cfg, 0)
@@ -778,9 +779,17 @@ def test_auto_routes_small_batches_to_clusters(L):
     cond, u = synth.make_batch(cfg, N, list(range(4)), hop)
     one = m.generate(dev(cond), dev(u), hop).cpu().numpy()
     assert m.info()["last_kernel_name"] == "cluster"
-    big_c, big_u = synth.make_batch(cfg, 64, list(range(200)), hop)
+    mid_c, mid_u = synth.make_batch(cfg, 64, list(range(200)), hop)
+    mid = m.generate(dev(mid_c), dev(mid_u), hop).cpu().numpy()
+    assert m.info()["last_kernel_name"] == "cluster"
+    assert m.info()["last_grid"] < 200 * m.info()["last_cluster"]  # interleaved: fewer clusters than streams
+    big_c, big_u = synth.make_batch(cfg, 64, list(range(600)), hop)
     m.generate(dev(big_c), dev(big_u), hop)
     assert m.info()["last_kernel_name"] == "tc"
+    for st in (0, 199):
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, mid_c[st], hop, 64, uniforms=mid_u[st],
+                               dilations=cfg.dilation_list(), want_logits=False)
+        assert np.array_equal(mid[st], ref), st
     sess = m.session(4)
     parts = [sess.generate(dev(cond), dev(u[:, a:b]).contiguous(), hop).cpu().numpy() for a, b in ((0, 100), (100, 256))]
     assert m.info()["last_kernel_name"] == "cluster"
