@@ -1355,27 +1355,36 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
   };
   // item `it` published by A and finished by B: forward its h layer by layer, then its x into its
   // stream's queues; release item it + 1 to A when `rel`
+  // forward layer jl's h of item I to its skip CTA or (last two layers) the heads.  Consecutive
+  // layers' hand-offs from different warps: an st.async holds its warp for about one hop, so the
+  // sends of layers jl and jl + 1 overlap instead of queueing on one warp
+  auto forward = [&](const Item& I, int jl) {
+    const int j = first + jl;
+    if (j >= pl.L - 2) {
+      const int sl = pl.L - 1 - j;
+      const int ht = at - 64 * (jl & 1);
+      if (ht >= 0 && ht < 16 * NH) {
+        const int hh = ht >> 4, e = ht & 15, off = 20 * (e >> 2) + 4 * (e & 3);
+        ptx::st_async4(remote(mb_hbuf<true>(cx, sl, I.s) + off, pl.nc + hh), lds4(&m.hs[I.p][jl][off]),
+                       remote(b_h<true>(cx, sl, I.s), pl.nc + hh));
+      }
+    } else if ((at >> 5) == (jl & 3) && (at & 31) < 16 && pl.layer_skip_cta[j] >= 0) {
+      const int st = at & 31, off = 20 * (st >> 2) + 4 * (st & 3);
+      const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
+      ptx::st_async4(remote(mb_hbuf<true>(cx, sl, I.s) + off, kk), lds4(&m.hs[I.p][jl][off]),
+                     remote(b_h<true>(cx, sl, I.s), kk));
+    }
+  };
+  // item `it` published by A and finished by B: forward its h layer by layer, its x into its
+  // stream's queues.  With `rel`, item it + 1 is released to A as soon as X holds everything it
+  // still needs from item it's buffers (its x rows in registers, its h in the history ring):
+  // the last layer's forward and the queue stores follow the release.  A overwrites hs[p] / B
+  // xs[p] (p = it's parity) only for item it + 2, released after retire(it + 1).
   auto retire = [&](int64_t it, bool rel) {
     const Item I = item_of<true>(it, cx.wc);
     for (int jl = 0; jl < nl; ++jl) {
-      const int j = first + jl;
       ptx::bar_sync(kBarHX + jl, kMain);
-      // consecutive layers' hand-offs from different warps: an st.async holds its warp for about
-      // one hop, so the sends of layers jl and jl + 1 overlap instead of queueing on one warp
-      if (j >= pl.L - 2) {
-        const int sl = pl.L - 1 - j;
-        const int ht = at - 64 * (jl & 1);
-        if (ht >= 0 && ht < 16 * NH) {
-          const int hh = ht >> 4, e = ht & 15, off = 20 * (e >> 2) + 4 * (e & 3);
-          ptx::st_async4(remote(mb_hbuf<true>(cx, sl, I.s) + off, pl.nc + hh), lds4(&m.hs[I.p][jl][off]),
-                         remote(b_h<true>(cx, sl, I.s), pl.nc + hh));
-        }
-      } else if ((at >> 5) == (jl & 3) && (at & 31) < 16 && pl.layer_skip_cta[j] >= 0) {
-        const int st = at & 31, off = 20 * (st >> 2) + 4 * (st & 3);
-        const int kk = pl.layer_skip_cta[j], sl = pl.layer_skip_slot[j];
-        ptx::st_async4(remote(mb_hbuf<true>(cx, sl, I.s) + off, kk), lds4(&m.hs[I.p][jl][off]),
-                       remote(b_h<true>(cx, sl, I.s), kk));
-      }
+      if (jl + 1 < nl || !rel) forward(I, jl);
     }
     wait(cx, &m.bar_done, (uint32_t)I.p, 14);
     if constexpr (LP == 4) {
@@ -1384,15 +1393,24 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
         for (int i = at; i < nl * kHLen; i += kAux) hh[i] = m.hs[I.p][i / kHLen][i % kHLen];
       }
     }
+    float xq[LPC];
+#pragma unroll
+    for (int jl = 0; jl < LPC; ++jl) xq[jl] = (at < R && jl < nl) ? m.xs[I.p][jl][pad16(at)] : 0.0f;
+    ptx::bar_sync(kBarAux, kAux);
+    if (rel) {
+      release(it + 1);
+      forward(I, nl - 1);
+    }
     if (at < R) {
       float* ringb = A.ring + (cx.sidx + I.s) * A.ring_floats;
-      for (int jl = 0; jl < nl; ++jl) {
-        const int d = A.dil[first + jl];
-        ringb[A.ring_off[first + jl] + ((uint32_t)I.n % (uint32_t)d) * R + at] = m.xs[I.p][jl][pad16(at)];
+#pragma unroll
+      for (int jl = 0; jl < LPC; ++jl) {
+        if (jl < nl) {
+          const int d = A.dil[first + jl];
+          ringb[A.ring_off[first + jl] + ((uint32_t)I.n % (uint32_t)d) * R + at] = xq[jl];
+        }
       }
     }
-    ptx::bar_sync(kBarAux, kAux);
-    if (rel) release(it + 1);
   };
   if (nit == 0) return;
   // chain-skip batch ending at item `it` (after its retirement; the history slots are X-private)

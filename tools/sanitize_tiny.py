@@ -18,7 +18,8 @@ from paper_1702_07825_b200 import synth  # noqa: E402
 from paper_1702_07825_b200._lib import Conditioner, Model  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--kernel", default="cluster", choices=["cluster", "stream", "tc", "parallel", "conditioner"])
+ap.add_argument("--kernel", default="cluster",
+                choices=["cluster", "cluster_pipe", "cluster_pipe40", "stream", "tc", "parallel", "conditioner"])
 args = ap.parse_args()
 
 hop = 8
@@ -34,9 +35,16 @@ if args.kernel == "conditioner":
 cfg = synth.Config(4, 64, 128) if args.kernel != "tc" else synth.Config(2, 64, 128)
 N = 48 if args.kernel != "tc" else 12
 S = 2 if args.kernel in ("tc", "cluster") else 1
+kern = args.kernel
+if args.kernel == "cluster_pipe":  # multi-stream variant, LP = 3: 5 streams, 4 per cluster (ragged)
+    S, kern = 5, "cluster"
+    os.environ["DVW_CLUSTER_W"] = "4"
+elif args.kernel == "cluster_pipe40":  # multi-stream variant, LP = 4 with chain-skip batches (l = 40)
+    cfg, N, S, kern = synth.C3, 12, 3, "cluster"
+    os.environ["DVW_CLUSTER_W"] = "3"
 w = synth.make_weights(cfg, 0)
 cond, u = synth.make_batch(cfg, N, list(range(S)), hop)
-m = Model.from_config(cfg).load(w).set_kernel(args.kernel)
+m = Model.from_config(cfg).load(w).set_kernel(kern)
 dc, du = torch.from_numpy(cond).cuda(), torch.from_numpy(u).cuda()
 if args.kernel == "parallel":
     codes = np.stack([synth.make_codes(N, s) for s in range(S)])
@@ -49,6 +57,7 @@ else:
     codes = m.generate(dc, du, hop).cpu().numpy()
     m.sync()
     for s in range(S):
-        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[s], hop, N, uniforms=u[s])
+        ref, _, _ = oracle.run(cfg.n_layers, cfg.residual, cfg.skip, w, cond[s], hop, N, uniforms=u[s],
+                               dilations=cfg.dilation_list())
         assert np.array_equal(codes[s], ref), s
     print(args.kernel, "ok", m.info())
