@@ -85,6 +85,25 @@ constexpr int kWChunk = 8 * 128 * 4;
 #define DVW_XSTREAM 0
 #endif
 constexpr bool kXStream = DVW_XSTREAM != 0;
+// Timing diagnostic of the multi-stream variant (build with -DDVW_PTRACE=1 into a scratch copy,
+// tools/ptrace_pipe.py): %globaltimer stamps of cluster 0's items [kPT0, kPT0 + 64) per CTA and
+// event, read back with dvw_diag_ptrace.  Not compiled into the production library.
+#ifndef DVW_PTRACE
+#define DVW_PTRACE 0
+#endif
+#if DVW_PTRACE
+constexpr int kPT0 = 256;
+__device__ unsigned long long g_pt[kCMaxCta][64][16];
+#endif
+__device__ __forceinline__ void ptr(int64_t it, int ev) {
+#if DVW_PTRACE
+  if (it >= kPT0 && it < kPT0 + 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x == ptx::cluster_rank()) g_pt[ptx::cluster_rank()][it - kPT0][ev] = t;  // cluster 0
+  }
+#endif
+}
 constexpr uint64_t kTimeoutNs = 2000000000ull;
 
 // named barriers (0 is __syncthreads).  A producer that only arrives gets one id per use
@@ -572,6 +591,7 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
       if (wait(cx, b_logits<PIPE>(cx, I.s), (uint32_t)((n - 1) & 1), 11) && k == 0 && !cx.dead)
         ptx::mbar_arm(ptx::smem_u32(b_logits<PIPE>(cx, I.s)), kLevels * 4);
       stamp<TRACE>(tp, 1);
+      if (PIPE && k == 0) ptr(n * cx.wc + I.s, 6);
       if (k == 0) trace<TRACE>(A, n - 1, 3);
       int y;
       if (fb) {
@@ -587,6 +607,7 @@ __device__ __forceinline__ void sample_and_embed(const Params& P, const Ctx& cx,
         if (k == 0) s_codes(A, cx, I.s)[n - 1] = (uint8_t)y;
       }
       if (k == 0) trace<TRACE>(A, n, 20);
+      if (PIPE && k == 0) ptr(n * cx.wc + I.s, 7);
       y2 = y1;
       y1 = y;
     } else {
@@ -698,9 +719,11 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
       if (wait(cx, b_hin<PIPE>(cx, I.s), I.par, 12) && a == 0 && !cx.dead) ptx::mbar_arm(ptx::smem_u32(b_hin<PIPE>(cx, I.s)), R * 4);
     }
     if (a == 0) trace<TRACE>(A, n, 0);
+    if (PIPE && a == 0) ptr(it, 1);
     uint64_t* tp = (a == 0) ? trace_slot<TRACE>(A, n) : nullptr;
     if constexpr (PIPE) wait(cx, &m.bar_pre2[it % kPR], (uint32_t)((it / kPR) & 1), 13);
     else wait(cx, &m.bar_pre, (uint32_t)p, 13);
+    if (PIPE && a == 0) ptr(it, 0);
     const float* prev_pre = PIPE ? mb_pre(cx, (int)(it % kPR)) : &m.pre[0][0];
     ptx::tmem_wait_ld<64>(w);
 #pragma unroll
@@ -729,6 +752,7 @@ __device__ void chain_A(const Params& P, const Ctx& cx, int c, const float* sw) 
                          : NL == 2 ? gate_appc(v[0] + pre0, v[1] + pre1)
                                    : gate_fast(v[0] + pre0, v[1] + pre1);
         stamp<TRACE>(tp, 27 + jl);
+        if (PIPE && a == 0) ptr(it, 2 + jl);
         if (jl + 1 == nl) {
           // the CTA's last layer: h goes straight to the next chain CTA (or, for layer l, to the
           // four heads) -- the only hop on the critical chain between two CTAs
@@ -836,6 +860,7 @@ __device__ void chain_B(const Params& P, const Ctx& cx, int c, const float* sw) 
     // every warp of B arrives once its own rows of xs[p] are stored (4 arrivals complete the phase):
     // X reads all 64 rows for the queues
     __syncwarp();
+    if (PIPE && b == 0) ptr(it, 13);
     if ((b & 31) == 0) {
       if (b == 0) trace<TRACE>(A, n, 2);
       ptx::mbar_arrive(ptx::smem_u32(&m.bar_done));
@@ -878,6 +903,7 @@ __device__ void chain_C(const Params& P, const Ctx& cx, int c, const float* sw) 
         if (jl == 0) {
           if (wait(cx, b_xin<PIPE>(cx, I.s), I.par, 15) && ct == 0 && !cx.dead)
             ptx::mbar_arm(ptx::smem_u32(b_xin<PIPE>(cx, I.s)), R * 4);
+          if (PIPE && ct == 0) ptr(it, 14);
           xv = mb_xin<PIPE>(cx, I.s);
         } else {
           if (jl - 1 >= xb) ptx::bar_sync(bar_xr(jl - 1), kMain);  // x_{j0+jl-1} from B
@@ -1382,11 +1408,14 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
   // xs[p] (p = it's parity) only for item it + 2, released after retire(it + 1).
   auto retire = [&](int64_t it, bool rel) {
     const Item I = item_of<true>(it, cx.wc);
+    if (at == 0) ptr(it, 8);
     for (int jl = 0; jl < nl; ++jl) {
       ptx::bar_sync(kBarHX + jl, kMain);
       if (jl + 1 < nl || !rel) forward(I, jl);
     }
+    if (at == 0) ptr(it, 9);
     wait(cx, &m.bar_done, (uint32_t)I.p, 14);
+    if (at == 0) ptr(it, 10);
     if constexpr (LP == 4) {
       if (xskip) {  // h of the item for its chain-skip batch (hs[p] is reused two items later)
         float* hh = mb_hist(cx, (int)(it % kXH));
@@ -1399,6 +1428,7 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
     ptx::bar_sync(kBarAux, kAux);
     if (rel) {
       release(it + 1);
+      if (at == 0) ptr(it, 11);
       forward(I, nl - 1);
     }
     if (at < R) {
@@ -1439,6 +1469,7 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
         const int cnt = (int)min((int64_t)pb, nit - nx);
         make_pre(nx, cnt);
         nx += cnt;
+        if (at == 0) ptr(it, 12);
       }
       skip_batch(it);
     }
@@ -1514,6 +1545,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
       ptx::tmem_load_async<RQ * 16>(tm + cSk2, w);  // W_skip^(l-1) tile
       if (wait(cx, b_h<PIPE>(cx, 1, I.s), par, 24) && k == 0 && !cx.dead)
         ptx::mbar_arm(ptx::smem_u32(b_h<PIPE>(cx, 1, I.s)), R * 4);
+      if (PIPE && k == 0) ptr(it, 0);
       if (k == 0) trace<TRACE>(A, n, 4);
       ptx::tmem_wait_ld<RQ * 16>(w);
       float v2[RQ];
@@ -1524,6 +1556,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     ptx::tmem_load_async<RQ * 16>(tm, w);  // W_skip^(l) tile, hidden behind the wait
     if (wait(cx, b_h<PIPE>(cx, 0, I.s), par, 21) && k == 0 && !cx.dead)
       ptx::mbar_arm(ptx::smem_u32(b_h<PIPE>(cx, 0, I.s)), R * 4);
+    if (PIPE && k == 0) ptr(it, 1);
     if (k == 0) trace<TRACE>(A, n, 0);
     ptx::tmem_wait_ld<RQ * 16>(w);
     float v[RQ];
@@ -1534,6 +1567,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
       if (wait(cx, b_part<PIPE>(cx, I.s), par, 22) && k == 0 && !cx.dead)
         ptx::mbar_arm(ptx::smem_u32(b_part<PIPE>(cx, I.s)), np * S * 4);
     }
+    if (PIPE && k == 0) ptr(it, 2);
     if (k == 0) trace<TRACE>(A, n, 1);
     if (qwriter) {
       float qv = bskip[qrow];
@@ -1562,6 +1596,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
     if (k == 0) trace<TRACE>(A, n, 9);
     if (wait(cx, b_za<PIPE>(cx, I.s), par, 23) && k == 0 && !cx.dead)
       ptx::mbar_arm(ptx::smem_u32(b_za<PIPE>(cx, I.s)), kLevels * 4);
+    if (PIPE && k == 0) ptr(it, 4);
     if (k == 0) trace<TRACE>(A, n, 2);
     // logits = W_out z_a + B_out
     ptx::tmem_wait_ld<64>(w);
@@ -1577,6 +1612,7 @@ __device__ void head_main(const Params& P, const Ctx& cx, int hidx, const float*
       ptx::st_async(remote(mb_logits<PIPE>(cx, I.s) + 64 * hidx + orow, 0), lg[0] + bout[orow],
                     remote(b_logits<PIPE>(cx, I.s), 0));
     if (k == 0) trace<TRACE>(A, n, 3);
+    if (PIPE && k == 0) ptr(it, 5);
   }
 }
 
@@ -1620,6 +1656,7 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
       if (in_tmem) ptx::tmem_load_async<QS>(tm + (sl - nsm) * QS, wl);
       if (wait(cx, b_h<PIPE>(cx, sl, I.s), par, 31) && t == 0 && !cx.dead)
         ptx::mbar_arm(ptx::smem_u32(b_h<PIPE>(cx, sl, I.s)), R * 4);
+      if (PIPE && t == 0 && (sl == 0 || sl == nown - 1)) ptr(it, sl == 0 ? 0 : 1);
       if (in_tmem) {
         ptx::tmem_wait_ld<QS>(wl);
       } else {
@@ -1650,6 +1687,7 @@ __device__ void skip_main(const Params& P, const Ctx& cx, int k, const float* sw
       ptx::st_async4(remote(mb_part<PIPE>(cx, k, I.s) + 4 * e, pl.nc + hh), lds4(&stage[4 * e]),
                      remote(b_part<PIPE>(cx, I.s), pl.nc + hh));
     }
+    if (PIPE && t == 0) ptr(it, 2);
   }
 }
 
@@ -2401,3 +2439,9 @@ cudaError_t measure_floor(int device, FloorProbe* f) {
 }
 
 }  // namespace dvw
+
+#if DVW_PTRACE
+extern "C" __attribute__((visibility("default"))) int dvw_diag_ptrace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, dvw::g_pt, sizeof(dvw::g_pt));
+}
+#endif

@@ -1,0 +1,9 @@
+mkdir -p gpurun_out/p14
+timeout 600 python -m pytest tests -m gpu -x -q -k "multi_stream or auto_routes" > gpurun_out/p14/tests_ms.txt 2>&1
+timeout 600 python tools/pipe_check.py > gpurun_out/p14/pipe_check.log 2>&1
+for a in "56 400" "14 400" "56 2000" "28 400" "9 300"; do timeout 120 python tools/ptcheck_tmp.py $a >> gpurun_out/p14/ptcheck.txt 2>&1; done
+for r in 1 2; do
+timeout 600 python bench.py --streams 56 --steps 3 --warmup 3 --samples 4000 --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('C2 streams 56', round(d['value']))" >> gpurun_out/p14/bench.txt
+timeout 600 python bench.py --workload C5 --samples 1000 --as-shard-of 8 --steps 3 --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read());print('C5x256', round(d['value']))" >> gpurun_out/p14/bench.txt
+done
+(cd ab/1 && python tools/ptrace_pipe.py > /root/repo/gpurun_out/p14/pt.txt 2>&1; PT_CFG=C3 python tools/ptrace_pipe.py >> /root/repo/gpurun_out/p14/pt.txt 2>&1)
