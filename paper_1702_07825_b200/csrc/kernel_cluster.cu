@@ -1294,13 +1294,17 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
       for (int rr = 0; rr < RR; ++rr) part[k][rr] = 0.0f;
     if constexpr (!kXStream) {
       // W_skip_j row block rr ([nxs][RR][16][128][4]) from L2, the thread's 16 float4 in flight at
-      // once, applied to every item of the batch; partials accumulate layer by layer (oracle order)
-      for (int jl = 0; jl < nl; ++jl) {
-        const int j = first + jl;
-        if (j >= pl.nxs) break;
-        if constexpr ((DVW_DIAG & 256) != 0) continue;
+      // once, applied to every item of the batch; partials accumulate layer by layer (oracle order).
+      // Row blocks outermost: one block's item partials live at a time (register pressure)
 #pragma unroll
-        for (int rr = 0; rr < RR; ++rr) {
+      for (int rr = 0; rr < RR; ++rr) {
+        float pr[kXH];
+#pragma unroll
+        for (int k = 0; k < kXH; ++k) pr[k] = 0.0f;
+        for (int jl = 0; jl < nl; ++jl) {
+          const int j = first + jl;
+          if (j >= pl.nxs) break;
+          if constexpr ((DVW_DIAG & 256) != 0) continue;
           const float* wsk = P.pk + pl.wskx_off + ((int64_t)j * RR + rr) * 16 * 128 * 4;
           float4 wv[16];
 #pragma unroll
@@ -1321,8 +1325,10 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
           }
 #pragma unroll
           for (int k = 0; k < kXH; ++k)
-            if (k < cnt) part[k][rr] += (s01[k].x + s01[k].y) + (s23[k].x + s23[k].y);
+            if (k < cnt) pr[k] += (s01[k].x + s01[k].y) + (s23[k].x + s23[k].y);
         }
+#pragma unroll
+        for (int k = 0; k < kXH; ++k) part[k][rr] = pr[k];
       }
     } else {
     // W_skip_j row block rr ([nxs][RR][16][128][4]) in chunks of 8 column quads: chunk
