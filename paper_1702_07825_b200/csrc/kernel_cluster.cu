@@ -1306,20 +1306,24 @@ __device__ void chain_aux_pipe(const Params& P, const Ctx& cx, int c, const floa
           if (j >= pl.nxs) break;
           if constexpr ((DVW_DIAG & 256) != 0) continue;
           const float* wsk = P.pk + pl.wskx_off + ((int64_t)j * RR + rr) * 16 * 128 * 4;
-          float4 wv[16];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) wv[q] = ldg4(wsk + (q * 128 + at) * 4);
           float2 s01[kXH], s23[kXH];
 #pragma unroll
           for (int k = 0; k < kXH; ++k) s01[k] = s23[k] = make_float2(0.f, 0.f);
+          // the row in two halves of 8 float4 (register pressure; same accumulation order)
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
+          for (int hq = 0; hq < 2; ++hq) {
+            float4 wv[8];
 #pragma unroll
-            for (int k = 0; k < kXH; ++k) {
-              if (k < cnt) {
-                const float4 x = lds4(mb_hist(cx, (int)((ilast - k) % kXH)) + jl * kHLen + pad16(4 * q));
-                s01[k] = ffma2(wv[q].x, wv[q].y, x.x, x.y, s01[k]);
-                s23[k] = ffma2(wv[q].z, wv[q].w, x.z, x.w, s23[k]);
+            for (int q = 0; q < 8; ++q) wv[q] = ldg4(wsk + ((8 * hq + q) * 128 + at) * 4);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+#pragma unroll
+              for (int k = 0; k < kXH; ++k) {
+                if (k < cnt) {
+                  const float4 x = lds4(mb_hist(cx, (int)((ilast - k) % kXH)) + jl * kHLen + pad16(4 * (8 * hq + q)));
+                  s01[k] = ffma2(wv[q].x, wv[q].y, x.x, x.y, s01[k]);
+                  s23[k] = ffma2(wv[q].z, wv[q].w, x.z, x.w, s23[k]);
+                }
               }
             }
           }
